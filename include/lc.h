@@ -1,0 +1,177 @@
+/*
+ * lc.h -- C-ABI of liblc.so: the B200 (sm_100a) hot path of the local
+ * character-based method for sequences of sparse solves A x = b
+ * (Ye, An, Xu, arXiv 2001.01158; "P:a-b" = /root/reference/PAPER.md lines).
+ *
+ * The method (Alg. 1), input (A, x0, b) -> output x:
+ *   lc_create_csr     A (Eq. 1) into the library's device layout
+ *   lc_select_domain  Omega_local (Alg. 2 P:480-500 / Alg. 3)      Alg. 1 l.2
+ *   lc_extract_sub    B, b_B - E x_C^(0) (Eq. 2-3)                 Alg. 1 l.3-4
+ *   lc_solve_local    xbar_B, then x~ = Q (xbar_B; x_C^(0)) (Eq. 4) Alg. 1 l.5-6
+ *   lc_solve_global   Eq. 6 check at x~, else the global solve from x~         Alg. 1 l.8-11
+ *   (method0 of P:987 = lc_solve_global from x0.)
+ *
+ * Conventions (all entry points):
+ *   - Plain pointers and sizes only.  "device" = a CUDA device pointer on the
+ *     current device; "host" = ordinary host memory.  `stream` is a cudaStream_t
+ *     passed as void* (NULL = legacy default stream); all device work of a call is
+ *     enqueued on it.
+ *   - Vectors b, x0, x are caller-owned DEVICE arrays of length n*block (f64).
+ *     They are read (b, x0) or read and written (x) on `stream`; the library never
+ *     frees them.  Inputs are never modified except `x`.
+ *   - Handles (lc_matrix, lc_domain, lc_sub) own their device buffers until the
+ *     matching lc_destroy_*; destroying NULL is a no-op.
+ *   - Every call returns lc_status; no exception crosses the ABI.  On error the
+ *     output handle is set to NULL and lc_last_error() returns a thread-local
+ *     message describing the failure.
+ *   - Synchronisation: a call returns once its host-visible outputs (K, tau,
+ *     solve info) are ready; these are the only host<->device syncs of the path.
+ *   - Indices are 0-based.  Column indices within a row must be strictly
+ *     ascending (the canonical per-row order of all row sums, R22).
+ *   - The library has no CPU fallback: without a usable sm_100 device every
+ *     call fails with LC_ERR_CUDA.
+ */
+#ifndef LC_H
+#define LC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LC_OK = 0,
+  LC_NOT_CONVERGED = 1,      /* non-fatal: x holds the best iterate; see lc_solve_info */
+  LC_ERR_INVALID_ARG = -1,   /* null pointer, bad enum, eps <= 0, alpha/theta not in [0,1], p not in (0,1) ... */
+  LC_ERR_DIMENSION = -2,     /* n, block, batch inconsistent (n % batch, n/batch > 2^31 ...) */
+  LC_ERR_PATTERN = -3,       /* columns unsorted / duplicated / out of range, or diagonal not stored */
+  LC_ERR_ZERO_DIAGONAL = -4, /* Jacobi / block-Jacobi needs a_ii != 0 (an invertible 3x3 cell block) */
+  LC_ERR_BREAKDOWN = -5,     /* PCG: p^T A p <= 0 (A not SPD) */
+  LC_ERR_NONFINITE = -6,     /* NaN / Inf in a reduction */
+  LC_ERR_CUDA = -7,          /* CUDA runtime error (message in lc_last_error) */
+  LC_ERR_OOM = -8            /* device allocation failed */
+} lc_status;
+
+/* internal storage format of lc_create_csr */
+enum { LC_FMT_SELL32 = 0 /* SELL-C-sigma, C = 32, sigma = 1 (row order kept) */ };
+/* local-domain criterion (lc_domain_params.criterion) */
+enum { LC_CRIT_RESIDUAL = 0 /* |r_i|, r = b - A x0 (Alg. 3 l.4) */,
+       LC_CRIT_GRADIENT = 1 /* g_i of Eq. 5 on x0 */ };
+/* threshold rule (lc_domain_params.threshold) */
+enum { LC_THR_PAPER = 0      /* tau = eps ||b||_2 / sqrt(N) (Eq. 7), param = eps */,
+       LC_THR_REL_MAX = 1    /* tau = theta * max_i c_i (Alg. 2 l.10), param = theta (= alpha) */,
+       LC_THR_PERCENTILE = 2 /* tau = nearest-rank p-quantile of c (R14), param = p */ };
+/* solver (lc_solver_params.method / precond) */
+enum { LC_PCG = 0, LC_GMRES = 1 };
+enum { LC_JACOBI = 0, LC_BLOCK_JACOBI = 1 };
+
+typedef struct lc_matrix_s* lc_matrix;
+typedef struct lc_domain_s* lc_domain;
+typedef struct lc_sub_s* lc_sub;
+
+/*
+ * A (Eq. 1).  block = 1: n scalar rows, CSR row_ptr[n+1] (int64), col_idx[nnz]
+ * (int32), values[nnz] (f64).  block = 3: n = number of cells (block rows),
+ * row_ptr/col_idx are block-level and values holds 9 f64 per block, row-major;
+ * unknowns are interleaved per cell.  batch = G >= 1: A is
+ * block-diagonal with G equal independent segments of n/G rows (the G group
+ * systems of multi-group diffusion, solved together); b and x stack the
+ * segments.  inputs_on_device != 0: the three arrays are device pointers,
+ * else host pointers.  The arrays are COPIED (the caller keeps ownership).
+ * The pattern is validated on the device (sorted, unique, in range, diagonal
+ * stored) -> LC_ERR_PATTERN; a zero diagonal (singular cell block) ->
+ * LC_ERR_ZERO_DIAGONAL.  fmt must be LC_FMT_SELL32.
+ */
+lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, const int64_t* row_ptr, const int32_t* col_idx,
+                        const double* values, int32_t inputs_on_device, int32_t fmt, void* stream, lc_matrix* A);
+
+typedef struct {
+  int32_t criterion;     /* LC_CRIT_* */
+  int32_t threshold;     /* LC_THR_* */
+  double param;          /* eps (> 0) | theta in [0,1] (0 => Omega) | p in (0,1) */
+  int32_t expand_rounds; /* Alg. 3 E_max, residual criterion only; 0 = none; <= 64 */
+  int32_t dilate_hops;   /* unconditional dilation by graph hops of A's pattern (R15); 0 = none */
+} lc_domain_params;
+
+/*
+ * Omega_local (Alg. 1 l.2).  Per segment g: criterion c_u, threshold tau_g,
+ * Omega_g = {u : c_u > tau_g} (strict, R10), then E_max expansion rounds of
+ * Alg. 3 (admit neighbour j iff |r_j| + sum_{l in Omega} |a_jl x0_l| > tau, all
+ * admissions of a round simultaneous, stop early when a round admits nothing)
+ * and dilate_hops unconditional neighbour unions.  For block = 3 the unit is the
+ * cell (R16): c = max of the three |r| components, cells enter whole; the
+ * gradient criterion needs block = 1.  b, x0: device [n*block].
+ * K_host (host, [batch]): number of scalar unknowns in Omega_g.  Syncs `stream`.
+ */
+lc_status lc_select_domain(lc_matrix A, const double* b, const double* x0, const lc_domain_params* p, void* stream,
+                           lc_domain* dom, int64_t* K_host);
+
+/*
+ * Copy out Omega_local.  idx_dev (device, optional, [sum K]): the ascending
+ * global scalar-row indices of Omega (segment by segment).  tau_host (host,
+ * optional, [batch]).  crit_dev (device, optional, [n]): the per-unit criterion
+ * c_u (|r| max over the cell, or g).  adm_dev (device, optional, [n]): per unit,
+ * the Eq. 8 admission value of the last expansion round in which the unit was a
+ * neighbour of Omega, NaN if never.  Syncs `stream`.
+ */
+lc_status lc_domain_export(lc_domain dom, int32_t* idx_dev, double* tau_host, double* crit_dev, double* adm_dev,
+                           void* stream);
+
+/*
+ * B = A[Omega, Omega] in local numbering (Eq. 2; F and C are never formed),
+ * b_sub = b_B - E x_C^(0) (Eq. 3; per row the fma chain over stored columns
+ * outside Omega, ascending, then one subtraction), x_B0 = x0[Omega] and the
+ * (block-)Jacobi inverse diagonal of B.  K = 0 gives an empty handle.
+ */
+lc_status lc_extract_sub(lc_matrix A, lc_domain dom, const double* b, const double* x0, void* stream, lc_sub* sub);
+
+typedef struct {
+  int32_t method;    /* LC_PCG (Jacobi-preconditioned CG, SPD systems) | LC_GMRES (right-preconditioned
+                        block-Jacobi GMRES(restart) with CGS2, nonsymmetric block = 3 systems) */
+  int32_t precond;   /* LC_JACOBI for LC_PCG; LC_BLOCK_JACOBI (3x3 cell blocks) for LC_GMRES */
+  int32_t restart;   /* GMRES restart length (30); ignored by PCG; <= 64 */
+  double rel_tol;    /* eps of Eq. 6: stop when ||b - A x||_2 <= eps ||b||_2 (absolute if b = 0) */
+  int32_t max_iters; /* PCG: SpMVs with p; GMRES: Arnoldi steps.  Exceeding -> LC_NOT_CONVERGED */
+} lc_solver_params;
+
+typedef struct {
+  int32_t iterations;       /* PCG SpMVs with p / cumulative GMRES Arnoldi steps (R30) */
+  int32_t status;           /* LC_OK | LC_NOT_CONVERGED | LC_ERR_BREAKDOWN | LC_ERR_NONFINITE */
+  double rel_residual;      /* ||b - A x||_2 / ||b||_2 of the returned x (true residual) */
+  double seconds;           /* device time of the solve (CUDA events) */
+} lc_solve_info;
+
+/*
+ * Alg. 1 l.5-6: solve B xbar_B = b_sub from x_B0 to ||b_sub - B xbar|| <= eps ||b_sub||
+ * (R17), then x~: x[Omega] = xbar_B, the complement untouched (Eq. 4).
+ * x: device [n*block], in = x0, out = x~.  info: host [batch] (per segment).
+ * Returns the worst per-segment status (LC_NOT_CONVERGED is non-fatal, R18).
+ */
+lc_status lc_solve_local(lc_sub sub, const lc_solver_params* p, double* x, void* stream, lc_solve_info* info);
+
+/*
+ * Alg. 1 l.8-11 (and method0): r = b - A x; if Eq. 6 holds, 0 iterations; else
+ * the Krylov solve of the whole system warm-started from x.  x: device, in/out.
+ */
+lc_status lc_solve_global(lc_matrix A, const double* b, double* x, const lc_solver_params* p, void* stream,
+                          lc_solve_info* info);
+
+/* introspection (host ints): rows n*block, stored scalars, batch, SELL slices, max row length */
+lc_status lc_matrix_info(lc_matrix A, int64_t* n_unknowns, int64_t* nnz, int32_t* batch, int64_t* nslices,
+                         int32_t* max_row);
+
+void lc_destroy_matrix(lc_matrix A);
+void lc_destroy_domain(lc_domain dom);
+void lc_destroy_sub(lc_sub sub);
+
+/* thread-local message of the last failing call on this thread ("" if none) */
+const char* lc_last_error(void);
+
+/* number of CUDA kernels this library has launched in the process (for the bench's gpu_launches) */
+int64_t lc_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LC_H */

@@ -1,0 +1,282 @@
+// common.cu -- error plumbing, stream-ordered allocation, the decoupled
+// look-back scan / stream compaction, SELL slice maps.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+
+#include "lc_internal.cuh"
+
+namespace lc {
+
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+void set_error(const std::string& msg) { g_err = msg; }
+lc_status cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  if (e == cudaErrorMemoryAllocation) return LC_ERR_OOM;
+  return LC_ERR_CUDA;
+}
+void count_launch(int n) { g_launches += n; }
+
+static bool g_pool_init = false;
+lc_status dalloc(void** p, size_t bytes, cudaStream_t s) {
+  if (!g_pool_init) {
+    int dev = 0;
+    LC_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    LC_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;
+    LC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    g_pool_init = true;
+  }
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMallocAsync(p, bytes, s);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return cuda_fail(e, "cudaMallocAsync");
+  }
+  return LC_OK;
+}
+void dfree(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+void Sell::release(cudaStream_t s) {
+  dfree(slice_ptr, s); dfree(slice_row0, s); dfree(slice_seg, s); dfree(seg_unit0, s); dfree(seg_slice0, s);
+  dfree(col, s); dfree(val, s); dfree(rowlen, s); dfree(dinv, s);
+  slice_ptr = nullptr; slice_row0 = slice_seg = seg_unit0 = nullptr; seg_slice0 = nullptr;
+  col = nullptr; val = nullptr; rowlen = nullptr; dinv = nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// Decoupled look-back (single pass, dynamic tile ids for forward progress).
+// Status word: bits 62-63 = 0 invalid / 1 aggregate / 2 inclusive prefix.
+// ---------------------------------------------------------------------------
+constexpr unsigned long long kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// called by all 32 lanes of warp 0; returns the exclusive prefix of `tile` (broadcast to all lanes)
+__device__ long long lookback(unsigned long long* status, long long tile, long long aggregate) {
+  int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_release(&status[0], kFlagP | (unsigned long long)aggregate);
+    return 0;
+  }
+  if (lane == 0) st_release(&status[tile], kFlagA | (unsigned long long)aggregate);
+  long long acc = 0, pred = tile - 1;
+  for (;;) {
+    long long t = pred - lane;
+    unsigned long long w = (t >= 0) ? ld_acquire(&status[t]) : kFlagP;
+    while (__any_sync(0xffffffffu, (w >> 62) == 0)) {
+      if ((w >> 62) == 0) w = ld_acquire(&status[t]);
+    }
+    unsigned pm = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+    if (pm) {
+      int first = __ffs(pm) - 1;
+      acc += warp_sum_ll(lane <= first ? (long long)(w & kValMask) : 0);
+      break;
+    }
+    acc += warp_sum_ll((long long)(w & kValMask));
+    pred -= 32;
+  }
+  if (lane == 0) st_release(&status[tile], kFlagP | (unsigned long long)(acc + aggregate));
+  return acc;
+}
+
+constexpr int kCtThreads = 256, kCtItems = 16, kCtTile = kCtThreads * kCtItems;
+
+// Stable stream compaction of {u : flag[u] != 255}: warp ballot/popc counts, CTA scan, look-back.
+__global__ void __launch_bounds__(kCtThreads) k_compact(const uint8_t* __restrict__ flag, int64_t m,
+                                                        int32_t* __restrict__ idx, int32_t* __restrict__ inv,
+                                                        unsigned long long* status, unsigned* tile_counter,
+                                                        int64_t* count_out, int64_t ntiles) {
+  __shared__ unsigned s_tile;
+  __shared__ int s_warp[kCtThreads / 32];
+  __shared__ long long s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const long long tile = s_tile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // item k of thread t covers unit tile*4096 + k*256 + t: each warp-wide load is coalesced and the
+  // ballot of item k gives the warp's 32 consecutive units in order.
+  const int64_t base = tile * kCtTile;
+  unsigned masks[kCtItems];
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < kCtItems; ++k) {
+    int64_t u = base + k * kCtThreads + threadIdx.x;
+    bool in = (u < m) && (flag[u] != 255);
+    masks[k] = __ballot_sync(0xffffffffu, in);
+    cnt += __popc(masks[k]);   // warp-level count (same in all lanes)
+  }
+  // per (item k, warp w) offsets: order = k major, then warp, then lane
+  __shared__ int s_cnt[kCtItems][kCtThreads / 32];
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < kCtItems; ++k) s_cnt[k][warp] = __popc(masks[k]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int k = 0; k < kCtItems; ++k)
+      for (int w = 0; w < kCtThreads / 32; ++w) { int c = s_cnt[k][w]; s_cnt[k][w] = run; run += c; }
+    s_warp[0] = run;
+  }
+  __syncthreads();
+  const int total = s_warp[0];
+  if (warp == 0) {
+    long long ex = lookback(status, tile, total);
+    if (lane == 0) s_excl = ex;
+  }
+  __syncthreads();
+  const long long ex = s_excl;
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int k = 0; k < kCtItems; ++k) {
+    int64_t u = base + k * kCtThreads + threadIdx.x;
+    if (u < m) {
+      bool in = (masks[k] >> lane) & 1u;
+      if (in) {
+        long long pos = ex + s_cnt[k][warp] + __popc(masks[k] & lt);
+        idx[pos] = (int32_t)u;
+        inv[u] = (int32_t)pos;
+      } else {
+        inv[u] = -1;
+      }
+    }
+  }
+  if (tile == ntiles - 1 && threadIdx.x == 0) *count_out = ex + total;
+  (void)cnt;
+}
+
+lc_status compact_flags(const uint8_t* flag, int64_t m, int32_t* idx, int32_t* inv, int64_t* count_dev,
+                        cudaStream_t s) {
+  if (m == 0) {
+    LC_CUDA(cudaMemsetAsync(count_dev, 0, sizeof(int64_t), s));
+    return LC_OK;
+  }
+  int64_t ntiles = (m + kCtTile - 1) / kCtTile;
+  void* ws = nullptr;
+  size_t bytes = sizeof(unsigned long long) * ntiles + 16;
+  lc_status st = dalloc(&ws, bytes, s);
+  if (st) return st;
+  LC_CUDA(cudaMemsetAsync(ws, 0, bytes, s));
+  unsigned long long* status = (unsigned long long*)ws;
+  unsigned* counter = (unsigned*)((char*)ws + sizeof(unsigned long long) * ntiles);
+  k_compact<<<(unsigned)ntiles, kCtThreads, 0, s>>>(flag, m, idx, inv, status, counter, count_dev, ntiles);
+  LC_LAUNCHED();
+  dfree(ws, s);
+  return LC_OK;
+}
+
+// Exclusive scan of int64 (slice widths -> slice_ptr).  out has n+1 entries.
+constexpr int kScItems = 8, kScTile = kCtThreads * kScItems;
+__global__ void __launch_bounds__(kCtThreads) k_scan_i64(const int64_t* __restrict__ in, int64_t* __restrict__ out,
+                                                         int64_t n, unsigned long long* status,
+                                                         unsigned* tile_counter, int64_t ntiles) {
+  __shared__ unsigned s_tile;
+  __shared__ long long s_w[kCtThreads / 32];
+  __shared__ long long s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const long long tile = s_tile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t base = tile * kScTile + (int64_t)threadIdx.x * kScItems;
+  long long v[kScItems], sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScItems; ++k) { v[k] = (base + k < n) ? in[base + k] : 0; sum += v[k]; }
+  long long incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  long long woff = 0, total = 0;
+  for (int w = 0; w < kCtThreads / 32; ++w) { if (w < warp) woff += s_w[w]; total += s_w[w]; }
+  if (warp == 0) {
+    long long ex = lookback(status, tile, total);
+    if (lane == 0) s_excl = ex;
+  }
+  __syncthreads();
+  long long run = s_excl + woff + incl - sum;
+#pragma unroll
+  for (int k = 0; k < kScItems; ++k) {
+    if (base + k < n) out[base + k] = run;
+    run += v[k];
+  }
+  if (tile == ntiles - 1 && threadIdx.x == 0) out[n] = s_excl + total;
+}
+
+lc_status scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s) {
+  if (n == 0) {
+    LC_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), s));
+    return LC_OK;
+  }
+  int64_t ntiles = (n + kScTile - 1) / kScTile;
+  void* ws = nullptr;
+  size_t bytes = sizeof(unsigned long long) * ntiles + 16;
+  lc_status st = dalloc(&ws, bytes, s);
+  if (st) return st;
+  LC_CUDA(cudaMemsetAsync(ws, 0, bytes, s));
+  k_scan_i64<<<(unsigned)ntiles, kCtThreads, 0, s>>>(in, out, n, (unsigned long long*)ws,
+                                                      (unsigned*)((char*)ws + sizeof(unsigned long long) * ntiles),
+                                                      ntiles);
+  LC_LAUNCHED();
+  dfree(ws, s);
+  return LC_OK;
+}
+
+// slice -> (first unit, segment) from the per-segment unit / slice offsets
+__global__ void k_slice_map(int64_t nslices, int nseg, const int32_t* __restrict__ seg_unit0,
+                            const int64_t* __restrict__ seg_slice0, int32_t* row0, int32_t* sseg) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= nslices) return;
+  int lo = 0, hi = nseg - 1;   // last g with seg_slice0[g] <= s
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (seg_slice0[mid] <= s) lo = mid; else hi = mid - 1;
+  }
+  row0[s] = seg_unit0[lo] + (int32_t)(32 * (s - seg_slice0[lo]));
+  sseg[s] = lo;
+}
+
+lc_status build_slice_map(Sell& M, cudaStream_t s) {
+  if (M.nslices == 0) return LC_OK;
+  k_slice_map<<<(unsigned)((M.nslices + 255) / 256), 256, 0, s>>>(M.nslices, M.nseg, M.seg_unit0, M.seg_slice0,
+                                                                   M.slice_row0, M.slice_seg);
+  LC_LAUNCHED();
+  return LC_OK;
+}
+
+}  // namespace lc
+
+void lc_domain_s::release(cudaStream_t s) {
+  lc::dfree(flag, s); lc::dfree(idx, s); lc::dfree(inv, s); lc::dfree(crit, s); lc::dfree(adm, s);
+  lc::dfree(r, s); lc::dfree(seg_base, s);
+  flag = nullptr; idx = inv = nullptr; crit = adm = r = nullptr; seg_base = nullptr;
+}
+void lc_sub_s::release(cudaStream_t s) {
+  B.release(s);
+  lc::dfree(idx, s); lc::dfree(bsub, s); lc::dfree(xB0, s);
+  idx = nullptr; bsub = xB0 = nullptr;
+}
+
+extern "C" const char* lc_last_error(void) { return lc::g_err.c_str(); }
+extern "C" int64_t lc_kernel_launches(void) { return (int64_t)lc::g_launches.load(); }

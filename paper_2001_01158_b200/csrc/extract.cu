@@ -1,0 +1,170 @@
+// extract.cu -- lc_extract_sub: B = A[Omega, Omega] in local numbering
+// (Eq. 2), b_sub = b_B - E x_C^(0) (Eq. 3), x_B0 = x0[Omega], and B's
+// (block-)Jacobi inverse diagonal, in one gather pass.  B is stored as SELL-32 with
+// the uniform width of A's longest row, so no count pass is needed; each segment of
+// a batched system keeps its own slices (local ranks [seg_base[g], seg_base[g+1])).
+#include <cstring>
+
+#include "lc_internal.cuh"
+
+namespace lc {
+
+constexpr int kTB = 256;
+
+template <int BS>
+__global__ void __launch_bounds__(kTB) k_extract(SellView A, SellView B, int W, const int32_t* __restrict__ idx,
+                                                 const int32_t* __restrict__ inv, const double* __restrict__ b,
+                                                 const double* __restrict__ x0, int32_t* __restrict__ Bcol,
+                                                 double* __restrict__ Bval, uint8_t* __restrict__ Browlen,
+                                                 double* __restrict__ Bdinv, double* __restrict__ bsub,
+                                                 double* __restrict__ xB0, int64_t* __restrict__ Bslice_ptr) {
+  int64_t sB = (blockIdx.x * (int64_t)kTB + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (sB >= B.nslices) return;
+  if (lane == 0) {
+    Bslice_ptr[sB] = 32ll * W * sB;
+    if (sB == B.nslices - 1) Bslice_ptr[sB + 1] = 32ll * W * (sB + 1);
+  }
+  int g = B.slice_seg[sB];
+  int64_t row0 = B.slice_row0[sB];
+  int64_t l = row0 + lane;
+  bool valid = l < B.seg_unit0[g + 1];
+  const int64_t pB = 32ll * W * sB;
+  int kb = 0;
+  if (valid) {
+    int64_t i = idx[l];
+    int64_t lu = i - A.seg_unit0[g];
+    int64_t sA = A.seg_slice0[g] + (lu >> 5);
+    int laneA = (int)(lu & 31);
+    int64_t pA = A.slice_ptr[sA];
+    int len = A.rowlen[i];
+    double acc[BS];
+#pragma unroll
+    for (int a = 0; a < BS; ++a) acc[a] = 0.0;
+    for (int k = 0; k < len; ++k) {
+      int64_t slotA = pA + 32ll * k + laneA;
+      int c = A.col[slotA];
+      int ic = inv[c];
+      if (ic >= 0) {                                   // B block: column in local numbering
+        int64_t slotB = pB + 32ll * kb + lane;
+        Bcol[slotB] = ic;
+        if (BS == 1) {
+          Bval[slotB] = A.val[slotA];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 9; ++q)
+            Bval[9 * (pB + 32ll * kb) + 32 * q + lane] = A.val[9 * (pA + 32ll * k) + 32 * q + laneA];
+        }
+        ++kb;
+      } else {                                         // E x_C^(0): fma chain, ascending columns
+        if (BS == 1) {
+          acc[0] = __fma_rn(A.val[slotA], x0[c], acc[0]);
+        } else {
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int be = 0; be < 3; ++be)
+              acc[a] = __fma_rn(A.val[9 * (pA + 32ll * k) + 32 * (3 * a + be) + laneA], x0[3ll * c + be], acc[a]);
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < BS; ++a) {
+      bsub[BS * l + a] = b[BS * i + a] - acc[a];
+      xB0[BS * l + a] = x0[BS * i + a];
+    }
+#pragma unroll
+    for (int q = 0; q < BS * BS; ++q) Bdinv[BS * BS * l + q] = A.dinv[BS * BS * i + q];
+    Browlen[l] = (uint8_t)kb;
+  }
+  int padc = valid ? (int)l : (int)row0;
+  for (int k = kb; k < W; ++k) {
+    int64_t slotB = pB + 32ll * k + lane;
+    Bcol[slotB] = padc;
+    if (BS == 1) {
+      Bval[slotB] = 0.0;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) Bval[9 * (pB + 32ll * k) + 32 * q + lane] = 0.0;
+    }
+  }
+}
+
+}  // namespace lc
+
+using namespace lc;
+
+extern "C" lc_status lc_extract_sub(lc_matrix M, lc_domain D, const double* b, const double* x0, void* stream,
+                                    lc_sub* out) {
+  if (!out) { set_error("lc_extract_sub: out is NULL"); return LC_ERR_INVALID_ARG; }
+  *out = nullptr;
+  if (!M || !D || !b || !x0 || D->A != M) {
+    set_error("lc_extract_sub: null argument or domain of another matrix");
+    return LC_ERR_INVALID_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int bs = M->block, G = M->batch, bb = bs * bs;
+  lc_sub_s* S = new lc_sub_s();
+  S->block = bs; S->nseg = G; S->K_units = D->K_units; S->h_seg_base = D->h_seg_base;
+  Sell& B = S->B;
+  B.block = bs; B.nunits = D->K_units; B.nseg = G; B.maxw = M->A.maxw;
+  B.h_seg_unit0.resize(G + 1);
+  B.h_seg_slice0.resize(G + 1);
+  int64_t nsl = 0;
+  for (int g = 0; g <= G; ++g) {
+    B.h_seg_unit0[g] = (int32_t)D->h_seg_base[g];
+    B.h_seg_slice0[g] = nsl;
+    if (g < G) nsl += (D->h_seg_base[g + 1] - D->h_seg_base[g] + 31) / 32;
+  }
+  B.nslices = nsl;
+  B.nslots = 32ll * B.maxw * nsl;
+  if (S->K_units == 0) { *out = S; return LC_OK; }
+  lc_status st = LC_OK;
+  const int64_t K = S->K_units;
+#define CK(x) do { st = (x); if (st) goto fail; } while (0)
+#define CKC(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { st = cuda_fail(_e, #x); goto fail; } } while (0)
+  CK(dalloc((void**)&B.seg_unit0, sizeof(int32_t) * (G + 1), s));
+  CK(dalloc((void**)&B.seg_slice0, sizeof(int64_t) * (G + 1), s));
+  CKC(cudaMemcpyAsync(B.seg_unit0, D->seg_base, sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToDevice, s));
+  CKC(cudaMemcpyAsync(B.seg_slice0, B.h_seg_slice0.data(), sizeof(int64_t) * (G + 1), cudaMemcpyHostToDevice, s));
+  CK(dalloc((void**)&B.slice_row0, sizeof(int32_t) * nsl, s));
+  CK(dalloc((void**)&B.slice_seg, sizeof(int32_t) * nsl, s));
+  CK(build_slice_map(B, s));
+  CK(dalloc((void**)&B.slice_ptr, sizeof(int64_t) * (nsl + 1), s));
+  CK(dalloc((void**)&B.col, sizeof(int32_t) * B.nslots, s));
+  CK(dalloc((void**)&B.val, sizeof(double) * B.nslots * bb, s));
+  CK(dalloc((void**)&B.rowlen, K, s));
+  CK(dalloc((void**)&B.dinv, sizeof(double) * K * bb, s));
+  CK(dalloc((void**)&S->bsub, sizeof(double) * K * bs, s));
+  CK(dalloc((void**)&S->xB0, sizeof(double) * K * bs, s));
+  CK(dalloc((void**)&S->idx, sizeof(int32_t) * K, s));
+  CKC(cudaMemcpyAsync(S->idx, D->idx, sizeof(int32_t) * K, cudaMemcpyDeviceToDevice, s));
+  {
+    unsigned nb = (unsigned)((nsl * 32 + kTB - 1) / kTB);
+    SellView VA = view(M->A), VB = view(B);
+    if (bs == 1)
+      k_extract<1><<<nb, kTB, 0, s>>>(VA, VB, B.maxw, D->idx, D->inv, b, x0, B.col, B.val, B.rowlen, B.dinv, S->bsub,
+                                      S->xB0, B.slice_ptr);
+    else
+      k_extract<3><<<nb, kTB, 0, s>>>(VA, VB, B.maxw, D->idx, D->inv, b, x0, B.col, B.val, B.rowlen, B.dinv, S->bsub,
+                                      S->xB0, B.slice_ptr);
+    count_launch();
+    CKC(cudaGetLastError());
+  }
+  *out = S;
+  return LC_OK;
+fail:
+  S->release(s);
+  cudaStreamSynchronize(s);
+  delete S;
+  return st;
+#undef CK
+#undef CKC
+}
+
+extern "C" void lc_destroy_sub(lc_sub S) {
+  if (!S) return;
+  S->release(0);
+  cudaStreamSynchronize(0);
+  delete S;
+}

@@ -1,0 +1,422 @@
+// gmres.cu -- right-preconditioned (block-)Jacobi GMRES(m) with CGS2 as ONE
+// persistent cooperative kernel (SURVEY 8(a) a7/a9 for the nonsymmetric 3T
+// systems of config 4; readings R20/R21/R33).
+//
+// One Arnoldi step = four grid-synchronised passes, each fused with its dots:
+//   1a  v_j = src / h (src = r or the last w), t = M^-1 v_j        (block inverse per cell)
+//   1b  w = A t (BSR-in-SELL SpMV) fused with h_i = V_i^T w, i <= j  (CGS pass 1 dots)
+//   2   w -= V h fused with h2_i = V_i^T w                           (CGS pass 2 dots)
+//   3   w -= V h2 fused with ||w||^2
+// The Hessenberg column, Givens rotations and the residual estimate |g_{j+1}|
+// are computed redundantly (bitwise identically) by every CTA from the same
+// fixed-order reductions, so control flow is grid-uniform without any host
+// round trip.  End of cycle: x += M^-1 (V y), then the true residual (R19).
+#include <cmath>
+
+#include "lc_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace lc {
+
+constexpr int kGT = 512;
+constexpr int kGW = kGT / 32;
+constexpr int kMaxM = 64;
+
+struct GmresArgs {
+  SellView A;
+  const double* b;
+  double* x;
+  double* r;
+  double* w;
+  double* t;
+  double* V;            // (m+1) vectors of n scalars
+  double* part;         // [(m+2) * nCTA]
+  int* out;             // [0] iters, [1] status
+  double* out_relres;
+  const int32_t* scatter_idx;
+  double* x_full;
+  int64_t n;            // scalar unknowns
+  double eps;
+  int m;
+  int max_iters;
+};
+
+template <int BS>
+__device__ __forceinline__ void block_apply(const double* __restrict__ Mi, const double* v, double* t) {
+#pragma unroll
+  for (int a = 0; a < BS; ++a) {
+    double s = 0.0;
+#pragma unroll
+    for (int be = 0; be < BS; ++be) s = __fma_rn(Mi[a * BS + be], v[be], s);
+    t[a] = s;
+  }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
+  cg::grid_group grid = cg::this_grid();
+  const SellView& A = P.A;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nCTA = gridDim.x, bid = blockIdx.x;
+  const int64_t s_begin = bid * kGW + warp, s_step = nCTA * kGW;
+  const int64_t nunits = A.seg_unit0[1];
+  const int64_t n = P.n;
+  const int m = P.m;
+  __shared__ double H[(kMaxM + 1) * kMaxM];
+  __shared__ double gv[kMaxM + 1], cs[kMaxM], sn[kMaxM], yv[kMaxM];
+  __shared__ double red[kMaxM + 2];
+  __shared__ double s_acc[kGW][kMaxM + 2];
+
+  // per-lane accumulators -> per-warp smem -> CTA partial part[q*nCTA + bid]
+  auto clear = [&](int nq) {
+    for (int t = threadIdx.x; t < kGW * (kMaxM + 2); t += kGT) (&s_acc[0][0])[t] = 0.0;
+    __syncthreads();
+    (void)nq;
+  };
+  auto publish = [&](int nq) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < nq; q += kGT) {
+      double v = 0.0;
+      for (int w = 0; w < kGW; ++w) v += s_acc[w][q];
+      P.part[q * nCTA + bid] = v;
+    }
+  };
+  // fixed-order reduction of nq quantities over all CTAs into red[]
+  auto reduce = [&](int nq) {
+    for (int q = warp; q < nq; q += kGW) {
+      double v = 0.0;
+      for (int64_t c = lane; c < nCTA; c += 32) v += P.part[q * nCTA + c];
+      v = warp_sum(v);
+      if (lane == 0) red[q] = v;
+    }
+    __syncthreads();
+  };
+  auto lane_flush = [&](int q, double v) {
+    v = warp_sum(v);
+    if (lane == 0) s_acc[warp][q] += v;
+  };
+
+  int it = 0;
+  bool first = true;
+  double nb = 0.0, tgt = 0.0;
+  int status = LC_NOT_CONVERGED;
+  double relres = 0.0;
+  for (;;) {
+    // ------------------------------------------------ true residual -------
+    clear(2);
+    {
+      double a0 = 0.0, a1 = 0.0;
+      for (int64_t s = s_begin; s < A.nslices; s += s_step) {
+        int64_t u = A.slice_row0[s] + lane;
+        if (u >= nunits) continue;
+        int64_t p0 = A.slice_ptr[s];
+        int wd = (int)((A.slice_ptr[s + 1] - p0) >> 5);
+        double acc[BS];
+#pragma unroll
+        for (int a = 0; a < BS; ++a) acc[a] = 0.0;
+        for (int k = 0; k < wd; ++k) {
+          int c = A.col[p0 + 32 * k + lane];
+          if (BS == 1) {
+            acc[0] = __fma_rn(A.val[p0 + 32 * k + lane], P.x[c], acc[0]);
+          } else {
+            const double* vb = A.val + 9 * (p0 + 32ll * k) + lane;
+            double y0 = P.x[3ll * c], y1 = P.x[3ll * c + 1], y2 = P.x[3ll * c + 2];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              acc[a] = __fma_rn(vb[32 * (3 * a)], y0, acc[a]);
+              acc[a] = __fma_rn(vb[32 * (3 * a + 1)], y1, acc[a]);
+              acc[a] = __fma_rn(vb[32 * (3 * a + 2)], y2, acc[a]);
+            }
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < BS; ++a) {
+          double bi = P.b[BS * u + a];
+          double ri = bi - acc[a];
+          P.r[BS * u + a] = ri;
+          a0 = __fma_rn(ri, ri, a0);
+          a1 = __fma_rn(bi, bi, a1);
+        }
+      }
+      lane_flush(0, a0);
+      lane_flush(1, a1);
+    }
+    publish(2);
+    grid.sync();
+    reduce(2);
+    double beta = sqrt(red[0]);
+    if (first) { nb = sqrt(red[1]); tgt = nb > 0 ? P.eps * nb : P.eps; }
+    relres = nb > 0 ? beta / nb : beta;
+    if (!isfinite(beta)) { status = LC_ERR_NONFINITE; break; }
+    if (beta <= tgt) { status = LC_OK; break; }
+    if (it >= P.max_iters) { status = LC_NOT_CONVERGED; break; }
+    first = false;
+    if (threadIdx.x <= m) gv[threadIdx.x] = 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) gv[0] = beta;
+    __syncthreads();
+    double hnorm = beta;
+    const double* src = P.r;
+    int jend = 0;
+    for (int j = 0; j < m; ++j) {
+      double* Vj = P.V + (size_t)j * n;
+      // ---- 1a: v_j = src / h, t = M^-1 v_j
+      for (int64_t s = s_begin; s < A.nslices; s += s_step) {
+        int64_t u = A.slice_row0[s] + lane;
+        if (u >= nunits) continue;
+        double v[BS], tt[BS];
+#pragma unroll
+        for (int a = 0; a < BS; ++a) { v[a] = src[BS * u + a] / hnorm; Vj[BS * u + a] = v[a]; }
+        block_apply<BS>(A.dinv + BS * BS * u, v, tt);
+#pragma unroll
+        for (int a = 0; a < BS; ++a) P.t[BS * u + a] = tt[a];
+      }
+      grid.sync();
+      // ---- 1b: w = A t, h_i = V_i . w
+      clear(j + 1);
+      {
+        double dacc[kMaxM + 1];
+        for (int i = 0; i <= j; ++i) dacc[i] = 0.0;
+        for (int64_t s = s_begin; s < A.nslices; s += s_step) {
+          int64_t u = A.slice_row0[s] + lane;
+          bool valid = u < nunits;
+          double acc[BS];
+#pragma unroll
+          for (int a = 0; a < BS; ++a) acc[a] = 0.0;
+          if (valid) {
+            int64_t p0 = A.slice_ptr[s];
+            int wd = (int)((A.slice_ptr[s + 1] - p0) >> 5);
+            for (int k = 0; k < wd; ++k) {
+              int c = A.col[p0 + 32 * k + lane];
+              if (BS == 1) {
+                acc[0] = __fma_rn(A.val[p0 + 32 * k + lane], P.t[c], acc[0]);
+              } else {
+                const double* vb = A.val + 9 * (p0 + 32ll * k) + lane;
+                double y0 = P.t[3ll * c], y1 = P.t[3ll * c + 1], y2 = P.t[3ll * c + 2];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                  acc[a] = __fma_rn(vb[32 * (3 * a)], y0, acc[a]);
+                  acc[a] = __fma_rn(vb[32 * (3 * a + 1)], y1, acc[a]);
+                  acc[a] = __fma_rn(vb[32 * (3 * a + 2)], y2, acc[a]);
+                }
+              }
+            }
+#pragma unroll
+            for (int a = 0; a < BS; ++a) P.w[BS * u + a] = acc[a];
+          }
+          if (valid) {
+            for (int i = 0; i <= j; ++i) {
+              const double* Vi = P.V + (size_t)i * n;
+              double d = dacc[i];
+#pragma unroll
+              for (int a = 0; a < BS; ++a) d = __fma_rn(Vi[BS * u + a], acc[a], d);
+              dacc[i] = d;
+            }
+          }
+        }
+        for (int i = 0; i <= j; ++i) lane_flush(i, dacc[i]);
+      }
+      publish(j + 1);
+      grid.sync();
+      reduce(j + 1);
+      // keep h in smem column j of H (pass-1 part)
+      if (threadIdx.x <= j) H[threadIdx.x * m + j] = red[threadIdx.x];
+      __syncthreads();
+      // ---- 2: w -= V h, h2_i = V_i . w
+      clear(j + 1);
+      {
+      double dacc[kMaxM + 1];
+      for (int i = 0; i <= j; ++i) dacc[i] = 0.0;
+      for (int64_t s = s_begin; s < A.nslices; s += s_step) {
+        int64_t u = A.slice_row0[s] + lane;
+        bool valid = u < nunits;
+        double ww[BS];
+        if (valid) {
+#pragma unroll
+          for (int a = 0; a < BS; ++a) ww[a] = P.w[BS * u + a];
+          for (int i = 0; i <= j; ++i) {
+            const double* Vi = P.V + (size_t)i * n;
+            double hi = H[i * m + j];
+#pragma unroll
+            for (int a = 0; a < BS; ++a) ww[a] = __fma_rn(-hi, Vi[BS * u + a], ww[a]);
+          }
+#pragma unroll
+          for (int a = 0; a < BS; ++a) P.w[BS * u + a] = ww[a];
+          for (int i = 0; i <= j; ++i) {
+            const double* Vi = P.V + (size_t)i * n;
+            double d = dacc[i];
+#pragma unroll
+            for (int a = 0; a < BS; ++a) d = __fma_rn(Vi[BS * u + a], ww[a], d);
+            dacc[i] = d;
+          }
+        }
+      }
+      for (int i = 0; i <= j; ++i) lane_flush(i, dacc[i]);
+      }
+      publish(j + 1);
+      grid.sync();
+      reduce(j + 1);
+      // ---- 3: w -= V h2, ||w||^2
+      clear(1);
+      {
+        double a0 = 0.0;
+        for (int64_t s = s_begin; s < A.nslices; s += s_step) {
+          int64_t u = A.slice_row0[s] + lane;
+          if (u >= nunits) continue;
+          double ww[BS];
+#pragma unroll
+          for (int a = 0; a < BS; ++a) ww[a] = P.w[BS * u + a];
+          for (int i = 0; i <= j; ++i) {
+            const double* Vi = P.V + (size_t)i * n;
+            double h2 = red[i];
+#pragma unroll
+            for (int a = 0; a < BS; ++a) ww[a] = __fma_rn(-h2, Vi[BS * u + a], ww[a]);
+          }
+#pragma unroll
+          for (int a = 0; a < BS; ++a) { P.w[BS * u + a] = ww[a]; a0 = __fma_rn(ww[a], ww[a], a0); }
+        }
+        // red[] still holds h2: add it to H before it is overwritten
+        __syncthreads();
+        if (threadIdx.x <= j) H[threadIdx.x * m + j] += red[threadIdx.x];
+        lane_flush(0, a0);
+      }
+      publish(1);
+      grid.sync();
+      reduce(1);
+      if (threadIdx.x == 0) {
+        double hn = sqrt(red[0]);
+        H[(j + 1) * m + j] = hn;
+        for (int i = 0; i < j; ++i) {
+          double t0 = H[i * m + j], t1 = H[(i + 1) * m + j];
+          H[i * m + j] = cs[i] * t0 + sn[i] * t1;
+          H[(i + 1) * m + j] = -sn[i] * t0 + cs[i] * t1;
+        }
+        double hd = H[j * m + j], hs = H[(j + 1) * m + j];
+        double den = sqrt(hd * hd + hs * hs);
+        if (den == 0.0) { cs[j] = 1.0; sn[j] = 0.0; } else { cs[j] = hd / den; sn[j] = hs / den; }
+        H[j * m + j] = cs[j] * hd + sn[j] * hs;
+        H[(j + 1) * m + j] = 0.0;
+        gv[j + 1] = -sn[j] * gv[j];
+        gv[j] = cs[j] * gv[j];
+        red[kMaxM + 1] = hn;
+      }
+      __syncthreads();
+      hnorm = red[kMaxM + 1];
+      ++it;
+      jend = j + 1;
+      src = P.w;
+      double gj = gv[j + 1];
+      if (!isfinite(gj)) { status = LC_ERR_NONFINITE; break; }
+      if (fabs(gj) <= tgt || hnorm == 0.0 || it >= P.max_iters) break;
+    }
+    if (status == LC_ERR_NONFINITE) break;
+    // ---- y = H^-1 g (upper triangular), x += M^-1 (V y)
+    if (threadIdx.x == 0) {
+      for (int i = jend - 1; i >= 0; --i) {
+        double s = gv[i];
+        for (int k = i + 1; k < jend; ++k) s -= H[i * m + k] * yv[k];
+        yv[i] = s / H[i * m + i];
+      }
+    }
+    __syncthreads();
+    for (int64_t s = s_begin; s < A.nslices; s += s_step) {
+      int64_t u = A.slice_row0[s] + lane;
+      if (u >= nunits) continue;
+      double acc[BS], tt[BS];
+#pragma unroll
+      for (int a = 0; a < BS; ++a) acc[a] = 0.0;
+      for (int i = 0; i < jend; ++i) {
+        const double* Vi = P.V + (size_t)i * n;
+        double yi = yv[i];
+#pragma unroll
+        for (int a = 0; a < BS; ++a) acc[a] = __fma_rn(yi, Vi[BS * u + a], acc[a]);
+      }
+      block_apply<BS>(A.dinv + BS * BS * u, acc, tt);
+#pragma unroll
+      for (int a = 0; a < BS; ++a) P.x[BS * u + a] += tt[a];
+    }
+    grid.sync();
+  }
+  if (bid == 0 && threadIdx.x == 0) { P.out[0] = it; P.out[1] = status; *P.out_relres = relres; }
+  if (P.scatter_idx) {
+    for (int64_t s = s_begin; s < A.nslices; s += s_step) {
+      int64_t u = A.slice_row0[s] + lane;
+      if (u >= nunits) continue;
+      int64_t gidx = P.scatter_idx[u];
+#pragma unroll
+      for (int a = 0; a < BS; ++a) P.x_full[BS * gidx + a] = P.x[BS * u + a];
+    }
+  }
+}
+
+static int g_gm_ctas[2] = {0, 0};
+
+lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* scatter_idx, double* x_full,
+                    const double* x_init, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
+  if (M.nseg != 1) { set_error("GMRES: batched (block-diagonal) systems are not supported"); return LC_ERR_DIMENSION; }
+  const int BS = M.block;
+  const int m = p->restart;
+  const int64_t n = M.nunits * BS;
+  int ci = BS == 1 ? 0 : 1;
+  void* fn = BS == 1 ? (void*)k_gmres<1> : (void*)k_gmres<3>;
+  if (!g_gm_ctas[ci]) {
+    int per_sm = 0;
+    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGT, 0));
+    if (per_sm < 1) { set_error("GMRES kernel does not fit on an SM"); return LC_ERR_CUDA; }
+    g_gm_ctas[ci] = std::min(per_sm, 2) * num_sms();
+  }
+  int64_t nCTA = std::min<int64_t>(g_gm_ctas[ci], (M.nslices + kGW - 1) / kGW);
+  if (nCTA < 1) nCTA = 1;
+  size_t vbytes = ((sizeof(double) * (size_t)n) + 255) & ~(size_t)255;
+  size_t bytes = vbytes * (3 + (m + 1) + (scatter_idx ? 1 : 0)) + sizeof(double) * (m + 2) * nCTA + 64;
+  void* ws = nullptr;
+  lc_status st = dalloc(&ws, bytes, s);
+  if (st) return st;
+  char* w = (char*)ws;
+  GmresArgs a;
+  a.A = view(M);
+  a.b = b;
+  a.r = (double*)w; w += vbytes;
+  a.w = (double*)w; w += vbytes;
+  a.t = (double*)w; w += vbytes;
+  a.V = (double*)w; w += vbytes * (m + 1);
+  if (scatter_idx) {
+    a.x = (double*)w; w += vbytes;
+    cudaError_t e = cudaMemcpyAsync(a.x, x_init, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) { dfree(ws, s); return cuda_fail(e, "cudaMemcpyAsync"); }
+  } else {
+    a.x = x;
+  }
+  a.part = (double*)w; w += sizeof(double) * (m + 2) * nCTA;
+  a.out = (int*)w;
+  a.out_relres = (double*)(w + 16);
+  a.scatter_idx = scatter_idx;
+  a.x_full = x_full;
+  a.n = n;
+  a.eps = p->rel_tol;
+  a.m = m;
+  a.max_iters = p->max_iters;
+  int out[2] = {0, 0};
+  double rr = 0.0;
+  float ms = 0.f;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+  void* args[] = {&a};
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kGT), args, 0, s);
+  count_launch();
+  cudaEventRecord(e1, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, a.out, 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&rr, a.out_relres, 8, cudaMemcpyDeviceToHost, s);
+  dfree(ws, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  if (e != cudaSuccess) return cuda_fail(e, "GMRES kernel");
+  if (info) { info[0].iterations = out[0]; info[0].status = out[1]; info[0].rel_residual = rr; info[0].seconds = ms * 1e-3; }
+  if (out[1] < 0) set_error("GMRES: non-finite value");
+  return (lc_status)out[1];
+}
+
+}  // namespace lc

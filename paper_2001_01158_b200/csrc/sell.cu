@@ -1,0 +1,261 @@
+// sell.cu -- lc_create_csr: CSR/BSR input -> SELL-32 (sigma = 1) on the device,
+// with on-device pattern validation and the (block-)Jacobi inverse diagonal.
+#include <cstring>
+
+#include "lc_internal.cuh"
+
+namespace lc {
+
+enum : unsigned { kErrPattern = 1u, kErrZeroDiag = 2u, kErrRowLen = 4u };
+
+// one warp per slice: validate rows, record rowlen, slice width (in slots * 32)
+__global__ void k_slice_width(int64_t nslices, int seg_units, int spg, const int64_t* __restrict__ rp,
+                              const int32_t* __restrict__ ci, int64_t* __restrict__ widths,
+                              uint8_t* __restrict__ rowlen, unsigned* err, int* maxw) {
+  int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (s >= nslices) return;
+  int64_t g = s / spg;
+  int64_t lu = (s - g * spg) * 32 + lane;
+  int64_t seg0 = g * (int64_t)seg_units, seg1 = seg0 + seg_units;
+  int len = 0;
+  if (lu < seg_units) {
+    int64_t u = seg0 + lu;
+    int64_t k0 = rp[u], k1 = rp[u + 1];
+    int64_t l = k1 - k0;
+    unsigned e = 0;
+    if (l < 1 || l > 255) e |= kErrRowLen;
+    bool diag = false;
+    int prev = -1;
+    for (int64_t k = k0; k < k1 && !(e & kErrRowLen); ++k) {
+      int c = ci[k];
+      if (c <= prev || c < seg0 || c >= seg1) e |= kErrPattern;
+      if (c == u) diag = true;
+      prev = c;
+    }
+    if (!diag) e |= kErrPattern;
+    if (e) atomicOr(err, e);
+    len = (l > 255) ? 255 : (int)l;
+    rowlen[u] = (uint8_t)len;
+  }
+  int w = len;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, o));
+  if (lane == 0) {
+    widths[s] = 32ll * w;
+    atomicMax(maxw, w);
+  }
+}
+
+__device__ bool inv3(const double* A, double* Ai) {
+  // LU without pivoting (diagonally dominant cell blocks), then solve for each unit vector
+  double L10, L20, L21, U[9];
+  for (int i = 0; i < 9; ++i) U[i] = A[i];
+  if (U[0] == 0.0) return false;
+  L10 = U[3] / U[0]; L20 = U[6] / U[0];
+  U[4] -= L10 * U[1]; U[5] -= L10 * U[2];
+  U[7] -= L20 * U[1]; U[8] -= L20 * U[2];
+  if (U[4] == 0.0) return false;
+  L21 = U[7] / U[4];
+  U[8] -= L21 * U[5];
+  if (U[8] == 0.0) return false;
+  for (int c = 0; c < 3; ++c) {
+    double y0 = (c == 0), y1 = (c == 1) - L10 * y0, y2 = (c == 2) - L20 * y0 - L21 * y1;
+    double x2 = y2 / U[8];
+    double x1 = (y1 - U[5] * x2) / U[4];
+    double x0 = (y0 - U[1] * x1 - U[2] * x2) / U[0];
+    Ai[c] = x0; Ai[3 + c] = x1; Ai[6 + c] = x2;
+  }
+  return isfinite(Ai[0]) && isfinite(Ai[4]) && isfinite(Ai[8]);
+}
+
+// one warp per slice: scatter rows into SELL slots (pad with col = own unit, value 0)
+template <int BS>
+__global__ void k_fill(int64_t nslices, int seg_units, int spg, const int64_t* __restrict__ rp,
+                       const int32_t* __restrict__ ci, const double* __restrict__ va,
+                       const int64_t* __restrict__ slice_ptr, int32_t* __restrict__ col, double* __restrict__ val,
+                       double* __restrict__ dinv, unsigned* err) {
+  int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (s >= nslices) return;
+  int64_t g = s / spg;
+  int64_t lu = (s - g * spg) * 32 + lane;
+  bool valid = lu < seg_units;
+  int64_t u = g * (int64_t)seg_units + lu;
+  int64_t p0 = slice_ptr[s];
+  int w = (int)((slice_ptr[s + 1] - p0) >> 5);
+  int64_t k0 = valid ? rp[u] : 0, k1 = valid ? rp[u + 1] : 0;
+  double D[BS * BS];
+#pragma unroll
+  for (int q = 0; q < BS * BS; ++q) D[q] = 0.0;
+  for (int k = 0; k < w; ++k) {
+    int64_t slot = p0 + 32ll * k + lane;
+    int64_t e = k0 + k;
+    bool real = valid && e < k1;
+    int c = real ? ci[e] : (valid ? (int)u : 0);
+    col[slot] = c;
+    if (BS == 1) {
+      double v = real ? va[e] : 0.0;
+      val[slot] = v;
+      if (real && c == u) D[0] = v;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        double v = real ? va[9 * e + q] : 0.0;
+        val[9 * (p0 + 32ll * k) + 32 * q + lane] = v;
+        if (real && c == u) D[q] = v;
+      }
+    }
+  }
+  if (!valid) return;
+  if (BS == 1) {
+    if (D[0] == 0.0) atomicOr(err, kErrZeroDiag);
+    dinv[u] = 1.0 / D[0];
+  } else {
+    double Ai[9];
+    if (!inv3(D, Ai)) atomicOr(err, kErrZeroDiag);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) dinv[9 * u + q] = Ai[q];
+  }
+}
+
+}  // namespace lc
+
+using namespace lc;
+
+extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, const int64_t* row_ptr,
+                                   const int32_t* col_idx, const double* values, int32_t inputs_on_device,
+                                   int32_t fmt, void* stream, lc_matrix* out) {
+  if (!out) { set_error("lc_create_csr: out is NULL"); return LC_ERR_INVALID_ARG; }
+  *out = nullptr;
+  if (!row_ptr || !col_idx || !values) { set_error("lc_create_csr: null array"); return LC_ERR_INVALID_ARG; }
+  if (fmt != LC_FMT_SELL32) { set_error("lc_create_csr: fmt must be LC_FMT_SELL32"); return LC_ERR_INVALID_ARG; }
+  if (block != 1 && block != 3) { set_error("lc_create_csr: block must be 1 or 3"); return LC_ERR_DIMENSION; }
+  if (batch < 1 || batch > 64 || n < 1 || n % batch != 0 || n / batch > (int64_t)INT32_MAX - 64 ||
+      n > (int64_t)INT32_MAX - 64) {
+    set_error("lc_create_csr: need n >= 1, 1 <= batch <= 64, batch | n, n < 2^31");
+    return LC_ERR_DIMENSION;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  int bb = block * block;
+  // row_ptr end -> nnz
+  int64_t nnz = 0;
+  if (inputs_on_device) {
+    LC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    LC_CUDA(cudaStreamSynchronize(s));
+  } else {
+    nnz = row_ptr[n];
+  }
+  if (nnz < n || nnz > (int64_t)INT32_MAX * 4) { set_error("lc_create_csr: bad nnz"); return LC_ERR_PATTERN; }
+
+  lc_matrix_s* M = new lc_matrix_s();
+  M->n = n; M->block = block; M->batch = batch; M->nnz = nnz; M->seg_units = (int32_t)(n / batch);
+  Sell& A = M->A;
+  A.block = block; A.nunits = n; A.nseg = batch;
+  int spg = (M->seg_units + 31) / 32;
+  A.nslices = (int64_t)spg * batch;
+  lc_status st = LC_OK;
+  const int64_t* d_rp = row_ptr;
+  const int32_t* d_ci = col_idx;
+  const double* d_va = values;
+  void *t_rp = nullptr, *t_ci = nullptr, *t_va = nullptr, *t_w = nullptr, *t_err = nullptr;
+  unsigned h_err = 0;
+  int h_maxw = 0;
+#define CK(x) do { st = (x); if (st) goto fail; } while (0)
+#define CKC(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { st = cuda_fail(_e, #x); goto fail; } } while (0)
+  if (!inputs_on_device) {
+    CK(dalloc(&t_rp, sizeof(int64_t) * (n + 1), s));
+    CK(dalloc(&t_ci, sizeof(int32_t) * nnz, s));
+    CK(dalloc(&t_va, sizeof(double) * nnz * bb, s));
+    CKC(cudaMemcpyAsync(t_rp, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+    CKC(cudaMemcpyAsync(t_ci, col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+    CKC(cudaMemcpyAsync(t_va, values, sizeof(double) * nnz * bb, cudaMemcpyHostToDevice, s));
+    d_rp = (const int64_t*)t_rp; d_ci = (const int32_t*)t_ci; d_va = (const double*)t_va;
+  }
+  CK(dalloc(&t_w, sizeof(int64_t) * (A.nslices + 1), s));
+  CK(dalloc(&t_err, 16, s));
+  CKC(cudaMemsetAsync(t_err, 0, 16, s));
+  CK(dalloc((void**)&A.rowlen, n, s));
+  CK(dalloc((void**)&A.slice_ptr, sizeof(int64_t) * (A.nslices + 1), s));
+  {
+    unsigned blocks = (unsigned)((A.nslices * 32 + 255) / 256);
+    k_slice_width<<<blocks, 256, 0, s>>>(A.nslices, M->seg_units, spg, d_rp, d_ci, (int64_t*)t_w, A.rowlen,
+                                         (unsigned*)t_err, (int*)((char*)t_err + 8));
+    count_launch();
+    CKC(cudaGetLastError());
+  }
+  CK(scan_exclusive_i64((const int64_t*)t_w, A.slice_ptr, A.nslices, s));
+  CKC(cudaMemcpyAsync(&A.nslots, A.slice_ptr + A.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CKC(cudaMemcpyAsync(&h_err, t_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  CKC(cudaMemcpyAsync(&h_maxw, (char*)t_err + 8, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CKC(cudaStreamSynchronize(s));
+  if (h_err) {
+    st = (h_err & kErrRowLen) ? LC_ERR_PATTERN : LC_ERR_PATTERN;
+    set_error(h_err & kErrRowLen ? "lc_create_csr: row length must be in [1, 255]"
+                                 : "lc_create_csr: columns must be strictly ascending, inside the row's "
+                                   "segment, with the diagonal stored");
+    goto fail;
+  }
+  A.maxw = h_maxw;
+  CK(dalloc((void**)&A.col, sizeof(int32_t) * A.nslots, s));
+  CK(dalloc((void**)&A.val, sizeof(double) * A.nslots * bb, s));
+  CK(dalloc((void**)&A.dinv, sizeof(double) * n * bb, s));
+  {
+    unsigned blocks = (unsigned)((A.nslices * 32 + 255) / 256);
+    if (block == 1)
+      k_fill<1><<<blocks, 256, 0, s>>>(A.nslices, M->seg_units, spg, d_rp, d_ci, d_va, A.slice_ptr, A.col, A.val,
+                                       A.dinv, (unsigned*)t_err);
+    else
+      k_fill<3><<<blocks, 256, 0, s>>>(A.nslices, M->seg_units, spg, d_rp, d_ci, d_va, A.slice_ptr, A.col, A.val,
+                                       A.dinv, (unsigned*)t_err);
+    count_launch();
+    CKC(cudaGetLastError());
+  }
+  // segment maps
+  A.h_seg_unit0.resize(batch + 1);
+  A.h_seg_slice0.resize(batch + 1);
+  for (int g = 0; g <= batch; ++g) { A.h_seg_unit0[g] = g * M->seg_units; A.h_seg_slice0[g] = (int64_t)g * spg; }
+  CK(dalloc((void**)&A.seg_unit0, sizeof(int32_t) * (batch + 1), s));
+  CK(dalloc((void**)&A.seg_slice0, sizeof(int64_t) * (batch + 1), s));
+  CKC(cudaMemcpyAsync(A.seg_unit0, A.h_seg_unit0.data(), sizeof(int32_t) * (batch + 1), cudaMemcpyHostToDevice, s));
+  CKC(cudaMemcpyAsync(A.seg_slice0, A.h_seg_slice0.data(), sizeof(int64_t) * (batch + 1), cudaMemcpyHostToDevice, s));
+  CK(dalloc((void**)&A.slice_row0, sizeof(int32_t) * A.nslices, s));
+  CK(dalloc((void**)&A.slice_seg, sizeof(int32_t) * A.nslices, s));
+  CK(build_slice_map(A, s));
+  CKC(cudaMemcpyAsync(&h_err, t_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  CKC(cudaStreamSynchronize(s));
+  if (h_err & kErrZeroDiag) {
+    st = LC_ERR_ZERO_DIAGONAL;
+    set_error("lc_create_csr: zero diagonal (or singular 3x3 cell block)");
+    goto fail;
+  }
+  dfree(t_rp, s); dfree(t_ci, s); dfree(t_va, s); dfree(t_w, s); dfree(t_err, s);
+  *out = M;
+  return LC_OK;
+fail:
+  dfree(t_rp, s); dfree(t_ci, s); dfree(t_va, s); dfree(t_w, s); dfree(t_err, s);
+  A.release(s);
+  cudaStreamSynchronize(s);
+  delete M;
+  return st;
+#undef CK
+#undef CKC
+}
+
+extern "C" lc_status lc_matrix_info(lc_matrix A, int64_t* n_unknowns, int64_t* nnz, int32_t* batch,
+                                    int64_t* nslices, int32_t* max_row) {
+  if (!A) { set_error("lc_matrix_info: NULL handle"); return LC_ERR_INVALID_ARG; }
+  if (n_unknowns) *n_unknowns = A->n * A->block;
+  if (nnz) *nnz = A->nnz * A->block * A->block;
+  if (batch) *batch = A->batch;
+  if (nslices) *nslices = A->A.nslices;
+  if (max_row) *max_row = A->A.maxw;
+  return LC_OK;
+}
+
+extern "C" void lc_destroy_matrix(lc_matrix A) {
+  if (!A) return;
+  A->A.release(0);
+  cudaStreamSynchronize(0);
+  delete A;
+}

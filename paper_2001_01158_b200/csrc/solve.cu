@@ -1,0 +1,54 @@
+// solve.cu -- lc_solve_local / lc_solve_global: dispatch to the persistent
+// Krylov kernels (pcg.cu, gmres.cu).
+#include "lc_internal.cuh"
+
+namespace lc {
+lc_status run_pcg(const Sell& M, const double* b, double* x, const int32_t* scatter_idx, double* x_full,
+                  const double* x_init, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info);
+lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* scatter_idx, double* x_full,
+                    const double* x_init, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info);
+
+static lc_status check_params(const lc_solver_params* p) {
+  if (!p) { set_error("solver params NULL"); return LC_ERR_INVALID_ARG; }
+  if (!(p->rel_tol > 0) || p->max_iters < 0) { set_error("solver: need rel_tol > 0, max_iters >= 0"); return LC_ERR_INVALID_ARG; }
+  if (p->method == LC_PCG) {
+    if (p->precond != LC_JACOBI) { set_error("PCG uses LC_JACOBI"); return LC_ERR_INVALID_ARG; }
+  } else if (p->method == LC_GMRES) {
+    if (p->precond != LC_BLOCK_JACOBI && p->precond != LC_JACOBI) { set_error("GMRES: bad precond"); return LC_ERR_INVALID_ARG; }
+    if (p->restart < 1 || p->restart > 64) { set_error("GMRES: restart in [1, 64]"); return LC_ERR_INVALID_ARG; }
+  } else {
+    set_error("solver: method must be LC_PCG or LC_GMRES");
+    return LC_ERR_INVALID_ARG;
+  }
+  return LC_OK;
+}
+
+static lc_status run(const Sell& M, const double* b, double* x, const int32_t* scatter_idx, double* x_full,
+                     const double* x_init, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
+  if (p->method == LC_PCG) return run_pcg(M, b, x, scatter_idx, x_full, x_init, p, s, info);
+  return run_gmres(M, b, x, scatter_idx, x_full, x_init, p, s, info);
+}
+}  // namespace lc
+
+using namespace lc;
+
+extern "C" lc_status lc_solve_local(lc_sub S, const lc_solver_params* p, double* x, void* stream,
+                                    lc_solve_info* info) {
+  if (!S || !x) { set_error("lc_solve_local: null argument"); return LC_ERR_INVALID_ARG; }
+  lc_status st = check_params(p);
+  if (st) return st;
+  if (S->K_units == 0) {   // empty Omega: x~ = x0 (R12)
+    if (info)
+      for (int g = 0; g < S->nseg; ++g) info[g] = lc_solve_info{0, LC_OK, 0.0, 0.0};
+    return LC_OK;
+  }
+  return run(S->B, S->bsub, nullptr, S->idx, x, S->xB0, p, (cudaStream_t)stream, info);
+}
+
+extern "C" lc_status lc_solve_global(lc_matrix A, const double* b, double* x, const lc_solver_params* p, void* stream,
+                                     lc_solve_info* info) {
+  if (!A || !b || !x) { set_error("lc_solve_global: null argument"); return LC_ERR_INVALID_ARG; }
+  lc_status st = check_params(p);
+  if (st) return st;
+  return run(A->A, b, x, nullptr, nullptr, nullptr, p, (cudaStream_t)stream, info);
+}

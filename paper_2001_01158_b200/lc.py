@@ -1,0 +1,253 @@
+"""Thin ctypes binding of liblc.so (include/lc.h).  Argument marshalling only:
+every step of the path runs in the library's sm_100a kernels.  PyTorch supplies
+device memory and the current CUDA stream.
+
+There is NO CPU fallback: if liblc.so is missing or CUDA is unavailable, every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblc.so")
+
+LC_OK, LC_NOT_CONVERGED = 0, 1
+FMT_SELL32 = 0
+CRIT_RESIDUAL, CRIT_GRADIENT = 0, 1
+THR_PAPER, THR_REL_MAX, THR_PERCENTILE = 0, 1, 2
+PCG, GMRES = 0, 1
+JACOBI, BLOCK_JACOBI = 0, 1
+
+_STATUS = {0: "LC_OK", 1: "LC_NOT_CONVERGED", -1: "LC_ERR_INVALID_ARG", -2: "LC_ERR_DIMENSION",
+           -3: "LC_ERR_PATTERN", -4: "LC_ERR_ZERO_DIAGONAL", -5: "LC_ERR_BREAKDOWN", -6: "LC_ERR_NONFINITE",
+           -7: "LC_ERR_CUDA", -8: "LC_ERR_OOM"}
+
+EXPORTED = ["lc_create_csr", "lc_select_domain", "lc_domain_export", "lc_extract_sub", "lc_solve_local",
+            "lc_solve_global", "lc_matrix_info", "lc_destroy_matrix", "lc_destroy_domain", "lc_destroy_sub",
+            "lc_last_error", "lc_kernel_launches"]
+
+
+class LcError(RuntimeError):
+    def __init__(self, status, where, msg):
+        super().__init__(f"{where}: {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class DomainParams(ctypes.Structure):
+    _fields_ = [("criterion", ctypes.c_int32), ("threshold", ctypes.c_int32), ("param", ctypes.c_double),
+                ("expand_rounds", ctypes.c_int32), ("dilate_hops", ctypes.c_int32)]
+
+
+class SolverParams(ctypes.Structure):
+    _fields_ = [("method", ctypes.c_int32), ("precond", ctypes.c_int32), ("restart", ctypes.c_int32),
+                ("rel_tol", ctypes.c_double), ("max_iters", ctypes.c_int32)]
+
+
+class SolveInfo(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("status", ctypes.c_int32), ("rel_residual", ctypes.c_double),
+                ("seconds", ctypes.c_double)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load liblc.so and declare the C signatures (no device needed)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built (run __graft_entry__.build()); there is no CPU fallback")
+    lib = ctypes.CDLL(path)
+    P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+    lib.lc_create_csr.argtypes = [I64, I32, I32, P, P, P, I32, I32, P, ctypes.POINTER(P)]
+    lib.lc_select_domain.argtypes = [P, P, P, ctypes.POINTER(DomainParams), P, ctypes.POINTER(P), P]
+    lib.lc_domain_export.argtypes = [P, P, P, P, P, P]
+    lib.lc_extract_sub.argtypes = [P, P, P, P, P, ctypes.POINTER(P)]
+    lib.lc_solve_local.argtypes = [P, ctypes.POINTER(SolverParams), P, P, P]
+    lib.lc_solve_global.argtypes = [P, P, P, ctypes.POINTER(SolverParams), P, P]
+    lib.lc_matrix_info.argtypes = [P, P, P, P, P, P]
+    for f in ("lc_create_csr", "lc_select_domain", "lc_domain_export", "lc_extract_sub", "lc_solve_local",
+              "lc_solve_global", "lc_matrix_info"):
+        getattr(lib, f).restype = ctypes.c_int
+    for f in ("lc_destroy_matrix", "lc_destroy_domain", "lc_destroy_sub"):
+        getattr(lib, f).argtypes = [P]
+        getattr(lib, f).restype = None
+    lib.lc_last_error.restype = ctypes.c_char_p
+    lib.lc_kernel_launches.restype = ctypes.c_int64
+    _lib = lib
+    return lib
+
+
+def _check(st, where, ok=(LC_OK, LC_NOT_CONVERGED)):
+    if st not in ok:
+        raise LcError(st, where, _lib.lc_last_error().decode())
+    return st
+
+
+def _stream():
+    if not torch.cuda.is_available():
+        raise RuntimeError("CUDA device required: liblc has no CPU path")
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dptr(t: torch.Tensor, dtype, n=None):
+    if not t.is_cuda or t.dtype != dtype or not t.is_contiguous():
+        raise TypeError(f"expected a contiguous CUDA {dtype} tensor, got {t.dtype} on {t.device}")
+    if n is not None and t.numel() < n:
+        raise ValueError(f"tensor has {t.numel()} elements, need {n}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def kernel_launches() -> int:
+    return int(load_library().lc_kernel_launches())
+
+
+class Matrix:
+    """A (Eq. 1) in the library's SELL-32 layout.  row_ptr/col_idx/values may be host numpy arrays or CUDA
+    tensors (copied either way).  block = 3: BSR with 9 f64 per block; batch = G equal diagonal segments."""
+
+    def __init__(self, n, row_ptr, col_idx, values, block=1, batch=1):
+        lib = load_library()
+        s = _stream()
+        self.n_units, self.block, self.batch = int(n), int(block), int(batch)
+        h = ctypes.c_void_p()
+        if isinstance(row_ptr, torch.Tensor) and row_ptr.is_cuda:
+            st = lib.lc_create_csr(n, block, batch, _dptr(row_ptr, torch.int64), _dptr(col_idx, torch.int32),
+                                   _dptr(values, torch.float64), 1, FMT_SELL32, s, ctypes.byref(h))
+        else:
+            import numpy as np
+            rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+            ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+            va = np.ascontiguousarray(values, dtype=np.float64)
+            st = lib.lc_create_csr(n, block, batch, rp.ctypes.data, ci.ctypes.data, va.ctypes.data, 0, FMT_SELL32,
+                                   s, ctypes.byref(h))
+        _check(st, "lc_create_csr", ok=(LC_OK,))
+        self.h = h
+
+    @property
+    def N(self):
+        return self.n_units * self.block
+
+    def info(self):
+        vals = [ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32()]
+        _check(_lib.lc_matrix_info(self.h, *[ctypes.byref(v) for v in vals]), "lc_matrix_info")
+        return dict(N=vals[0].value, nnz=vals[1].value, batch=vals[2].value, nslices=vals[3].value,
+                    max_row=vals[4].value)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.lc_destroy_matrix(self.h)
+            self.h = None
+
+
+@dataclass
+class DomainResult:
+    dom: "Domain"
+    K: list
+
+
+class Domain:
+    def __init__(self, A: Matrix, h, K):
+        self.A, self.h, self.K = A, h, K
+
+    def export(self, want_crit=False, want_adm=False):
+        """-> (idx int32 CUDA tensor [sum K], tau list [batch], crit [n_units] or None, adm or None)"""
+        s = _stream()
+        dev = torch.device("cuda")
+        total = int(sum(self.K))
+        idx = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        tau = (ctypes.c_double * self.A.batch)()
+        crit = torch.empty(self.A.n_units, dtype=torch.float64, device=dev) if want_crit else None
+        adm = torch.empty(self.A.n_units, dtype=torch.float64, device=dev) if want_adm else None
+        _check(_lib.lc_domain_export(self.h, ctypes.c_void_p(idx.data_ptr()), tau,
+                                     ctypes.c_void_p(crit.data_ptr()) if crit is not None else None,
+                                     ctypes.c_void_p(adm.data_ptr()) if adm is not None else None, s),
+               "lc_domain_export")
+        return idx[:total], list(tau), crit, adm
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.lc_destroy_domain(self.h)
+            self.h = None
+
+
+def select_domain(A: Matrix, b: torch.Tensor, x0: torch.Tensor, criterion=CRIT_RESIDUAL, threshold=THR_PAPER,
+                  param=1e-10, expand_rounds=0, dilate_hops=0) -> Domain:
+    s = _stream()
+    p = DomainParams(criterion, threshold, param, expand_rounds, dilate_hops)
+    h = ctypes.c_void_p()
+    K = (ctypes.c_int64 * A.batch)()
+    _check(_lib.lc_select_domain(A.h, _dptr(b, torch.float64, A.N), _dptr(x0, torch.float64, A.N), ctypes.byref(p),
+                                 s, ctypes.byref(h), K), "lc_select_domain", ok=(LC_OK,))
+    return Domain(A, h, list(K))
+
+
+class Sub:
+    def __init__(self, A: Matrix, dom: Domain, b, x0):
+        s = _stream()
+        h = ctypes.c_void_p()
+        _check(_lib.lc_extract_sub(A.h, dom.h, _dptr(b, torch.float64, A.N), _dptr(x0, torch.float64, A.N), s,
+                                   ctypes.byref(h)), "lc_extract_sub", ok=(LC_OK,))
+        self.h, self.A, self.K = h, A, list(dom.K)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.lc_destroy_sub(self.h)
+            self.h = None
+
+
+def extract_sub(A: Matrix, dom: Domain, b, x0) -> Sub:
+    return Sub(A, dom, b, x0)
+
+
+def _solver(method, rel_tol, max_iters, restart):
+    if method == PCG:
+        return SolverParams(PCG, JACOBI, restart, rel_tol, max_iters)
+    return SolverParams(GMRES, BLOCK_JACOBI, restart, rel_tol, max_iters)
+
+
+def _infos(arr):
+    return [dict(iterations=i.iterations, status=i.status, rel_residual=i.rel_residual, seconds=i.seconds)
+            for i in arr]
+
+
+def solve_local(sub: Sub, x: torch.Tensor, method=PCG, rel_tol=1e-10, max_iters=20000, restart=30):
+    """Alg. 1 l.5-6: x (in = x0) becomes x~ (Omega entries replaced by the subsystem solution)."""
+    s = _stream()
+    p = _solver(method, rel_tol, max_iters, restart)
+    info = (SolveInfo * sub.A.batch)()
+    st = _lib.lc_solve_local(sub.h, ctypes.byref(p), _dptr(x, torch.float64, sub.A.N), s, info)
+    _check(st, "lc_solve_local")
+    return _infos(info)
+
+
+def solve_global(A: Matrix, b: torch.Tensor, x: torch.Tensor, method=PCG, rel_tol=1e-10, max_iters=20000,
+                 restart=30):
+    """Alg. 1 l.8-11 (or method0 when x = x0): in-place solve of A x = b from the warm start x."""
+    s = _stream()
+    p = _solver(method, rel_tol, max_iters, restart)
+    info = (SolveInfo * A.batch)()
+    st = _lib.lc_solve_global(A.h, _dptr(b, torch.float64, A.N), _dptr(x, torch.float64, A.N), ctypes.byref(p), s,
+                              info)
+    _check(st, "lc_solve_global")
+    return _infos(info)
+
+
+def local_method(A: Matrix, b, x0, domain: dict | None, method=PCG, rel_tol=1e-10, max_iters=20000, restart=30):
+    """Alg. 1 composed from the five C-ABI calls (domain=None: method0).  Returns (x, report dict)."""
+    x = x0.clone()
+    rep = {"K": [0] * A.batch}
+    if domain is not None:
+        dom = select_domain(A, b, x0, **domain)
+        rep["K"] = dom.K
+        if sum(dom.K) > 0:
+            sub = extract_sub(A, dom, b, x0)
+            rep["local"] = solve_local(sub, x, method, rel_tol, max_iters, restart)
+    rep["global"] = solve_global(A, b, x, method, rel_tol, max_iters, restart)
+    return x, rep

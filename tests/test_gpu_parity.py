@@ -1,0 +1,355 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same
+seeded inputs.  Bars (BASELINE.json north_star):
+  - local-domain index sets bit-exact, except units whose criterion / admission value
+    lies within 1e-12 relative of tau (counted, and cascades of those through growth);
+  - iteration counts within +-1 (local and global separately);
+  - final solutions within 1e-9 relative L2, stopping tolerance 1e-10.
+Sizes: reduced grids that still span many 32-row slices, ragged tails and (for
+config 3) ragged segments; the full BASELINE sizes are covered for the domain
+selection (index sets vs the oracle) and for Eq. 6 / the manufactured bound.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2001_01158_b200 import build as lcbuild
+    from paper_2001_01158_b200 import lc
+    lcbuild.build()
+
+DEV = "cuda"
+EPS = 1e-10
+
+# domain rules per config (readings R13-R16)
+RULES = {
+    1: [dict(criterion=0, threshold=1, param=1e-3, expand_rounds=0, dilate_hops=0)],
+    2: [dict(criterion=1, threshold=2, param=0.9, expand_rounds=0, dilate_hops=2)],
+    3: [dict(criterion=0, threshold=0, param=1e-10, expand_rounds=1, dilate_hops=0)],
+    4: [dict(criterion=0, threshold=0, param=1e-10, expand_rounds=1, dilate_hops=0)],
+    5: [dict(criterion=0, threshold=0, param=1e-10, expand_rounds=1, dilate_hops=0),
+        dict(criterion=1, threshold=1, param=1e-4, expand_rounds=0, dilate_hops=0)],
+}
+
+
+def method_of(cfg):
+    return lc.GMRES if cfg == 4 else lc.PCG
+
+
+def oracle_csr(sy):
+    if sy.block == 3:
+        return orc.Csr.from_bsr(sy.rp, sy.ci, sy.val)
+    return orc.Csr(sy.rp, sy.ci, sy.val)
+
+
+def segments(sy):
+    N = sy.N
+    G = sy.batch
+    return [(g * N // G, (g + 1) * N // G) for g in range(G)]
+
+
+def oracle_dp(rule, cell):
+    return orc.DomainParams(rule["criterion"], rule["threshold"], rule["param"], rule["expand_rounds"],
+                            rule["dilate_hops"], cell)
+
+
+def oracle_sp(cfg):
+    return orc.SolverParams(1 if cfg == 4 else 0, 3, 30, EPS, 3000 if cfg == 4 else 20000)
+
+
+def neighbours(A: orc.Csr, u, cell):
+    out = set()
+    for a in range(cell):
+        i = u * cell + a
+        for k in range(A.rp[i], A.rp[i + 1]):
+            v = A.ci[k] // cell
+            if v != u:
+                out.add(v)
+    return out
+
+
+def compare_sets(A, gpu_units, d: orc.Domain, cell, tol=1e-12):
+    """Index-set parity: returns (#near-threshold, #cascaded); asserts nothing else differs."""
+    ora = np.flatnonzero(d.flag.reshape(-1, cell)[:, 0])
+    gs, os_ = set(map(int, gpu_units)), set(map(int, ora))
+    diff = sorted(gs ^ os_)
+    near = set()
+    for u in diff:
+        c = d.crit[u]; a = d.adm[u]
+        if abs(c - d.tau) <= tol * abs(d.tau) or (np.isfinite(a) and abs(a - d.tau) <= tol * abs(d.tau)):
+            near.add(u)
+    cascade = set()
+    frontier = set(near)
+    for _ in range(8):
+        nxt = set()
+        for u in frontier:
+            for v in neighbours(A, u, cell):
+                if v in diff and v not in near and v not in cascade:
+                    cascade.add(v); nxt.add(v)
+        frontier = nxt
+    bad = [u for u in diff if u not in near and u not in cascade]
+    assert not bad, f"{len(bad)} index-set differences outside the 1e-12 window, e.g. {bad[:5]}"
+    return len(near), len(cascade)
+
+
+def gpu_matrix(sy):
+    return lc.Matrix(sy.nrows, sy.rp, sy.ci, sy.val, block=sy.block, batch=sy.batch)
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def check_system(sy, rule, check_solution=True):
+    cfg = sy.config
+    cell = sy.block
+    Ao = oracle_csr(sy)
+    A = gpu_matrix(sy)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    dom = lc.select_domain(A, b, x0, **rule)
+    idx, taus, crit, adm = dom.export(want_crit=True, want_adm=True)
+    idx = idx.cpu().numpy()
+    x_gpu, rep = lc.local_method(A, b, x0, rule, method=method_of(cfg))
+    x_gpu = x_gpu.cpu().numpy()
+    stats = []
+    off = 0
+    for g, (r0, r1) in enumerate(segments(sy)):
+        As = Ao.segment(r0, r1) if sy.batch > 1 else Ao
+        bs_, x0s = sy.b[r0:r1], sy.x0[r0:r1]
+        d = orc.select_domain(As, bs_, x0s, rule["criterion"], rule["threshold"], rule["param"],
+                              rule["expand_rounds"], rule["dilate_hops"], cell)
+        Kg = rep["K"][g]
+        gi = idx[off:off + Kg]
+        off += Kg
+        units = (gi[::cell] - r0) // cell
+        assert np.all(np.diff(gi) > 0), "GPU index set not ascending"
+        # tau agreement (same arithmetic up to the DD rounding, R23)
+        assert taus[g] == pytest.approx(d.tau, rel=1e-14, abs=0)
+        # criterion values agree (bit-exact by construction for |r|, g)
+        cg = crit.cpu().numpy()[(r0 // cell):(r1 // cell)]
+        np.testing.assert_array_equal(cg, d.crit)
+        near, casc = compare_sets(As, units, d, cell)
+        xo, _, ro = orc.local_method(As, bs_, x0s, oracle_dp(rule, cell), oracle_sp(cfg))
+        if Kg > 0 and d.K > 0:
+            assert abs(rep["local"][g]["iterations"] - ro.it_local) <= 1, (g, rep["local"][g], ro.it_local)
+        assert abs(rep["global"][g]["iterations"] - ro.it_global) <= 1, (g, rep["global"][g], ro.it_global)
+        xs = x_gpu[r0:r1]
+        if check_solution:
+            err = np.linalg.norm(xs - xo) / np.linalg.norm(xo)
+            assert err <= 1e-9, err
+            # Eq. 6 re-checked independently, and the manufactured bound (R31)
+            res = np.linalg.norm(orc.residual(As, bs_, xs))
+            assert res <= EPS * np.linalg.norm(bs_) * (1 + 1e-6)
+        stats.append((Kg, near, casc))
+    return stats
+
+
+# ------------------------------------------------------------ reduced sizes --
+
+@pytest.mark.parametrize("s", range(10))
+def test_config1_full_size_sequence(s):
+    """Config 1 at its BASELINE size (64x64), all 10 systems of the sequence."""
+    sy = synth.system(1, s)
+    check_system(sy, RULES[1][0])
+
+
+@pytest.mark.parametrize("n,s", [(96, 0), (100, 7), (128, 49)])
+def test_config2_reduced(n, s):
+    sy = synth.system(2, s, n=n)
+    check_system(sy, RULES[2][0])
+
+
+@pytest.mark.parametrize("n,G,s", [(30, 4, 0), (48, 5, 6), (32, 20, 19)])
+def test_config3_reduced_batched(n, G, s):
+    """Batched groups; n = 30 makes every segment a ragged 900-row block (not a multiple of 32)."""
+    sy = synth.system(3, s, n=n, G=G)
+    check_system(sy, RULES[3][0])
+
+
+@pytest.mark.parametrize("n,s", [(20, 0), (45, 4), (64, 29)])
+def test_config4_reduced_gmres(n, s):
+    sy = synth.system(4, s, n=n)
+    check_system(sy, RULES[4][0])
+
+
+@pytest.mark.parametrize("rule", [0, 1])
+@pytest.mark.parametrize("n,s", [(20, 3), (33, 10)])
+def test_config5_reduced(n, s, rule):
+    sy = synth.system(5, s, n=n)
+    check_system(sy, RULES[5][rule])
+
+
+# ------------------------------------------------------------- edge cases ---
+
+def test_example1_on_gpu_table1():
+    """Example 1 / Table 1 through the C-ABI: a single ragged 9-row slice, E_max = 6."""
+    n = 9
+    M = np.eye(n)
+    for i in range(n - 1):
+        M[i, i + 1] = M[i + 1, i] = -1.0 / (i + 2)
+    x = 10.0 ** -np.arange(1, 10)
+    x0 = np.array([1, 1e-1] + [1.001 * 10.0 ** -(k) for k in range(3, 10)])
+    b = M @ x
+    Ao = orc.Csr.from_dense(M)
+    A = lc.Matrix(n, Ao.rp, Ao.ci, Ao.val)
+    dom = lc.select_domain(A, to_dev(b), to_dev(x0), criterion=0, threshold=0, param=1e-5, expand_rounds=6)
+    idx, tau, crit, adm = dom.export(want_crit=True, want_adm=True)
+    assert list(idx.cpu().numpy() + 1) == [1, 2, 3, 4, 5, 6]
+    assert float(f"{tau[0]:.2e}") == 3.44e-7
+    a = adm.cpu().numpy()
+    for j, v in zip([4, 5, 6, 7], [2.504e-4, 2.003e-5, 1.669e-6, 1.430e-7]):
+        assert float(f"{a[j - 1]:.3e}") == v
+
+
+def test_empty_domain_and_exact_start():
+    """x0 = x*: r = 0 -> K = 0 in every segment; local solve is a no-op; global converges with 0 iterations."""
+    sy = synth.system(3, 2, n=24, G=3)
+    A = gpu_matrix(sy)
+    b, xs = to_dev(sy.b), to_dev(sy.xs)
+    x, rep = lc.local_method(A, b, xs, RULES[3][0])
+    assert rep["K"] == [0, 0, 0]
+    assert all(g["iterations"] == 0 for g in rep["global"])
+    assert torch.equal(x, xs)
+
+
+def test_full_domain_equals_method0_bitwise():
+    """Omega = Omega (theta = 0) => the local method returns method0's result bitwise, 0 global iterations."""
+    sy = synth.system(5, 5, n=16)
+    A = gpu_matrix(sy)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    x_full, rep = lc.local_method(A, b, x0, dict(criterion=0, threshold=1, param=0.0))
+    x_m0, rep0 = lc.local_method(A, b, x0, None)
+    assert rep["K"][0] == sy.N
+    assert rep["global"][0]["iterations"] == 0
+    assert torch.equal(x_full, x_m0)
+    assert rep["local"][0]["iterations"] == rep0["global"][0]["iterations"]
+
+
+def test_partially_empty_batch():
+    """One group starts exact (K_g = 0) while the others need work: masking per segment."""
+    sy = synth.system(3, 4, n=40, G=4)
+    x0 = sy.x0.copy()
+    Ng = 40 * 40
+    x0[Ng:2 * Ng] = sy.xs[Ng:2 * Ng]
+    A = gpu_matrix(sy)
+    x, rep = lc.local_method(A, to_dev(sy.b), to_dev(x0), RULES[3][0])
+    assert rep["K"][1] == 0 and min(rep["K"][0], rep["K"][2], rep["K"][3]) > 0
+    assert rep["global"][1]["iterations"] == 0
+    xn = x.cpu().numpy()
+    Ao = oracle_csr(sy)
+    for g in range(4):
+        As = Ao.segment(g * Ng, (g + 1) * Ng)
+        r = orc.residual(As, sy.b[g * Ng:(g + 1) * Ng], xn[g * Ng:(g + 1) * Ng])
+        assert np.linalg.norm(r) <= EPS * np.linalg.norm(sy.b[g * Ng:(g + 1) * Ng]) * (1 + 1e-6)
+
+
+def test_determinism_bitwise():
+    """Fixed-grid, fixed-order reductions: two runs give bitwise identical results."""
+    sy = synth.system(5, 7, n=24)
+    A = gpu_matrix(sy)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    x1, r1 = lc.local_method(A, b, x0, RULES[5][0])
+    x2, r2 = lc.local_method(A, b, x0, RULES[5][0])
+    assert torch.equal(x1, x2)
+    assert r1["K"] == r2["K"]
+    assert [i["iterations"] for i in r1["local"]] == [i["iterations"] for i in r2["local"]]
+    assert [i["iterations"] for i in r1["global"]] == [i["iterations"] for i in r2["global"]]
+
+
+def test_errors_zero_diagonal_and_pattern():
+    with pytest.raises(lc.LcError) as e:
+        lc.Matrix(2, [0, 1, 2], [0, 1], [1.0, 0.0])
+    assert e.value.status == -4
+    with pytest.raises(lc.LcError) as e:
+        lc.Matrix(2, [0, 2, 3], [1, 0, 1], [1.0, 1.0, 1.0])     # unsorted columns in row 0
+    assert e.value.status == -3
+    with pytest.raises(lc.LcError) as e:
+        lc.Matrix(2, [0, 1, 2], [1, 1], [1.0, 1.0])             # diagonal of row 0 not stored
+    assert e.value.status == -3
+
+
+def test_random_tiny_systems_vs_dense():
+    """Tiny random diagonally dominant systems (single ragged slice) vs dense LU."""
+    for seed in range(4):
+        s = synth.random_system(37, bw=3, spd=True, seed=seed + 50)
+        A = lc.Matrix(37, s.rp, s.ci, s.val)
+        x = to_dev(s.x0)
+        info = lc.solve_global(A, to_dev(s.b), x)
+        D = orc.Csr(s.rp, s.ci, s.val).to_dense()
+        xlu = np.linalg.solve(D, s.b)
+        assert info[0]["status"] == 0
+        assert np.linalg.norm(x.cpu().numpy() - xlu) / np.linalg.norm(xlu) <= 1e-8
+
+
+def test_gmres_scalar_jacobi():
+    """GMRES with block = 1 (Jacobi) on a nonsymmetric random system vs the oracle's GMRES."""
+    s = synth.random_system(200, bw=4, spd=False, seed=9)
+    A = lc.Matrix(200, s.rp, s.ci, s.val)
+    x = to_dev(s.x0)
+    info = lc.solve_global(A, to_dev(s.b), x, method=lc.GMRES)
+    xo, it, st, _ = orc.gmres_bj(orc.Csr(s.rp, s.ci, s.val), s.b, s.x0, bs=1)
+    assert info[0]["status"] == 0 and abs(info[0]["iterations"] - it) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xo) / np.linalg.norm(xo) <= 1e-9
+
+
+# --------------------------------------------------------------- full size ---
+
+FULL = [(1, 9), (2, 25), (3, 10), (4, 15), (5, 10)]
+
+
+@pytest.mark.parametrize("cfg,s", FULL)
+def test_full_size_domain_sets(cfg, s):
+    """BASELINE sizes: domain index sets vs the oracle (O(nnz) per rule), tau, criterion bit-exact."""
+    sy = synth.system(cfg, s)
+    cell = sy.block
+    Ao = oracle_csr(sy)
+    A = gpu_matrix(sy)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    for rule in RULES[cfg]:
+        dom = lc.select_domain(A, b, x0, **rule)
+        idx, taus, crit, adm = dom.export(want_crit=True, want_adm=True)
+        idx = idx.cpu().numpy(); crit = crit.cpu().numpy(); adm = adm.cpu().numpy()
+        off = 0
+        for g, (r0, r1) in enumerate(segments(sy)):
+            As = Ao.segment(r0, r1) if sy.batch > 1 else Ao
+            d = orc.select_domain(As, sy.b[r0:r1], sy.x0[r0:r1], rule["criterion"], rule["threshold"],
+                                  rule["param"], rule["expand_rounds"], rule["dilate_hops"], cell)
+            Kg = dom.K[g]
+            units = (idx[off:off + Kg][::cell] - r0) // cell
+            off += Kg
+            assert taus[g] == pytest.approx(d.tau, rel=1e-14, abs=0)
+            np.testing.assert_array_equal(crit[r0 // cell:r1 // cell], d.crit)
+            if Kg != d.K:
+                compare_sets(As, units, d, cell)
+            else:
+                if not np.array_equal(units, np.flatnonzero(d.flag.reshape(-1, cell)[:, 0])):
+                    compare_sets(As, units, d, cell)
+
+
+@pytest.mark.parametrize("cfg,s", FULL)
+def test_full_size_solution_properties(cfg, s):
+    """BASELINE sizes, in the bench's launch configuration: the local method's x satisfies Eq. 6
+    (re-checked by the oracle's residual) and the manufactured bound ||x - x*|| <= ||b - A x|| (R31)."""
+    sy = synth.system(cfg, s)
+    Ao = oracle_csr(sy)
+    A = gpu_matrix(sy)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    for rule in RULES[cfg]:
+        x, rep = lc.local_method(A, b, x0, rule, method=method_of(cfg))
+        xn = x.cpu().numpy()
+        for g, (r0, r1) in enumerate(segments(sy)):
+            As = Ao.segment(r0, r1) if sy.batch > 1 else Ao
+            r = orc.residual(As, sy.b[r0:r1], xn[r0:r1])
+            nr = np.linalg.norm(r)
+            assert nr <= EPS * np.linalg.norm(sy.b[r0:r1]) * (1 + 1e-6), (g, nr)
+            assert rep["global"][g]["status"] == 0
+            if cfg != 4:   # SPD with D >= I: ||A^-1||_2 <= 1
+                assert np.linalg.norm(xn[r0:r1] - sy.xs[r0:r1]) <= nr * (1 + 1e-6) + 1e-300
+            else:          # margin-1 row dominance: ||A^-1||_inf <= 1
+                assert np.max(np.abs(xn[r0:r1] - sy.xs[r0:r1])) <= np.max(np.abs(r)) * (1 + 1e-6) + 1e-300
