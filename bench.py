@@ -70,6 +70,17 @@ def systems_for_rank(rank, count, nsys):
     return [(rank * 7 + i) % nsys for i in range(count)]
 
 
+def aggregate(ms, solves, world, dist=None, device=None):
+    """Whole-job throughput: max elapsed over ranks, sum of solves over ranks -> (ms_max, solves/s)."""
+    import torch
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    n = torch.tensor([float(solves)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(n, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(n.item()) / (float(t.item()) * 1e-3)
+
+
 # ----------------------------------------------------------------- clocks ---
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -198,13 +209,7 @@ def run_lc(args):
         torch.cuda.synchronize()
     launches = lc.kernel_launches() - l0
     ms = ev0.elapsed_time(ev1)
-    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
-    tot = torch.tensor([float(solves)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-    ms_max = float(t_max.item())
-    value = float(tot.item()) / (ms_max * 1e-3)
+    ms_max, value = aggregate(ms, solves, world, dist, dev)
 
     # ---- per-method breakdown and roofline of the dominant kernel (global PCG launches on A)
     by = {}
@@ -264,12 +269,8 @@ def run_lc(args):
                 xh.copy_(xo, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
-        ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        esol = torch.tensor([float(sol)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-            dist.all_reduce(esol, op=dist.ReduceOp.SUM)
-        e2e = {"value": round(float(esol.item()) / (float(ems.item()) * 1e-3), 4), "unit": "solves/s",
+        _, evalue = aggregate(e0.elapsed_time(e1), sol, world, dist, dev)
+        e2e = {"value": round(evalue, 4), "unit": "solves/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
     cpu = None

@@ -102,28 +102,50 @@ __global__ void __launch_bounds__(kTB) k_gradient(SellView A, const double* __re
 }
 
 // ---------------------------------------------------------------- a3 -------
-// one CTA per segment: fixed-order reduction of the slice partials -> tau_cmp[g], tau_rep[g]
-__global__ void k_tau(SellView A, int mode, double param, const double* __restrict__ p_max,
-                      const double* __restrict__ p_hi, const double* __restrict__ p_lo, double* tau_cmp,
-                      double* tau_rep) {
-  int g = blockIdx.x;
+// fixed-order two-level reduction of the slice partials -> tau_cmp[g], tau_rep[g]
+constexpr int kTauParts = 64;
+__global__ void __launch_bounds__(256) k_tau_part(SellView A, int mode, const double* __restrict__ p_max,
+                                                  const double* __restrict__ p_hi, const double* __restrict__ p_lo,
+                                                  double* __restrict__ q) {
+  int g = blockIdx.x / kTauParts, j = blockIdx.x % kTauParts;
   int64_t s0 = A.seg_slice0[g], s1 = A.seg_slice0[g + 1];
+  int64_t len = s1 - s0;
+  int64_t a = s0 + len * j / kTauParts, b = s0 + len * (j + 1) / kTauParts;
   double mx = 0.0, hi = 0.0, lo = 0.0;
-  for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
+#pragma unroll 4
+  for (int64_t s = a + threadIdx.x; s < b; s += blockDim.x) {
     mx = fmax(mx, p_max[s]);
     if (mode == LC_THR_PAPER) dd_add(hi, lo, p_hi[s], p_lo[s]);
   }
-  __shared__ double sm[32], sh[32], sl[32];
+  __shared__ double sm[8], sh[8], sl[8];
   mx = warp_max(mx);
   warp_dd_sum(hi, lo);
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (lane == 0) { sm[w] = mx; sh[w] = hi; sl[w] = lo; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int nw = blockDim.x >> 5;
-    for (int i = 1; i < nw; ++i) { mx = fmax(mx, sm[i]); }
+    for (int i = 1; i < 8; ++i) { mx = fmax(mx, sm[i]); }
     hi = sh[0]; lo = sl[0];
-    for (int i = 1; i < nw; ++i) dd_add(hi, lo, sh[i], sl[i]);
+    for (int i = 1; i < 8; ++i) dd_add(hi, lo, sh[i], sl[i]);
+    q[3 * blockIdx.x] = mx; q[3 * blockIdx.x + 1] = hi; q[3 * blockIdx.x + 2] = lo;
+  }
+}
+
+__global__ void k_tau(SellView A, int mode, double param, const double* __restrict__ q, double* tau_cmp,
+                      double* tau_rep) {
+  int g = blockIdx.x;
+  int lane = threadIdx.x;   // blockDim = 64 = kTauParts
+  const double* qq = q + 3 * (g * kTauParts + lane);
+  double mx = qq[0], hi = qq[1], lo = qq[2];
+  __shared__ double sm[2], sh[2], sl[2];
+  mx = warp_max(mx);
+  warp_dd_sum(hi, lo);
+  if ((lane & 31) == 0) { sm[lane >> 5] = mx; sh[lane >> 5] = hi; sl[lane >> 5] = lo; }
+  __syncthreads();
+  if (lane == 0) {
+    mx = fmax(sm[0], sm[1]);
+    hi = sh[0]; lo = sl[0];
+    dd_add(hi, lo, sh[1], sl[1]);
     double t, tc;
     if (mode == LC_THR_PAPER) {
       int64_t N = (int64_t)(A.seg_unit0[g + 1] - A.seg_unit0[g]) * A.block;   // scalar unknowns
@@ -353,7 +375,7 @@ extern "C" lc_status lc_select_domain(lc_matrix M, const double* b, const double
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
   size_t o_pmax = carve(8 * ns), o_phi = carve(8 * ns), o_plo = carve(8 * ns), o_tc = carve(8 * G),
          o_tr = carve(8 * G), o_cnt = carve(4 * 256), o_K = carve(8), o_rst = carve(sizeof(RadixState) * G),
-         o_hist = carve(4 * 256 * G);
+         o_hist = carve(4 * 256 * G), o_tq = carve(8 * 3 * kTauParts * G);
   std::vector<int32_t> h_base(G + 1);
   const unsigned nb_sl = (unsigned)((ns * 32 + kTB - 1) / kTB);
   const unsigned nb_u = (unsigned)((m + 255) / 256);
@@ -397,7 +419,10 @@ extern "C" lc_status lc_select_domain(lc_matrix M, const double* b, const double
       CKL();
     }
   } else {
-    k_tau<<<G, 256, 0, s>>>(V, p->threshold, p->param, p_max, p_hi, p_lo, tau_cmp, tau_rep);
+    double* tq = (double*)((char*)ws + o_tq);
+    k_tau_part<<<G * kTauParts, 256, 0, s>>>(V, p->threshold, p_max, p_hi, p_lo, tq);
+    CKL();
+    k_tau<<<G, kTauParts, 0, s>>>(V, p->threshold, p->param, tq, tau_cmp, tau_rep);
     CKL();
   }
   k_mark<<<nb_u, 256, 0, s>>>(D->crit, m, M->seg_units, tau_cmp, D->flag);

@@ -49,6 +49,7 @@ struct PcgArgs {
   double eps;
   int max_iters;
   int interleave;       // 1: slices strided over all warps of the grid (single segment)
+  int vec2;             // 1: single segment and 16-byte aligned vectors -> flat double2 update pass
   int64_t chunk;        // contiguous slices per CTA (interleave == 0)
 };
 
@@ -63,6 +64,34 @@ __device__ __forceinline__ void flush(double (*acc)[kMaxSeg][2], int warp, int g
   if ((threadIdx.x & 31) == 0) { acc[warp][gi][0] += a0; acc[warp][gi][1] += a1; }
 }
 
+// One SELL row (lane of slice) dotted with an operand y(c) given by `ld`.  WM > 0: the slice width is
+// at most WM, the loop is fully unrolled so all column/value loads issue before the dependent gathers
+// (memory-level parallelism); slots k >= w are predicated off.  WM == 0: generic loop.
+template <int WM, class Ld>
+__device__ __forceinline__ double sell_row(const int32_t* __restrict__ cp, const double* __restrict__ vp, int w,
+                                           Ld ld) {
+  double acc = 0.0;
+  if (WM > 0) {
+    constexpr int WA = WM > 0 ? WM : 1;
+    int c[WA];
+    double v[WA], y[WA];
+#pragma unroll
+    for (int k = 0; k < WM; ++k) {
+      c[k] = (k < w) ? __ldg(cp + 32 * k) : 0;
+      v[k] = (k < w) ? __ldg(vp + 32 * k) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < WM; ++k) y[k] = (k < w) ? ld(c[k]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < WM; ++k)
+      if (k < w) acc = __fma_rn(v[k], y[k], acc);
+  } else {
+    for (int k = 0; k < w; ++k) acc = __fma_rn(__ldg(vp + 32 * k), ld(__ldg(cp + 32 * k)), acc);
+  }
+  return acc;
+}
+
+template <int WM>
 __global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ SegState S[kMaxSeg];
@@ -159,10 +188,9 @@ __global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
         int w = (int)((A.slice_ptr[s + 1] - p0) >> 5);
         const int32_t* cp = A.col + p0 + lane;
         const double* vp = A.val + p0 + lane;
-        double acc = 0.0;
         if (mode == M_INIT || mode == M_CONFIRM) {
           const double* xx = P.x;
-          for (int k = 0; k < w; ++k) acc = __fma_rn(vp[32 * k], xx[cp[32 * k]], acc);
+          double acc = sell_row<WM>(cp, vp, w, [&](int c) { return xx[c]; });
           double bi = P.b[u];
           double ri = bi - acc;
           P.r[u] = ri;
@@ -170,17 +198,14 @@ __global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
           if (mode == M_INIT) a1 = __fma_rn(bi, bi, a1);
         } else if (mode == M_FIRST) {
           const double* zz = P.z;
-          for (int k = 0; k < w; ++k) acc = __fma_rn(vp[32 * k], zz[cp[32 * k]], acc);
+          double acc = sell_row<WM>(cp, vp, w, [&](int c) { return zz[c]; });
           double pi = zz[u];
           pnew[u] = pi;
           P.q[u] = acc;
           a0 = __fma_rn(pi, acc, a0);
         } else {  // M_NORMAL: p = z + beta p_old on the fly
           const double* zz = P.z;
-          for (int k = 0; k < w; ++k) {
-            int c = cp[32 * k];
-            acc = __fma_rn(vp[32 * k], __fma_rn(beta, pold[c], zz[c]), acc);
-          }
+          double acc = sell_row<WM>(cp, vp, w, [&](int c) { return __fma_rn(beta, pold[c], zz[c]); });
           double pi = __fma_rn(beta, pold[u], zz[u]);
           pnew[u] = pi;
           P.q[u] = acc;
@@ -220,7 +245,58 @@ __global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
     }
     // ------------------------------------------------------------ pass B ----
     clear_acc();
-    {
+    if (P.vec2) {
+      // single segment: flat grid-stride over row pairs with 16-byte loads/stores
+      const int mode = S[0].mode;
+      double a0 = 0.0, a1 = 0.0;
+      if (mode == M_UPDATE || mode == M_RESET) {
+        const double alpha = S[0].alpha;
+        const double2* pp = reinterpret_cast<const double2*>(S[0].par ? P.p1 : P.p0);
+        double2* x2 = reinterpret_cast<double2*>(P.x);
+        double2* r2 = reinterpret_cast<double2*>(P.r);
+        double2* z2 = reinterpret_cast<double2*>(P.z);
+        const double2* q2 = reinterpret_cast<const double2*>(P.q);
+        const double2* d2 = reinterpret_cast<const double2*>(A.dinv);
+        const int64_t n = A.seg_unit0[1], npair = n >> 1;
+        const int64_t gt = bid * kPT + threadIdx.x, gs = nCTA * kPT;
+        if (mode == M_UPDATE) {
+#pragma unroll 2
+          for (int64_t i = gt; i < npair; i += gs) {
+            double2 xv = x2[i], pv = pp[i], rv = r2[i], qv = q2[i], dv = d2[i];
+            xv.x = __fma_rn(alpha, pv.x, xv.x); xv.y = __fma_rn(alpha, pv.y, xv.y);
+            rv.x = __fma_rn(-alpha, qv.x, rv.x); rv.y = __fma_rn(-alpha, qv.y, rv.y);
+            double2 zv = make_double2(rv.x * dv.x, rv.y * dv.y);
+            x2[i] = xv; r2[i] = rv; z2[i] = zv;
+            a0 = __fma_rn(rv.x, zv.x, a0); a0 = __fma_rn(rv.y, zv.y, a0);
+            a1 = __fma_rn(rv.x, rv.x, a1); a1 = __fma_rn(rv.y, rv.y, a1);
+          }
+          if ((n & 1) && gt == 0) {
+            const double* p1 = S[0].par ? P.p1 : P.p0;
+            int64_t u = n - 1;
+            double xi = __fma_rn(alpha, p1[u], P.x[u]);
+            double ri = __fma_rn(-alpha, P.q[u], P.r[u]);
+            double zi = ri * A.dinv[u];
+            P.x[u] = xi; P.r[u] = ri; P.z[u] = zi;
+            a0 = __fma_rn(ri, zi, a0); a1 = __fma_rn(ri, ri, a1);
+          }
+        } else {
+#pragma unroll 2
+          for (int64_t i = gt; i < npair; i += gs) {
+            double2 rv = r2[i], dv = d2[i];
+            double2 zv = make_double2(rv.x * dv.x, rv.y * dv.y);
+            z2[i] = zv;
+            a0 = __fma_rn(rv.x, zv.x, a0); a0 = __fma_rn(rv.y, zv.y, a0);
+          }
+          if ((n & 1) && gt == 0) {
+            int64_t u = n - 1;
+            double zi = P.r[u] * A.dinv[u];
+            P.z[u] = zi;
+            a0 = __fma_rn(P.r[u], zi, a0);
+          }
+        }
+      }
+      flush(s_acc, warp, 0, a0, a1);
+    } else {
       int gcur = -1, mode = M_DONE;
       double a0 = 0.0, a1 = 0.0, alpha = 0.0;
       const double* pp = nullptr;
@@ -281,6 +357,7 @@ __global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
       }
       __syncthreads();
     }
+    __syncthreads();
     if (s_exit) break;
   }
   // a8: x~[Omega] = xbar_B (Eq. 4), fused into the local solve's exit
@@ -294,7 +371,7 @@ __global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
 }
 
 // ---------------------------------------------------------------- host ----
-static int g_pcg_max_ctas = 0;
+static int g_pcg_max_ctas[3] = {0, 0, 0};
 
 lc_status run_pcg(const Sell& M, const double* b, double* x, const int32_t* scatter_idx, double* x_full,
                   const double* x_init, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
@@ -307,14 +384,16 @@ lc_status run_pcg(const Sell& M, const double* b, double* x, const int32_t* scat
   for (int g = 0; g < G; ++g) if (M.h_seg_slice0[g + 1] > M.h_seg_slice0[g]) ++n_active;
   float ms = 0.f;
   if (n_active > 0) {
-    if (!g_pcg_max_ctas) {
+    const int wi = M.maxw <= 5 ? 0 : M.maxw <= 7 ? 1 : 2;
+    void* fn = wi == 0 ? (void*)k_pcg<5> : wi == 1 ? (void*)k_pcg<7> : (void*)k_pcg<0>;
+    if (!g_pcg_max_ctas[wi]) {
       int per_sm = 0;
-      LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg, kPT, 0));
+      LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPT, 0));
       if (per_sm < 1) { set_error("PCG kernel does not fit on an SM"); return LC_ERR_CUDA; }
-      g_pcg_max_ctas = per_sm * num_sms();
+      g_pcg_max_ctas[wi] = per_sm * num_sms();
     }
     const int64_t n = M.nunits;
-    int64_t nCTA = std::min<int64_t>(g_pcg_max_ctas, (M.nslices + kPW - 1) / kPW);
+    int64_t nCTA = std::min<int64_t>(g_pcg_max_ctas[wi], (M.nslices + kPW - 1) / kPW);
     if (nCTA < 1) nCTA = 1;
     int interleave = (G == 1) ? 1 : 0;
     int64_t chunk = (M.nslices + nCTA - 1) / nCTA;
@@ -351,6 +430,8 @@ lc_status run_pcg(const Sell& M, const double* b, double* x, const int32_t* scat
     a.eps = p->rel_tol;
     a.max_iters = p->max_iters;
     a.interleave = interleave;
+    a.vec2 = (interleave && ((((uintptr_t)a.x) | ((uintptr_t)a.r) | ((uintptr_t)a.z) | ((uintptr_t)a.q) |
+                              ((uintptr_t)a.p0) | ((uintptr_t)a.p1) | ((uintptr_t)M.dinv)) & 15) == 0) ? 1 : 0;
     a.chunk = chunk;
     cudaError_t e = cudaMemcpyAsync(a.n_active, &n_active, sizeof(int), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(a.out_iters, 0, 8 * G, s);
@@ -359,7 +440,7 @@ lc_status run_pcg(const Sell& M, const double* b, double* x, const int32_t* scat
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
     void* args[] = {&a};
-    if (e == cudaSuccess) e = cudaLaunchCooperativeKernel((void*)k_pcg, dim3((unsigned)nCTA), dim3(kPT), args, 0, s);
+    if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kPT), args, 0, s);
     count_launch();
     cudaEventRecord(e1, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(it.data(), a.out_iters, 4 * G, cudaMemcpyDeviceToHost, s);
