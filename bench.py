@@ -212,6 +212,10 @@ def run_lc(args):
     ms_max, value = aggregate(ms, solves, world, dist, dev)
 
     # ---- per-method breakdown and roofline of the dominant kernel (global PCG launches on A)
+    Ainfo = lc.Matrix(sy0.nrows, dev_in[0]["rp"], dev_in[0]["ci"], dev_in[0]["val"], block=sy0.block,
+                      batch=sy0.batch).info()
+    per_nnz = 8.0 if Ainfo["layout"] == "stencil" else 12.0
+    it_bytes = per_nnz * nnz + 96.0 * N      # matrix once + pass A 32 B/row + pass B 64 B/row
     by = {}
     pcg_bytes = 0.0
     pcg_sec = 0.0
@@ -224,7 +228,7 @@ def run_lc(args):
         for inf in rep["global"]:
             d["it_global"] += inf["iterations"]; d["t_global"] += inf["seconds"]
             if solver == "pcg":
-                pcg_bytes += inf["iterations"] * (12.0 * nnz + 96.0 * N) / sy0.batch
+                pcg_bytes += inf["iterations"] * it_bytes / sy0.batch
         if solver == "pcg":
             pcg_sec += max(inf["seconds"] for inf in rep["global"])
     breakdown = {k: dict(eta=round(v["K"] / (v["n"] * N), 5), it_local=v["it_local"] / v["n"],
@@ -242,7 +246,8 @@ def run_lc(args):
         roof = {"kernel": "k_pcg (global Jacobi-PCG, one cooperative launch per solve)", "bound": "hbm",
                 "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
                 "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
-                "bytes_per_iteration": 12 * nnz + 96 * N}
+                "layout": Ainfo["layout"], "bytes_per_iteration": int(it_bytes),
+                "bytes_rule": f"{int(per_nnz)} B/nnz matrix + 96 B/row vectors per PCG iteration"}
 
     # ---- e2e: host buffers through the C-ABI, H2D + D2H inside the timed region
     e2e = None

@@ -157,9 +157,14 @@ lc_status lc_solve_local(lc_sub sub, const lc_solver_params* p, double* x, void*
 lc_status lc_solve_global(lc_matrix A, const double* b, double* x, const lc_solver_params* p, void* stream,
                           lc_solve_info* info);
 
-/* introspection (host ints): rows n*block, stored scalars, batch, SELL slices, max row length */
+/* storage layout chosen by lc_create_csr */
+enum { LC_LAYOUT_SELL = 0     /* SELL-32 with explicit int32 column per slot (12 B per slot) */,
+       LC_LAYOUT_STENCIL = 1  /* every row's column offsets lie in one sorted set of <= 8 offsets: values only,
+                                 slot k = column row + off[k] (zero "holes" where a row lacks it), 8 B per slot */ };
+/* introspection (host outputs, each optional): unknowns n*block, stored scalars, batch, SELL slices, max row
+   length (slots), layout (LC_LAYOUT_*), bytes one SpMV streams for the matrix (values + columns + metadata) */
 lc_status lc_matrix_info(lc_matrix A, int64_t* n_unknowns, int64_t* nnz, int32_t* batch, int64_t* nslices,
-                         int32_t* max_row);
+                         int32_t* max_row, int32_t* layout, int64_t* matrix_bytes);
 
 void lc_destroy_matrix(lc_matrix A);
 void lc_destroy_domain(lc_domain dom);

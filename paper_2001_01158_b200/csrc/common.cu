@@ -53,7 +53,8 @@ int num_sms() {
 
 void Sell::release(cudaStream_t s) {
   dfree(slice_ptr, s); dfree(slice_row0, s); dfree(slice_seg, s); dfree(seg_unit0, s); dfree(seg_slice0, s);
-  dfree(col, s); dfree(val, s); dfree(rowlen, s); dfree(dinv, s);
+  dfree(col, s); dfree(val, s); dfree(rowlen, s); dfree(dinv, s); dfree(mask, s);
+  mask = nullptr;
   slice_ptr = nullptr; slice_row0 = slice_seg = seg_unit0 = nullptr; seg_slice0 = nullptr;
   col = nullptr; val = nullptr; rowlen = nullptr; dinv = nullptr;
 }
@@ -275,7 +276,8 @@ void lc_domain_s::release(cudaStream_t s) {
 void lc_sub_s::release(cudaStream_t s) {
   B.release(s);
   lc::dfree(idx, s); lc::dfree(bsub, s); lc::dfree(xB0, s);
-  idx = nullptr; bsub = xB0 = nullptr;
+  lc::dfree(bs, s); lc::dfree(xm0, s); lc::dfree(omega, s); lc::dfree(slist, s); lc::dfree(nlist, s);
+  idx = nullptr; bsub = xB0 = nullptr; bs = xm0 = nullptr; omega = nullptr; slist = nullptr; nlist = nullptr;
 }
 
 extern "C" const char* lc_last_error(void) { return lc::g_err.c_str(); }

@@ -38,9 +38,8 @@ __global__ void __launch_bounds__(kTB) k_residual_crit(SellView A, const double*
   double cmax = 0.0, hi = 0.0, lo = 0.0;
   if (BS == 1) {
     double acc = 0.0;
-    const int32_t* cp = A.col + p0 + lane;
     const double* vp = A.val + p0 + lane;
-    for (int k = 0; k < w; ++k) acc = __fma_rn(vp[32 * k], __ldg(x + cp[32 * k]), acc);
+    for (int k = 0; k < w; ++k) acc = __fma_rn(vp[32 * k], __ldg(x + sv_col(A, p0 + lane, k, u)), acc);
     if (valid) {
       double bi = b[u];
       double ri = bi - acc;
@@ -52,9 +51,9 @@ __global__ void __launch_bounds__(kTB) k_residual_crit(SellView A, const double*
   } else {
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
     for (int k = 0; k < w; ++k) {
-      int c = A.col[p0 + 32 * k + lane];
+      int64_t c = sv_col(A, p0 + lane, k, u);
       const double* vb = A.val + 9 * (p0 + 32ll * k) + lane;
-      double y0 = __ldg(x + 3ll * c), y1 = __ldg(x + 3ll * c + 1), y2 = __ldg(x + 3ll * c + 2);
+      double y0 = __ldg(x + 3 * c), y1 = __ldg(x + 3 * c + 1), y2 = __ldg(x + 3 * c + 2);
       acc0 = __fma_rn(vb[0], y0, acc0); acc0 = __fma_rn(vb[32], y1, acc0); acc0 = __fma_rn(vb[64], y2, acc0);
       acc1 = __fma_rn(vb[96], y0, acc1); acc1 = __fma_rn(vb[128], y1, acc1); acc1 = __fma_rn(vb[160], y2, acc1);
       acc2 = __fma_rn(vb[192], y0, acc2); acc2 = __fma_rn(vb[224], y1, acc2); acc2 = __fma_rn(vb[256], y2, acc2);
@@ -89,10 +88,10 @@ __global__ void __launch_bounds__(kTB) k_gradient(SellView A, const double* __re
   double gmax = 0.0;
   if (valid) {
     double xi = x[u], acc = 0.0;
-    const int32_t* cp = A.col + p0 + lane;
     for (int k = 0; k < w; ++k) {
-      int c = cp[32 * k];
-      if (c != u) acc = acc + fabs(xi - __ldg(x + c));   // padding slots carry c == u
+      if (!sv_real(A, k, u)) continue;                    // padding / stencil holes
+      int64_t c = sv_col(A, p0 + lane, k, u);
+      if (c != u) acc = acc + fabs(xi - __ldg(x + c));
     }
     crit[u] = acc;
     gmax = acc;
@@ -252,24 +251,26 @@ __global__ void __launch_bounds__(kTB) k_expand(SellView A, const double* __rest
   if (u >= A.seg_unit0[g + 1]) return;
   if (flag[u] < stage) return;
   int64_t p0 = A.slice_ptr[s];
-  int len = A.rowlen[u];
+  int len = sv_len(A, u);
   bool nb = false;
   double best;
   if (BS == 1) {
     double sum = 0.0;
     for (int k = 0; k < len; ++k) {
-      int c = A.col[p0 + 32 * k + lane];
+      if (!sv_real(A, k, u)) continue;
+      int64_t c = sv_col(A, p0 + lane, k, u);
       if (flag[c] < stage) { nb = true; sum = sum + fabs(A.val[p0 + 32 * k + lane] * x0[c]); }
     }
     best = fabs(r[u]) + sum;
   } else {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
     for (int k = 0; k < len; ++k) {
-      int c = A.col[p0 + 32 * k + lane];
+      if (!sv_real(A, k, u)) continue;
+      int64_t c = sv_col(A, p0 + lane, k, u);
       if (flag[c] < stage) {
         nb = true;
         const double* vb = A.val + 9 * (p0 + 32ll * k) + lane;
-        double y0 = x0[3ll * c], y1 = x0[3ll * c + 1], y2 = x0[3ll * c + 2];
+        double y0 = x0[3 * c], y1 = x0[3 * c + 1], y2 = x0[3 * c + 2];
         s0 = s0 + fabs(vb[0] * y0); s0 = s0 + fabs(vb[32] * y1); s0 = s0 + fabs(vb[64] * y2);
         s1 = s1 + fabs(vb[96] * y0); s1 = s1 + fabs(vb[128] * y1); s1 = s1 + fabs(vb[160] * y2);
         s2 = s2 + fabs(vb[192] * y0); s2 = s2 + fabs(vb[224] * y1); s2 = s2 + fabs(vb[256] * y2);
@@ -298,9 +299,10 @@ __global__ void __launch_bounds__(kTB) k_dilate(SellView A, uint8_t* __restrict_
   if (u >= A.seg_unit0[g + 1]) return;
   if (flag[u] < stage) return;
   int64_t p0 = A.slice_ptr[s];
-  int len = A.rowlen[u];
+  int len = sv_len(A, u);
   for (int k = 0; k < len; ++k) {
-    int c = A.col[p0 + 32 * k + lane];
+    if (!sv_real(A, k, u)) continue;
+    int64_t c = sv_col(A, p0 + lane, k, u);
     if (c != u && flag[c] < stage) { flag[u] = (uint8_t)stage; return; }
   }
 }

@@ -37,13 +37,14 @@ __global__ void __launch_bounds__(kTB) k_extract(SellView A, SellView B, int W, 
     int64_t sA = A.seg_slice0[g] + (lu >> 5);
     int laneA = (int)(lu & 31);
     int64_t pA = A.slice_ptr[sA];
-    int len = A.rowlen[i];
+    int len = sv_len(A, i);
     double acc[BS];
 #pragma unroll
     for (int a = 0; a < BS; ++a) acc[a] = 0.0;
     for (int k = 0; k < len; ++k) {
+      if (!sv_real(A, k, i)) continue;                 // padding / stencil holes
       int64_t slotA = pA + 32ll * k + laneA;
-      int c = A.col[slotA];
+      int64_t c = sv_col(A, pA + laneA, k, i);
       int ic = inv[c];
       if (ic >= 0) {                                   // B block: column in local numbering
         int64_t slotB = pB + 32ll * kb + lane;
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(kTB) k_extract(SellView A, SellView B, int W, 
           for (int a = 0; a < 3; ++a)
 #pragma unroll
             for (int be = 0; be < 3; ++be)
-              acc[a] = __fma_rn(A.val[9 * (pA + 32ll * k) + 32 * (3 * a + be) + laneA], x0[3ll * c + be], acc[a]);
+              acc[a] = __fma_rn(A.val[9 * (pA + 32ll * k) + 32 * (3 * a + be) + laneA], x0[3 * c + be], acc[a]);
         }
       }
     }
@@ -88,6 +89,32 @@ __global__ void __launch_bounds__(kTB) k_extract(SellView A, SellView B, int W, 
       for (int q = 0; q < 9; ++q) Bval[9 * (pB + 32ll * k) + 32 * q + lane] = 0.0;
     }
   }
+}
+
+// Masked representation (stencil-layout A, block 1): per Omega row i (global numbering)
+//   bs[i]  = b_i - (fma chain over stored columns outside Omega, ascending)   (Eq. 3)
+//   xm0[i] = x0_i,  and the slice of i is marked active.
+__global__ void __launch_bounds__(kTB) k_bsub_masked(SellView A, int seg_units, int spg,
+                                                     const int32_t* __restrict__ idx, int64_t K,
+                                                     const int32_t* __restrict__ inv, const double* __restrict__ b,
+                                                     const double* __restrict__ x0, double* __restrict__ bs,
+                                                     double* __restrict__ xm0, uint8_t* __restrict__ sflag) {
+  int64_t l = blockIdx.x * (int64_t)kTB + threadIdx.x;
+  if (l >= K) return;
+  int64_t i = idx[l];
+  int64_t g = i / seg_units, lu = i - g * seg_units;
+  int64_t s = g * spg + (lu >> 5);
+  int laneA = (int)(lu & 31);
+  int64_t pA = 32ll * A.W * s;
+  double acc = 0.0;
+  for (int k = 0; k < A.W; ++k) {
+    if (!sv_real(A, k, i)) continue;
+    int64_t c = sv_col(A, pA + laneA, k, i);
+    if (inv[c] < 0) acc = __fma_rn(A.val[pA + 32ll * k + laneA], x0[c], acc);
+  }
+  bs[i] = b[i] - acc;
+  xm0[i] = x0[i];
+  sflag[s] = 0;
 }
 
 }  // namespace lc
@@ -121,8 +148,39 @@ extern "C" lc_status lc_extract_sub(lc_matrix M, lc_domain D, const double* b, c
   if (S->K_units == 0) { *out = S; return LC_OK; }
   lc_status st = LC_OK;
   const int64_t K = S->K_units;
+  const int64_t n = M->n;
 #define CK(x) do { st = (x); if (st) goto fail; } while (0)
 #define CKC(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { st = cuda_fail(_e, #x); goto fail; } } while (0)
+  if (M->A.stencil && bs == 1) {
+    // ---- masked representation: B = A[Omega, Omega] applied implicitly on A's stencil layout
+    S->masked = 1;
+    S->A = M;
+    const int64_t nsA = M->A.nslices;
+    const int spg = (M->seg_units + 31) / 32;
+    void* t = nullptr;
+    CK(dalloc((void**)&S->bs, sizeof(double) * n, s));
+    CK(dalloc((void**)&S->xm0, sizeof(double) * n, s));
+    CK(dalloc((void**)&S->omega, n, s));
+    CK(dalloc((void**)&S->slist, sizeof(int32_t) * nsA, s));
+    CK(dalloc((void**)&S->nlist, sizeof(int64_t), s));
+    CK(dalloc(&t, (sizeof(int32_t) + 1) * nsA + 16, s));
+    CKC(cudaMemsetAsync(S->bs, 0, sizeof(double) * n, s));
+    CKC(cudaMemsetAsync(S->xm0, 0, sizeof(double) * n, s));
+    CKC(cudaMemcpyAsync(S->omega, D->flag, n, cudaMemcpyDeviceToDevice, s));
+    {
+      uint8_t* sflag = (uint8_t*)t;
+      int32_t* sinv = (int32_t*)((char*)t + ((nsA + 15) & ~(int64_t)15));
+      CKC(cudaMemsetAsync(sflag, 255, nsA, s));
+      k_bsub_masked<<<(unsigned)((K + kTB - 1) / kTB), kTB, 0, s>>>(view(M->A), M->seg_units, spg, D->idx, K, D->inv,
+                                                                   b, x0, S->bs, S->xm0, sflag);
+      count_launch();
+      CKC(cudaGetLastError());
+      CK(compact_flags(sflag, nsA, S->slist, sinv, S->nlist, s));
+    }
+    dfree(t, s);
+    *out = S;
+    return LC_OK;
+  }
   CK(dalloc((void**)&B.seg_unit0, sizeof(int32_t) * (G + 1), s));
   CK(dalloc((void**)&B.seg_slice0, sizeof(int64_t) * (G + 1), s));
   CKC(cudaMemcpyAsync(B.seg_unit0, D->seg_base, sizeof(int32_t) * (G + 1), cudaMemcpyDeviceToDevice, s));

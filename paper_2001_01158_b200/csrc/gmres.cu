@@ -32,6 +32,7 @@ struct GmresArgs {
   double* t;
   double* V;            // (m+1) vectors of n scalars
   double* part;         // [(m+2) * nCTA]
+  GridBar* bar;
   int* out;             // [0] iters, [1] status
   double* out_relres;
   const int32_t* scatter_idx;
@@ -55,7 +56,6 @@ __device__ __forceinline__ void block_apply(const double* __restrict__ Mi, const
 
 template <int BS>
 __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
-  cg::grid_group grid = cg::this_grid();
   const SellView& A = P.A;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nCTA = gridDim.x, bid = blockIdx.x;
@@ -116,12 +116,12 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
 #pragma unroll
         for (int a = 0; a < BS; ++a) acc[a] = 0.0;
         for (int k = 0; k < wd; ++k) {
-          int c = A.col[p0 + 32 * k + lane];
+          int64_t c = sv_col(A, p0 + lane, k, u);
           if (BS == 1) {
             acc[0] = __fma_rn(A.val[p0 + 32 * k + lane], P.x[c], acc[0]);
           } else {
             const double* vb = A.val + 9 * (p0 + 32ll * k) + lane;
-            double y0 = P.x[3ll * c], y1 = P.x[3ll * c + 1], y2 = P.x[3ll * c + 2];
+            double y0 = P.x[3 * c], y1 = P.x[3 * c + 1], y2 = P.x[3 * c + 2];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
               acc[a] = __fma_rn(vb[32 * (3 * a)], y0, acc[a]);
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
       lane_flush(1, a1);
     }
     publish(2);
-    grid.sync();
+    grid_barrier(P.bar);
     reduce(2);
     double beta = sqrt(red[0]);
     if (first) { nb = sqrt(red[1]); tgt = nb > 0 ? P.eps * nb : P.eps; }
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
 #pragma unroll
         for (int a = 0; a < BS; ++a) P.t[BS * u + a] = tt[a];
       }
-      grid.sync();
+      grid_barrier(P.bar);
       // ---- 1b: w = A t, h_i = V_i . w
       clear(j + 1);
       {
@@ -188,12 +188,12 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
             int64_t p0 = A.slice_ptr[s];
             int wd = (int)((A.slice_ptr[s + 1] - p0) >> 5);
             for (int k = 0; k < wd; ++k) {
-              int c = A.col[p0 + 32 * k + lane];
+              int64_t c = sv_col(A, p0 + lane, k, u);
               if (BS == 1) {
                 acc[0] = __fma_rn(A.val[p0 + 32 * k + lane], P.t[c], acc[0]);
               } else {
                 const double* vb = A.val + 9 * (p0 + 32ll * k) + lane;
-                double y0 = P.t[3ll * c], y1 = P.t[3ll * c + 1], y2 = P.t[3ll * c + 2];
+                double y0 = P.t[3 * c], y1 = P.t[3 * c + 1], y2 = P.t[3 * c + 2];
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
                   acc[a] = __fma_rn(vb[32 * (3 * a)], y0, acc[a]);
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
         for (int i = 0; i <= j; ++i) lane_flush(i, dacc[i]);
       }
       publish(j + 1);
-      grid.sync();
+      grid_barrier(P.bar);
       reduce(j + 1);
       // keep h in smem column j of H (pass-1 part)
       if (threadIdx.x <= j) H[threadIdx.x * m + j] = red[threadIdx.x];
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
       for (int i = 0; i <= j; ++i) lane_flush(i, dacc[i]);
       }
       publish(j + 1);
-      grid.sync();
+      grid_barrier(P.bar);
       reduce(j + 1);
       // ---- 3: w -= V h2, ||w||^2
       clear(1);
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
         lane_flush(0, a0);
       }
       publish(1);
-      grid.sync();
+      grid_barrier(P.bar);
       reduce(1);
       if (threadIdx.x == 0) {
         double hn = sqrt(red[0]);
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
 #pragma unroll
       for (int a = 0; a < BS; ++a) P.x[BS * u + a] += tt[a];
     }
-    grid.sync();
+    grid_barrier(P.bar);
   }
   if (bid == 0 && threadIdx.x == 0) { P.out[0] = it; P.out[1] = status; *P.out_relres = relres; }
   if (P.scatter_idx) {
@@ -369,7 +369,7 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   int64_t nCTA = std::min<int64_t>(g_gm_ctas[ci], (M.nslices + kGW - 1) / kGW);
   if (nCTA < 1) nCTA = 1;
   size_t vbytes = ((sizeof(double) * (size_t)n) + 255) & ~(size_t)255;
-  size_t bytes = vbytes * (3 + (m + 1) + (scatter_idx ? 1 : 0)) + sizeof(double) * (m + 2) * nCTA + 64;
+  size_t bytes = vbytes * (3 + (m + 1) + (scatter_idx ? 1 : 0)) + sizeof(double) * (m + 2) * nCTA + 256;
   void* ws = nullptr;
   lc_status st = dalloc(&ws, bytes, s);
   if (st) return st;
@@ -389,6 +389,7 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
     a.x = x;
   }
   a.part = (double*)w; w += sizeof(double) * (m + 2) * nCTA;
+  a.bar = (GridBar*)w; w += 64;
   a.out = (int*)w;
   a.out_relres = (double*)(w + 16);
   a.scatter_idx = scatter_idx;
@@ -402,9 +403,10 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   float ms = 0.f;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaError_t e = cudaMemsetAsync(a.bar, 0, 64, s);
   cudaEventRecord(e0, s);
   void* args[] = {&a};
-  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kGT), args, 0, s);
+  if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kGT), args, 0, s);
   count_launch();
   cudaEventRecord(e1, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(out, a.out, 8, cudaMemcpyDeviceToHost, s);

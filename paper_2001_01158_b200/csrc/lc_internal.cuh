@@ -25,6 +25,7 @@
 namespace lc {
 
 constexpr int kWarp = 32;
+constexpr int kMaxOff = 8;   // stencil layout: at most 8 slots (offsets) per row
 
 // ---------------------------------------------------------------- errors ----
 void set_error(const std::string& msg);
@@ -43,6 +44,23 @@ void count_launch(int n = 1);
     cudaError_t _e = cudaGetLastError();                               \
     if (_e != cudaSuccess) return ::lc::cuda_fail(_e, "kernel launch"); \
   } while (0)
+
+// one Krylov solve for run_pcg (pcg.cu)
+struct Sell;
+struct PcgJob {
+  const Sell* M = nullptr;        // operator layout
+  const double* b = nullptr;      // right-hand side in M's numbering
+  double* x = nullptr;            // iterate updated in place (x_init == nullptr)
+  const double* x_init = nullptr; // else: solve on a workspace copy of x_init
+  const int32_t* slist = nullptr; // optional active-slice list, device count at nlist_dev
+  const int64_t* nlist_dev = nullptr;
+  int64_t nlist_max = 0;          // host upper bound of the list length
+  const uint8_t* omega = nullptr; // masked solve: rows with omega[u] != 255
+  const int32_t* scatter_idx = nullptr;  // explicit local solve: x_full[scatter_idx[l]] = x[l]
+  double* x_full = nullptr;
+  double* x_user = nullptr;       // masked local solve: x_user[u] = x[u] on Omega
+  int reg_units = 0, spg = 0;     // equal segments of reg_units units with spg slices each (A), else 0
+};
 
 // stream-ordered device allocation (pool with unlimited release threshold)
 lc_status dalloc(void** p, size_t bytes, cudaStream_t s);
@@ -66,6 +84,11 @@ struct Sell {
   double* val = nullptr;          // [nslots * block*block]
   uint8_t* rowlen = nullptr;      // [nunits]
   double* dinv = nullptr;         // [nunits * block*block]: 1/a_ii or the inverse cell block (row-major)
+  // stencil layout: every row's column offsets (col - row) lie in one sorted set off[0..W);
+  // slot k of a row holds the entry at column row + off[k] or a zero "hole"; no col array is stored.
+  int stencil = 0;
+  int32_t off[kMaxOff] = {0};
+  uint8_t* mask = nullptr;        // [nunits] bit k = slot k holds a stored entry (stencil layout)
   std::vector<int32_t> h_seg_unit0;
   std::vector<int64_t> h_seg_slice0;
   void release(cudaStream_t s);
@@ -74,6 +97,11 @@ struct Sell {
 // Device view passed by value to kernels
 struct SellView {
   int block;
+  int stencil;              // 1: col(u, k) = u + off[k] (clamped), real(u, k) = mask[u] bit k
+  int W;                    // stencil width (= maxw)
+  int32_t off[kMaxOff];
+  const uint8_t* mask;
+  int64_t nunits;
   int64_t nslices;
   int nseg;
   const int64_t* slice_ptr;
@@ -87,9 +115,30 @@ struct SellView {
   const double* dinv;
 };
 inline SellView view(const Sell& m) {
-  return SellView{m.block, m.nslices, m.nseg, m.slice_ptr, m.slice_row0, m.slice_seg, m.seg_unit0,
-                  m.seg_slice0, m.col, m.val, m.rowlen, m.dinv};
+  SellView v;
+  v.block = m.block; v.stencil = m.stencil; v.W = m.maxw;
+  for (int k = 0; k < kMaxOff; ++k) v.off[k] = m.off[k];
+  v.mask = m.mask; v.nunits = m.nunits;
+  v.nslices = m.nslices; v.nseg = m.nseg; v.slice_ptr = m.slice_ptr; v.slice_row0 = m.slice_row0;
+  v.slice_seg = m.slice_seg; v.seg_unit0 = m.seg_unit0; v.seg_slice0 = m.seg_slice0; v.col = m.col;
+  v.val = m.val; v.rowlen = m.rowlen; v.dinv = m.dinv;
+  return v;
 }
+
+// column of slot k of unit u (lane offset pl = slice_ptr[s] + lane); stencil: u + off[k] clamped to [0, n)
+__device__ __forceinline__ int64_t sv_col(const SellView& A, int64_t pl, int k, int64_t u) {
+  if (A.stencil) {
+    int64_t c = u + A.off[k];
+    return c < 0 ? 0 : (c >= A.nunits ? A.nunits - 1 : c);
+  }
+  return A.col[pl + 32ll * k];
+}
+// slot k of unit u holds a stored entry (not padding, not a hole)
+__device__ __forceinline__ bool sv_real(const SellView& A, int k, int64_t u) {
+  return A.stencil ? ((A.mask[u] >> k) & 1) : (k < A.rowlen[u]);
+}
+// number of slots to walk for unit u
+__device__ __forceinline__ int sv_len(const SellView& A, int64_t u) { return A.stencil ? A.W : A.rowlen[u]; }
 
 // --------------------------------------------------------------- handles ----
 }  // namespace lc
@@ -122,6 +171,15 @@ struct lc_domain_s {
 struct lc_sub_s {
   int32_t block = 1, nseg = 1;
   int64_t K_units = 0;
+  // masked representation (stencil-layout A, block 1): B = A[Omega, Omega] applied implicitly on A's layout
+  int masked = 0;
+  lc_matrix_s* A = nullptr;       // the matrix handle (must outlive the sub)
+  double* bs = nullptr;           // [n] b_sub on Omega rows (global numbering), 0 elsewhere
+  double* xm0 = nullptr;          // [n] x0 on Omega rows, 0 elsewhere
+  uint8_t* omega = nullptr;       // [n] copy of the domain flags (255 = outside Omega)
+  int32_t* slist = nullptr;       // active slices of A (ascending), count at *nlist
+  int64_t* nlist = nullptr;
+  // explicit representation (otherwise)
   lc::Sell B;               // K_units rows/cells, segments = ranks [seg_base[g], seg_base[g+1])
   int32_t* idx = nullptr;   // [K_units] global units (owned copy)
   double* bsub = nullptr;   // [K_units*block]
@@ -174,6 +232,36 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 }
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Grid-wide barrier for cooperative (co-resident) launches: one arrive per CTA on a counter, the last
+// arriver resets it and bumps a generation word with release semantics; the others spin on the
+// generation with acquire loads (no sleep back-off, unlike cooperative_groups' grid sync, whose wake-up
+// latency measured 2-7 us per barrier on small grids: profiles/r01_d).  Both words must be zero at launch.
+struct GridBar { unsigned count; unsigned gen; };
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void grid_barrier(GridBar* gb) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g0 = ld_acquire_u32(&gb->gen);
+    __threadfence();                                    // publish this CTA's writes (cumulative via bar.sync)
+    if (atomicAdd(&gb->count, 1u) == gridDim.x - 1) {
+      gb->count = 0;
+      st_release_u32(&gb->gen, g0 + 1);
+    } else {
+      while (ld_acquire_u32(&gb->gen) == g0) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
 }
 
 // ------------------------------------------------------------ launchers -----

@@ -1,10 +1,8 @@
 // pcg.cu -- Jacobi-preconditioned CG as ONE persistent cooperative kernel
 // (SURVEY 8(a) a7 local solve, a8 assembly, a9 global solve, a10 method0).
 //
-// The Krylov loop never returns to the host: scalars live in shared memory,
-// reductions are fixed-order (per-CTA partials, then every CTA that needs a
-// segment's scalar sums that segment's partials in the same order), and two
-// grid-wide barriers separate the two fused passes of an iteration:
+// The Krylov loop never returns to the host.  Two grid-wide barriers separate
+// the two fused passes of an iteration:
 //
 //   pass A  q = A p with the p-update p = z + beta p_old applied on the fly to
 //           every operand (own row written to the other p buffer), fused with
@@ -13,10 +11,23 @@
 //
 // Step order and the true-residual confirmation follow the oracle (or_pcg):
 // tolerance eps ||b||_2 (Eq. 6), recursive test then the true
-// residual (R19); iterations = SpMVs with p (R30).  Batched block-diagonal
-// systems (config 3) carry one state machine per segment; converged segments
-// drop out of both passes while the others continue.
+// residual (R19); iterations = SpMVs with p (R30).
+//
+// Work distribution: the slices (all of them, or an active-slice list) are
+// interleaved over every warp of the grid, so the grid sweeps one contiguous
+// window of rows (plane neighbours of a 7-point stencil stay L2 hits) and a
+// batched block-diagonal system (config 3) keeps every SM busy until its last
+// group converges.  Every CTA holds the scalar state of ALL segments and
+// updates it identically from fixed-order reductions (G = 1: each CTA sums the
+// per-CTA partials; G > 1: CTA g reduces segment g, one extra grid barrier),
+// so control flow is grid-uniform and results are bitwise deterministic.
+//
+// Masked local solves (stencil layout): B = A[Omega, Omega] is applied as the
+// stencil SpMV restricted to rows in Omega on vectors that are zero outside
+// Omega, over the slices that contain Omega rows.  The dropped couplings
+// multiply exact zeros, so each row's fma chain equals B's chain (R22).
 #include <cmath>
+#include <cstdlib>
 
 #include "lc_internal.cuh"
 
@@ -33,24 +44,30 @@ enum Mode : int { M_INIT = 0, M_RESET, M_FIRST, M_NORMAL, M_UPDATE, M_CONFIRM, M
 struct PcgArgs {
   SellView A;
   const double* b;
-  double* x;            // iterate (n)
+  double* x;
   double* r;
   double* z;
   double* q;
   double* p0;
   double* p1;
-  double* part;         // [(nCTA + nseg) * 2]
-  int* n_active;
-  int* out_iters;       // [nseg]
+  double* part;                 // [nCTA][G][2]
+  double* red;                  // [G][2]  (G > 1)
+  GridBar* bar;                 // zeroed at launch
+  int* out_iters;               // [G]
   int* out_status;
   double* out_relres;
-  const int32_t* scatter_idx;   // local solve: x_full[scatter_idx[l]] = x[l] at exit
+  const int32_t* slist;         // optional active slices (ascending)
+  const int64_t* nlist;         // device count of slist
+  const uint8_t* omega;         // optional: unit u is a row of the subsystem iff omega[u] != 255
+  const int32_t* scatter_idx;   // explicit local solve: x_full[scatter_idx[l]] = x[l] at exit
   double* x_full;
+  double* x_user;               // masked local solve: x_user[u] = x[u] for u in Omega at exit
   double eps;
   int max_iters;
-  int interleave;       // 1: slices strided over all warps of the grid (single segment)
-  int vec2;             // 1: single segment and 16-byte aligned vectors -> flat double2 update pass
-  int64_t chunk;        // contiguous slices per CTA (interleave == 0)
+  int G;
+  int reg_units;                // > 0: equal segments of reg_units units, spg slices each (arithmetic maps)
+  int spg;
+  int vec2;                     // flat double2 update pass (G = 1, no list, aligned)
 };
 
 struct SegState {
@@ -58,122 +75,251 @@ struct SegState {
   double rho, alpha, beta, tgt, nb;
 };
 
-__device__ __forceinline__ void flush(double (*acc)[kMaxSeg][2], int warp, int gi, double a0, double a1) {
-  a0 = warp_sum(a0);
-  a1 = warp_sum(a1);
-  if ((threadIdx.x & 31) == 0) { acc[warp][gi][0] += a0; acc[warp][gi][1] += a1; }
+__device__ __forceinline__ void slice_map(const PcgArgs& P, int64_t s, int& g, int64_t& row0, int64_t& end) {
+  if (P.reg_units > 0) {
+    if (P.G == 1) {
+      g = 0; row0 = 32 * s; end = P.reg_units;
+    } else {
+      g = (int)(s / P.spg);
+      row0 = (int64_t)g * P.reg_units + 32 * (s - (int64_t)g * P.spg);
+      end = (int64_t)(g + 1) * P.reg_units;
+    }
+  } else {
+    g = P.A.slice_seg[s];
+    row0 = P.A.slice_row0[s];
+    end = P.A.seg_unit0[g + 1];
+  }
 }
 
-// One SELL row (lane of slice) dotted with an operand y(c) given by `ld`.  WM > 0: the slice width is
-// at most WM, the loop is fully unrolled so all column/value loads issue before the dependent gathers
-// (memory-level parallelism); slots k >= w are predicated off.  WM == 0: generic loop.
-template <int WM, class Ld>
-__device__ __forceinline__ double sell_row(const int32_t* __restrict__ cp, const double* __restrict__ vp, int w,
-                                           Ld ld) {
+// One row of a slice times an operand y(c).  WM > 0: slice width bound known at compile time; the
+// loop is fully unrolled so all value loads and gathers issue together (stencil: columns are
+// u + off[k], no column loads at all).  Returns the fma chain; *own = y at the diagonal slot when
+// ST (the own p value comes from the diagonal gather).
+template <int WM, int ST, class Ld>
+__device__ __forceinline__ double row_dot(const SellView& A, int64_t pl, int w, int64_t u, Ld ld, double* own) {
   double acc = 0.0;
+  const double* vp = A.val + pl;
   if (WM > 0) {
     constexpr int WA = WM > 0 ? WM : 1;
-    int c[WA];
     double v[WA], y[WA];
+    const int nu1 = (int)A.nunits - 1;   // n < 2^31 (checked in lc_create_csr): 32-bit index math
+    const int ui = (int)u;
 #pragma unroll
     for (int k = 0; k < WM; ++k) {
-      c[k] = (k < w) ? __ldg(cp + 32 * k) : 0;
-      v[k] = (k < w) ? __ldg(vp + 32 * k) : 0.0;
+      int c;
+      if (ST) {
+        c = ui + A.off[k];
+        c = c < 0 ? 0 : (c > nu1 ? nu1 : c);
+      } else {
+        c = (k < w) ? __ldg(A.col + pl + 32 * k) : 0;
+      }
+      v[k] = (ST || k < w) ? __ldg(vp + 32 * k) : 0.0;
+      y[k] = (ST || k < w) ? ld(c) : 0.0;
     }
 #pragma unroll
-    for (int k = 0; k < WM; ++k) y[k] = (k < w) ? ld(c[k]) : 0.0;
-#pragma unroll
     for (int k = 0; k < WM; ++k)
-      if (k < w) acc = __fma_rn(v[k], y[k], acc);
+      if (ST || k < w) acc = __fma_rn(v[k], y[k], acc);
+    if (ST) {
+#pragma unroll
+      for (int k = 0; k < WM; ++k)
+        if (A.off[k] == 0) *own = y[k];
+    }
   } else {
-    for (int k = 0; k < w; ++k) acc = __fma_rn(__ldg(vp + 32 * k), ld(__ldg(cp + 32 * k)), acc);
+    for (int k = 0; k < w; ++k) {
+      int c = (int)sv_col(A, pl, k, u);
+      double yk = ld(c);
+      if (ST && c == u) *own = yk;
+      acc = __fma_rn(__ldg(vp + 32 * k), yk, acc);
+    }
   }
   return acc;
 }
 
-template <int WM>
-__global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
-  cg::grid_group grid = cg::this_grid();
+// Pass A slice loop for one mode (single segment: the mode is grid-uniform, so it is hoisted out of
+// the loop and each mode gets a small loop body).  MODE 0: r = b - A x (INIT/CONFIRM, init adds b^T b);
+// 1: FIRST (p = z); 2: NORMAL (p = z + beta p_old on the fly).
+template <int WM, int ST, int MODE>
+__device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_t jlim, int64_t jstep, int lane,
+                                            bool init, double beta, const double* __restrict__ pold,
+                                            double* __restrict__ pnew, double& a0, double& a1) {
+  const SellView& A = P.A;
+#pragma unroll 1
+  for (int64_t j = j0; j < jlim; j += jstep) {
+    const int64_t s = P.slist ? (int64_t)P.slist[j] : j;
+    int g;
+    int64_t row0, end;
+    slice_map(P, s, g, row0, end);
+    const int64_t u = row0 + lane;
+    if (u >= end) continue;
+    const int64_t pl = (ST ? 32ll * A.W * s : A.slice_ptr[s]) + lane;
+    const int w = ST ? A.W : (int)((A.slice_ptr[s + 1] - (pl - lane)) >> 5);
+    double own = 0.0;
+    const bool in = !P.omega || P.omega[u] != 255;
+    if (MODE == 0) {
+      const double* xx = P.x;
+      double acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return xx[c]; }, &own);
+      if (in) {
+        double bi = P.b[u];
+        double ri = bi - acc;
+        P.r[u] = ri;
+        a0 = __fma_rn(ri, ri, a0);
+        if (init) a1 = __fma_rn(bi, bi, a1);
+      }
+    } else {
+      const double* zz = P.z;
+      double acc;
+      if (MODE == 1) acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return zz[c]; }, &own);
+      else acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return __fma_rn(beta, pold[c], zz[c]); }, &own);
+      if (in) {
+        double pi = ST ? own : (MODE == 1 ? zz[u] : __fma_rn(beta, pold[u], zz[u]));
+        pnew[u] = pi;
+        P.q[u] = acc;
+        a0 = __fma_rn(pi, acc, a0);
+      }
+    }
+  }
+}
+
+#ifdef LC_DEBUG_TIMELINE
+__device__ unsigned long long g_tl[8192];
+__device__ __forceinline__ void tl_mark(int& k) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && k < 8192) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tl[k] = t;
+  }
+  ++k;
+}
+#define TL(k) tl_mark(k)
+#else
+#define TL(k) (void)0
+#endif
+#ifndef LCV_MINB
+#define LCV_MINB 4
+#endif
+template <int WM, int ST>
+__global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   __shared__ SegState S[kMaxSeg];
   __shared__ double s_acc[kPW][kMaxSeg][2];
   __shared__ double s_red[kPW][2];
+  __shared__ double s_sum[kMaxSeg][2];
   __shared__ int s_exit;
   const SellView& A = P.A;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nCTA = gridDim.x, bid = blockIdx.x;
-  int64_t s_begin, s_lim, s_step;
-  int g_lo, g_hi;
-  if (P.interleave) {
-    s_begin = bid * kPW + warp; s_lim = A.nslices; s_step = nCTA * kPW;
-    g_lo = 0; g_hi = 0;
-  } else {
-    int64_t c0 = bid * P.chunk, c1 = min(A.nslices, c0 + P.chunk);
-    s_begin = c0 + warp; s_lim = c1; s_step = kPW;
-    if (c0 < c1) { g_lo = A.slice_seg[c0]; g_hi = A.slice_seg[c1 - 1]; } else { g_lo = 1; g_hi = 0; }
-  }
-  const int nsegs_here = g_hi - g_lo + 1;
+  const int G = P.G;
+  const int64_t j0 = bid * kPW + warp, jstep = nCTA * kPW;
+  const int64_t jlim = P.slist ? *P.nlist : A.nslices;
   if (threadIdx.x < kMaxSeg) {
     S[threadIdx.x].mode = M_INIT; S[threadIdx.x].par = 0; S[threadIdx.x].it = 0; S[threadIdx.x].final_ = 0;
+    S[threadIdx.x].beta = 0.0; S[threadIdx.x].alpha = 0.0; S[threadIdx.x].rho = 0.0;
   }
   __syncthreads();
 
-  // partial sums of segment g of this CTA go to part[(bid + g)*2 + {0,1}]
-  auto write_partials = [&]() {
-    __syncthreads();
-    for (int t = threadIdx.x; t < nsegs_here * 2; t += kPT) {
-      int gi = t >> 1, j = t & 1;
-      double v = 0.0;
-      for (int w = 0; w < kPW; ++w) v += s_acc[w][gi][j];
-      P.part[(bid + g_lo + gi) * 2 + j] = v;
-    }
-  };
   auto clear_acc = [&]() {
-    for (int t = threadIdx.x; t < kPW * kMaxSeg * 2; t += kPT) (&s_acc[0][0][0])[t] = 0.0;
-    __syncthreads();
-  };
-  // fixed-order sum of segment g's partials over the CTAs that touch it
-  auto seg_sum = [&](int g, double& o0, double& o1) {
-    int64_t c_lo, c_hi;
-    if (P.interleave) { c_lo = 0; c_hi = nCTA - 1; }
-    else { c_lo = A.seg_slice0[g] / P.chunk; c_hi = (A.seg_slice0[g + 1] - 1) / P.chunk; }
-    double a0 = 0.0, a1 = 0.0;
-    for (int64_t c = c_lo + threadIdx.x; c <= c_hi; c += kPT) {
-      a0 += P.part[(c + g) * 2]; a1 += P.part[(c + g) * 2 + 1];
+    for (int t = threadIdx.x; t < kPW * G * 2; t += kPT) {
+      int w = t / (G * 2), rest = t % (G * 2);
+      s_acc[w][rest >> 1][rest & 1] = 0.0;
     }
-    a0 = warp_sum(a0); a1 = warp_sum(a1);
     __syncthreads();
-    if (lane == 0) { s_red[warp][0] = a0; s_red[warp][1] = a1; }
-    __syncthreads();
-    o0 = 0.0; o1 = 0.0;
-    for (int w = 0; w < kPW; ++w) { o0 += s_red[w][0]; o1 += s_red[w][1]; }
   };
-  auto owner = [&](int g) -> bool {
-    if (P.interleave) return bid == 0;
-    return bid == A.seg_slice0[g] / P.chunk;
+  auto flush = [&](int g, double a0, double a1) {
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    if (lane == 0) { s_acc[warp][g][0] += a0; s_acc[warp][g][1] += a1; }
+  };
+  // per-CTA partials -> part[bid][g][j]; then every CTA obtains s_sum[g][j] for all g (fixed order)
+  auto reduce_all = [&]() {
+    __syncthreads();
+    for (int t = threadIdx.x; t < G * 2; t += kPT) {
+      double v = 0.0;
+      for (int w = 0; w < kPW; ++w) v += s_acc[w][t >> 1][t & 1];
+      P.part[(bid * G) * 2 + t] = v;
+    }
+    grid_barrier(P.bar);
+    if (G == 1) {
+      double a0 = 0.0, a1 = 0.0;
+      for (int64_t c = threadIdx.x; c < nCTA; c += kPT) { a0 += P.part[2 * c]; a1 += P.part[2 * c + 1]; }
+      a0 = warp_sum(a0); a1 = warp_sum(a1);
+      if (lane == 0) { s_red[warp][0] = a0; s_red[warp][1] = a1; }
+      __syncthreads();
+#if LCV_RED_ALL
+      {
+        double o0 = 0.0, o1 = 0.0;
+        for (int w = 0; w < kPW; ++w) { o0 += s_red[w][0]; o1 += s_red[w][1]; }
+        if (threadIdx.x == 0) { s_sum[0][0] = o0; s_sum[0][1] = o1; }
+      }
+#else
+      if (threadIdx.x < 2) {
+        double o = 0.0;
+        for (int w = 0; w < kPW; ++w) o += s_red[w][threadIdx.x];
+        s_sum[0][threadIdx.x] = o;
+      }
+#endif
+    } else {
+      for (int g = (int)bid; g < G; g += (int)nCTA) {       // stage 1: CTA g reduces segment g
+        double a0 = 0.0, a1 = 0.0;
+        for (int64_t c = threadIdx.x; c < nCTA; c += kPT) {
+          a0 += P.part[(c * G + g) * 2]; a1 += P.part[(c * G + g) * 2 + 1];
+        }
+        a0 = warp_sum(a0); a1 = warp_sum(a1);
+        if (lane == 0) { s_red[warp][0] = a0; s_red[warp][1] = a1; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          double o0 = 0.0, o1 = 0.0;
+          for (int w = 0; w < kPW; ++w) { o0 += s_red[w][0]; o1 += s_red[w][1]; }
+          P.red[2 * g] = o0; P.red[2 * g + 1] = o1;
+        }
+        __syncthreads();
+      }
+      grid_barrier(P.bar);
+      for (int t = threadIdx.x; t < G * 2; t += kPT) s_sum[t >> 1][t & 1] = P.red[t];   // stage 2
+    }
+    __syncthreads();
   };
   auto finish = [&](int g, int status, double rn) {
     SegState& T = S[g];
     T.mode = M_DONE;
-    if (owner(g)) {
+    if (bid == g % nCTA) {
       P.out_iters[g] = T.it;
       P.out_status[g] = status;
       P.out_relres[g] = T.nb > 0 ? rn / T.nb : rn;
-      atomicSub(P.n_active, 1);
     }
   };
+  auto in_omega = [&](int64_t u) -> bool { return !P.omega || P.omega[u] != 255; };
 
+#ifdef LC_DEBUG_TIMELINE
+  int tlk = 0;
+#endif
   for (;;) {
     // ------------------------------------------------------------ pass A ----
+    TL(tlk);
     clear_acc();
-    {
+    if (G == 1) {
+      const int mode = S[0].mode;
+      double a0 = 0.0, a1 = 0.0;
+      const double beta = S[0].beta;
+      const double* pold = S[0].par ? P.p1 : P.p0;
+      double* pnew = S[0].par ? P.p0 : P.p1;
+      if (mode == M_INIT || mode == M_CONFIRM)
+        pass_a_loop<WM, ST, 0>(P, j0, jlim, jstep, lane, mode == M_INIT, beta, pold, pnew, a0, a1);
+      else if (mode == M_FIRST)
+        pass_a_loop<WM, ST, 1>(P, j0, jlim, jstep, lane, false, beta, pold, pnew, a0, a1);
+      else if (mode == M_NORMAL)
+        pass_a_loop<WM, ST, 2>(P, j0, jlim, jstep, lane, false, beta, pold, pnew, a0, a1);
+      flush(0, a0, a1);
+    } else {
       int gcur = -1, mode = M_DONE;
       double a0 = 0.0, a1 = 0.0, beta = 0.0;
-      const double *pold = nullptr;
+      const double* pold = nullptr;
       double* pnew = nullptr;
-      for (int64_t s = s_begin; s < s_lim; s += s_step) {
-        int g = A.slice_seg[s];
+      for (int64_t j = j0; j < jlim; j += jstep) {
+        const int64_t s = P.slist ? (int64_t)P.slist[j] : j;
+        int g;
+        int64_t row0, end;
+        slice_map(P, s, g, row0, end);
         if (g != gcur) {
-          if (gcur >= 0) flush(s_acc, warp, gcur - g_lo, a0, a1);
+          if (gcur >= 0) flush(gcur, a0, a1);
           a0 = a1 = 0.0;
           gcur = g;
           mode = S[g].mode;
@@ -182,46 +328,44 @@ __global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
           pnew = S[g].par ? P.p0 : P.p1;
         }
         if (mode == M_DONE || mode == M_RESET) continue;
-        int64_t u = A.slice_row0[s] + lane;
-        if (u >= A.seg_unit0[g + 1]) continue;
-        int64_t p0 = A.slice_ptr[s];
-        int w = (int)((A.slice_ptr[s + 1] - p0) >> 5);
-        const int32_t* cp = A.col + p0 + lane;
-        const double* vp = A.val + p0 + lane;
+        const int64_t u = row0 + lane;
+        if (u >= end) continue;
+        const int64_t pl = (ST ? 32ll * A.W * s : A.slice_ptr[s]) + lane;
+        const int w = ST ? A.W : (int)((A.slice_ptr[s + 1] - (pl - lane)) >> 5);
+        double own = 0.0;
         if (mode == M_INIT || mode == M_CONFIRM) {
           const double* xx = P.x;
-          double acc = sell_row<WM>(cp, vp, w, [&](int c) { return xx[c]; });
-          double bi = P.b[u];
-          double ri = bi - acc;
-          P.r[u] = ri;
-          a0 = __fma_rn(ri, ri, a0);
-          if (mode == M_INIT) a1 = __fma_rn(bi, bi, a1);
-        } else if (mode == M_FIRST) {
+          double acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return xx[c]; }, &own);
+          if (in_omega(u)) {
+            double bi = P.b[u];
+            double ri = bi - acc;
+            P.r[u] = ri;
+            a0 = __fma_rn(ri, ri, a0);
+            if (mode == M_INIT) a1 = __fma_rn(bi, bi, a1);
+          }
+        } else {
           const double* zz = P.z;
-          double acc = sell_row<WM>(cp, vp, w, [&](int c) { return zz[c]; });
-          double pi = zz[u];
-          pnew[u] = pi;
-          P.q[u] = acc;
-          a0 = __fma_rn(pi, acc, a0);
-        } else {  // M_NORMAL: p = z + beta p_old on the fly
-          const double* zz = P.z;
-          double acc = sell_row<WM>(cp, vp, w, [&](int c) { return __fma_rn(beta, pold[c], zz[c]); });
-          double pi = __fma_rn(beta, pold[u], zz[u]);
-          pnew[u] = pi;
-          P.q[u] = acc;
-          a0 = __fma_rn(pi, acc, a0);
+          double acc;
+          if (mode == M_FIRST) acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return zz[c]; }, &own);
+          else acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return __fma_rn(beta, pold[c], zz[c]); }, &own);
+          if (in_omega(u)) {
+            double pi = ST ? own : (mode == M_FIRST ? zz[u] : __fma_rn(beta, pold[u], zz[u]));
+            pnew[u] = pi;
+            P.q[u] = acc;
+            a0 = __fma_rn(pi, acc, a0);
+          }
         }
       }
-      if (gcur >= 0) flush(s_acc, warp, gcur - g_lo, a0, a1);
+      if (gcur >= 0) flush(gcur, a0, a1);
     }
-    write_partials();
-    grid.sync();
+    TL(tlk);
+    reduce_all();
+    TL(tlk);
     // ---------------------------------------------------- pass A scalars ----
-    for (int g = g_lo; g <= g_hi; ++g) {
-      double s0, s1;
-      seg_sum(g, s0, s1);
-      if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      for (int g = 0; g < G; ++g) {
         SegState& T = S[g];
+        double s0 = s_sum[g][0], s1 = s_sum[g][1];
         if (T.mode == M_INIT) {
           T.nb = sqrt(s1);
           T.tgt = T.nb > 0 ? P.eps * T.nb : P.eps;
@@ -241,12 +385,13 @@ __global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
           else T.mode = M_RESET;
         }
       }
-      __syncthreads();
     }
+    __syncthreads();
     // ------------------------------------------------------------ pass B ----
+    TL(tlk);
     clear_acc();
     if (P.vec2) {
-      // single segment: flat grid-stride over row pairs with 16-byte loads/stores
+      // single segment over all rows: flat grid-stride over row pairs with 16-byte loads/stores
       const int mode = S[0].mode;
       double a0 = 0.0, a1 = 0.0;
       if (mode == M_UPDATE || mode == M_RESET) {
@@ -257,7 +402,7 @@ __global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
         double2* z2 = reinterpret_cast<double2*>(P.z);
         const double2* q2 = reinterpret_cast<const double2*>(P.q);
         const double2* d2 = reinterpret_cast<const double2*>(A.dinv);
-        const int64_t n = A.seg_unit0[1], npair = n >> 1;
+        const int64_t n = A.nunits, npair = n >> 1;
         const int64_t gt = bid * kPT + threadIdx.x, gs = nCTA * kPT;
         if (mode == M_UPDATE) {
 #pragma unroll 2
@@ -295,15 +440,18 @@ __global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
           }
         }
       }
-      flush(s_acc, warp, 0, a0, a1);
+      flush(0, a0, a1);
     } else {
       int gcur = -1, mode = M_DONE;
       double a0 = 0.0, a1 = 0.0, alpha = 0.0;
       const double* pp = nullptr;
-      for (int64_t s = s_begin; s < s_lim; s += s_step) {
-        int g = A.slice_seg[s];
+      for (int64_t j = j0; j < jlim; j += jstep) {
+        const int64_t s = P.slist ? (int64_t)P.slist[j] : j;
+        int g;
+        int64_t row0, end;
+        slice_map(P, s, g, row0, end);
         if (g != gcur) {
-          if (gcur >= 0) flush(s_acc, warp, gcur - g_lo, a0, a1);
+          if (gcur >= 0) flush(gcur, a0, a1);
           a0 = a1 = 0.0;
           gcur = g;
           mode = S[g].mode;
@@ -311,8 +459,9 @@ __global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
           pp = S[g].par ? P.p1 : P.p0;
         }
         if (mode != M_UPDATE && mode != M_RESET) continue;
-        int64_t u = A.slice_row0[s] + lane;
-        if (u >= A.seg_unit0[g + 1]) continue;
+        const int64_t u = row0 + lane;
+        if (u >= end) continue;
+        // rows outside Omega (masked solves) hold p = q = r = 0, so the update leaves them 0
         double di = A.dinv[u];
         if (mode == M_UPDATE) {
           double xi = __fma_rn(alpha, pp[u], P.x[u]);
@@ -328,17 +477,17 @@ __global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
           a0 = __fma_rn(ri, zi, a0);
         }
       }
-      if (gcur >= 0) flush(s_acc, warp, gcur - g_lo, a0, a1);
+      if (gcur >= 0) flush(gcur, a0, a1);
     }
-    write_partials();
-    grid.sync();
+    TL(tlk);
+    reduce_all();
+    TL(tlk);
     // ---------------------------------------------------- pass B scalars ----
-    if (threadIdx.x == 0) s_exit = (atomicAdd(P.n_active, 0) == 0);
-    for (int g = g_lo; g <= g_hi; ++g) {
-      double s0, s1;
-      seg_sum(g, s0, s1);
-      if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      int active = 0;
+      for (int g = 0; g < G; ++g) {
         SegState& T = S[g];
+        double s0 = s_sum[g][0], s1 = s_sum[g][1];
         if (T.mode == M_UPDATE) {
           T.it += 1;
           double rz = s0, rr = s1;
@@ -354,107 +503,117 @@ __global__ void __launch_bounds__(kPT) k_pcg(PcgArgs P) {
           T.rho = s0;
           T.mode = M_FIRST;
         }
+        active += (T.mode != M_DONE);
       }
-      __syncthreads();
+      s_exit = (active == 0);
     }
     __syncthreads();
     if (s_exit) break;
   }
   // a8: x~[Omega] = xbar_B (Eq. 4), fused into the local solve's exit
-  if (P.scatter_idx) {
-    for (int64_t s = s_begin; s < s_lim; s += s_step) {
-      int g = A.slice_seg[s];
-      int64_t u = A.slice_row0[s] + lane;
-      if (u < A.seg_unit0[g + 1]) P.x_full[P.scatter_idx[u]] = P.x[u];
+  if (P.scatter_idx || P.x_user) {
+    for (int64_t j = j0; j < jlim; j += jstep) {
+      const int64_t s = P.slist ? (int64_t)P.slist[j] : j;
+      int g;
+      int64_t row0, end;
+      slice_map(P, s, g, row0, end);
+      const int64_t u = row0 + lane;
+      if (u >= end) continue;
+      if (P.scatter_idx) P.x_full[P.scatter_idx[u]] = P.x[u];
+      else if (in_omega(u)) P.x_user[u] = P.x[u];
     }
   }
 }
 
 // ---------------------------------------------------------------- host ----
-static int g_pcg_max_ctas[3] = {0, 0, 0};
+static int g_pcg_max_ctas[6] = {0, 0, 0, 0, 0, 0};
 
-lc_status run_pcg(const Sell& M, const double* b, double* x, const int32_t* scatter_idx, double* x_full,
-                  const double* x_init, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
+lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
+  const Sell& M = *job.M;
   const int G = M.nseg;
   if (G > kMaxSeg) { set_error("PCG: at most 64 segments"); return LC_ERR_DIMENSION; }
   if (M.block != 1) { set_error("PCG: needs block = 1 (use LC_GMRES for block systems)"); return LC_ERR_INVALID_ARG; }
   std::vector<int> it(G, 0), stt(G, LC_OK);
   std::vector<double> rr(G, 0.0);
-  int n_active = 0;
-  for (int g = 0; g < G; ++g) if (M.h_seg_slice0[g + 1] > M.h_seg_slice0[g]) ++n_active;
   float ms = 0.f;
-  if (n_active > 0) {
-    const int wi = M.maxw <= 5 ? 0 : M.maxw <= 7 ? 1 : 2;
-    void* fn = wi == 0 ? (void*)k_pcg<5> : wi == 1 ? (void*)k_pcg<7> : (void*)k_pcg<0>;
-    if (!g_pcg_max_ctas[wi]) {
-      int per_sm = 0;
-      LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPT, 0));
-      if (per_sm < 1) { set_error("PCG kernel does not fit on an SM"); return LC_ERR_CUDA; }
-      g_pcg_max_ctas[wi] = per_sm * num_sms();
-    }
-    const int64_t n = M.nunits;
-    int64_t nCTA = std::min<int64_t>(g_pcg_max_ctas[wi], (M.nslices + kPW - 1) / kPW);
-    if (nCTA < 1) nCTA = 1;
-    int interleave = (G == 1) ? 1 : 0;
-    int64_t chunk = (M.nslices + nCTA - 1) / nCTA;
-    if (!interleave) nCTA = (M.nslices + chunk - 1) / chunk;
-    void* ws = nullptr;
-    size_t vec = sizeof(double) * (size_t)n;
-    size_t vbytes = (vec + 255) & ~(size_t)255;
-    size_t bytes = vbytes * (scatter_idx ? 6 : 5) + sizeof(double) * 2 * (nCTA + G + 1) + 64 + 16 * G + 64;
-    lc_status st = dalloc(&ws, bytes, s);
-    if (st) return st;
-    char* w = (char*)ws;
-    PcgArgs a;
-    a.A = view(M);
-    a.b = b;
-    a.r = (double*)w; w += vbytes;
-    a.z = (double*)w; w += vbytes;
-    a.q = (double*)w; w += vbytes;
-    a.p0 = (double*)w; w += vbytes;
-    a.p1 = (double*)w; w += vbytes;
-    if (scatter_idx) {
-      a.x = (double*)w; w += vbytes;
-      cudaError_t e = cudaMemcpyAsync(a.x, x_init, vec, cudaMemcpyDeviceToDevice, s);
-      if (e != cudaSuccess) { dfree(ws, s); return cuda_fail(e, "cudaMemcpyAsync"); }
-    } else {
-      a.x = x;
-    }
-    a.part = (double*)w; w += sizeof(double) * 2 * (nCTA + G + 1);
-    a.n_active = (int*)w; w += 64;
-    a.out_iters = (int*)w; w += 4 * G;
-    a.out_status = (int*)w; w += 4 * G;
-    a.out_relres = (double*)((((uintptr_t)w) + 7) & ~(uintptr_t)7);
-    a.scatter_idx = scatter_idx;
-    a.x_full = x_full;
-    a.eps = p->rel_tol;
-    a.max_iters = p->max_iters;
-    a.interleave = interleave;
-    a.vec2 = (interleave && ((((uintptr_t)a.x) | ((uintptr_t)a.r) | ((uintptr_t)a.z) | ((uintptr_t)a.q) |
-                              ((uintptr_t)a.p0) | ((uintptr_t)a.p1) | ((uintptr_t)M.dinv)) & 15) == 0) ? 1 : 0;
-    a.chunk = chunk;
-    cudaError_t e = cudaMemcpyAsync(a.n_active, &n_active, sizeof(int), cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(a.out_iters, 0, 8 * G, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(a.out_relres, 0, 8 * G, s);
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0); cudaEventCreate(&e1);
-    cudaEventRecord(e0, s);
-    void* args[] = {&a};
-    if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kPT), args, 0, s);
-    count_launch();
-    cudaEventRecord(e1, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(it.data(), a.out_iters, 4 * G, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(stt.data(), a.out_status, 4 * G, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(rr.data(), a.out_relres, 8 * G, cudaMemcpyDeviceToHost, s);
-    dfree(ws, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0); cudaEventDestroy(e1);
-    if (e != cudaSuccess) return cuda_fail(e, "PCG kernel");
+  const int wi = (M.maxw <= 5 ? 0 : M.maxw <= 7 ? 1 : 2) + (M.stencil ? 3 : 0);
+  void* const fns[6] = {(void*)k_pcg<5, 0>, (void*)k_pcg<7, 0>, (void*)k_pcg<0, 0>,
+                        (void*)k_pcg<5, 1>, (void*)k_pcg<7, 1>, (void*)k_pcg<0, 1>};
+  void* fn = fns[wi];
+  if (!g_pcg_max_ctas[wi]) {
+    int per_sm = 0;
+    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPT, 0));
+    if (per_sm < 1) { set_error("PCG kernel does not fit on an SM"); return LC_ERR_CUDA; }
+    g_pcg_max_ctas[wi] = per_sm * num_sms();
   }
+  const int64_t n = M.nunits;
+  const int64_t work = job.slist ? job.nlist_max : M.nslices;
+  int64_t nCTA = std::min<int64_t>(g_pcg_max_ctas[wi], (std::max<int64_t>(work, 1) + kPW - 1) / kPW);
+  if (nCTA < 1) nCTA = 1;
+  void* ws = nullptr;
+  const size_t vec = sizeof(double) * (size_t)n;
+  const size_t vbytes = (vec + 255) & ~(size_t)255;
+  const bool own_x = job.x_init != nullptr;
+  const size_t bytes = vbytes * (own_x ? 6 : 5) + sizeof(double) * 2 * G * (nCTA + 1) + 16 * G + 512;
+  lc_status st = dalloc(&ws, bytes, s);
+  if (st) return st;
+  char* w = (char*)ws;
+  PcgArgs a;
+  a.A = view(M);
+  a.b = job.b;
+  a.r = (double*)w; w += vbytes;
+  a.z = (double*)w; w += vbytes;
+  a.q = (double*)w; w += vbytes;
+  a.p0 = (double*)w; w += vbytes;
+  a.p1 = (double*)w; w += vbytes;
+  cudaError_t e = cudaSuccess;
+  if (own_x) {
+    a.x = (double*)w; w += vbytes;
+    e = cudaMemcpyAsync(a.x, job.x_init, vec, cudaMemcpyDeviceToDevice, s);
+  } else {
+    a.x = job.x;
+  }
+  if (job.omega && e == cudaSuccess) e = cudaMemsetAsync(a.r, 0, vbytes * 5, s);   // zero outside Omega
+  a.part = (double*)w; w += sizeof(double) * 2 * G * nCTA;
+  a.red = (double*)w; w += sizeof(double) * 2 * G;
+  a.bar = (GridBar*)w; w += 64;
+  a.out_iters = (int*)w; w += 4 * G;
+  a.out_status = (int*)w; w += 4 * G;
+  a.out_relres = (double*)((((uintptr_t)w) + 7) & ~(uintptr_t)7);
+  a.slist = job.slist;
+  a.nlist = job.nlist_dev;
+  a.omega = job.omega;
+  a.scatter_idx = job.scatter_idx;
+  a.x_full = job.x_full;
+  a.x_user = job.x_user;
+  a.eps = p->rel_tol;
+  a.max_iters = p->max_iters;
+  a.G = G;
+  a.reg_units = job.reg_units;
+  a.spg = job.spg;
+  a.vec2 = (G == 1 && !job.slist && !job.omega &&
+            ((((uintptr_t)a.x) | ((uintptr_t)a.r) | ((uintptr_t)a.z) | ((uintptr_t)a.q) | ((uintptr_t)a.p0) |
+              ((uintptr_t)a.p1) | ((uintptr_t)M.dinv)) & 15) == 0) ? 1 : 0;
+  if (e == cudaSuccess) e = cudaMemsetAsync(a.bar, 0, 64, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(a.out_iters, 0, 8 * G, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(a.out_relres, 0, 8 * G, s);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+  void* args[] = {&a};
+  if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kPT), args, 0, s);
+  count_launch();
+  cudaEventRecord(e1, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(it.data(), a.out_iters, 4 * G, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(stt.data(), a.out_status, 4 * G, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(rr.data(), a.out_relres, 8 * G, cudaMemcpyDeviceToHost, s);
+  dfree(ws, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  if (e != cudaSuccess) return cuda_fail(e, "PCG kernel");
   lc_status worst = LC_OK;
   for (int g = 0; g < G; ++g) {
-    if (M.h_seg_slice0[g + 1] == M.h_seg_slice0[g]) { it[g] = 0; stt[g] = LC_OK; rr[g] = 0.0; }
     if (info) {
       info[g].iterations = it[g];
       info[g].status = stt[g];
@@ -469,3 +628,9 @@ lc_status run_pcg(const Sell& M, const double* b, double* x, const int32_t* scat
 }
 
 }  // namespace lc
+
+#ifdef LC_DEBUG_TIMELINE
+extern "C" int lc_debug_timeline(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, lc::g_tl, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -1;
+}
+#endif

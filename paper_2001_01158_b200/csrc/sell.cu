@@ -1,12 +1,87 @@
 // sell.cu -- lc_create_csr: CSR/BSR input -> SELL-32 (sigma = 1) on the device,
 // with on-device pattern validation and the (block-)Jacobi inverse diagonal.
+#include <climits>
+#include <cstdlib>
 #include <cstring>
 
 #include "lc_internal.cuh"
 
 namespace lc {
 
-enum : unsigned { kErrPattern = 1u, kErrZeroDiag = 2u, kErrRowLen = 4u };
+enum : unsigned { kErrPattern = 1u, kErrZeroDiag = 2u, kErrRowLen = 4u, kErrNotStencil = 8u };
+
+__device__ bool inv3(const double* A, double* Ai);
+
+struct Offsets { int W; int32_t off[kMaxOff]; };
+
+// first row whose length equals the maximal row length (its offsets are the stencil candidate)
+__global__ void k_first_maxrow(int64_t n, const int64_t* __restrict__ rp, int maxw, int* best) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u < n && rp[u + 1] - rp[u] == maxw) atomicMin(best, (int)u);
+}
+
+// every stored (u, c) must have c - u in the candidate offset set
+__global__ void k_check_stencil(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, Offsets O,
+                                unsigned* err) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
+    int64_t d = (int64_t)ci[e] - u;
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < kMaxOff; ++k) hit |= (k < O.W && O.off[k] == d);
+    if (!hit) { atomicOr(err, kErrNotStencil); return; }
+  }
+}
+
+// stencil layout fill: thread per unit; slot k of the row = the entry at column u + off[k] (holes stay 0)
+template <int BS>
+__global__ void k_fill_stencil(int64_t n, int seg_units, int spg, const int64_t* __restrict__ rp,
+                               const int32_t* __restrict__ ci, const double* __restrict__ va, Offsets O,
+                               double* __restrict__ val, uint8_t* __restrict__ mask, double* __restrict__ dinv,
+                               unsigned* err) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  int64_t g = u / seg_units, lu = u - g * seg_units;
+  int64_t s = g * spg + (lu >> 5);
+  int lane = (int)(lu & 31);
+  unsigned m = 0;
+  double D[BS * BS];
+#pragma unroll
+  for (int q = 0; q < BS * BS; ++q) D[q] = 0.0;
+  int k = 0;
+  for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
+    int64_t d = (int64_t)ci[e] - u;
+    while (k < O.W && O.off[k] != d) ++k;     // offsets and columns are both ascending
+    m |= 1u << k;
+    int64_t base = (s * O.W + k) * 32;
+    if (BS == 1) {
+      val[base + lane] = va[e];
+      if (d == 0) D[0] = va[e];
+    } else {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        val[9 * base + 32 * q + lane] = va[9 * e + q];
+        if (d == 0) D[q] = va[9 * e + q];
+      }
+    }
+  }
+  mask[u] = (uint8_t)m;
+  if (BS == 1) {
+    if (D[0] == 0.0) atomicOr(err, kErrZeroDiag);
+    dinv[u] = 1.0 / D[0];
+  } else {
+    double Ai[9];
+    if (!inv3(D, Ai)) atomicOr(err, kErrZeroDiag);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) dinv[9 * u + q] = Ai[q];
+  }
+}
+
+__global__ void k_uniform_slice_ptr(int64_t nslices, int W, int64_t* slice_ptr) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s <= nslices) slice_ptr[s] = 32ll * W * s;
+}
 
 // one warp per slice: validate rows, record rowlen, slice width (in slots * 32)
 __global__ void k_slice_width(int64_t nslices, int seg_units, int spg, const int64_t* __restrict__ rp,
@@ -197,10 +272,58 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
     goto fail;
   }
   A.maxw = h_maxw;
-  CK(dalloc((void**)&A.col, sizeof(int32_t) * A.nslots, s));
-  CK(dalloc((void**)&A.val, sizeof(double) * A.nslots * bb, s));
   CK(dalloc((void**)&A.dinv, sizeof(double) * n * bb, s));
   {
+    // ---- stencil detection: candidate offsets = those of the first longest row
+    const char* no_st = getenv("LC_DISABLE_STENCIL");
+    if (h_maxw <= kMaxOff && !(no_st && no_st[0] == '1')) {
+      int big = INT32_MAX;
+      CKC(cudaMemcpyAsync((char*)t_err + 12, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+      unsigned nb = (unsigned)((n + 255) / 256);
+      k_first_maxrow<<<nb, 256, 0, s>>>(n, d_rp, h_maxw, (int*)((char*)t_err + 12));
+      count_launch();
+      int best = 0;
+      int64_t k0 = 0;
+      int32_t cols[kMaxOff];
+      CKC(cudaMemcpyAsync(&best, (char*)t_err + 12, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CKC(cudaStreamSynchronize(s));
+      CKC(cudaMemcpyAsync(&k0, d_rp + best, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      CKC(cudaStreamSynchronize(s));
+      CKC(cudaMemcpyAsync(cols, d_ci + k0, sizeof(int32_t) * h_maxw, cudaMemcpyDeviceToHost, s));
+      CKC(cudaStreamSynchronize(s));
+      Offsets O;
+      O.W = h_maxw;
+      for (int k = 0; k < kMaxOff; ++k) O.off[k] = k < h_maxw ? cols[k] - best : 0;
+      k_check_stencil<<<nb, 256, 0, s>>>(n, d_rp, d_ci, O, (unsigned*)t_err);
+      count_launch();
+      CKC(cudaMemcpyAsync(&h_err, t_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+      CKC(cudaStreamSynchronize(s));
+      if (!(h_err & kErrNotStencil)) {
+        A.stencil = 1;
+        for (int k = 0; k < kMaxOff; ++k) A.off[k] = O.off[k];
+        A.nslots = 32ll * h_maxw * A.nslices;
+        CK(dalloc((void**)&A.val, sizeof(double) * A.nslots * bb, s));
+        CK(dalloc((void**)&A.mask, n, s));
+        CKC(cudaMemsetAsync(A.val, 0, sizeof(double) * A.nslots * bb, s));
+        k_uniform_slice_ptr<<<(unsigned)((A.nslices + 256) / 256), 256, 0, s>>>(A.nslices, h_maxw, A.slice_ptr);
+        count_launch();
+        if (block == 1)
+          k_fill_stencil<1><<<nb, 256, 0, s>>>(n, M->seg_units, spg, d_rp, d_ci, d_va, O, A.val, A.mask, A.dinv,
+                                               (unsigned*)t_err);
+        else
+          k_fill_stencil<3><<<nb, 256, 0, s>>>(n, M->seg_units, spg, d_rp, d_ci, d_va, O, A.val, A.mask, A.dinv,
+                                               (unsigned*)t_err);
+        count_launch();
+        CKC(cudaGetLastError());
+      } else {
+        h_err = 0;
+        CKC(cudaMemsetAsync(t_err, 0, sizeof(unsigned), s));
+      }
+    }
+  }
+  if (!A.stencil) {
+    CK(dalloc((void**)&A.col, sizeof(int32_t) * A.nslots, s));
+    CK(dalloc((void**)&A.val, sizeof(double) * A.nslots * bb, s));
     unsigned blocks = (unsigned)((A.nslices * 32 + 255) / 256);
     if (block == 1)
       k_fill<1><<<blocks, 256, 0, s>>>(A.nslices, M->seg_units, spg, d_rp, d_ci, d_va, A.slice_ptr, A.col, A.val,
@@ -243,8 +366,13 @@ fail:
 }
 
 extern "C" lc_status lc_matrix_info(lc_matrix A, int64_t* n_unknowns, int64_t* nnz, int32_t* batch,
-                                    int64_t* nslices, int32_t* max_row) {
+                                    int64_t* nslices, int32_t* max_row, int32_t* layout, int64_t* matrix_bytes) {
   if (!A) { set_error("lc_matrix_info: NULL handle"); return LC_ERR_INVALID_ARG; }
+  const int bb = A->block * A->block;
+  if (layout) *layout = A->A.stencil ? LC_LAYOUT_STENCIL : LC_LAYOUT_SELL;
+  if (matrix_bytes)
+    *matrix_bytes = A->A.stencil ? (int64_t)8 * bb * A->A.nslots
+                                 : (int64_t)(8 * bb + 4) * A->A.nslots + 8 * (A->A.nslices + 1) + 8 * A->A.nslices;
   if (n_unknowns) *n_unknowns = A->n * A->block;
   if (nnz) *nnz = A->nnz * A->block * A->block;
   if (batch) *batch = A->batch;

@@ -1,10 +1,11 @@
 // solve.cu -- lc_solve_local / lc_solve_global: dispatch to the persistent
 // Krylov kernels (pcg.cu, gmres.cu).
+#include <algorithm>
+
 #include "lc_internal.cuh"
 
 namespace lc {
-lc_status run_pcg(const Sell& M, const double* b, double* x, const int32_t* scatter_idx, double* x_full,
-                  const double* x_init, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info);
+lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info);
 lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* scatter_idx, double* x_full,
                     const double* x_init, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info);
 
@@ -24,8 +25,14 @@ static lc_status check_params(const lc_solver_params* p) {
 }
 
 static lc_status run(const Sell& M, const double* b, double* x, const int32_t* scatter_idx, double* x_full,
-                     const double* x_init, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
-  if (p->method == LC_PCG) return run_pcg(M, b, x, scatter_idx, x_full, x_init, p, s, info);
+                     const double* x_init, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info,
+                     int reg_units, int spg) {
+  if (p->method == LC_PCG) {
+    PcgJob job;
+    job.M = &M; job.b = b; job.x = x; job.x_init = x_init; job.scatter_idx = scatter_idx; job.x_full = x_full;
+    job.reg_units = reg_units; job.spg = spg;
+    return run_pcg(job, p, s, info);
+  }
   return run_gmres(M, b, x, scatter_idx, x_full, x_init, p, s, info);
 }
 }  // namespace lc
@@ -42,7 +49,20 @@ extern "C" lc_status lc_solve_local(lc_sub S, const lc_solver_params* p, double*
       for (int g = 0; g < S->nseg; ++g) info[g] = lc_solve_info{0, LC_OK, 0.0, 0.0};
     return LC_OK;
   }
-  return run(S->B, S->bsub, nullptr, S->idx, x, S->xB0, p, (cudaStream_t)stream, info);
+  if (S->masked) {
+    if (p->method != LC_PCG) {
+      set_error("lc_solve_local: GMRES on a masked (stencil, block = 1) subsystem is not supported");
+      return LC_ERR_INVALID_ARG;
+    }
+    const lc_matrix_s* A = S->A;
+    PcgJob job;
+    job.M = &A->A; job.b = S->bs; job.x_init = S->xm0; job.slist = S->slist; job.nlist_dev = S->nlist;
+    job.nlist_max = std::min<int64_t>(A->A.nslices, S->K_units);
+    job.omega = S->omega; job.x_user = x;
+    job.reg_units = A->seg_units; job.spg = (A->seg_units + 31) / 32;
+    return run_pcg(job, p, (cudaStream_t)stream, info);
+  }
+  return run(S->B, S->bsub, nullptr, S->idx, x, S->xB0, p, (cudaStream_t)stream, info, 0, 0);
 }
 
 extern "C" lc_status lc_solve_global(lc_matrix A, const double* b, double* x, const lc_solver_params* p, void* stream,
@@ -50,5 +70,6 @@ extern "C" lc_status lc_solve_global(lc_matrix A, const double* b, double* x, co
   if (!A || !b || !x) { set_error("lc_solve_global: null argument"); return LC_ERR_INVALID_ARG; }
   lc_status st = check_params(p);
   if (st) return st;
-  return run(A->A, b, x, nullptr, nullptr, nullptr, p, (cudaStream_t)stream, info);
+  return run(A->A, b, x, nullptr, nullptr, nullptr, p, (cudaStream_t)stream, info, A->seg_units,
+             (A->seg_units + 31) / 32);
 }

@@ -71,7 +71,7 @@ def load_library(path: str = LIB_PATH):
     lib.lc_extract_sub.argtypes = [P, P, P, P, P, ctypes.POINTER(P)]
     lib.lc_solve_local.argtypes = [P, ctypes.POINTER(SolverParams), P, P, P]
     lib.lc_solve_global.argtypes = [P, P, P, ctypes.POINTER(SolverParams), P, P]
-    lib.lc_matrix_info.argtypes = [P, P, P, P, P, P]
+    lib.lc_matrix_info.argtypes = [P, P, P, P, P, P, P, P]
     for f in ("lc_create_csr", "lc_select_domain", "lc_domain_export", "lc_extract_sub", "lc_solve_local",
               "lc_solve_global", "lc_matrix_info"):
         getattr(lib, f).restype = ctypes.c_int
@@ -135,10 +135,12 @@ class Matrix:
         return self.n_units * self.block
 
     def info(self):
-        vals = [ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32()]
+        vals = [ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32(),
+                ctypes.c_int32(), ctypes.c_int64()]
         _check(_lib.lc_matrix_info(self.h, *[ctypes.byref(v) for v in vals]), "lc_matrix_info")
         return dict(N=vals[0].value, nnz=vals[1].value, batch=vals[2].value, nslices=vals[3].value,
-                    max_row=vals[4].value)
+                    max_row=vals[4].value, layout="stencil" if vals[5].value == 1 else "sell",
+                    matrix_bytes=vals[6].value)
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:

