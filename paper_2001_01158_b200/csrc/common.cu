@@ -276,8 +276,8 @@ void lc_domain_s::release(cudaStream_t s) {
 void lc_sub_s::release(cudaStream_t s) {
   B.release(s);
   lc::dfree(idx, s); lc::dfree(bsub, s); lc::dfree(xB0, s);
-  lc::dfree(bs, s); lc::dfree(xm0, s); lc::dfree(omega, s); lc::dfree(slist, s); lc::dfree(nlist, s);
-  idx = nullptr; bsub = xB0 = nullptr; bs = xm0 = nullptr; omega = nullptr; slist = nullptr; nlist = nullptr;
+  lc::dfree(bs, s); lc::dfree(xm0, s); lc::dfree(omega, s); lc::dfree(slist, s); lc::dfree(nlist, s); lc::dfree(lseg, s);
+  idx = nullptr; bsub = xB0 = nullptr; bs = xm0 = nullptr; omega = nullptr; slist = nullptr; nlist = nullptr; lseg = nullptr;
 }
 
 extern "C" const char* lc_last_error(void) { return lc::g_err.c_str(); }

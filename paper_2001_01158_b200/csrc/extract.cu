@@ -117,6 +117,20 @@ __global__ void __launch_bounds__(kTB) k_bsub_masked(SellView A, int seg_units, 
   sflag[s] = 0;
 }
 
+// lseg[g] = first position in the ascending slice list with slice >= g * spg (segment runs)
+__global__ void k_seg_list_start(const int32_t* __restrict__ slist, const int64_t* __restrict__ nlist, int G,
+                                 int spg, int64_t* lseg) {
+  int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g > G) return;
+  int64_t lo = 0, hi = *nlist;
+  int64_t key = (int64_t)g * spg;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (slist[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  lseg[g] = lo;
+}
+
 }  // namespace lc
 
 using namespace lc;
@@ -176,6 +190,10 @@ extern "C" lc_status lc_extract_sub(lc_matrix M, lc_domain D, const double* b, c
       count_launch();
       CKC(cudaGetLastError());
       CK(compact_flags(sflag, nsA, S->slist, sinv, S->nlist, s));
+      CK(dalloc((void**)&S->lseg, sizeof(int64_t) * (G + 1), s));
+      k_seg_list_start<<<(G + 1 + 63) / 64, 64, 0, s>>>(S->slist, S->nlist, G, spg, S->lseg);
+      count_launch();
+      CKC(cudaGetLastError());
     }
     dfree(t, s);
     *out = S;

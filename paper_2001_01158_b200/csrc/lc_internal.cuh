@@ -54,6 +54,7 @@ struct PcgJob {
   const double* x_init = nullptr; // else: solve on a workspace copy of x_init
   const int32_t* slist = nullptr; // optional active-slice list, device count at nlist_dev
   const int64_t* nlist_dev = nullptr;
+  const int64_t* lseg = nullptr;  // [G+1] start of each segment's run in slist
   int64_t nlist_max = 0;          // host upper bound of the list length
   const uint8_t* omega = nullptr; // masked solve: rows with omega[u] != 255
   const int32_t* scatter_idx = nullptr;  // explicit local solve: x_full[scatter_idx[l]] = x[l]
@@ -179,6 +180,7 @@ struct lc_sub_s {
   uint8_t* omega = nullptr;       // [n] copy of the domain flags (255 = outside Omega)
   int32_t* slist = nullptr;       // active slices of A (ascending), count at *nlist
   int64_t* nlist = nullptr;
+  int64_t* lseg = nullptr;        // [nseg+1] start of segment g's slices in slist
   // explicit representation (otherwise)
   lc::Sell B;               // K_units rows/cells, segments = ranks [seg_base[g], seg_base[g+1])
   int32_t* idx = nullptr;   // [K_units] global units (owned copy)

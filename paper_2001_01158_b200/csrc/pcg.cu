@@ -59,6 +59,7 @@ struct PcgArgs {
   const int32_t* slist;         // optional active slices (ascending)
   const int64_t* nlist;         // device count of slist
   const uint8_t* omega;         // optional: unit u is a row of the subsystem iff omega[u] != 255
+  const int64_t* seg_j0;        // [G+1] start of each segment's run in the slice space (list or slices)
   const int32_t* scatter_idx;   // explicit local solve: x_full[scatter_idx[l]] = x[l] at exit
   double* x_full;
   double* x_user;               // masked local solve: x_user[u] = x[u] for u in Omega at exit
@@ -204,12 +205,16 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   __shared__ double s_red[kPW][2];
   __shared__ double s_sum[kMaxSeg][2];
   __shared__ int s_exit;
+  __shared__ long long s_segj0[kMaxSeg + 1];   // segment runs in slice space
+  __shared__ int s_act[kMaxSeg + 1];           // active segments of the current pass (+ sentinel)
+  __shared__ long long s_actj[kMaxSeg + 1];    // their runs concatenated
   const SellView& A = P.A;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nCTA = gridDim.x, bid = blockIdx.x;
   const int G = P.G;
   const int64_t j0 = bid * kPW + warp, jstep = nCTA * kPW;
   const int64_t jlim = P.slist ? *P.nlist : A.nslices;
+  for (int g = threadIdx.x; g <= G; g += kPT) s_segj0[g] = P.seg_j0[g];
   if (threadIdx.x < kMaxSeg) {
     S[threadIdx.x].mode = M_INIT; S[threadIdx.x].par = 0; S[threadIdx.x].it = 0; S[threadIdx.x].final_ = 0;
     S[threadIdx.x].beta = 0.0; S[threadIdx.x].alpha = 0.0; S[threadIdx.x].rho = 0.0;
@@ -287,6 +292,26 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
     }
   };
   auto in_omega = [&](int64_t u) -> bool { return !P.omega || P.omega[u] != 255; };
+  // G > 1: the slice space of a pass = the runs of the segments active in that pass, concatenated, so all
+  // warps share the remaining groups' work once others have converged.  Returns the total length.
+  auto build_active = [&](int pass) -> int64_t {
+    if (threadIdx.x == 0) {
+      long long J = 0;
+      int na = 0;
+      for (int g = 0; g < G; ++g) {
+        int md = S[g].mode;
+        bool act = pass == 0 ? (md == M_INIT || md == M_CONFIRM || md == M_FIRST || md == M_NORMAL)
+                             : (md == M_UPDATE || md == M_RESET);
+        if (act) { s_act[na] = g; s_actj[na] = J; J += s_segj0[g + 1] - s_segj0[g]; ++na; }
+      }
+      s_actj[na] = J;
+      s_act[na] = G;
+    }
+    __syncthreads();
+    int na = 0;
+    while (s_act[na] != G) ++na;
+    return s_actj[na];
+  };
 
 #ifdef LC_DEBUG_TIMELINE
   int tlk = 0;
@@ -309,12 +334,15 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
         pass_a_loop<WM, ST, 2>(P, j0, jlim, jstep, lane, false, beta, pold, pnew, a0, a1);
       flush(0, a0, a1);
     } else {
-      int gcur = -1, mode = M_DONE;
+      const int64_t J = build_active(0);
+      int gcur = -1, mode = M_DONE, ka = 0;
       double a0 = 0.0, a1 = 0.0, beta = 0.0;
       const double* pold = nullptr;
       double* pnew = nullptr;
-      for (int64_t j = j0; j < jlim; j += jstep) {
-        const int64_t s = P.slist ? (int64_t)P.slist[j] : j;
+      for (int64_t j = j0; j < J; j += jstep) {
+        while (s_actj[ka + 1] <= j) ++ka;
+        const int64_t jj = s_segj0[s_act[ka]] + (j - s_actj[ka]);
+        const int64_t s = P.slist ? (int64_t)P.slist[jj] : jj;
         int g;
         int64_t row0, end;
         slice_map(P, s, g, row0, end);
@@ -442,11 +470,19 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       }
       flush(0, a0, a1);
     } else {
-      int gcur = -1, mode = M_DONE;
+      const int64_t J = G == 1 ? jlim : build_active(1);
+      int gcur = -1, mode = M_DONE, ka = 0;
       double a0 = 0.0, a1 = 0.0, alpha = 0.0;
       const double* pp = nullptr;
-      for (int64_t j = j0; j < jlim; j += jstep) {
-        const int64_t s = P.slist ? (int64_t)P.slist[j] : j;
+      for (int64_t j = j0; j < J; j += jstep) {
+        int64_t s;
+        if (G == 1) {
+          s = P.slist ? (int64_t)P.slist[j] : j;
+        } else {
+          while (s_actj[ka + 1] <= j) ++ka;
+          const int64_t jj = s_segj0[s_act[ka]] + (j - s_actj[ka]);
+          s = P.slist ? (int64_t)P.slist[jj] : jj;
+        }
         int g;
         int64_t row0, end;
         slice_map(P, s, g, row0, end);
@@ -583,6 +619,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   a.slist = job.slist;
   a.nlist = job.nlist_dev;
   a.omega = job.omega;
+  a.seg_j0 = job.slist ? job.lseg : M.seg_slice0;
   a.scatter_idx = job.scatter_idx;
   a.x_full = job.x_full;
   a.x_user = job.x_user;
