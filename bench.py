@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="grid override (testing only)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gs", type=int, default=0, help="Gauss-Seidel sweeps of Alg. 1 l.7 (paper: 1; parity path: 0)")
     return ap.parse_args()
 
 
@@ -180,7 +181,8 @@ def run_lc(args):
         A = lc.Matrix(sy0.nrows, inp["rp"], inp["ci"], inp["val"], block=sy0.block, batch=sy0.batch)
         nsolves = 0
         for name, rule in rules:
-            x, rep = lc.local_method(A, inp["b"], inp["x0"], rule, method=method, rel_tol=EPS)
+            x, rep = lc.local_method(A, inp["b"], inp["x0"], rule, method=method, rel_tol=EPS,
+                                     gs_sweeps=args.gs if rule is not None else 0)
             nsolves += sy0.batch
             if out_x is not None:
                 out_x.append(x)

@@ -161,6 +161,15 @@ lc_status lc_solve_global(lc_matrix A, const double* b, double* x, const lc_solv
 enum { LC_LAYOUT_SELL = 0     /* SELL-32 with explicit int32 column per slot (12 B per slot) */,
        LC_LAYOUT_STENCIL = 1  /* every row's column offsets lie in one sorted set of <= 8 offsets: values only,
                                  slot k = column row + off[k] (zero "holes" where a row lacks it), 8 B per slot */ };
+/*
+ * Alg. 1 l.7 (one sweep in the paper's runs): `sweeps` forward Gauss-Seidel sweeps
+ * in natural row order on A x = b, in place on x (device [n]): x_i <- (b_i - sum_{j != i} a_ij x_j) / a_ii
+ * with the sum over stored j != i in ascending order (R22), j < i already updated.  Bit-exact with
+ * the sequential definition.  Needs block = 1, rows of at most 16 entries and a structurally
+ * symmetric pattern (LC_ERR_PATTERN otherwise).  Syncs `stream`.
+ */
+lc_status lc_smooth_gs(lc_matrix A, const double* b, double* x, int32_t sweeps, void* stream);
+
 /* introspection (host outputs, each optional): unknowns n*block, stored scalars, batch, SELL slices, max row
    length (slots), layout (LC_LAYOUT_*), bytes one SpMV streams for the matrix (values + columns + metadata) */
 lc_status lc_matrix_info(lc_matrix A, int64_t* n_unknowns, int64_t* nnz, int32_t* batch, int64_t* nslices,

@@ -43,7 +43,7 @@ class Trace(ctypes.Structure):
 
 class SolverParams(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int32), ("bs", ctypes.c_int32), ("restart", ctypes.c_int32),
-                ("eps", ctypes.c_double), ("max_iters", ctypes.c_int32)]
+                ("eps", ctypes.c_double), ("max_iters", ctypes.c_int32), ("gs_sweeps", ctypes.c_int32)]
 
 
 class Report(ctypes.Structure):
@@ -72,6 +72,8 @@ def _load():
         lib.or_assemble.argtypes = [I64, P, P, P]
         lib.or_pcg.argtypes = [I64, P, P, P, P, P, D, I32, P, P]
         lib.or_gmres_bj.argtypes = [I64, P, P, P, I32, P, P, D, I32, I32, P, P]
+        lib.or_gauss_seidel.argtypes = [I64, P, P, P, P, P, I32]
+        lib.or_gauss_seidel.restype = I32
         lib.or_local_method.argtypes = [I64, P, P, P, P, P, ctypes.POINTER(DomainParams),
                                         ctypes.POINTER(SolverParams), P, ctypes.POINTER(Report)]
         for f in ("or_select_domain", "or_extract", "or_pcg", "or_gmres_bj", "or_local_method"):
@@ -223,6 +225,15 @@ def gmres_bj(A: Csr, b, x0, bs=3, eps=1e-10, restart=30, max_iters=3000):
     st = _load().or_gmres_bj(A.n, _p(A.rp), _p(A.ci), _p(A.val), bs, _p(b), _p(x), eps, restart, max_iters,
                              _p(it), _p(rr))
     return x, int(it[0]), st, float(rr[0])
+
+
+def gauss_seidel(A: Csr, b, x, sweeps=1):
+    """Alg. 1 l.7: forward natural-order Gauss-Seidel sweeps (returns a new vector)."""
+    b = _c(b, np.float64); y = np.array(x, dtype=np.float64, copy=True)
+    st = _load().or_gauss_seidel(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(b), _p(y), sweeps)
+    if st != 0:
+        raise ValueError(f"or_gauss_seidel status {st}")
+    return y
 
 
 def local_method(A: Csr, b, x0, domain: DomainParams | None, solver: SolverParams):

@@ -521,7 +521,29 @@ done:
 }
 
 /* ------------------------------------------------------------------------ */
-/* Alg. 1 end to end (lines 2-6 and 8-11; line 7 GS smoothing = 0 sweeps, R8) */
+/* Alg. 1 l.7: Gauss-Seidel smoothing of x~ (NEXT-1)       */
+/* ------------------------------------------------------------------------ */
+
+/* `sweeps` forward Gauss-Seidel sweeps in natural row order, in place:
+   x_i <- (b_i - sum_{j != i} a_ij x_j) / a_ii, the sum the R22 fma chain over stored j != i ascending
+   (j < i already updated in this sweep, j > i from the previous one).  SPEC S:145-153. */
+int or_gauss_seidel(int64_t n, const int64_t* rp, const int32_t* ci, const double* a, const double* b, double* x,
+                    int sweeps) {
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int64_t i = 0; i < n; ++i) {
+      double acc = 0.0, d = 0.0;
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+        if (ci[k] == i) { d = a[k]; continue; }
+        acc = fma(a[k], x[ci[k]], acc);
+      }
+      if (d == 0.0) return OR_ERR_ZERO_DIAGONAL;
+      x[i] = (b[i] - acc) / d;
+    }
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Alg. 1 end to end (lines 2-11; line 7 = gs_sweeps Gauss-Seidel sweeps, R8) */
 /* ------------------------------------------------------------------------ */
 
 typedef struct {
@@ -530,6 +552,7 @@ typedef struct {
   int32_t restart;    /* GMRES(m) */
   double eps;         /* Eq. 6 tolerance */
   int32_t max_iters;
+  int32_t gs_sweeps;  /* Alg. 1 l.7 smoothing sweeps before the convergence check (0 on the parity path) */
 } or_solver_params;
 
 typedef struct {
@@ -587,6 +610,10 @@ int or_local_method(int64_t n, const int64_t* rp, const int32_t* ci, const doubl
       free(idx); free(Brp); free(Bci); free(Ba); free(bsub); free(xB);
     }
     free(flag);
+    if (sp->gs_sweeps > 0) {                                                                 /* l.7 */
+      st = or_gauss_seidel(n, rp, ci, a, b, x, sp->gs_sweeps);
+      if (st != OR_OK) return st;
+    }
   }
   double t3 = now_s();
   st = solve(n, rp, ci, a, b, x, sp, &rep->it_global, &rep->relres_global);                  /* l.8-11 */

@@ -1,0 +1,145 @@
+// gs.cu -- lc_smooth_gs: forward Gauss-Seidel sweeps in natural row order (Alg. 1 l.7, P:381-382;
+// one sweep in the paper's runs), bit-exact with the sequential oracle.
+//
+// Natural-order GS is a sparse triangular sweep: row i needs the NEW values of its lower neighbours
+// (j < i) and the OLD values of its upper neighbours.  The sweep runs sync-free:
+//   - warps claim 32-row slices in increasing order from an atomic counter (dynamic ids => a warp
+//     only ever waits on slices claimed before it, which are running: forward progress);
+//   - lower neighbours in earlier slices are waited for on per-slice flags (ld.acquire / st.release);
+//   - upper neighbours are read before the slice writes anything (a structurally symmetric pattern
+//     guarantees that any later row coupled to this slice waits for its flag, so they are still old);
+//   - dependencies inside the slice are resolved by stepping through the 32 lanes in order, the new
+//     values passed through shared memory.
+// Each row evaluates exactly the oracle's expression: acc = fma chain over stored j != i ascending,
+// x_i = (b_i - acc) / a_ii.
+#include <algorithm>
+#include <cstdint>
+
+#include "lc_internal.cuh"
+
+namespace lc {
+
+constexpr int kGST = 256;
+constexpr int kGSW = kGST / 32;
+constexpr int kGSMaxW = 16;   // slots gathered per row in registers (wider rows take the generic path)
+
+template <int ST>
+__global__ void __launch_bounds__(kGST) k_gs_sweep(SellView A, int reg_units, int spg, const double* __restrict__ b,
+                                                   double* x, unsigned* flags, unsigned sweep, unsigned* counter,
+                                                   unsigned* err) {
+  __shared__ double xs[kGSW][32];
+  __shared__ unsigned s_claim[kGSW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nu1 = A.nunits - 1;
+  for (;;) {
+    if (lane == 0) s_claim[warp] = atomicAdd(counter, 1u);
+    __syncwarp();
+    const int64_t s = s_claim[warp];
+    __syncwarp();
+    if (s >= A.nslices) break;
+    const int64_t g = s / spg;
+    const int64_t row0 = g * reg_units + 32 * (s - g * spg), end = (g + 1) * reg_units;
+    const int64_t u = row0 + lane;
+    const bool valid = u < end;
+    const int64_t pl = (ST ? 32ll * A.W * s : A.slice_ptr[s]) + lane;
+    const int w = ST ? A.W : (int)((A.slice_ptr[s + 1] - (pl - lane)) >> 5);
+    double av[kGSMaxW], yv[kGSMaxW];
+    int64_t cv[kGSMaxW];
+    double d = 0.0;
+    // ---- phase 1: gather operands (wait for lower slices; read upper values before any write)
+    if (valid) {
+      for (int k = 0; k < w && k < kGSMaxW; ++k) {
+        bool real = sv_real(A, k, u);
+        int64_t c = real ? sv_col(A, pl, k, u) : u;
+        cv[k] = real ? c : -1;
+        av[k] = A.val[pl + 32ll * k];
+        yv[k] = 0.0;
+        if (!real) continue;
+        if (c == u) { d = av[k]; continue; }
+        if (c < row0) {                                   // lower neighbour in an earlier slice: wait
+          const int64_t sc = (c - g * reg_units) / 32 + g * spg;
+          unsigned spins = 0;
+          while (ld_acquire_u32(&flags[sc]) != sweep) {
+            if (++spins > (1u << 22)) { atomicOr(err, 1u); break; }
+          }
+          yv[k] = __ldcg(x + c);                          // L2 (coherent), not a possibly stale L1 line
+        } else if (c > u) {
+          yv[k] = x[c];                                   // upper neighbour: old value
+        }
+      }
+    }
+    __syncwarp();
+    // ---- phase 2: lanes in order; intra-slice lower neighbours come from xs (this sweep's values)
+    for (int t = 0; t < 32; ++t) {
+      if (lane == t && valid) {
+        double acc = 0.0;
+        for (int k = 0; k < w && k < kGSMaxW; ++k) {
+          const int64_t c = cv[k];
+          if (c < 0 || c == u) continue;
+          double y = (c >= row0 && c < u) ? xs[warp][c - row0] : yv[k];
+          acc = __fma_rn(av[k], y, acc);
+        }
+        double xn = (b[u] - acc) / d;
+        xs[warp][lane] = xn;
+        x[u] = xn;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      __threadfence();
+      st_release_u32(&flags[s], sweep);
+    }
+    __syncwarp();
+    (void)nu1;
+  }
+}
+
+}  // namespace lc
+
+using namespace lc;
+
+extern "C" lc_status lc_smooth_gs(lc_matrix M, const double* b, double* x, int32_t sweeps, void* stream) {
+  if (!M || !b || !x || sweeps < 0) { set_error("lc_smooth_gs: null argument or sweeps < 0"); return LC_ERR_INVALID_ARG; }
+  if (M->block != 1) { set_error("lc_smooth_gs: needs block = 1"); return LC_ERR_INVALID_ARG; }
+  if (M->A.maxw > kGSMaxW) { set_error("lc_smooth_gs: rows longer than 16 entries are not supported"); return LC_ERR_PATTERN; }
+  if (M->A.stencil) {   // structural symmetry of the stencil: the offset set must be symmetric
+    for (int k = 0; k < M->A.maxw; ++k) {
+      bool found = false;
+      for (int l = 0; l < M->A.maxw; ++l) found |= (M->A.off[l] == -M->A.off[k]);
+      if (!found) { set_error("lc_smooth_gs: pattern must be structurally symmetric"); return LC_ERR_PATTERN; }
+    }
+  }
+  if (sweeps == 0) return LC_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const Sell& A = M->A;
+  void* ws = nullptr;
+  const size_t fbytes = sizeof(unsigned) * (size_t)(A.nslices + 1);
+  lc_status st = dalloc(&ws, fbytes + 64 * (sweeps + 1), s);
+  if (st) return st;
+  unsigned* flags = (unsigned*)ws;
+  unsigned* counters = (unsigned*)((char*)ws + ((fbytes + 63) & ~(size_t)63));
+  unsigned* err = counters + 16 * sweeps;
+  LC_CUDA(cudaMemsetAsync(ws, 0, fbytes + 64 * (sweeps + 1), s));
+  const int spg = (M->seg_units + 31) / 32;
+  int per_sm = 0;
+  void* fn = A.stencil ? (void*)k_gs_sweep<1> : (void*)k_gs_sweep<0>;
+  LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGST, 0));
+  int64_t nCTA = std::min<int64_t>((int64_t)std::max(per_sm, 1) * num_sms(), (A.nslices + kGSW - 1) / kGSW);
+  if (nCTA < 1) nCTA = 1;
+  SellView V = view(A);
+  for (int sw = 1; sw <= sweeps; ++sw) {
+    if (A.stencil)
+      k_gs_sweep<1><<<(unsigned)nCTA, kGST, 0, s>>>(V, M->seg_units, spg, b, x, flags, (unsigned)sw,
+                                                    counters + 16 * (sw - 1), err);
+    else
+      k_gs_sweep<0><<<(unsigned)nCTA, kGST, 0, s>>>(V, M->seg_units, spg, b, x, flags, (unsigned)sw,
+                                                    counters + 16 * (sw - 1), err);
+    LC_LAUNCHED();
+  }
+  unsigned h_err = 0;
+  LC_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  dfree(ws, s);
+  LC_CUDA(cudaStreamSynchronize(s));
+  if (h_err) { set_error("lc_smooth_gs: dependency wait timed out"); return LC_ERR_CUDA; }
+  return LC_OK;
+}

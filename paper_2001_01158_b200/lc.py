@@ -28,7 +28,8 @@ _STATUS = {0: "LC_OK", 1: "LC_NOT_CONVERGED", -1: "LC_ERR_INVALID_ARG", -2: "LC_
            -7: "LC_ERR_CUDA", -8: "LC_ERR_OOM"}
 
 EXPORTED = ["lc_create_csr", "lc_select_domain", "lc_domain_export", "lc_extract_sub", "lc_solve_local",
-            "lc_solve_global", "lc_matrix_info", "lc_destroy_matrix", "lc_destroy_domain", "lc_destroy_sub",
+            "lc_solve_global", "lc_smooth_gs", "lc_matrix_info", "lc_destroy_matrix", "lc_destroy_domain",
+            "lc_destroy_sub",
             "lc_last_error", "lc_kernel_launches"]
 
 
@@ -72,8 +73,9 @@ def load_library(path: str = LIB_PATH):
     lib.lc_solve_local.argtypes = [P, ctypes.POINTER(SolverParams), P, P, P]
     lib.lc_solve_global.argtypes = [P, P, P, ctypes.POINTER(SolverParams), P, P]
     lib.lc_matrix_info.argtypes = [P, P, P, P, P, P, P, P]
+    lib.lc_smooth_gs.argtypes = [P, P, P, I32, P]
     for f in ("lc_create_csr", "lc_select_domain", "lc_domain_export", "lc_extract_sub", "lc_solve_local",
-              "lc_solve_global", "lc_matrix_info"):
+              "lc_solve_global", "lc_matrix_info", "lc_smooth_gs"):
         getattr(lib, f).restype = ctypes.c_int
     for f in ("lc_destroy_matrix", "lc_destroy_domain", "lc_destroy_sub"):
         getattr(lib, f).argtypes = [P]
@@ -241,8 +243,17 @@ def solve_global(A: Matrix, b: torch.Tensor, x: torch.Tensor, method=PCG, rel_to
     return _infos(info)
 
 
-def local_method(A: Matrix, b, x0, domain: dict | None, method=PCG, rel_tol=1e-10, max_iters=20000, restart=30):
-    """Alg. 1 composed from the five C-ABI calls (domain=None: method0).  Returns (x, report dict)."""
+def smooth_gs(A: Matrix, b: torch.Tensor, x: torch.Tensor, sweeps=1):
+    """Alg. 1 l.7: forward natural-order Gauss-Seidel sweeps on x, in place."""
+    _check(_lib.lc_smooth_gs(A.h, _dptr(b, torch.float64, A.N), _dptr(x, torch.float64, A.N), sweeps, _stream()),
+           "lc_smooth_gs", ok=(LC_OK,))
+
+
+def local_method(A: Matrix, b, x0, domain: dict | None, method=PCG, rel_tol=1e-10, max_iters=20000, restart=30,
+                 gs_sweeps=0):
+    """Alg. 1 composed from the C-ABI calls (domain=None: method0): domain (l.2), extraction (l.3-4),
+    local solve + assembly (l.5-6), gs_sweeps Gauss-Seidel sweeps (l.7), global solve (l.8-11).
+    Returns (x, report dict)."""
     x = x0.clone()
     rep = {"K": [0] * A.batch}
     if domain is not None:
@@ -251,5 +262,7 @@ def local_method(A: Matrix, b, x0, domain: dict | None, method=PCG, rel_tol=1e-1
         if sum(dom.K) > 0:
             sub = extract_sub(A, dom, b, x0)
             rep["local"] = solve_local(sub, x, method, rel_tol, max_iters, restart)
+        if gs_sweeps > 0:
+            smooth_gs(A, b, x, gs_sweeps)
     rep["global"] = solve_global(A, b, x, method, rel_tol, max_iters, restart)
     return x, rep

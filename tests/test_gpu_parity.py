@@ -386,3 +386,48 @@ def test_irregular_pattern_uses_general_layout():
     xo, it, st, _ = orc.pcg(Ao, b, np.zeros(n))
     assert info[0]["status"] == 0 and abs(info[0]["iterations"] - it) <= 1
     assert np.linalg.norm(x.cpu().numpy() - xo) / np.linalg.norm(xo) <= 1e-9
+
+
+# ------------------------------------------------- NEXT-1: Gauss-Seidel smoothing --
+
+@pytest.mark.parametrize("case", ["c1", "c5", "c3", "band", "general", "sweeps3"])
+def test_gs_sweep_bitexact(case, monkeypatch):
+    """lc_smooth_gs reproduces the sequential natural-order sweep of the oracle bit for bit."""
+    sweeps = 1
+    if case == "c1":
+        sy = synth.system(1, 5)
+    elif case == "c5":
+        sy = synth.system(5, 5, n=20)
+    elif case == "c3":
+        sy = synth.system(3, 5, n=30, G=4)
+    elif case == "band":
+        sy = synth.random_system(1000, bw=3, spd=True, seed=77)
+    elif case == "general":
+        monkeypatch.setenv("LC_DISABLE_STENCIL", "1")
+        sy = synth.system(5, 2, n=18)
+    else:
+        sy = synth.system(1, 2, n=40)
+        sweeps = 3
+    A = gpu_matrix(sy)
+    x = to_dev(sy.x0)
+    lc.smooth_gs(A, to_dev(sy.b), x, sweeps)
+    Ao = oracle_csr(sy)
+    xo = orc.gauss_seidel(Ao, sy.b, sy.x0, sweeps)
+    np.testing.assert_array_equal(x.cpu().numpy(), xo)
+
+
+@pytest.mark.parametrize("cfg,n,s", [(1, 64, 3), (5, 20, 4), (3, 30, 2)])
+def test_local_method_with_gs_parity(cfg, n, s):
+    """Alg. 1 with the paper's one GS sweep vs the oracle's Alg. 1 with gs_sweeps = 1."""
+    sy = synth.system(cfg, s, n=n, G=4)
+    rule = RULES[cfg][0]
+    Ao = oracle_csr(sy)
+    A = gpu_matrix(sy)
+    x, rep = lc.local_method(A, to_dev(sy.b), to_dev(sy.x0), rule, gs_sweeps=1)
+    xg = x.cpu().numpy()
+    for g, (r0, r1) in enumerate(segments(sy)):
+        As = Ao.segment(r0, r1) if sy.batch > 1 else Ao
+        sp = orc.SolverParams(0, 1, 30, EPS, 20000, 1)
+        xo, _, ro = orc.local_method(As, sy.b[r0:r1], sy.x0[r0:r1], oracle_dp(rule, 1), sp)
+        assert abs(rep["global"][g]["iterations"] - ro.it_global) <= 1
+        assert np.linalg.norm(xg[r0:r1] - xo) / np.linalg.norm(xo) <= 1e-9

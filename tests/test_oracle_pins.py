@@ -119,7 +119,7 @@ def test_example1_local_solve_annihilates_and_skips_global():
     g, A, x, x0, b = example1()
     Ac = orc.Csr.from_dense(A)
     dp = orc.DomainParams(orc.CRIT_RESIDUAL, orc.THR_PAPER, 1e-5, 6, 0, 1)
-    sp = orc.SolverParams(0, 1, 30, 1e-5, 20000)
+    sp = orc.SolverParams(0, 1, 30, 1e-5, 20000, 0)
     xs, flag, rep = orc.local_method(Ac, b, x0, dp, sp)
     assert rep.K == 6 and rep.it_global == 0 and rep.st_global == 0
     assert rep.it_local <= 6                      # CG: at most K distinct eigenvalues
@@ -380,7 +380,7 @@ def test_full_domain_reduces_to_global_solve():
     """BASELINE.json invariant: Omega_local = Omega => the local method returns method0's result
     bitwise, with 0 global iterations."""
     sy, A = _heat()
-    sp = orc.SolverParams(0, 1, 30, 1e-10, 20000)
+    sp = orc.SolverParams(0, 1, 30, 1e-10, 20000, 0)
     x0m, _, rep0 = orc.local_method(A, sy.b, sy.x0, None, sp)
     full = orc.DomainParams(orc.CRIT_RESIDUAL, orc.THR_REL_MAX, 0.0, 0, 0, 1)
     x1, flag, rep1 = orc.local_method(A, sy.b, sy.x0, full, sp)
@@ -392,7 +392,7 @@ def test_full_domain_reduces_to_global_solve():
 def test_empty_domain_is_method0():
     """Omega = {} (x0 exact in the criterion's eyes) => x~ = x0 and the result is method0's bitwise (R12)."""
     sy, A = _heat()
-    sp = orc.SolverParams(0, 1, 30, 1e-10, 20000)
+    sp = orc.SolverParams(0, 1, 30, 1e-10, 20000, 0)
     x0m, _, _ = orc.local_method(A, sy.b, sy.x0, None, sp)
     empty = orc.DomainParams(orc.CRIT_GRADIENT, orc.THR_REL_MAX, 1.0, 0, 0, 1)
     x1, flag, rep = orc.local_method(A, sy.b, sy.x0, empty, sp)
@@ -406,7 +406,7 @@ def test_manufactured_solution_bound(cfg, n):
     ||x - x*|| <= ||b - A x|| <= 1e-10 ||b|| (R31) -- for method0 and for the local method."""
     sy = synth.system(cfg, 2, n=n, G=3)
     A = orc.Csr(sy.rp, sy.ci, sy.val)
-    sp = orc.SolverParams(0, 1, 30, 1e-10, 20000)
+    sp = orc.SolverParams(0, 1, 30, 1e-10, 20000, 0)
     segs = [(0, A.n)] if cfg != 3 else [(g * n * n, (g + 1) * n * n) for g in range(3)]
     for r0, r1 in segs:
         As = A.segment(r0, r1)
@@ -446,3 +446,54 @@ def test_cell_granular_domain():
     mark = d.flag.reshape(-1, 3)
     assert np.all(mark.min(axis=1) == mark.max(axis=1))
     np.testing.assert_array_equal(mark[~near, 0], (cells > tau)[~near])
+
+
+# ------------------------------------------------ NEXT-1: Gauss-Seidel (Alg. 1 l.7) --
+
+def test_gs_spec_2x2_hand_value():
+    """[[2,1],[1,2]], b = (3,3), x = 0, one sweep -> (1.5, 0.75) (hand recurrence)."""
+    A = orc.Csr.from_dense(np.array([[2.0, 1.0], [1.0, 2.0]]))
+    np.testing.assert_array_equal(orc.gauss_seidel(A, [3.0, 3.0], [0.0, 0.0], 1), [1.5, 0.75])
+
+
+def test_gs_identity_and_fixed_point():
+    """A = I -> x = b after one sweep; the exact solution of a tiny diagonal system is a fixed point."""
+    n = 7
+    A = orc.Csr.from_dense(np.eye(n))
+    b = np.arange(1.0, n + 1)
+    np.testing.assert_array_equal(orc.gauss_seidel(A, b, np.zeros(n)), b)
+    D = orc.Csr.from_dense(np.diag([2.0, 4.0, 8.0]))
+    np.testing.assert_array_equal(orc.gauss_seidel(D, [2.0, 4.0, 8.0], [1.0, 1.0, 1.0], 3), [1.0, 1.0, 1.0])
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_gs_vs_triangular_solve(seed):
+    """One forward sweep = (D + L)^{-1} (b - U x_old) (dense triangular solve, library routine)."""
+    import scipy.linalg
+    s = synth.random_system(25, bw=3, spd=seed % 2 == 0, seed=300 + seed)
+    A = orc.Csr(s.rp, s.ci, s.val); M = A.to_dense()
+    L = np.tril(M); U = np.triu(M, 1)
+    expect = scipy.linalg.solve_triangular(L, s.b - U @ s.x0, lower=True)
+    np.testing.assert_allclose(orc.gauss_seidel(A, s.b, s.x0, 1), expect, rtol=1e-12, atol=1e-14)
+
+
+def test_gs_decreases_energy_error():
+    """For SPD A one GS sweep does not increase the A-norm of the error (invariant)."""
+    sy = synth.system(1, 4, n=20)
+    A = orc.Csr(sy.rp, sy.ci, sy.val); M = A.to_dense()
+    e0 = sy.x0 - sy.xs
+    x1 = orc.gauss_seidel(A, sy.b, sy.x0, 1)
+    e1 = x1 - sy.xs
+    assert e1 @ M @ e1 <= e0 @ M @ e0
+
+
+def test_local_method_with_gs_sweep():
+    """Alg. 1 with the paper's one GS sweep: the smoothed x~ still converges to Eq. 6 and the sweep
+    never needs more global iterations than without it on the heat sequence."""
+    sy = synth.system(5, 6, n=12)
+    A = orc.Csr(sy.rp, sy.ci, sy.val)
+    dp = orc.DomainParams(orc.CRIT_RESIDUAL, orc.THR_PAPER, 1e-10, 1, 0, 1)
+    x0s, _, r0 = orc.local_method(A, sy.b, sy.x0, dp, orc.SolverParams(0, 1, 30, 1e-10, 20000, 0))
+    x1s, _, r1 = orc.local_method(A, sy.b, sy.x0, dp, orc.SolverParams(0, 1, 30, 1e-10, 20000, 1))
+    assert r1.st_global == 0 and r0.st_global == 0
+    assert np.linalg.norm(orc.residual(A, sy.b, x1s)) <= 1e-10 * np.linalg.norm(sy.b) * (1 + 1e-6)
