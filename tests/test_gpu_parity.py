@@ -431,3 +431,67 @@ def test_local_method_with_gs_parity(cfg, n, s):
         xo, _, ro = orc.local_method(As, sy.b[r0:r1], sy.x0[r0:r1], oracle_dp(rule, 1), sp)
         assert abs(rep["global"][g]["iterations"] - ro.it_global) <= 1
         assert np.linalg.norm(xg[r0:r1] - xo) / np.linalg.norm(xo) <= 1e-9
+
+
+# --------------------------------------------- NEXT-3: parameter studies --
+
+def test_alpha_sweep_nesting_and_limits():
+    """eta(alpha) is monotone non-increasing and the gradient domains are nested (P:1595-1596, S:262);
+    alpha = 1 -> empty, alpha = 0 -> Omega; each set equals the oracle's."""
+    sy = synth.system(5, 8, n=24)
+    A = gpu_matrix(sy)
+    Ao = oracle_csr(sy)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    prev = None
+    for a in [1.0] + [10.0 ** -k for k in range(1, 12)] + [0.0]:
+        dom = lc.select_domain(A, b, x0, criterion=1, threshold=1, param=a)
+        idx = set(dom.export()[0].cpu().numpy().tolist())
+        d = orc.select_domain(Ao, sy.b, sy.x0, 1, 1, a)
+        if len(idx ^ set(d.idx.tolist())):
+            compare_sets(Ao, np.array(sorted(idx)), d, 1)
+        if prev is not None:
+            assert prev <= idx
+        prev = idx
+        if a == 1.0:
+            assert len(idx) == 0
+        if a == 0.0:
+            assert len(idx) == sy.N
+
+
+def test_emax_sweep_nesting():
+    """Alg. 3 domains are nested in E_max and K is non-decreasing, on the 3T system."""
+    sy = synth.system(4, 6, n=40)
+    A = gpu_matrix(sy)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    prev = None
+    for em in range(0, 7):
+        dom = lc.select_domain(A, b, x0, criterion=0, threshold=0, param=EPS, expand_rounds=em)
+        idx = set(dom.export()[0].cpu().numpy().tolist())
+        if prev is not None:
+            assert prev <= idx
+        prev = idx
+
+
+def test_alpha_opt_decision_matches_oracle():
+    """R37: alpha_opt = the largest alpha of the grid whose x~ (local solve only) satisfies Eq. 6; the
+    GPU and the oracle take the same decision for every alpha of the grid (reduced multi-group group)."""
+    sy = synth.system(3, 6, n=32, G=1)
+    A = gpu_matrix(sy)
+    Ao = oracle_csr(sy)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    for a in [10.0 ** -k for k in range(0, 12)]:
+        rule = dict(criterion=1, threshold=1, param=a)
+        xt = x0.clone()
+        dom = lc.select_domain(A, b, x0, **rule)
+        if sum(dom.K) > 0:
+            lc.solve_local(lc.extract_sub(A, dom, b, x0), xt)
+        gpu_ok = lc.solve_global(A, b, xt, max_iters=0)[0]["status"] == 0
+        d = orc.select_domain(Ao, sy.b, sy.x0, 1, 1, a)
+        xo = sy.x0.copy()
+        if d.K > 0:
+            sub = orc.extract(Ao, sy.b, sy.x0, d.flag)
+            xb, _, _, _ = orc.pcg(sub.B, sub.bsub, sub.xB0)
+            xo = orc.assemble(sub, xb, sy.x0)
+        rr = np.linalg.norm(orc.residual(Ao, sy.b, xo)) / orc.norm2(sy.b)
+        if abs(rr - EPS) > 1e-3 * EPS:          # skip decisions within rounding of the tolerance
+            assert gpu_ok == (rr <= EPS), (a, rr)
