@@ -74,6 +74,10 @@ def _load():
         lib.or_gmres_bj.argtypes = [I64, P, P, P, I32, P, P, D, I32, I32, P, P]
         lib.or_gauss_seidel.argtypes = [I64, P, P, P, P, P, I32]
         lib.or_gauss_seidel.restype = I32
+        lib.or_heat_assemble.argtypes = [I32, I32, D, I32, D, D, P, P, P, P, P, P]
+        lib.or_heat_run.argtypes = [I32, I32, D, I32, D, D, I32, D, I32, ctypes.POINTER(DomainParams),
+                                    ctypes.POINTER(SolverParams), P, P, ctypes.c_void_p]
+        lib.or_heat_run.restype = I32
         lib.or_local_method.argtypes = [I64, P, P, P, P, P, ctypes.POINTER(DomainParams),
                                         ctypes.POINTER(SolverParams), P, ctypes.POINTER(Report)]
         for f in ("or_select_domain", "or_extract", "or_pcg", "or_gmres_bj", "or_local_method"):
@@ -234,6 +238,41 @@ def gauss_seidel(A: Csr, b, x, sweeps=1):
     if st != 0:
         raise ValueError(f"or_gauss_seidel status {st}")
     return y
+
+
+class HeatReport(ctypes.Structure):
+    _fields_ = [("steps", ctypes.c_int32), ("picard_total", ctypes.c_int32), ("picard_max_hit", ctypes.c_int32),
+                ("it_local", ctypes.c_int64), ("it_global", ctypes.c_int64), ("eta_sum", ctypes.c_double),
+                ("seconds", ctypes.c_double)]
+
+
+def heat_assemble(nx, ny, dt, Ts, Told, khalf=3, Tl=1.0, Tr=1e-4):
+    """The paper's 2-D heat Picard system at the iterate Ts: (Csr, b)."""
+    n = nx * ny
+    rp = np.empty(n + 1, np.int64); ci = np.empty(5 * n, np.int32); a = np.empty(5 * n); b = np.empty(n)
+    _load().or_heat_assemble(nx, ny, dt, khalf, Tl, Tr, _p(_c(Ts, np.float64)), _p(_c(Told, np.float64)), _p(rp),
+                             _p(ci), _p(a), _p(b))
+    z = int(rp[-1])
+    return Csr(rp, ci[:z], a[:z]), b
+
+
+def heat_run(nx, ny, T0, steps, domain: DomainParams | None, solver: SolverParams, dt=1e-2, khalf=3, Tl=1.0,
+             Tr=1e-4, picard_tol=1e-8, picard_max=100):
+    """Alg. 6 on the CPU oracle.  Returns (T_final, picard counts per step, HeatReport)."""
+    T = np.array(T0, dtype=np.float64, copy=True)
+    per = np.zeros(max(steps, 1), np.int32); rep = HeatReport()
+    st = _load().or_heat_run(nx, ny, dt, khalf, Tl, Tr, steps, picard_tol, picard_max,
+                             ctypes.byref(domain) if domain is not None else None, ctypes.byref(solver), _p(T),
+                             _p(per), ctypes.byref(rep))
+    if st < 0:
+        raise RuntimeError(f"or_heat_run status {st}")
+    return T, per[:steps], rep
+
+
+def heat_initial(nx, ny, Tl=1.0, Tr=1e-4):
+    """T_0(x, y) = e^{-100 x} T_l + T_r at the interior nodes x_p = (p+1)/(nx+1)."""
+    x = (np.arange(nx) + 1.0) / (nx + 1)
+    return np.tile(np.exp(-100.0 * x) * Tl + Tr, ny)
 
 
 def local_method(A: Csr, b, x0, domain: DomainParams | None, solver: SolverParams):

@@ -621,3 +621,96 @@ int or_local_method(int64_t n, const int64_t* rp, const int32_t* ci, const doubl
   rep->t_global = now_s() - t3;
   return st;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-2: the paper's 2-D nonlinear heat model and Alg. 6     */
+/* ------------------------------------------------------------------------ */
+
+/* kappa(T) = T^(k + 1/2) evaluated as T^k * sqrt(T) (R38: IEEE-exact operations, so the CPU and GPU
+   assemblies are bitwise identical; the paper's T^3.5 is k = 3) */
+static double kappa_pow(double t, int k) {
+  double v = 1.0;
+  for (int i = 0; i < k; ++i) v = v * t;
+  return v * sqrt(t);
+}
+
+/* Backward Euler + five-point FV on nx x ny interior nodes x_p = (p+1) h, h = 1/(nx+1) (SPEC heat-model),
+   Dirichlet T_l at x = 0 and T_r at x = 1 (ghost nodes at distance h), homogeneous Neumann at y = 0, 1
+   (no flux), face conductivity the arithmetic mean (R26), kappa frozen at the Picard iterate Ts (Eq.
+   picard-equs).  Row i = p + nx q, columns ascending:
+     (1 + lam sum_f kf) T_i - lam sum_{f interior} kf T_nb = T_old_i + lam sum_{f boundary} kf T_bnd,
+   lam = dt / h^2.  rp[nx ny + 1], ci, a (5 nx ny - 2 nx - 2 ny), b[nx ny]. */
+void or_heat_assemble(int nx, int ny, double dt, int khalf, double Tl, double Tr, const double* Ts,
+                      const double* Told, int64_t* rp, int32_t* ci, double* a, double* b) {
+  double h = 1.0 / (nx + 1), lam = dt / (h * h);
+  double kl = kappa_pow(Tl, khalf), kr = kappa_pow(Tr, khalf);
+  int64_t z = 0;
+  for (int q = 0; q < ny; ++q)
+    for (int p = 0; p < nx; ++p) {
+      int64_t i = p + (int64_t)nx * q;
+      double ki = kappa_pow(Ts[i], khalf);
+      double diag = 0.0, rhs = Told[i];
+      rp[i] = z;
+      if (q > 0) { double kf = 0.5 * (ki + kappa_pow(Ts[i - nx], khalf)); ci[z] = (int32_t)(i - nx); a[z++] = -lam * kf; diag += kf; }
+      if (p > 0) { double kf = 0.5 * (ki + kappa_pow(Ts[i - 1], khalf)); ci[z] = (int32_t)(i - 1); a[z++] = -lam * kf; diag += kf; }
+      else { double kf = 0.5 * (ki + kl); diag += kf; rhs += lam * kf * Tl; }
+      int64_t zd = z++;
+      if (p < nx - 1) { double kf = 0.5 * (ki + kappa_pow(Ts[i + 1], khalf)); ci[z] = (int32_t)(i + 1); a[z++] = -lam * kf; diag += kf; }
+      else { double kf = 0.5 * (ki + kr); diag += kf; rhs += lam * kf * Tr; }
+      if (q < ny - 1) { double kf = 0.5 * (ki + kappa_pow(Ts[i + nx], khalf)); ci[z] = (int32_t)(i + nx); a[z++] = -lam * kf; diag += kf; }
+      ci[zd] = (int32_t)i;
+      a[zd] = 1.0 + lam * diag;
+      b[i] = rhs;
+    }
+  rp[(int64_t)nx * ny] = z;
+}
+
+typedef struct {
+  int32_t steps, picard_total, picard_max_hit;
+  int64_t it_local, it_global;
+  double eta_sum;          /* sum over linear solves of K/N */
+  double seconds;
+} or_heat_report;
+
+/* Alg. 6: for n: T^{n+1,0} = T^n; for s: assemble at T^{n+1,s}, solve with x0 = T^{n+1,s}
+   (method0 if dp == NULL, else Alg. 1 with dp, sp), stop when ||T^{n+1,s+1} - T^{n+1,s}||_2 < picard_tol.
+   T: in = T^0, out = T^steps.  picard_per_step (optional, [steps]) receives the Picard counts. */
+int or_heat_run(int nx, int ny, double dt, int khalf, double Tl, double Tr, int steps, double picard_tol,
+                int picard_max, const or_domain_params* dp, const or_solver_params* sp, double* T,
+                int32_t* picard_per_step, or_heat_report* rep) {
+  int64_t n = (int64_t)nx * ny, nnz = 5 * n;
+  int64_t* rp = (int64_t*)malloc(sizeof(int64_t) * (n + 1));
+  int32_t* ci = (int32_t*)malloc(sizeof(int32_t) * nnz);
+  double* a = (double*)malloc(sizeof(double) * nnz);
+  double* b = (double*)malloc(sizeof(double) * n);
+  double* Ts = (double*)malloc(sizeof(double) * n);
+  double* Tn = (double*)malloc(sizeof(double) * n);
+  memset(rep, 0, sizeof(*rep));
+  double t0 = now_s();
+  int st = OR_OK;
+  for (int step = 0; step < steps; ++step) {
+    memcpy(Ts, T, sizeof(double) * n);                         /* T^{n+1,0} = T^n */
+    int s;
+    for (s = 0; s < picard_max; ++s) {
+      or_heat_assemble(nx, ny, dt, khalf, Tl, Tr, Ts, T, rp, ci, a, b);
+      memcpy(Tn, Ts, sizeof(double) * n);                      /* x0 = previous Picard iterate */
+      or_report r;
+      st = or_local_method(n, rp, ci, a, b, Tn, dp, sp, NULL, &r);
+      if (st < 0) goto done;
+      rep->it_local += r.it_local; rep->it_global += r.it_global; rep->eta_sum += (double)r.K / n;
+      rep->picard_total += 1;
+      double d2 = 0.0;
+      for (int64_t i = 0; i < n; ++i) { double d = Tn[i] - Ts[i]; d2 = fma(d, d, d2); }
+      memcpy(Ts, Tn, sizeof(double) * n);
+      if (sqrt(d2) < picard_tol) { ++s; break; }
+    }
+    if (s >= picard_max) rep->picard_max_hit += 1;
+    if (picard_per_step) picard_per_step[step] = s;
+    memcpy(T, Ts, sizeof(double) * n);
+    rep->steps = step + 1;
+  }
+done:
+  rep->seconds = now_s() - t0;
+  free(rp); free(ci); free(a); free(b); free(Ts); free(Tn);
+  return st < 0 ? st : OR_OK;
+}

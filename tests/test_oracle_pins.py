@@ -497,3 +497,67 @@ def test_local_method_with_gs_sweep():
     x1s, _, r1 = orc.local_method(A, sy.b, sy.x0, dp, orc.SolverParams(0, 1, 30, 1e-10, 20000, 1))
     assert r1.st_global == 0 and r0.st_global == 0
     assert np.linalg.norm(orc.residual(A, sy.b, x1s)) <= 1e-10 * np.linalg.norm(sy.b) * (1 + 1e-6)
+
+
+# ------------------------------------------------ NEXT-2: the paper's heat model --
+
+def test_heat_assembly_constant_kappa_is_textbook_stencil():
+    """T = 1 everywhere -> kappa = 1 on every face: the textbook implicit 5-point stencil, diag 1 + lam*(number of
+    faces incl. the Dirichlet x faces), off-diagonals -lam, Neumann y faces dropped; b = T_old + lam*kf*T_bnd with
+    kf = (1 + kappa(T_bnd))/2 on the boundary faces (SPEC heat-model, hand derivation)."""
+    nx, ny, dt = 4, 3, 1e-2
+    h = 1.0 / (nx + 1); lam = dt / h ** 2
+    Ts = np.ones(nx * ny); Told = np.full(nx * ny, 0.5)
+    A, b = orc.heat_assemble(nx, ny, dt, Ts, Told, khalf=3, Tl=1.0, Tr=1e-4)
+    M = A.to_dense()
+    kr = (1.0 + (1e-4) ** 3.5) / 2
+    for q in range(ny):
+        for p in range(nx):
+            i = p + nx * q
+            faces = 4 - (q == 0) - (q == ny - 1)
+            extra = (kr - 1.0) if p == nx - 1 else 0.0      # the right Dirichlet face has kf = kr, not 1
+            assert M[i, i] == pytest.approx(1 + lam * (faces + extra), rel=1e-14)
+            for j in range(nx * ny):
+                if j != i:
+                    adj = abs(j - i) == nx or (abs(j - i) == 1 and j // nx == i // nx)
+                    assert M[i, j] == (-lam if adj else 0.0)
+            rhs = 0.5 + (lam * 1.0 * 1.0 if p == 0 else 0.0) + (lam * kr * 1e-4 if p == nx - 1 else 0.0)
+            assert b[i] == pytest.approx(rhs, rel=1e-14)
+    np.testing.assert_array_equal(M, M.T)
+
+
+def test_heat_uniform_steady_state():
+    """T_l = T_r = T0 = c: the uniform field is the solution; Picard stops after one iteration."""
+    nx = ny = 6
+    T0 = np.full(nx * ny, 0.7)
+    T, per, rep = orc.heat_run(nx, ny, T0, 3, None, orc.SolverParams(0, 1, 30, 1e-12, 20000, 0), Tl=0.7, Tr=0.7)
+    np.testing.assert_allclose(T, 0.7, rtol=1e-12)
+    assert list(per) == [1, 1, 1]
+
+
+def test_heat_run_maximum_principle_and_y_symmetry():
+    """The discrete maximum principle holds and y-independent data stays y-independent (SPEC heat-model
+    invariants) over a short run of Alg. 6; every Picard loop converges.  The exact discrete solution is
+    y-uniform; each solve is only accurate to ||x - x*|| <= ||r|| <= 1e-10 ||b|| (R31, lambda_min >= 1), so
+    rows may differ by up to 2e-10 ||b|| (||b|| <= ||T|| + lam kf T_l sqrt(ny) bounded by 2 ||T|| + 1e3 here)."""
+    nx, ny = 15, 7
+    T0 = orc.heat_initial(nx, ny)
+    T, per, rep = orc.heat_run(nx, ny, T0, 5, None, orc.SolverParams(0, 1, 30, 1e-10, 20000, 0))
+    lo, hi = min(1e-4, T0.min()), max(1.0, T0.max())
+    assert T.min() >= lo - 1e-12 and T.max() <= hi + 1e-12
+    G = T.reshape(ny, nx)
+    assert np.max(np.abs(G - G[0])) <= 2e-10 * (2 * np.linalg.norm(T) + 1e3)
+    assert rep.picard_max_hit == 0 and all(p >= 2 for p in per)
+
+
+def test_heat_methods_agree_like_fig2():
+    """Fig. 2 / P:1106-1107: the local methods' fields agree with method0's (the paper reports <= 7.6e-9
+    relative); here after 4 steps of the 99x99 problem, methods 1 and 2 with one GS sweep."""
+    nx = ny = 99
+    T0 = orc.heat_initial(nx, ny)
+    sp = orc.SolverParams(0, 1, 30, 1e-10, 20000, 1)
+    T0m, _, _ = orc.heat_run(nx, ny, T0, 4, None, orc.SolverParams(0, 1, 30, 1e-10, 20000, 0))
+    T1m, _, r1 = orc.heat_run(nx, ny, T0, 4, orc.DomainParams(1, 1, 1e-4, 0, 0, 1), sp)
+    T2m, _, r2 = orc.heat_run(nx, ny, T0, 4, orc.DomainParams(0, 0, 1e-10, 1, 0, 1), sp)
+    for Tm in (T1m, T2m):
+        assert np.linalg.norm(Tm - T0m) / np.linalg.norm(T0m) <= 7.6e-9
