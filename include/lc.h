@@ -170,6 +170,52 @@ enum { LC_LAYOUT_SELL = 0     /* SELL-32 with explicit int32 column per slot (12
  */
 lc_status lc_smooth_gs(lc_matrix A, const double* b, double* x, int32_t sweeps, void* stream);
 
+/* ---- NEXT-2: the paper's own model workload, the 2-D nonlinear heat equation ---- */
+
+/*
+ * Backward-Euler / five-point Picard system at the iterate Ts (Eq. picard-equs) on nx x ny
+ * interior nodes x_p = (p+1)/(nx+1) (row i = p + nx q): kappa(T) = T^(khalf + 1/2) (paper: khalf = 3,
+ * evaluated as T^khalf sqrt(T), R38), face kappa the arithmetic mean (R26), Dirichlet t_left
+ * at x = 0 and t_right at x = 1, no flux at y = 0, 1:
+ *   (1 + lam sum_f kf) T_i - lam sum_{interior f} kf T_nb = Told_i + lam sum_{boundary f} kf T_bnd,
+ * lam = dt (nx+1)^2.  Device arrays: Ts, Told [nx ny]; outputs row_ptr [nx ny + 1], col_idx and values
+ * [5 nx ny - 2 nx - 2 ny] (ascending columns), b [nx ny].  Enqueued on `stream`, no sync.
+ */
+lc_status lc_heat_assemble(int32_t nx, int32_t ny, double dt, int32_t khalf, double t_left, double t_right,
+                           const double* Ts, const double* Told, int64_t* row_ptr, int32_t* col_idx, double* values,
+                           double* b, void* stream);
+
+typedef struct {
+  int32_t nx, ny;        /* interior nodes (paper: 99 x 99) */
+  double dt;             /* time step (paper: 1e-2) */
+  int32_t khalf;         /* kappa = T^(khalf + 1/2) (paper: 3) */
+  double t_left, t_right;/* Dirichlet values (paper: 1, 1e-4) */
+  int32_t steps;         /* time steps (paper: 100) */
+  double picard_tol;     /* ||T^{n+1,s+1} - T^{n+1,s}||_2 < picard_tol (paper: 1e-8) */
+  int32_t picard_max;    /* Picard cap per step */
+  int32_t method;        /* 0 = method0 (global PCG), 1 = method1 (Alg. 2), 2 = method2 (Alg. 3) */
+  double alpha;          /* method1 alpha (paper: 1e-4) */
+  int32_t e_max;         /* method2 E_max (paper: 1) */
+  int32_t gs_sweeps;     /* Alg. 1 l.7 sweeps (paper: 1) */
+  double rel_tol;        /* linear tolerance eps (paper: 1e-10); also eps of method2's tau */
+} lc_heat_params;
+
+typedef struct {
+  int32_t steps, picard_total, picard_max_hit;
+  int64_t it_local, it_global;   /* summed Krylov iterations */
+  double eta_sum;                /* sum over linear solves of K / N */
+  double seconds;                /* host wall time of the run */
+} lc_heat_report;
+
+/*
+ * Alg. 6 on the device: T (device [nx ny]) in = T^0, out = T^steps.  Every Picard linear
+ * system is assembled by lc_heat_assemble and solved by the selected method with x0 = the previous
+ * Picard iterate.  picard_per_step / eta_per_step (host, optional, [steps]) receive the
+ * Picard count and the mean eta of each step.  Syncs `stream` once per Picard iteration.
+ */
+lc_status lc_heat_run(const lc_heat_params* p, double* T, int32_t* picard_per_step, double* eta_per_step,
+                      void* stream, lc_heat_report* rep);
+
 /* introspection (host outputs, each optional): unknowns n*block, stored scalars, batch, SELL slices, max row
    length (slots), layout (LC_LAYOUT_*), bytes one SpMV streams for the matrix (values + columns + metadata) */
 lc_status lc_matrix_info(lc_matrix A, int64_t* n_unknowns, int64_t* nnz, int32_t* batch, int64_t* nslices,

@@ -28,7 +28,7 @@ _STATUS = {0: "LC_OK", 1: "LC_NOT_CONVERGED", -1: "LC_ERR_INVALID_ARG", -2: "LC_
            -7: "LC_ERR_CUDA", -8: "LC_ERR_OOM"}
 
 EXPORTED = ["lc_create_csr", "lc_select_domain", "lc_domain_export", "lc_extract_sub", "lc_solve_local",
-            "lc_solve_global", "lc_smooth_gs", "lc_matrix_info", "lc_destroy_matrix", "lc_destroy_domain",
+            "lc_solve_global", "lc_smooth_gs", "lc_heat_assemble", "lc_heat_run", "lc_matrix_info", "lc_destroy_matrix", "lc_destroy_domain",
             "lc_destroy_sub",
             "lc_last_error", "lc_kernel_launches"]
 
@@ -47,6 +47,20 @@ class DomainParams(ctypes.Structure):
 class SolverParams(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int32), ("precond", ctypes.c_int32), ("restart", ctypes.c_int32),
                 ("rel_tol", ctypes.c_double), ("max_iters", ctypes.c_int32)]
+
+
+class HeatParams(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("dt", ctypes.c_double), ("khalf", ctypes.c_int32),
+                ("t_left", ctypes.c_double), ("t_right", ctypes.c_double), ("steps", ctypes.c_int32),
+                ("picard_tol", ctypes.c_double), ("picard_max", ctypes.c_int32), ("method", ctypes.c_int32),
+                ("alpha", ctypes.c_double), ("e_max", ctypes.c_int32), ("gs_sweeps", ctypes.c_int32),
+                ("rel_tol", ctypes.c_double)]
+
+
+class HeatReport(ctypes.Structure):
+    _fields_ = [("steps", ctypes.c_int32), ("picard_total", ctypes.c_int32), ("picard_max_hit", ctypes.c_int32),
+                ("it_local", ctypes.c_int64), ("it_global", ctypes.c_int64), ("eta_sum", ctypes.c_double),
+                ("seconds", ctypes.c_double)]
 
 
 class SolveInfo(ctypes.Structure):
@@ -74,8 +88,10 @@ def load_library(path: str = LIB_PATH):
     lib.lc_solve_global.argtypes = [P, P, P, ctypes.POINTER(SolverParams), P, P]
     lib.lc_matrix_info.argtypes = [P, P, P, P, P, P, P, P]
     lib.lc_smooth_gs.argtypes = [P, P, P, I32, P]
+    lib.lc_heat_assemble.argtypes = [I32, I32, D, I32, D, D, P, P, P, P, P, P, P]
+    lib.lc_heat_run.argtypes = [ctypes.POINTER(HeatParams), P, P, P, P, ctypes.POINTER(HeatReport)]
     for f in ("lc_create_csr", "lc_select_domain", "lc_domain_export", "lc_extract_sub", "lc_solve_local",
-              "lc_solve_global", "lc_matrix_info", "lc_smooth_gs"):
+              "lc_solve_global", "lc_matrix_info", "lc_smooth_gs", "lc_heat_assemble", "lc_heat_run"):
         getattr(lib, f).restype = ctypes.c_int
     for f in ("lc_destroy_matrix", "lc_destroy_domain", "lc_destroy_sub"):
         getattr(lib, f).argtypes = [P]
@@ -266,3 +282,34 @@ def local_method(A: Matrix, b, x0, domain: dict | None, method=PCG, rel_tol=1e-1
             smooth_gs(A, b, x, gs_sweeps)
     rep["global"] = solve_global(A, b, x, method, rel_tol, max_iters, restart)
     return x, rep
+
+
+def heat_assemble(nx, ny, dt, Ts: torch.Tensor, Told: torch.Tensor, khalf=3, t_left=1.0, t_right=1e-4):
+    """The paper's heat Picard system on the device -> (row_ptr, col_idx, values, b) CUDA tensors."""
+    n = nx * ny
+    nnz = 5 * n - 2 * nx - 2 * ny
+    dev = Ts.device
+    rp = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    ci = torch.empty(nnz, dtype=torch.int32, device=dev)
+    va = torch.empty(nnz, dtype=torch.float64, device=dev)
+    b = torch.empty(n, dtype=torch.float64, device=dev)
+    _check(_lib.lc_heat_assemble(nx, ny, dt, khalf, t_left, t_right, _dptr(Ts, torch.float64, n),
+                                 _dptr(Told, torch.float64, n), _dptr(rp, torch.int64), _dptr(ci, torch.int32),
+                                 _dptr(va, torch.float64), _dptr(b, torch.float64), _stream()), "lc_heat_assemble",
+           ok=(LC_OK,))
+    return rp, ci, va, b
+
+
+def heat_run(nx, ny, T0: torch.Tensor, steps, method=0, alpha=1e-4, e_max=1, gs_sweeps=1, dt=1e-2, khalf=3,
+             t_left=1.0, t_right=1e-4, picard_tol=1e-8, picard_max=100, rel_tol=1e-10):
+    """Alg. 6 on the device (lc_heat_run).  Returns (T, picard counts per step, mean eta per step, report)."""
+    import numpy as np
+    p = HeatParams(nx, ny, dt, khalf, t_left, t_right, steps, picard_tol, picard_max, method, alpha, e_max,
+                   gs_sweeps, rel_tol)
+    T = T0.clone()
+    per = np.zeros(max(steps, 1), np.int32)
+    eta = np.zeros(max(steps, 1), np.float64)
+    rep = HeatReport()
+    _check(_lib.lc_heat_run(ctypes.byref(p), _dptr(T, torch.float64, nx * ny), per.ctypes.data, eta.ctypes.data,
+                            _stream(), ctypes.byref(rep)), "lc_heat_run", ok=(LC_OK,))
+    return T, per[:steps], eta[:steps], rep

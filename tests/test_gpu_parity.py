@@ -495,3 +495,47 @@ def test_alpha_opt_decision_matches_oracle():
         rr = np.linalg.norm(orc.residual(Ao, sy.b, xo)) / orc.norm2(sy.b)
         if abs(rr - EPS) > 1e-3 * EPS:          # skip decisions within rounding of the tolerance
             assert gpu_ok == (rr <= EPS), (a, rr)
+
+
+# -------------------------------------- NEXT-2: the paper's heat model on the device --
+
+def test_heat_assembly_bitexact():
+    """lc_heat_assemble reproduces the oracle's Picard system bit for bit (same IEEE operations, R38)."""
+    nx, ny = 37, 23
+    rng = np.random.default_rng(5)
+    Ts = rng.uniform(1e-4, 1.0, nx * ny)
+    Told = rng.uniform(1e-4, 1.0, nx * ny)
+    rp, ci, va, b = lc.heat_assemble(nx, ny, 1e-2, to_dev(Ts), to_dev(Told))
+    Ao, bo = orc.heat_assemble(nx, ny, 1e-2, Ts, Told)
+    np.testing.assert_array_equal(rp.cpu().numpy(), Ao.rp)
+    np.testing.assert_array_equal(ci.cpu().numpy(), Ao.ci)
+    np.testing.assert_array_equal(va.cpu().numpy(), Ao.val)
+    np.testing.assert_array_equal(b.cpu().numpy(), bo)
+
+
+@pytest.mark.parametrize("method", [0, 1, 2])
+def test_heat_run_vs_oracle(method):
+    """Alg. 6 on the device vs the oracle's driver (20 x 20 grid, 6 steps): Picard counts per step +-1, and
+    the final fields within 1e-8 relative (the Picard stop ||dT|| < 1e-8 bounds the difference one extra
+    or missing Picard iteration can make; ||T|| >= 1 here)."""
+    nx = ny = 20
+    T0 = orc.heat_initial(nx, ny)
+    dp = {0: None, 1: orc.DomainParams(1, 1, 1e-4, 0, 0, 1), 2: orc.DomainParams(0, 0, 1e-10, 1, 0, 1)}[method]
+    To, per_o, rep_o = orc.heat_run(nx, ny, T0, 6, dp, orc.SolverParams(0, 1, 30, 1e-10, 20000, 1 if method else 0))
+    Tg, per_g, eta_g, rep_g = lc.heat_run(nx, ny, to_dev(T0), 6, method=method, gs_sweeps=1 if method else 0)
+    assert np.all(np.abs(per_g - per_o) <= 1), (per_g, per_o)
+    Tg = Tg.cpu().numpy()
+    assert np.linalg.norm(Tg - To) / np.linalg.norm(To) <= 1e-8
+    assert rep_g.picard_max_hit == 0
+
+
+def test_heat_fig2_agreement_on_gpu():
+    """Fig. 2 on the device, 99 x 99 for 5 steps: methods 1 and 2 (alpha = 1e-4, E_max = 1,
+    one GS sweep) agree with method0 to the paper's 7.6e-9 relative."""
+    nx = ny = 99
+    T0 = to_dev(orc.heat_initial(nx, ny))
+    T0m = lc.heat_run(nx, ny, T0, 5, method=0)[0]
+    for m in (1, 2):
+        Tm, per, eta, rep = lc.heat_run(nx, ny, T0, 5, method=m)
+        assert (torch.linalg.norm(Tm - T0m) / torch.linalg.norm(T0m)).item() <= 7.6e-9
+        assert 0.0 < eta.mean() < 1.0
