@@ -104,7 +104,7 @@ def load_library(path: str = LIB_PATH):
 
 def _check(st, where, ok=(LC_OK, LC_NOT_CONVERGED)):
     if st not in ok:
-        raise LcError(st, where, _lib.lc_last_error().decode())
+        raise LcError(st, where, load_library().lc_last_error().decode())
     return st
 
 
@@ -155,7 +155,7 @@ class Matrix:
     def info(self):
         vals = [ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32(),
                 ctypes.c_int32(), ctypes.c_int64()]
-        _check(_lib.lc_matrix_info(self.h, *[ctypes.byref(v) for v in vals]), "lc_matrix_info")
+        _check(load_library().lc_matrix_info(self.h, *[ctypes.byref(v) for v in vals]), "lc_matrix_info")
         return dict(N=vals[0].value, nnz=vals[1].value, batch=vals[2].value, nslices=vals[3].value,
                     max_row=vals[4].value, layout="stencil" if vals[5].value == 1 else "sell",
                     matrix_bytes=vals[6].value)
@@ -185,7 +185,7 @@ class Domain:
         tau = (ctypes.c_double * self.A.batch)()
         crit = torch.empty(self.A.n_units, dtype=torch.float64, device=dev) if want_crit else None
         adm = torch.empty(self.A.n_units, dtype=torch.float64, device=dev) if want_adm else None
-        _check(_lib.lc_domain_export(self.h, ctypes.c_void_p(idx.data_ptr()), tau,
+        _check(load_library().lc_domain_export(self.h, ctypes.c_void_p(idx.data_ptr()), tau,
                                      ctypes.c_void_p(crit.data_ptr()) if crit is not None else None,
                                      ctypes.c_void_p(adm.data_ptr()) if adm is not None else None, s),
                "lc_domain_export")
@@ -203,7 +203,7 @@ def select_domain(A: Matrix, b: torch.Tensor, x0: torch.Tensor, criterion=CRIT_R
     p = DomainParams(criterion, threshold, param, expand_rounds, dilate_hops)
     h = ctypes.c_void_p()
     K = (ctypes.c_int64 * A.batch)()
-    _check(_lib.lc_select_domain(A.h, _dptr(b, torch.float64, A.N), _dptr(x0, torch.float64, A.N), ctypes.byref(p),
+    _check(load_library().lc_select_domain(A.h, _dptr(b, torch.float64, A.N), _dptr(x0, torch.float64, A.N), ctypes.byref(p),
                                  s, ctypes.byref(h), K), "lc_select_domain", ok=(LC_OK,))
     return Domain(A, h, list(K))
 
@@ -212,7 +212,7 @@ class Sub:
     def __init__(self, A: Matrix, dom: Domain, b, x0):
         s = _stream()
         h = ctypes.c_void_p()
-        _check(_lib.lc_extract_sub(A.h, dom.h, _dptr(b, torch.float64, A.N), _dptr(x0, torch.float64, A.N), s,
+        _check(load_library().lc_extract_sub(A.h, dom.h, _dptr(b, torch.float64, A.N), _dptr(x0, torch.float64, A.N), s,
                                    ctypes.byref(h)), "lc_extract_sub", ok=(LC_OK,))
         self.h, self.A, self.K = h, A, list(dom.K)
 
@@ -242,7 +242,7 @@ def solve_local(sub: Sub, x: torch.Tensor, method=PCG, rel_tol=1e-10, max_iters=
     s = _stream()
     p = _solver(method, rel_tol, max_iters, restart)
     info = (SolveInfo * sub.A.batch)()
-    st = _lib.lc_solve_local(sub.h, ctypes.byref(p), _dptr(x, torch.float64, sub.A.N), s, info)
+    st = load_library().lc_solve_local(sub.h, ctypes.byref(p), _dptr(x, torch.float64, sub.A.N), s, info)
     _check(st, "lc_solve_local")
     return _infos(info)
 
@@ -253,7 +253,7 @@ def solve_global(A: Matrix, b: torch.Tensor, x: torch.Tensor, method=PCG, rel_to
     s = _stream()
     p = _solver(method, rel_tol, max_iters, restart)
     info = (SolveInfo * A.batch)()
-    st = _lib.lc_solve_global(A.h, _dptr(b, torch.float64, A.N), _dptr(x, torch.float64, A.N), ctypes.byref(p), s,
+    st = load_library().lc_solve_global(A.h, _dptr(b, torch.float64, A.N), _dptr(x, torch.float64, A.N), ctypes.byref(p), s,
                               info)
     _check(st, "lc_solve_global")
     return _infos(info)
@@ -261,7 +261,7 @@ def solve_global(A: Matrix, b: torch.Tensor, x: torch.Tensor, method=PCG, rel_to
 
 def smooth_gs(A: Matrix, b: torch.Tensor, x: torch.Tensor, sweeps=1):
     """Alg. 1 l.7: forward natural-order Gauss-Seidel sweeps on x, in place."""
-    _check(_lib.lc_smooth_gs(A.h, _dptr(b, torch.float64, A.N), _dptr(x, torch.float64, A.N), sweeps, _stream()),
+    _check(load_library().lc_smooth_gs(A.h, _dptr(b, torch.float64, A.N), _dptr(x, torch.float64, A.N), sweeps, _stream()),
            "lc_smooth_gs", ok=(LC_OK,))
 
 
@@ -293,7 +293,7 @@ def heat_assemble(nx, ny, dt, Ts: torch.Tensor, Told: torch.Tensor, khalf=3, t_l
     ci = torch.empty(nnz, dtype=torch.int32, device=dev)
     va = torch.empty(nnz, dtype=torch.float64, device=dev)
     b = torch.empty(n, dtype=torch.float64, device=dev)
-    _check(_lib.lc_heat_assemble(nx, ny, dt, khalf, t_left, t_right, _dptr(Ts, torch.float64, n),
+    _check(load_library().lc_heat_assemble(nx, ny, dt, khalf, t_left, t_right, _dptr(Ts, torch.float64, n),
                                  _dptr(Told, torch.float64, n), _dptr(rp, torch.int64), _dptr(ci, torch.int32),
                                  _dptr(va, torch.float64), _dptr(b, torch.float64), _stream()), "lc_heat_assemble",
            ok=(LC_OK,))
@@ -310,6 +310,6 @@ def heat_run(nx, ny, T0: torch.Tensor, steps, method=0, alpha=1e-4, e_max=1, gs_
     per = np.zeros(max(steps, 1), np.int32)
     eta = np.zeros(max(steps, 1), np.float64)
     rep = HeatReport()
-    _check(_lib.lc_heat_run(ctypes.byref(p), _dptr(T, torch.float64, nx * ny), per.ctypes.data, eta.ctypes.data,
+    _check(load_library().lc_heat_run(ctypes.byref(p), _dptr(T, torch.float64, nx * ny), per.ctypes.data, eta.ctypes.data,
                             _stream(), ctypes.byref(rep)), "lc_heat_run", ok=(LC_OK,))
     return T, per[:steps], eta[:steps], rep
