@@ -94,6 +94,62 @@ __global__ void __launch_bounds__(kGST) k_gs_sweep(SellView A, int reg_units, in
   }
 }
 
+// Level-scheduled sweep for regular-grid stencils (offsets {-nx ny, -nx, -1, 0, 1, nx, nx ny} or the 2-D
+// subset): in natural order row (ix, iy, iz) depends only on rows with smaller ix + iy + iz, so the rows
+// of one level L = ix + iy + iz are independent and the levels run in order, separated by a grid
+// barrier (or __syncthreads for a single CTA).  Same per-row arithmetic as above (bit-exact).  x is read
+// through L2 (__ldcg): values written by other CTAs in earlier levels must not come from a stale L1 line.
+struct Grid3 { int nx, ny, nz; };
+__global__ void __launch_bounds__(kGST) k_gs_levels(SellView A, int reg_units, int spg, Grid3 gr, int G,
+                                                    const double* __restrict__ b, double* x, int sweeps,
+                                                    GridBar* bar) {
+  const int64_t plane = (int64_t)gr.nx * gr.ny;
+  const int64_t pairs = (int64_t)gr.ny * gr.nz;         // (iy, iz) candidates per level and segment
+  const int nlev = gr.nx + gr.ny + gr.nz - 2;
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int L = 0; L < nlev; ++L) {
+      for (int64_t t = gt; t < pairs * G; t += gs) {
+        const int g = (int)(t / pairs);
+        const int64_t pr = t - (int64_t)g * pairs;
+        const int iz = (int)(pr / gr.ny), iy = (int)(pr - (int64_t)iz * gr.ny);
+        const int ix = L - iy - iz;
+        if (ix < 0 || ix >= gr.nx) continue;
+        const int64_t lu = ix + (int64_t)gr.nx * iy + plane * iz;
+        const int64_t u = (int64_t)g * reg_units + lu;
+        const int64_t s = (int64_t)g * spg + (lu >> 5);
+        const int64_t pl = 32ll * A.W * s + (lu & 31);
+        double acc = 0.0, d = 0.0;
+        for (int k = 0; k < A.W; ++k) {
+          if (!((A.mask[u] >> k) & 1)) continue;
+          const double a = A.val[pl + 32ll * k];
+          const int64_t c = u + A.off[k];
+          if (c == u) { d = a; continue; }
+          acc = __fma_rn(a, __ldcg(x + c), acc);
+        }
+        x[u] = (b[u] - acc) / d;
+      }
+      if (gridDim.x == 1) __syncthreads();
+      else grid_barrier(bar);
+    }
+}
+
+// every stored coupling of a stencil row must be a true grid neighbour (else the level schedule is invalid)
+__global__ void k_check_grid(SellView A, int reg_units, Grid3 gr, int64_t n, unsigned* bad) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const int64_t lu = u % reg_units, plane = (int64_t)gr.nx * gr.ny;
+  const int ix = (int)(lu % gr.nx), iy = (int)((lu / gr.nx) % gr.ny), iz = (int)(lu / plane);
+  for (int k = 0; k < A.W; ++k) {
+    if (!((A.mask[u] >> k) & 1)) continue;
+    const int o = A.off[k];
+    bool ok = o == 0 || (o == -1 && ix > 0) || (o == 1 && ix < gr.nx - 1) ||
+              (o == -gr.nx && iy > 0) || (o == gr.nx && iy < gr.ny - 1) ||
+              (gr.nz > 1 && o == -plane && iz > 0) || (gr.nz > 1 && o == plane && iz < gr.nz - 1);
+    if (!ok) { atomicOr(bad, 1u); return; }
+  }
+}
+
 }  // namespace lc
 
 using namespace lc;
@@ -112,6 +168,53 @@ extern "C" lc_status lc_smooth_gs(lc_matrix M, const double* b, double* x, int32
   if (sweeps == 0) return LC_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const Sell& A = M->A;
+  // ---- regular-grid stencil?  offsets {-(nx ny), -nx, -1, 0, 1, nx, nx ny} (3-D) or {-nx, -1, 0, 1, nx}
+  Grid3 gr{0, 0, 0};
+  if (A.stencil) {
+    const int W = A.maxw;
+    const int64_t su = M->seg_units;
+    if (W == 5 && A.off[0] < -1 && A.off[1] == -1 && A.off[2] == 0 && A.off[3] == 1 && A.off[4] == -A.off[0]) {
+      int nx = -A.off[0];
+      if (su % nx == 0) gr = Grid3{nx, (int)(su / nx), 1};
+    } else if (W == 7 && A.off[2] == -1 && A.off[3] == 0 && A.off[4] == 1 && A.off[5] == -A.off[1] &&
+               A.off[6] == -A.off[0] && A.off[1] < -1 && A.off[0] < A.off[1] && (-A.off[0]) % (-A.off[1]) == 0) {
+      int nx = -A.off[1], ny = (-A.off[0]) / nx;
+      if (su % ((int64_t)nx * ny) == 0) gr = Grid3{nx, ny, (int)(su / ((int64_t)nx * ny))};
+    }
+  }
+  if (gr.nx > 0) {
+    void* ws = nullptr;
+    lc_status st = dalloc(&ws, 64, s);
+    if (st) return st;
+    LC_CUDA(cudaMemsetAsync(ws, 0, 64, s));
+    unsigned bad = 0;
+    k_check_grid<<<(unsigned)((M->n + 255) / 256), 256, 0, s>>>(view(A), M->seg_units, gr, M->n, (unsigned*)ws + 8);
+    count_launch();
+    LC_CUDA(cudaMemcpyAsync(&bad, (unsigned*)ws + 8, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    LC_CUDA(cudaStreamSynchronize(s));
+    if (bad) { dfree(ws, s); gr.nx = 0; }
+  }
+  if (gr.nx > 0) {
+    void* ws = nullptr;
+    lc_status st = dalloc(&ws, 64, s);
+    if (st) return st;
+    LC_CUDA(cudaMemsetAsync(ws, 0, 64, s));
+    const int64_t work = (int64_t)gr.ny * gr.nz * M->batch;
+    int per_sm = 0;
+    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_levels, kGST, 0));
+    int64_t nCTA = std::min<int64_t>((int64_t)std::max(per_sm, 1) * num_sms(), (work + kGST - 1) / kGST);
+    if (nCTA < 1) nCTA = 1;
+    SellView V = view(A);
+    const int spg = (M->seg_units + 31) / 32;
+    int ru = M->seg_units, G = M->batch;
+    GridBar* bar = (GridBar*)ws;
+    void* args[] = {&V, &ru, (void*)&spg, &gr, &G, (void*)&b, &x, &sweeps, &bar};
+    LC_CUDA(cudaLaunchCooperativeKernel((void*)k_gs_levels, dim3((unsigned)nCTA), dim3(kGST), args, 0, s));
+    count_launch();
+    dfree(ws, s);
+    LC_CUDA(cudaStreamSynchronize(s));
+    return LC_OK;
+  }
   void* ws = nullptr;
   const size_t fbytes = sizeof(unsigned) * (size_t)(A.nslices + 1);
   lc_status st = dalloc(&ws, fbytes + 64 * (sweeps + 1), s);

@@ -539,3 +539,22 @@ def test_heat_fig2_agreement_on_gpu():
         Tm, per, eta, rep = lc.heat_run(nx, ny, T0, 5, method=m)
         assert (torch.linalg.norm(Tm - T0m) / torch.linalg.norm(T0m)).item() <= 7.6e-9
         assert 0.0 < eta.mean() < 1.0
+
+
+@pytest.mark.parametrize("case", ["band5", "heat2d"])
+def test_gs_grid_detection_guard(case):
+    """A pentadiagonal band matrix has the 2 x n grid's offset set but couples across the grid edge: the
+    level schedule must not be used (the sweep must still match the oracle); the heat matrix takes it."""
+    if case == "band5":
+        sy = synth.random_system(600, bw=2, spd=True, seed=3)
+        Ao = oracle_csr(sy)
+        A, b, x0 = gpu_matrix(sy), sy.b, sy.x0
+    else:
+        nx, ny = 33, 17
+        rng = np.random.default_rng(1)
+        Ao, b = orc.heat_assemble(nx, ny, 1e-2, rng.uniform(0.1, 1, nx * ny), rng.uniform(0.1, 1, nx * ny))
+        A = lc.Matrix(nx * ny, Ao.rp, Ao.ci, Ao.val)
+        x0 = rng.uniform(0.1, 1, nx * ny)
+    x = to_dev(x0)
+    lc.smooth_gs(A, to_dev(b), x, 2)
+    np.testing.assert_array_equal(x.cpu().numpy(), orc.gauss_seidel(Ao, b, x0, 2))
