@@ -216,8 +216,13 @@ def run_lc(args):
     # ---- per-method breakdown and roofline of the dominant kernel (global PCG launches on A)
     Ainfo = lc.Matrix(sy0.nrows, dev_in[0]["rp"], dev_in[0]["ci"], dev_in[0]["val"], block=sy0.block,
                       batch=sy0.batch).info()
-    per_nnz = 8.0 if Ainfo["layout"] == "stencil" else 12.0
-    it_bytes = per_nnz * nnz + 96.0 * N      # matrix once + pass A 32 B/row + pass B 64 B/row
+    if Ainfo["layout"] == "symstencil":      # diagonal + upper values only: (nnz + N) / 2 stored values
+        mat_bytes, rule = 8.0 * (nnz + N) / 2.0, "8 B x (nnz + N)/2 symmetric-stencil values"
+    elif Ainfo["layout"] == "stencil":
+        mat_bytes, rule = 8.0 * nnz, "8 B/nnz stencil values"
+    else:
+        mat_bytes, rule = 12.0 * nnz, "12 B/nnz SELL values + columns"
+    it_bytes = mat_bytes + 96.0 * N          # matrix once + pass A 32 B/row + pass B 64 B/row
     try:
         trafficdb = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except OSError:
@@ -274,7 +279,7 @@ def run_lc(args):
                 "traffic": tr, "algorithmic_bytes_per_launch": int(pcg_bytes / max(nlaunch, 1)),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650",
                 "layout": Ainfo["layout"],
-                "bytes_rule": (f"{int(per_nnz)} B/nnz matrix + 96 B/row vectors per PCG iteration" if solver == "pcg"
+                "bytes_rule": (f"{rule} + 96 B/row vectors per PCG iteration" if solver == "pcg"
                                else "8 B/nnz + 88 B/unknown + 24 (j+1) B/unknown per Arnoldi step j")}
 
     # ---- e2e: host buffers through the C-ABI, H2D + D2H inside the timed region

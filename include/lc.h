@@ -160,7 +160,9 @@ lc_status lc_solve_global(lc_matrix A, const double* b, double* x, const lc_solv
 /* storage layout chosen by lc_create_csr */
 enum { LC_LAYOUT_SELL = 0     /* SELL-32 with explicit int32 column per slot (12 B per slot) */,
        LC_LAYOUT_STENCIL = 1  /* every row's column offsets lie in one sorted set of <= 8 offsets: values only,
-                                 slot k = column row + off[k] (zero "holes" where a row lacks it), 8 B per slot */ };
+                                 slot k = column row + off[k] (zero "holes" where a row lacks it), 8 B per slot */,
+       LC_LAYOUT_SYMSTENCIL = 2 /* stencil layout of a bitwise-symmetric matrix (block 1): only the diagonal and
+                                   upper-offset slots are stored; a_uv (v < u) is read as a_vu */ };
 /*
  * Alg. 1 l.7 (one sweep in the paper's runs): `sweeps` forward Gauss-Seidel sweeps
  * in natural row order on A x = b, in place on x (device [n]): x_i <- (b_i - sum_{j != i} a_ij x_j) / a_ii

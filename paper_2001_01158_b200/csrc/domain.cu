@@ -34,12 +34,11 @@ __global__ void __launch_bounds__(kTB) k_residual_crit(SellView A, const double*
   int64_t u = A.slice_row0[s] + lane;
   bool valid = u < A.seg_unit0[g + 1];
   int64_t p0 = A.slice_ptr[s];
-  int w = (int)((A.slice_ptr[s + 1] - p0) >> 5);
+  int w = A.stencil ? A.W : (int)((A.slice_ptr[s + 1] - p0) >> 5);
   double cmax = 0.0, hi = 0.0, lo = 0.0;
   if (BS == 1) {
     double acc = 0.0;
-    const double* vp = A.val + p0 + lane;
-    for (int k = 0; k < w; ++k) acc = __fma_rn(vp[32 * k], __ldg(x + sv_col(A, p0 + lane, k, u)), acc);
+    for (int k = 0; k < w; ++k) acc = __fma_rn(sv_val(A, p0 + lane, k, u), __ldg(x + sv_col(A, p0 + lane, k, u)), acc);
     if (valid) {
       double bi = b[u];
       double ri = bi - acc;
@@ -84,7 +83,7 @@ __global__ void __launch_bounds__(kTB) k_gradient(SellView A, const double* __re
   int64_t u = A.slice_row0[s] + lane;
   bool valid = u < A.seg_unit0[g + 1];
   int64_t p0 = A.slice_ptr[s];
-  int w = (int)((A.slice_ptr[s + 1] - p0) >> 5);
+  int w = A.stencil ? A.W : (int)((A.slice_ptr[s + 1] - p0) >> 5);
   double gmax = 0.0;
   if (valid) {
     double xi = x[u], acc = 0.0;
@@ -259,7 +258,7 @@ __global__ void __launch_bounds__(kTB) k_expand(SellView A, const double* __rest
     for (int k = 0; k < len; ++k) {
       if (!sv_real(A, k, u)) continue;
       int64_t c = sv_col(A, p0 + lane, k, u);
-      if (flag[c] < stage) { nb = true; sum = sum + fabs(A.val[p0 + 32 * k + lane] * x0[c]); }
+      if (flag[c] < stage) { nb = true; sum = sum + fabs(sv_val(A, p0 + lane, k, u) * x0[c]); }
     }
     best = fabs(r[u]) + sum;
   } else {

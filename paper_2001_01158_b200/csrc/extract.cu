@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(kTB) k_extract(SellView A, SellView B, int W, 
         int64_t slotB = pB + 32ll * kb + lane;
         Bcol[slotB] = ic;
         if (BS == 1) {
-          Bval[slotB] = A.val[slotA];
+          Bval[slotB] = sv_val(A, pA + laneA, k, i);
         } else {
 #pragma unroll
           for (int q = 0; q < 9; ++q)
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kTB) k_extract(SellView A, SellView B, int W, 
         ++kb;
       } else {                                         // E x_C^(0): fma chain, ascending columns
         if (BS == 1) {
-          acc[0] = __fma_rn(A.val[slotA], x0[c], acc[0]);
+          acc[0] = __fma_rn(sv_val(A, pA + laneA, k, i), x0[c], acc[0]);
         } else {
 #pragma unroll
           for (int a = 0; a < 3; ++a)
@@ -105,12 +105,12 @@ __global__ void __launch_bounds__(kTB) k_bsub_masked(SellView A, int seg_units, 
   int64_t g = i / seg_units, lu = i - g * seg_units;
   int64_t s = g * spg + (lu >> 5);
   int laneA = (int)(lu & 31);
-  int64_t pA = 32ll * A.W * s;
+  int64_t pA = A.slice_ptr[s];
   double acc = 0.0;
   for (int k = 0; k < A.W; ++k) {
     if (!sv_real(A, k, i)) continue;
     int64_t c = sv_col(A, pA + laneA, k, i);
-    if (inv[c] < 0) acc = __fma_rn(A.val[pA + 32ll * k + laneA], x0[c], acc);
+    if (inv[c] < 0) acc = __fma_rn(sv_val(A, pA + laneA, k, i), x0[c], acc);
   }
   bs[i] = b[i] - acc;
   xm0[i] = x0[i];

@@ -111,14 +111,14 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
         int64_t u = A.slice_row0[s] + lane;
         if (u >= nunits) continue;
         int64_t p0 = A.slice_ptr[s];
-        int wd = (int)((A.slice_ptr[s + 1] - p0) >> 5);
+        int wd = A.stencil ? A.W : (int)((A.slice_ptr[s + 1] - p0) >> 5);
         double acc[BS];
 #pragma unroll
         for (int a = 0; a < BS; ++a) acc[a] = 0.0;
         for (int k = 0; k < wd; ++k) {
           int64_t c = sv_col(A, p0 + lane, k, u);
           if (BS == 1) {
-            acc[0] = __fma_rn(A.val[p0 + 32 * k + lane], P.x[c], acc[0]);
+            acc[0] = __fma_rn(sv_val(A, p0 + lane, k, u), P.x[c], acc[0]);
           } else {
             const double* vb = A.val + 9 * (p0 + 32ll * k) + lane;
             double y0 = P.x[3 * c], y1 = P.x[3 * c + 1], y2 = P.x[3 * c + 2];
@@ -186,11 +186,11 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
           for (int a = 0; a < BS; ++a) acc[a] = 0.0;
           if (valid) {
             int64_t p0 = A.slice_ptr[s];
-            int wd = (int)((A.slice_ptr[s + 1] - p0) >> 5);
+            int wd = A.stencil ? A.W : (int)((A.slice_ptr[s + 1] - p0) >> 5);
             for (int k = 0; k < wd; ++k) {
               int64_t c = sv_col(A, p0 + lane, k, u);
               if (BS == 1) {
-                acc[0] = __fma_rn(A.val[p0 + 32 * k + lane], P.t[c], acc[0]);
+                acc[0] = __fma_rn(sv_val(A, p0 + lane, k, u), P.t[c], acc[0]);
               } else {
                 const double* vb = A.val + 9 * (p0 + 32ll * k) + lane;
                 double y0 = P.t[3 * c], y1 = P.t[3 * c + 1], y2 = P.t[3 * c + 2];

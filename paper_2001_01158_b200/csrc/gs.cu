@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(kGST) k_gs_sweep(SellView A, int reg_units, in
     const int64_t row0 = g * reg_units + 32 * (s - g * spg), end = (g + 1) * reg_units;
     const int64_t u = row0 + lane;
     const bool valid = u < end;
-    const int64_t pl = (ST ? 32ll * A.W * s : A.slice_ptr[s]) + lane;
+    const int64_t pl = (ST ? 32ll * A.vw * s : A.slice_ptr[s]) + lane;
     const int w = ST ? A.W : (int)((A.slice_ptr[s + 1] - (pl - lane)) >> 5);
     double av[kGSMaxW], yv[kGSMaxW];
     int64_t cv[kGSMaxW];
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kGST) k_gs_sweep(SellView A, int reg_units, in
         bool real = sv_real(A, k, u);
         int64_t c = real ? sv_col(A, pl, k, u) : u;
         cv[k] = real ? c : -1;
-        av[k] = A.val[pl + 32ll * k];
+        av[k] = sv_val(A, pl, k, u);
         yv[k] = 0.0;
         if (!real) continue;
         if (c == u) { d = av[k]; continue; }
@@ -118,11 +118,11 @@ __global__ void __launch_bounds__(kGST) k_gs_levels(SellView A, int reg_units, i
         const int64_t lu = ix + (int64_t)gr.nx * iy + plane * iz;
         const int64_t u = (int64_t)g * reg_units + lu;
         const int64_t s = (int64_t)g * spg + (lu >> 5);
-        const int64_t pl = 32ll * A.W * s + (lu & 31);
+        const int64_t pl = 32ll * A.vw * s + (lu & 31);
         double acc = 0.0, d = 0.0;
         for (int k = 0; k < A.W; ++k) {
           if (!((A.mask[u] >> k) & 1)) continue;
-          const double a = A.val[pl + 32ll * k];
+          const double a = sv_val(A, pl, k, u);
           const int64_t c = u + A.off[k];
           if (c == u) { d = a; continue; }
           acc = __fma_rn(a, __ldcg(x + c), acc);

@@ -90,6 +90,11 @@ struct Sell {
   int stencil = 0;
   int32_t off[kMaxOff] = {0};
   uint8_t* mask = nullptr;        // [nunits] bit k = slot k holds a stored entry (stencil layout)
+  // symmetric stencil layout (block 1, a_uv == a_vu bitwise): only slots k >= kd (diagonal + upper offsets)
+  // are stored, vw = W - kd per slice; a lower slot's value is read from the mirror row's upper slot mir[k]
+  int sym = 0, kd = 0, vw = 0;
+  int32_t mir[kMaxOff] = {0};
+  int reg_units = 0, spg = 0;     // equal segments (matrices from lc_create_csr)
   std::vector<int32_t> h_seg_unit0;
   std::vector<int64_t> h_seg_slice0;
   void release(cudaStream_t s);
@@ -103,6 +108,9 @@ struct SellView {
   int32_t off[kMaxOff];
   const uint8_t* mask;
   int64_t nunits;
+  int sym, kd, vw;          // symmetric stencil storage (see Sell)
+  int32_t mir[kMaxOff];
+  int ru, spg;
   int64_t nslices;
   int nseg;
   const int64_t* slice_ptr;
@@ -120,6 +128,9 @@ inline SellView view(const Sell& m) {
   v.block = m.block; v.stencil = m.stencil; v.W = m.maxw;
   for (int k = 0; k < kMaxOff; ++k) v.off[k] = m.off[k];
   v.mask = m.mask; v.nunits = m.nunits;
+  v.sym = m.sym; v.kd = m.kd; v.vw = m.stencil ? (m.sym ? m.vw : m.maxw) : 0;
+  for (int k = 0; k < kMaxOff; ++k) v.mir[k] = m.mir[k];
+  v.ru = m.reg_units; v.spg = m.spg;
   v.nslices = m.nslices; v.nseg = m.nseg; v.slice_ptr = m.slice_ptr; v.slice_row0 = m.slice_row0;
   v.slice_seg = m.slice_seg; v.seg_unit0 = m.seg_unit0; v.seg_slice0 = m.seg_slice0; v.col = m.col;
   v.val = m.val; v.rowlen = m.rowlen; v.dinv = m.dinv;
@@ -133,6 +144,16 @@ __device__ __forceinline__ int64_t sv_col(const SellView& A, int64_t pl, int k, 
     return c < 0 ? 0 : (c >= A.nunits ? A.nunits - 1 : c);
   }
   return A.col[pl + 32ll * k];
+}
+// value of scalar slot k of unit u (pl = slice_ptr[s] + lane, as for sv_col)
+__device__ __forceinline__ double sv_val(const SellView& A, int64_t pl, int k, int64_t u) {
+  if (!A.sym) return A.val[pl + 32ll * k];
+  if (k >= A.kd) return A.val[pl + 32ll * (k - A.kd)];
+  const int64_t v = u + A.off[k];              // mirror entry a_vu (row v, upper slot mir[k])
+  if (v < 0) return 0.0;
+  const int64_t g = v / A.ru, lv = v - g * A.ru;
+  const int64_t sv = g * A.spg + (lv >> 5);
+  return A.val[32ll * A.vw * sv + 32ll * A.mir[k] + (lv & 31)];
 }
 // slot k of unit u holds a stored entry (not padding, not a hole)
 __device__ __forceinline__ bool sv_real(const SellView& A, int k, int64_t u) {

@@ -96,6 +96,19 @@ __device__ __forceinline__ void slice_map(const PcgArgs& P, int64_t s, int& g, i
 // loop is fully unrolled so all value loads and gathers issue together (stencil: columns are
 // u + off[k], no column loads at all).  Returns the fma chain; *own = y at the diagonal slot when
 // ST (the own p value comes from the diagonal gather).
+// symmetric stencil storage: value of slot k of row u (ST == 2).  Upper slots (k >= kd) are stored with the
+// row; a lower slot is the mirror a_vu of row v = u + off[k], read from v's upper slot mir[k] (an L2 hit:
+// that row's values were streamed by a neighbouring warp moments earlier).
+__device__ __forceinline__ double sym_val(const SellView& A, const double* __restrict__ vp, int k, int ui) {
+  if (k >= A.kd) return __ldg(vp + 32 * (k - A.kd));
+  const int v = ui + A.off[k];
+  if (v < 0) return 0.0;
+  int sv, lv;
+  if (A.ru >= A.nunits) { sv = v >> 5; lv = v & 31; }
+  else { const int g = v / A.ru, r = v - g * A.ru; sv = g * A.spg + (r >> 5); lv = r & 31; }
+  return __ldg(A.val + 32ll * A.vw * sv + 32 * A.mir[k] + lv);
+}
+
 template <int WM, int ST, class Ld>
 __device__ __forceinline__ double row_dot(const SellView& A, int64_t pl, int w, int64_t u, Ld ld, double* own) {
   double acc = 0.0;
@@ -114,7 +127,7 @@ __device__ __forceinline__ double row_dot(const SellView& A, int64_t pl, int w, 
       } else {
         c = (k < w) ? __ldg(A.col + pl + 32 * k) : 0;
       }
-      v[k] = (ST || k < w) ? __ldg(vp + 32 * k) : 0.0;
+      v[k] = ST == 2 ? sym_val(A, vp, k, ui) : (ST || k < w) ? __ldg(vp + 32 * k) : 0.0;
       y[k] = (ST || k < w) ? ld(c) : 0.0;
     }
 #pragma unroll
@@ -130,7 +143,7 @@ __device__ __forceinline__ double row_dot(const SellView& A, int64_t pl, int w, 
       int c = (int)sv_col(A, pl, k, u);
       double yk = ld(c);
       if (ST && c == u) *own = yk;
-      acc = __fma_rn(__ldg(vp + 32 * k), yk, acc);
+      acc = __fma_rn(ST == 2 ? sym_val(A, vp, k, (int)u) : __ldg(vp + 32 * k), yk, acc);
     }
   }
   return acc;
@@ -152,7 +165,7 @@ __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_
     slice_map(P, s, g, row0, end);
     const int64_t u = row0 + lane;
     if (u >= end) continue;
-    const int64_t pl = (ST ? 32ll * A.W * s : A.slice_ptr[s]) + lane;
+    const int64_t pl = (ST ? 32ll * A.vw * s : A.slice_ptr[s]) + lane;
     const int w = ST ? A.W : (int)((A.slice_ptr[s + 1] - (pl - lane)) >> 5);
     double own = 0.0;
     const bool in = !P.omega || P.omega[u] != 255;
@@ -358,7 +371,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
         if (mode == M_DONE || mode == M_RESET) continue;
         const int64_t u = row0 + lane;
         if (u >= end) continue;
-        const int64_t pl = (ST ? 32ll * A.W * s : A.slice_ptr[s]) + lane;
+        const int64_t pl = (ST ? 32ll * A.vw * s : A.slice_ptr[s]) + lane;
         const int w = ST ? A.W : (int)((A.slice_ptr[s + 1] - (pl - lane)) >> 5);
         double own = 0.0;
         if (mode == M_INIT || mode == M_CONFIRM) {
@@ -562,7 +575,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
 }
 
 // ---------------------------------------------------------------- host ----
-static int g_pcg_max_ctas[6] = {0, 0, 0, 0, 0, 0};
+static int g_pcg_max_ctas[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
 
 lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
   const Sell& M = *job.M;
@@ -572,9 +585,10 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   std::vector<int> it(G, 0), stt(G, LC_OK);
   std::vector<double> rr(G, 0.0);
   float ms = 0.f;
-  const int wi = (M.maxw <= 5 ? 0 : M.maxw <= 7 ? 1 : 2) + (M.stencil ? 3 : 0);
-  void* const fns[6] = {(void*)k_pcg<5, 0>, (void*)k_pcg<7, 0>, (void*)k_pcg<0, 0>,
-                        (void*)k_pcg<5, 1>, (void*)k_pcg<7, 1>, (void*)k_pcg<0, 1>};
+  const int wi = (M.maxw <= 5 ? 0 : M.maxw <= 7 ? 1 : 2) + (M.sym ? 6 : M.stencil ? 3 : 0);
+  void* const fns[9] = {(void*)k_pcg<5, 0>, (void*)k_pcg<7, 0>, (void*)k_pcg<0, 0>,
+                        (void*)k_pcg<5, 1>, (void*)k_pcg<7, 1>, (void*)k_pcg<0, 1>,
+                        (void*)k_pcg<5, 2>, (void*)k_pcg<7, 2>, (void*)k_pcg<0, 2>};
   void* fn = fns[wi];
   if (!g_pcg_max_ctas[wi]) {
     int per_sm = 0;

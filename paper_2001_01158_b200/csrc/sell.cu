@@ -78,6 +78,38 @@ __global__ void k_fill_stencil(int64_t n, int seg_units, int spg, const int64_t*
   }
 }
 
+// value symmetry on the full stencil layout: every lower slot equals its mirror (row u + off[k], upper slot
+// of -off[k]); a lower slot whose mirror row lies outside the segment must be a zero hole.
+__global__ void k_check_sym(int64_t n, int seg_units, int spg, Offsets O, int kd, const double* __restrict__ val,
+                            unsigned* bad) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const int64_t g = u / seg_units, lu = u - g * seg_units;
+  const int64_t s = g * spg + (lu >> 5);
+  const int lane = (int)(lu & 31);
+  for (int k = 0; k < kd; ++k) {
+    const double a = val[(s * O.W + k) * 32 + lane];
+    const int64_t v = u + O.off[k];
+    const int64_t gv = v >= 0 ? v / seg_units : -1;
+    double m = 0.0;
+    if (v >= 0 && gv == g) {
+      const int64_t lv = v - g * seg_units, sv = g * spg + (lv >> 5);
+      m = val[(sv * O.W + (O.W - 1 - k)) * 32 + (lv & 31)];
+    }
+    if (__double_as_longlong(a) != __double_as_longlong(m)) { atomicOr(bad, 1u); return; }
+  }
+}
+
+__global__ void k_compact_upper(int64_t nslices, int W, int kd, const double* __restrict__ full,
+                                double* __restrict__ up) {
+  const int vw = W - kd;
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nslices * vw * 32) return;
+  const int64_t s = t / (vw * 32);
+  const int r = (int)(t - s * vw * 32);
+  up[t] = full[(s * W + kd) * 32 + r];
+}
+
 __global__ void k_uniform_slice_ptr(int64_t nslices, int W, int64_t* slice_ptr) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s <= nslices) slice_ptr[s] = 32ll * W * s;
@@ -315,6 +347,35 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
                                                (unsigned*)t_err);
         count_launch();
         CKC(cudaGetLastError());
+        // ---- symmetric stencil?  offsets symmetric and values equal to their mirrors (block 1)
+        bool offsym = (h_maxw % 2 == 1) && block == 1;
+        for (int k = 0; k < h_maxw && offsym; ++k) offsym = (O.off[k] == -O.off[h_maxw - 1 - k]);
+        const char* sym_env = getenv("LC_SYMMETRIC");     // opt-in until the value stream is TMA-staged
+        if (offsym && sym_env && sym_env[0] == '1') {
+          const int kd = h_maxw / 2;
+          unsigned bad = 0;
+          CKC(cudaMemsetAsync((char*)t_err + 4, 0, 4, s));
+          k_check_sym<<<nb, 256, 0, s>>>(n, M->seg_units, spg, O, kd, A.val, (unsigned*)((char*)t_err + 4));
+          count_launch();
+          CKC(cudaMemcpyAsync(&bad, (char*)t_err + 4, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+          CKC(cudaStreamSynchronize(s));
+          if (!bad) {
+            const int vw = h_maxw - kd;
+            double* up = nullptr;
+            CK(dalloc((void**)&up, sizeof(double) * 32 * vw * A.nslices, s));
+            const int64_t tot = 32ll * vw * A.nslices;
+            k_compact_upper<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(A.nslices, h_maxw, kd, A.val, up);
+            count_launch();
+            k_uniform_slice_ptr<<<(unsigned)((A.nslices + 256) / 256), 256, 0, s>>>(A.nslices, vw, A.slice_ptr);
+            count_launch();
+            CKC(cudaGetLastError());
+            dfree(A.val, s);
+            A.val = up;
+            A.sym = 1; A.kd = kd; A.vw = vw;
+            A.nslots = tot;
+            for (int k = 0; k < kd; ++k) A.mir[k] = (h_maxw - 1 - k) - kd;
+          }
+        }
       } else {
         h_err = 0;
         CKC(cudaMemsetAsync(t_err, 0, sizeof(unsigned), s));
@@ -334,6 +395,8 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
     count_launch();
     CKC(cudaGetLastError());
   }
+  A.reg_units = M->seg_units;
+  A.spg = spg;
   // segment maps
   A.h_seg_unit0.resize(batch + 1);
   A.h_seg_slice0.resize(batch + 1);
@@ -369,7 +432,7 @@ extern "C" lc_status lc_matrix_info(lc_matrix A, int64_t* n_unknowns, int64_t* n
                                     int64_t* nslices, int32_t* max_row, int32_t* layout, int64_t* matrix_bytes) {
   if (!A) { set_error("lc_matrix_info: NULL handle"); return LC_ERR_INVALID_ARG; }
   const int bb = A->block * A->block;
-  if (layout) *layout = A->A.stencil ? LC_LAYOUT_STENCIL : LC_LAYOUT_SELL;
+  if (layout) *layout = A->A.sym ? LC_LAYOUT_SYMSTENCIL : A->A.stencil ? LC_LAYOUT_STENCIL : LC_LAYOUT_SELL;
   if (matrix_bytes)
     *matrix_bytes = A->A.stencil ? (int64_t)8 * bb * A->A.nslots
                                  : (int64_t)(8 * bb + 4) * A->A.nslots + 8 * (A->A.nslices + 1) + 8 * A->A.nslices;

@@ -157,7 +157,7 @@ class Matrix:
                 ctypes.c_int32(), ctypes.c_int64()]
         _check(load_library().lc_matrix_info(self.h, *[ctypes.byref(v) for v in vals]), "lc_matrix_info")
         return dict(N=vals[0].value, nnz=vals[1].value, batch=vals[2].value, nslices=vals[3].value,
-                    max_row=vals[4].value, layout="stencil" if vals[5].value == 1 else "sell",
+                    max_row=vals[4].value, layout={0: "sell", 1: "stencil", 2: "symstencil"}[vals[5].value],
                     matrix_bytes=vals[6].value)
 
     def __del__(self):

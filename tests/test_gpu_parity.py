@@ -359,13 +359,26 @@ def test_full_size_solution_properties(cfg, s):
 
 # ------------------------------------------------- general (non-stencil) SELL --
 
+@pytest.mark.parametrize("layout", ["sell", "symstencil"])
 @pytest.mark.parametrize("cfg,n,s,rule", [(1, 64, 4, 0), (3, 30, 3, 0), (4, 24, 2, 0), (5, 20, 6, 0), (5, 20, 6, 1),
                                           (2, 64, 11, 0)])
-def test_general_sell_layout_parity(cfg, n, s, rule, monkeypatch):
-    """The explicit-column SELL-32 path (used when rows are not a common stencil) against the oracle."""
-    monkeypatch.setenv("LC_DISABLE_STENCIL", "1")
+def test_other_layouts_parity(cfg, n, s, rule, layout, monkeypatch):
+    """The explicit-column SELL-32 layout (rows without a common stencil) and the symmetric stencil layout
+    (opt-in, LC_SYMMETRIC=1) against the oracle; the default runs use the stencil layout."""
+    monkeypatch.setenv("LC_DISABLE_STENCIL" if layout == "sell" else "LC_SYMMETRIC", "1")
+    if cfg == 4 and layout == "symstencil":
+        layout = "stencil"                      # the 3T blocks are nonsymmetric: never symmetric storage
     sy = synth.system(cfg, s, n=n, G=4)
+    A = gpu_matrix(sy)
+    assert A.info()["layout"] == layout
     check_system(sy, RULES[cfg][rule])
+
+
+def test_default_layouts():
+    """All five configs are stencils: the default layout is the stencil layout."""
+    for cfg, n, expect in [(1, 64, "stencil"), (5, 12, "stencil"), (3, 16, "stencil"), (4, 16, "stencil")]:
+        sy = synth.system(cfg, 1, n=n, G=3)
+        assert gpu_matrix(sy).info()["layout"] == expect, cfg
 
 
 def test_irregular_pattern_uses_general_layout():
