@@ -69,6 +69,7 @@ struct PcgArgs {
   int reg_units;                // > 0: equal segments of reg_units units, spg slices each (arithmetic maps)
   int spg;
   int vec2;                     // flat double2 update pass (G = 1, no list, aligned)
+  int tma;                      // pass A values staged by TMA (G = 1, no list, stencil layout)
 };
 
 struct SegState {
@@ -211,6 +212,107 @@ __device__ __forceinline__ void tl_mark(int& k) {
 #ifndef LCV_MINB
 #define LCV_MINB 4
 #endif
+// Pass A with the value stream staged by TMA (single segment, stencil layouts, no slice list): CTA b owns
+// the chunks c = b + t nCTA of 8 consecutive slices (exactly the slices its 8 warps take in the
+// interleaved order); thread 0 keeps kStages chunks in flight with cp.async.bulk into a shared-memory
+// ring (mbarrier complete_tx), the warps read their slice's values from shared memory, so the DRAM
+// stream no longer waits on each warp's gather latency.  Gathers and the symmetric mirrors stay loads.
+constexpr int kStages = 2;
+template <int WM, int ST, int MODE>
+__device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64_t* bars, int64_t bid, int64_t nCTA,
+                                           int warp, int lane, bool init, double beta,
+                                           const double* __restrict__ pold, double* __restrict__ pnew, double& a0,
+                                           double& a1) {
+  const SellView& A = P.A;
+  constexpr int W = WM > 0 ? WM : 1;
+  const int vw = A.vw;
+  const int64_t njs = P.slist ? *P.nlist : A.nslices;          // index space: listed or all slices
+  const int64_t nch = (njs + kPW - 1) / kPW;
+  const int64_t chd = (int64_t)kPW * 32 * vw;                    // doubles per chunk
+  const int n = (int)A.nunits, nu1 = n - 1;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kStages; ++st) mbar_init(&bars[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int64_t t) {
+    const int64_t c = bid + t * nCTA;
+    if (c >= nch) return;
+    const int st = (int)(t % kStages);
+    const int64_t j0c = (int64_t)kPW * c;
+    const int nsl = (int)((njs - j0c) < kPW ? (njs - j0c) : kPW);
+    const unsigned sbytes = (unsigned)(32 * vw * 8);
+    if (!P.slist) {                                              // 8 consecutive slices: one copy
+      mbar_expect_tx(&bars[st], sbytes * nsl);
+      tma_bulk_g2s(stg + st * chd, A.val + j0c * 32 * vw, sbytes * nsl, &bars[st]);
+    } else {                                                     // listed slices: one copy each
+      mbar_expect_tx(&bars[st], sbytes * nsl);
+      for (int w = 0; w < nsl; ++w)
+        tma_bulk_g2s(stg + st * chd + (int64_t)w * 32 * vw, A.val + (int64_t)P.slist[j0c + w] * 32 * vw, sbytes,
+                     &bars[st]);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int t = 0; t < kStages; ++t) issue(t);
+#pragma unroll 1
+  for (int64_t t = 0;; ++t) {
+    const int64_t c = bid + t * nCTA;
+    if (c >= nch) break;
+    const int st = (int)(t % kStages);
+    mbar_wait(&bars[st], (unsigned)((t / kStages) & 1));
+    const int64_t js = (int64_t)kPW * c + warp;
+    const int64_t s = js < njs ? (P.slist ? (int64_t)P.slist[js] : js) : 0;
+    const int u = (int)(32 * s) + lane;
+    if (js < njs && u < n) {
+      const bool in = !P.omega || P.omega[u] != 255;
+      const double* sp = stg + st * chd + (int64_t)warp * 32 * vw + lane;
+      double v[W], y[W];
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        int cc = u + A.off[k];
+        cc = cc < 0 ? 0 : (cc > nu1 ? nu1 : cc);
+        if (ST == 2) {
+          if (k >= A.kd) v[k] = sp[32 * (k - A.kd)];
+          else {
+            const int vr = u + A.off[k];
+            v[k] = vr < 0 ? 0.0 : __ldg(A.val + 32ll * vw * (vr >> 5) + 32 * A.mir[k] + (vr & 31));
+          }
+        } else {
+          v[k] = sp[32 * k];
+        }
+        if (MODE == 0) y[k] = P.x[cc];
+        else if (MODE == 1) y[k] = P.z[cc];
+        else y[k] = __fma_rn(beta, pold[cc], P.z[cc]);
+      }
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < W; ++k) acc = __fma_rn(v[k], y[k], acc);
+      if (MODE == 0) {
+        if (in) {
+          const double bi = P.b[u];
+          const double ri = bi - acc;
+          P.r[u] = ri;
+          a0 = __fma_rn(ri, ri, a0);
+          if (init) a1 = __fma_rn(bi, bi, a1);
+        }
+      } else if (in) {
+        double pi = 0.0;
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+          if (A.off[k] == 0) pi = y[k];
+        pnew[u] = pi;
+        P.q[u] = acc;
+        a0 = __fma_rn(pi, acc, a0);
+      }
+    }
+    __syncthreads();                               // every warp is done with stage st
+    if (threadIdx.x == 0) {
+      fence_proxy_async_smem();                    // generic reads of st before the async-proxy refill
+      issue(t + kStages);
+    }
+  }
+}
+
 template <int WM, int ST>
 __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   __shared__ SegState S[kMaxSeg];
@@ -221,6 +323,8 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   __shared__ long long s_segj0[kMaxSeg + 1];   // segment runs in slice space
   __shared__ int s_act[kMaxSeg + 1];           // active segments of the current pass (+ sentinel)
   __shared__ long long s_actj[kMaxSeg + 1];    // their runs concatenated
+  extern __shared__ __align__(128) double dsm[];   // TMA stages (P.tma): kStages x 8 slices x 32 x vw values
+  __shared__ __align__(8) uint64_t s_bars[kStages];
   const SellView& A = P.A;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nCTA = gridDim.x, bid = blockIdx.x;
@@ -339,7 +443,14 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       const double beta = S[0].beta;
       const double* pold = S[0].par ? P.p1 : P.p0;
       double* pnew = S[0].par ? P.p0 : P.p1;
-      if (mode == M_INIT || mode == M_CONFIRM)
+      if (ST && WM > 0 && P.tma) {
+        if (mode == M_INIT || mode == M_CONFIRM)
+          pass_a_tma<WM, ST, 0>(P, dsm, s_bars, bid, nCTA, warp, lane, mode == M_INIT, beta, pold, pnew, a0, a1);
+        else if (mode == M_FIRST)
+          pass_a_tma<WM, ST, 1>(P, dsm, s_bars, bid, nCTA, warp, lane, false, beta, pold, pnew, a0, a1);
+        else if (mode == M_NORMAL)
+          pass_a_tma<WM, ST, 2>(P, dsm, s_bars, bid, nCTA, warp, lane, false, beta, pold, pnew, a0, a1);
+      } else if (mode == M_INIT || mode == M_CONFIRM)
         pass_a_loop<WM, ST, 0>(P, j0, jlim, jstep, lane, mode == M_INIT, beta, pold, pnew, a0, a1);
       else if (mode == M_FIRST)
         pass_a_loop<WM, ST, 1>(P, j0, jlim, jstep, lane, false, beta, pold, pnew, a0, a1);
@@ -575,7 +686,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
 }
 
 // ---------------------------------------------------------------- host ----
-static int g_pcg_max_ctas[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+static int g_pcg_max_ctas[18] = {0};
 
 lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
   const Sell& M = *job.M;
@@ -590,15 +701,21 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
                         (void*)k_pcg<5, 1>, (void*)k_pcg<7, 1>, (void*)k_pcg<0, 1>,
                         (void*)k_pcg<5, 2>, (void*)k_pcg<7, 2>, (void*)k_pcg<0, 2>};
   void* fn = fns[wi];
-  if (!g_pcg_max_ctas[wi]) {
+  // TMA staging for contiguous slice ranges (global solves); slice-list (masked) solves keep plain loads: the
+  // per-slice bulk copies were 4% slower there in the bench (profiles/r01_h_tma_ab.txt)
+  const bool tma = M.stencil && M.maxw <= 7 && G == 1 && !job.slist && getenv("LC_NO_TMA") == nullptr;
+  const size_t dsmem = tma ? (size_t)kStages * kPW * 32 * (M.sym ? M.vw : M.maxw) * sizeof(double) : 0;
+  const int ci = wi * 2 + (tma ? 1 : 0);
+  if (!g_pcg_max_ctas[ci]) {
+    if (dsmem > 48 * 1024) LC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
     int per_sm = 0;
-    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPT, 0));
+    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPT, dsmem));
     if (per_sm < 1) { set_error("PCG kernel does not fit on an SM"); return LC_ERR_CUDA; }
-    g_pcg_max_ctas[wi] = per_sm * num_sms();
+    g_pcg_max_ctas[ci] = per_sm * num_sms();
   }
   const int64_t n = M.nunits;
   const int64_t work = job.slist ? job.nlist_max : M.nslices;
-  int64_t nCTA = std::min<int64_t>(g_pcg_max_ctas[wi], (std::max<int64_t>(work, 1) + kPW - 1) / kPW);
+  int64_t nCTA = std::min<int64_t>(g_pcg_max_ctas[ci], (std::max<int64_t>(work, 1) + kPW - 1) / kPW);
   if (nCTA < 1) nCTA = 1;
   void* ws = nullptr;
   const size_t vec = sizeof(double) * (size_t)n;
@@ -642,6 +759,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   a.G = G;
   a.reg_units = job.reg_units;
   a.spg = job.spg;
+  a.tma = tma ? 1 : 0;
   a.vec2 = (G == 1 && !job.slist && !job.omega &&
             ((((uintptr_t)a.x) | ((uintptr_t)a.r) | ((uintptr_t)a.z) | ((uintptr_t)a.q) | ((uintptr_t)a.p0) |
               ((uintptr_t)a.p1) | ((uintptr_t)M.dinv)) & 15) == 0) ? 1 : 0;
@@ -652,7 +770,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0, s);
   void* args[] = {&a};
-  if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kPT), args, 0, s);
+  if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kPT), args, dsmem, s);
   count_launch();
   cudaEventRecord(e1, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(it.data(), a.out_iters, 4 * G, cudaMemcpyDeviceToHost, s);
