@@ -760,7 +760,8 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   a.reg_units = job.reg_units;
   a.spg = job.spg;
   a.tma = tma ? 1 : 0;
-  a.vec2 = (G == 1 && !job.slist && !job.omega &&
+  // (masked solves qualify too: rows outside Omega hold p = q = r = z = 0 and x = 0, the update keeps them 0)
+  a.vec2 = (G == 1 && !job.slist &&
             ((((uintptr_t)a.x) | ((uintptr_t)a.r) | ((uintptr_t)a.z) | ((uintptr_t)a.q) | ((uintptr_t)a.p0) |
               ((uintptr_t)a.p1) | ((uintptr_t)M.dinv)) & 15) == 0) ? 1 : 0;
   if (e == cudaSuccess) e = cudaMemsetAsync(a.bar, 0, 64, s);

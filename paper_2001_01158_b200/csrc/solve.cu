@@ -57,6 +57,8 @@ extern "C" lc_status lc_solve_local(lc_sub S, const lc_solver_params* p, double*
     const lc_matrix_s* A = S->A;
     PcgJob job;
     job.M = &A->A; job.b = S->bs; job.x_init = S->xm0; job.slist = S->slist; job.nlist_dev = S->nlist; job.lseg = S->lseg;
+    // near-full domains: sweep all slices with the Omega mask instead of the list (contiguous, TMA-staged)
+    if (A->batch == 1 && S->K_units * 10 >= A->n * 8) job.slist = nullptr;
     job.nlist_max = std::min<int64_t>(A->A.nslices, S->K_units);
     job.omega = S->omega; job.x_user = x;
     job.reg_units = A->seg_units; job.spg = (A->seg_units + 31) / 32;
