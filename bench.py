@@ -227,14 +227,15 @@ def run_lc(args):
         trafficdb = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except OSError:
         trafficdb = {}
-    # GMRES(m): per Arnoldi step j of a cycle: 8 nnz + 88 N + 24 (j+1) N bytes
+    # GMRES(m), low-sync CGS2 (R39): per Arnoldi step j: 8 nnz + 80 N + 16 (j+1) N bytes
+    # (M^-1 apply 48 N; SpMV + w write + one V read for h and the Gram column; one merged update pass)
     m_restart = 30
 
     def gmres_bytes(steps):
         tot, left = 0.0, steps
         while left > 0:
             L = min(m_restart, left)
-            tot += L * (8.0 * nnz + 88.0 * N) + 24.0 * N * L * (L + 1) / 2
+            tot += L * (8.0 * nnz + 80.0 * N) + 16.0 * N * L * (L + 1) / 2
             tot += 8.0 * nnz + 24.0 * N + (8.0 * L + 48.0) * N        # true residual + x update per cycle
             left -= L
         return tot
@@ -280,7 +281,7 @@ def run_lc(args):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650",
                 "layout": Ainfo["layout"],
                 "bytes_rule": (f"{rule} + 96 B/row vectors per PCG iteration" if solver == "pcg"
-                               else "8 B/nnz + 88 B/unknown + 24 (j+1) B/unknown per Arnoldi step j")}
+                               else "8 B/nnz + 80 B/unknown + 16 (j+1) B/unknown per Arnoldi step j")}
 
     # ---- e2e: host buffers through the C-ABI, H2D + D2H inside the timed region
     e2e = None

@@ -130,7 +130,7 @@ typedef struct {
   int32_t method;    /* LC_PCG (Jacobi-preconditioned CG, SPD systems) | LC_GMRES (right-preconditioned
                         block-Jacobi GMRES(restart) with CGS2, nonsymmetric block = 3 systems) */
   int32_t precond;   /* LC_JACOBI for LC_PCG; LC_BLOCK_JACOBI (3x3 cell blocks) for LC_GMRES */
-  int32_t restart;   /* GMRES restart length (30); ignored by PCG; <= 64 */
+  int32_t restart;   /* GMRES restart length (30); ignored by PCG; <= 40 */
   double rel_tol;    /* eps of Eq. 6: stop when ||b - A x||_2 <= eps ||b||_2 (absolute if b = 0) */
   int32_t max_iters; /* PCG: SpMVs with p; GMRES: Arnoldi steps.  Exceeding -> LC_NOT_CONVERGED */
 } lc_solver_params;

@@ -12,6 +12,7 @@
 // fixed-order reductions, so control flow is grid-uniform without any host
 // round trip.  End of cycle: x += M^-1 (V y), then the true residual (R19).
 #include <cmath>
+#include <cstdlib>
 
 #include "lc_internal.cuh"
 
@@ -21,7 +22,8 @@ namespace lc {
 
 constexpr int kGT = 512;
 constexpr int kGW = kGT / 32;
-constexpr int kMaxM = 64;
+constexpr int kMaxM = 40;
+constexpr int kMaxQ = 2 * (kMaxM + 1) + 2;   // reduced quantities per phase
 
 struct GmresArgs {
   SellView A;
@@ -41,6 +43,7 @@ struct GmresArgs {
   double eps;
   int m;
   int max_iters;
+  int exact_cgs2;       // 1: textbook two-pass CGS2 (4 barriers, 4 passes over V per step); 0: Gram form (R39)
 };
 
 template <int BS>
@@ -54,8 +57,19 @@ __device__ __forceinline__ void block_apply(const double* __restrict__ Mi, const
   }
 }
 
+#ifdef LC_DEBUG_TIMELINE
+__device__ unsigned long long g_tlg[16384];
+#define TLG(k) do { if (blockIdx.x == 0 && threadIdx.x == 0 && (k) < 16384) { unsigned long long _t; \
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t)); g_tlg[(k)] = _t; } ++(k); } while (0)
+#else
+#define TLG(k) (void)0
+#endif
+
 template <int BS>
-__global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
+__global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
+#ifdef LC_DEBUG_TIMELINE
+  int tk = 0;
+#endif
   const SellView& A = P.A;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nCTA = gridDim.x, bid = blockIdx.x;
@@ -65,12 +79,13 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
   const int m = P.m;
   __shared__ double H[(kMaxM + 1) * kMaxM];
   __shared__ double gv[kMaxM + 1], cs[kMaxM], sn[kMaxM], yv[kMaxM];
-  __shared__ double red[kMaxM + 2];
-  __shared__ double s_acc[kGW][kMaxM + 2];
+  __shared__ double red[kMaxQ];
+  __shared__ double s_acc[kGW][kMaxQ];
+  __shared__ double Gm[(kMaxM + 1) * (kMaxM + 1)];   // Gram matrix V^T V (low-sync CGS2, R39)
 
   // per-lane accumulators -> per-warp smem -> CTA partial part[q*nCTA + bid]
   auto clear = [&](int nq) {
-    for (int t = threadIdx.x; t < kGW * (kMaxM + 2); t += kGT) (&s_acc[0][0])[t] = 0.0;
+    for (int t = threadIdx.x; t < kGW * kMaxQ; t += kGT) (&s_acc[0][0])[t] = 0.0;
     __syncthreads();
     (void)nq;
   };
@@ -160,6 +175,7 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
     const double* src = P.r;
     int jend = 0;
     for (int j = 0; j < m; ++j) {
+      TLG(tk);
       double* Vj = P.V + (size_t)j * n;
       // ---- 1a: v_j = src / h, t = M^-1 v_j
       for (int64_t s = s_begin; s < A.nslices; s += s_step) {
@@ -172,91 +188,166 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
 #pragma unroll
         for (int a = 0; a < BS; ++a) P.t[BS * u + a] = tt[a];
       }
+      TLG(tk);
       grid_barrier(P.bar);
-      // ---- 1b: w = A t, h_i = V_i . w
+      TLG(tk);
+      // ---- 1b: w = A t, h_i = V_i . w.  A warp owns 1-2 slices per chunk: their w values stay in registers
+      // and the (j+1) dots are formed i by i (no per-thread accumulator array in local memory).
       clear(j + 1);
-      {
-        double dacc[kMaxM + 1];
-        for (int i = 0; i <= j; ++i) dacc[i] = 0.0;
-        for (int64_t s = s_begin; s < A.nslices; s += s_step) {
-          int64_t u = A.slice_row0[s] + lane;
-          bool valid = u < nunits;
-          double acc[BS];
+      for (int64_t s0 = s_begin; s0 < A.nslices; s0 += 2 * s_step) {
+        double wv[2][BS];
+        int64_t uu[2];
+        bool ok[2];
 #pragma unroll
-          for (int a = 0; a < BS; ++a) acc[a] = 0.0;
-          if (valid) {
-            int64_t p0 = A.slice_ptr[s];
-            int wd = A.stencil ? A.W : (int)((A.slice_ptr[s + 1] - p0) >> 5);
+        for (int cc = 0; cc < 2; ++cc) {
+          const int64_t s = s0 + cc * s_step;
+          uu[cc] = s < A.nslices ? A.slice_row0[s] + lane : nunits;
+          ok[cc] = uu[cc] < nunits;
+#pragma unroll
+          for (int a = 0; a < BS; ++a) wv[cc][a] = 0.0;
+          if (ok[cc]) {
+            const int64_t u = uu[cc];
+            const int64_t p0 = A.slice_ptr[s];
+            const int wd = A.stencil ? A.W : (int)((A.slice_ptr[s + 1] - p0) >> 5);
             for (int k = 0; k < wd; ++k) {
-              int64_t c = sv_col(A, p0 + lane, k, u);
+              const int64_t c = sv_col(A, p0 + lane, k, u);
               if (BS == 1) {
-                acc[0] = __fma_rn(sv_val(A, p0 + lane, k, u), P.t[c], acc[0]);
+                wv[cc][0] = __fma_rn(sv_val(A, p0 + lane, k, u), P.t[c], wv[cc][0]);
               } else {
                 const double* vb = A.val + 9 * (p0 + 32ll * k) + lane;
-                double y0 = P.t[3 * c], y1 = P.t[3 * c + 1], y2 = P.t[3 * c + 2];
+                const double y0 = P.t[3 * c], y1 = P.t[3 * c + 1], y2 = P.t[3 * c + 2];
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                  acc[a] = __fma_rn(vb[32 * (3 * a)], y0, acc[a]);
-                  acc[a] = __fma_rn(vb[32 * (3 * a + 1)], y1, acc[a]);
-                  acc[a] = __fma_rn(vb[32 * (3 * a + 2)], y2, acc[a]);
+                  wv[cc][a] = __fma_rn(vb[32 * (3 * a)], y0, wv[cc][a]);
+                  wv[cc][a] = __fma_rn(vb[32 * (3 * a + 1)], y1, wv[cc][a]);
+                  wv[cc][a] = __fma_rn(vb[32 * (3 * a + 2)], y2, wv[cc][a]);
                 }
               }
             }
 #pragma unroll
-            for (int a = 0; a < BS; ++a) P.w[BS * u + a] = acc[a];
-          }
-          if (valid) {
-            for (int i = 0; i <= j; ++i) {
-              const double* Vi = P.V + (size_t)i * n;
-              double d = dacc[i];
-#pragma unroll
-              for (int a = 0; a < BS; ++a) d = __fma_rn(Vi[BS * u + a], acc[a], d);
-              dacc[i] = d;
-            }
+            for (int a = 0; a < BS; ++a) P.w[BS * u + a] = wv[cc][a];
           }
         }
-        for (int i = 0; i <= j; ++i) lane_flush(i, dacc[i]);
+        const double* Vj = P.V + (size_t)j * n;
+        for (int i = 0; i <= j; ++i) {
+          const double* Vi = P.V + (size_t)i * n;
+          double d = 0.0, gq = 0.0;
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc)
+            if (ok[cc]) {
+#pragma unroll
+              for (int a = 0; a < BS; ++a) {
+                const double vi = Vi[BS * uu[cc] + a];
+                d = __fma_rn(vi, wv[cc][a], d);
+                if (!P.exact_cgs2) gq = __fma_rn(vi, Vj[BS * uu[cc] + a], gq);
+              }
+            }
+          lane_flush(i, d);
+          if (!P.exact_cgs2) lane_flush(j + 1 + i, gq);
+        }
       }
+      if (!P.exact_cgs2) {
+        // ---- low-sync CGS2 (R39): G = V^T V gains column j in the same pass; the second projection
+        // h2 = V^T (w - V h) = h - G h comes from scalars, and both updates merge into one pass.
+        publish(2 * (j + 1));
+        TLG(tk);
+        grid_barrier(P.bar);
+        reduce(2 * (j + 1));
+        TLG(tk);
+        if (threadIdx.x <= j) {
+          Gm[threadIdx.x * (kMaxM + 1) + j] = red[j + 1 + threadIdx.x];
+          Gm[j * (kMaxM + 1) + threadIdx.x] = red[j + 1 + threadIdx.x];
+          H[threadIdx.x * m + j] = red[threadIdx.x];
+        }
+        __syncthreads();
+        __shared__ double hh[kMaxM + 1];
+        if (threadIdx.x <= j) {
+          const int i = threadIdx.x;
+          double gh = 0.0;
+          for (int k = 0; k <= j; ++k) gh = __fma_rn(Gm[i * (kMaxM + 1) + k], H[k * m + j], gh);
+          hh[i] = H[i * m + j] + (H[i * m + j] - gh);        // h + h2, h2 = h - G h
+        }
+        __syncthreads();
+        if (threadIdx.x <= j) H[threadIdx.x * m + j] = hh[threadIdx.x];
+        __syncthreads();
+        clear(1);
+        {
+          double a0 = 0.0;
+          for (int64_t s = s_begin; s < A.nslices; s += s_step) {
+            int64_t u = A.slice_row0[s] + lane;
+            if (u >= nunits) continue;
+            double ww[BS];
+#pragma unroll
+            for (int a = 0; a < BS; ++a) ww[a] = P.w[BS * u + a];
+            for (int i = 0; i <= j; ++i) {
+              const double* Vi = P.V + (size_t)i * n;
+              const double hi = hh[i];
+#pragma unroll
+              for (int a = 0; a < BS; ++a) ww[a] = __fma_rn(-hi, Vi[BS * u + a], ww[a]);
+            }
+#pragma unroll
+            for (int a = 0; a < BS; ++a) { P.w[BS * u + a] = ww[a]; a0 = __fma_rn(ww[a], ww[a], a0); }
+          }
+          lane_flush(0, a0);
+        }
+        publish(1);
+        TLG(tk);
+        grid_barrier(P.bar);
+        reduce(1);
+        TLG(tk);
+      } else {
       publish(j + 1);
+      TLG(tk);
       grid_barrier(P.bar);
       reduce(j + 1);
+      TLG(tk);
       // keep h in smem column j of H (pass-1 part)
       if (threadIdx.x <= j) H[threadIdx.x * m + j] = red[threadIdx.x];
       __syncthreads();
-      // ---- 2: w -= V h, h2_i = V_i . w
+      // ---- 2: w -= V h, h2_i = V_i . w (same register chunking)
       clear(j + 1);
-      {
-      double dacc[kMaxM + 1];
-      for (int i = 0; i <= j; ++i) dacc[i] = 0.0;
-      for (int64_t s = s_begin; s < A.nslices; s += s_step) {
-        int64_t u = A.slice_row0[s] + lane;
-        bool valid = u < nunits;
-        double ww[BS];
-        if (valid) {
+      for (int64_t s0 = s_begin; s0 < A.nslices; s0 += 2 * s_step) {
+        double wv[2][BS];
+        int64_t uu[2];
+        bool ok[2];
 #pragma unroll
-          for (int a = 0; a < BS; ++a) ww[a] = P.w[BS * u + a];
-          for (int i = 0; i <= j; ++i) {
-            const double* Vi = P.V + (size_t)i * n;
-            double hi = H[i * m + j];
+        for (int cc = 0; cc < 2; ++cc) {
+          const int64_t s = s0 + cc * s_step;
+          uu[cc] = s < A.nslices ? A.slice_row0[s] + lane : nunits;
+          ok[cc] = uu[cc] < nunits;
 #pragma unroll
-            for (int a = 0; a < BS; ++a) ww[a] = __fma_rn(-hi, Vi[BS * u + a], ww[a]);
-          }
+          for (int a = 0; a < BS; ++a) wv[cc][a] = 0.0;
+          if (ok[cc]) {
+            const int64_t u = uu[cc];
 #pragma unroll
-          for (int a = 0; a < BS; ++a) P.w[BS * u + a] = ww[a];
-          for (int i = 0; i <= j; ++i) {
-            const double* Vi = P.V + (size_t)i * n;
-            double d = dacc[i];
+            for (int a = 0; a < BS; ++a) wv[cc][a] = P.w[BS * u + a];
+            for (int i = 0; i <= j; ++i) {
+              const double* Vi = P.V + (size_t)i * n;
+              const double hi = H[i * m + j];
 #pragma unroll
-            for (int a = 0; a < BS; ++a) d = __fma_rn(Vi[BS * u + a], ww[a], d);
-            dacc[i] = d;
+              for (int a = 0; a < BS; ++a) wv[cc][a] = __fma_rn(-hi, Vi[BS * u + a], wv[cc][a]);
+            }
+#pragma unroll
+            for (int a = 0; a < BS; ++a) P.w[BS * u + a] = wv[cc][a];
           }
         }
-      }
-      for (int i = 0; i <= j; ++i) lane_flush(i, dacc[i]);
+        for (int i = 0; i <= j; ++i) {
+          const double* Vi = P.V + (size_t)i * n;
+          double d = 0.0;
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc)
+            if (ok[cc]) {
+#pragma unroll
+              for (int a = 0; a < BS; ++a) d = __fma_rn(Vi[BS * uu[cc] + a], wv[cc][a], d);
+            }
+          lane_flush(i, d);
+        }
       }
       publish(j + 1);
+      TLG(tk);
       grid_barrier(P.bar);
       reduce(j + 1);
+      TLG(tk);
       // ---- 3: w -= V h2, ||w||^2
       clear(1);
       {
@@ -282,8 +373,11 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
         lane_flush(0, a0);
       }
       publish(1);
+      TLG(tk);
       grid_barrier(P.bar);
       reduce(1);
+      TLG(tk);
+      }
       if (threadIdx.x == 0) {
         double hn = sqrt(red[0]);
         H[(j + 1) * m + j] = hn;
@@ -299,10 +393,10 @@ __global__ void __launch_bounds__(kGT) k_gmres(GmresArgs P) {
         H[(j + 1) * m + j] = 0.0;
         gv[j + 1] = -sn[j] * gv[j];
         gv[j] = cs[j] * gv[j];
-        red[kMaxM + 1] = hn;
+        red[kMaxQ - 1] = hn;
       }
       __syncthreads();
-      hnorm = red[kMaxM + 1];
+      hnorm = red[kMaxQ - 1];
       ++it;
       jend = j + 1;
       src = P.w;
@@ -369,7 +463,7 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   int64_t nCTA = std::min<int64_t>(g_gm_ctas[ci], (M.nslices + kGW - 1) / kGW);
   if (nCTA < 1) nCTA = 1;
   size_t vbytes = ((sizeof(double) * (size_t)n) + 255) & ~(size_t)255;
-  size_t bytes = vbytes * (3 + (m + 1) + (scatter_idx ? 1 : 0)) + sizeof(double) * (m + 2) * nCTA + 256;
+  size_t bytes = vbytes * (3 + (m + 1) + (scatter_idx ? 1 : 0)) + sizeof(double) * kMaxQ * nCTA + 256;
   void* ws = nullptr;
   lc_status st = dalloc(&ws, bytes, s);
   if (st) return st;
@@ -388,7 +482,7 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   } else {
     a.x = x;
   }
-  a.part = (double*)w; w += sizeof(double) * (m + 2) * nCTA;
+  a.part = (double*)w; w += sizeof(double) * kMaxQ * nCTA;
   a.bar = (GridBar*)w; w += 64;
   a.out = (int*)w;
   a.out_relres = (double*)(w + 16);
@@ -398,6 +492,7 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   a.eps = p->rel_tol;
   a.m = m;
   a.max_iters = p->max_iters;
+  a.exact_cgs2 = getenv("LC_GMRES_EXACT_CGS2") != nullptr ? 1 : 0;
   int out[2] = {0, 0};
   double rr = 0.0;
   float ms = 0.f;
@@ -422,3 +517,9 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
 }
 
 }  // namespace lc
+
+#ifdef LC_DEBUG_TIMELINE
+extern "C" int lc_debug_timeline_gmres(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, lc::g_tlg, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -1;
+}
+#endif

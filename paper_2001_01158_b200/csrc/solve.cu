@@ -16,7 +16,7 @@ static lc_status check_params(const lc_solver_params* p) {
     if (p->precond != LC_JACOBI) { set_error("PCG uses LC_JACOBI"); return LC_ERR_INVALID_ARG; }
   } else if (p->method == LC_GMRES) {
     if (p->precond != LC_BLOCK_JACOBI && p->precond != LC_JACOBI) { set_error("GMRES: bad precond"); return LC_ERR_INVALID_ARG; }
-    if (p->restart < 1 || p->restart > 64) { set_error("GMRES: restart in [1, 64]"); return LC_ERR_INVALID_ARG; }
+    if (p->restart < 1 || p->restart > 40) { set_error("GMRES: restart in [1, 40]"); return LC_ERR_INVALID_ARG; }
   } else {
     set_error("solver: method must be LC_PCG or LC_GMRES");
     return LC_ERR_INVALID_ARG;

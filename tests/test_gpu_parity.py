@@ -571,3 +571,18 @@ def test_gs_grid_detection_guard(case):
     x = to_dev(x0)
     lc.smooth_gs(A, to_dev(b), x, 2)
     np.testing.assert_array_equal(x.cpu().numpy(), orc.gauss_seidel(Ao, b, x0, 2))
+
+
+@pytest.mark.parametrize("variant", ["gram", "exact"])
+def test_gmres_cgs2_variants(variant, monkeypatch):
+    """R39: the Gram-form CGS2 (default) and the textbook two-pass CGS2 both match the oracle's GMRES."""
+    if variant == "exact":
+        monkeypatch.setenv("LC_GMRES_EXACT_CGS2", "1")
+    sy = synth.system(4, 7, n=48)
+    Ao = oracle_csr(sy)
+    A = gpu_matrix(sy)
+    x = to_dev(sy.x0)
+    info = lc.solve_global(A, to_dev(sy.b), x, method=lc.GMRES)
+    xo, it, st, _ = orc.gmres_bj(Ao, sy.b, sy.x0, bs=3)
+    assert info[0]["status"] == 0 and abs(info[0]["iterations"] - it) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xo) / np.linalg.norm(xo) <= 1e-9
