@@ -463,7 +463,7 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   int64_t nCTA = std::min<int64_t>(g_gm_ctas[ci], (M.nslices + kGW - 1) / kGW);
   if (nCTA < 1) nCTA = 1;
   size_t vbytes = ((sizeof(double) * (size_t)n) + 255) & ~(size_t)255;
-  size_t bytes = vbytes * (3 + (m + 1) + (scatter_idx ? 1 : 0)) + sizeof(double) * kMaxQ * nCTA + 256;
+  size_t bytes = vbytes * (3 + (m + 1) + (scatter_idx ? 1 : 0)) + sizeof(double) * kMaxQ * nCTA + sizeof(GridBar) + 384;
   void* ws = nullptr;
   lc_status st = dalloc(&ws, bytes, s);
   if (st) return st;
@@ -483,7 +483,8 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
     a.x = x;
   }
   a.part = (double*)w; w += sizeof(double) * kMaxQ * nCTA;
-  a.bar = (GridBar*)w; w += 64;
+  w = (char*)((((uintptr_t)w) + 127) & ~(uintptr_t)127);
+  a.bar = (GridBar*)w; w += sizeof(GridBar);
   a.out = (int*)w;
   a.out_relres = (double*)(w + 16);
   a.scatter_idx = scatter_idx;
@@ -498,7 +499,7 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   float ms = 0.f;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
-  cudaError_t e = cudaMemsetAsync(a.bar, 0, 64, s);
+  cudaError_t e = cudaMemsetAsync(a.bar, 0, sizeof(GridBar), s);
   cudaEventRecord(e0, s);
   void* args[] = {&a};
   if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kGT), args, 0, s);

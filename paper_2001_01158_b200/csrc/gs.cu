@@ -188,17 +188,18 @@ extern "C" lc_status lc_smooth_gs(lc_matrix M, const double* b, double* x, int32
     if (st) return st;
     LC_CUDA(cudaMemsetAsync(ws, 0, 64, s));
     unsigned bad = 0;
-    k_check_grid<<<(unsigned)((M->n + 255) / 256), 256, 0, s>>>(view(A), M->seg_units, gr, M->n, (unsigned*)ws + 8);
+    k_check_grid<<<(unsigned)((M->n + 255) / 256), 256, 0, s>>>(view(A), M->seg_units, gr, M->n, (unsigned*)ws);
     count_launch();
-    LC_CUDA(cudaMemcpyAsync(&bad, (unsigned*)ws + 8, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    LC_CUDA(cudaMemcpyAsync(&bad, ws, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     LC_CUDA(cudaStreamSynchronize(s));
-    if (bad) { dfree(ws, s); gr.nx = 0; }
+    dfree(ws, s);
+    if (bad) gr.nx = 0;
   }
   if (gr.nx > 0) {
     void* ws = nullptr;
-    lc_status st = dalloc(&ws, 64, s);
+    lc_status st = dalloc(&ws, sizeof(GridBar), s);
     if (st) return st;
-    LC_CUDA(cudaMemsetAsync(ws, 0, 64, s));
+    LC_CUDA(cudaMemsetAsync(ws, 0, sizeof(GridBar), s));
     const int64_t work = (int64_t)gr.ny * gr.nz * M->batch;
     int per_sm = 0;
     LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_levels, kGST, 0));

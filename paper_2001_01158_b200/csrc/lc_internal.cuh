@@ -257,11 +257,20 @@ __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long 
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Grid-wide barrier for cooperative (co-resident) launches: one arrive per CTA on a counter, the last
-// arriver resets it and bumps a generation word with release semantics; the others spin on the
-// generation with acquire loads (no sleep back-off, unlike cooperative_groups' grid sync, whose wake-up
-// latency measured 2-7 us per barrier on small grids: profiles/r01_d).  Both words must be zero at launch.
-struct GridBar { unsigned count; unsigned gen; };
+// Grid-wide barrier for cooperative (co-resident) launches: arrivals on counters, the last arriver resets
+// them and bumps a generation word with release semantics; the others spin on the generation with acquire
+// loads (no sleep back-off, unlike cooperative_groups' grid sync, whose wake-up latency measured 2-7 us
+// per barrier on small grids: profiles/r01_d).  The whole struct must be zero at launch.
+// Two-level arrival: CTA b arrives on sub-counter b % kBarSub (each on its own 128-B line, so the arrivals
+// spread over L2 slices instead of serialising on one address: a single counter cost ~3 us with 592 CTAs),
+// the last arriver of each sub-group arrives on the top counter, the last of those releases the generation.
+constexpr int kBarSub = 16;
+struct GridBar {
+  unsigned sub[kBarSub][32];
+  unsigned top;
+  unsigned gen;
+  unsigned pad[30];
+};
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -273,10 +282,23 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
 __device__ __forceinline__ void grid_barrier(GridBar* gb) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    const unsigned nb = gridDim.x, b = blockIdx.x;
     const unsigned g0 = ld_acquire_u32(&gb->gen);
     __threadfence();                                    // publish this CTA's writes (cumulative via bar.sync)
-    if (atomicAdd(&gb->count, 1u) == gridDim.x - 1) {
-      gb->count = 0;
+    bool last = false;
+    if (nb <= 64) {                                     // small grids: one counter (one round trip)
+      last = atomicAdd(&gb->top, 1u) == nb - 1;
+    } else {
+      const unsigned k = b % kBarSub;
+      const unsigned nk = (nb - k + kBarSub - 1) / kBarSub;        // CTAs in sub-group k
+      if (atomicAdd(&gb->sub[k][0], 1u) == nk - 1) {
+        gb->sub[k][0] = 0;
+        __threadfence();
+        last = atomicAdd(&gb->top, 1u) == (unsigned)kBarSub - 1;
+      }
+    }
+    if (last) {
+      gb->top = 0;
       st_release_u32(&gb->gen, g0 + 1);
     } else {
       while (ld_acquire_u32(&gb->gen) == g0) {

@@ -323,6 +323,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   __shared__ long long s_segj0[kMaxSeg + 1];   // segment runs in slice space
   __shared__ int s_act[kMaxSeg + 1];           // active segments of the current pass (+ sentinel)
   __shared__ long long s_actj[kMaxSeg + 1];    // their runs concatenated
+  __shared__ int s_na;                         // number of active segments of the current pass
   extern __shared__ __align__(128) double dsm[];   // TMA stages (P.tma): kStages x 8 slices x 32 x vw values
   __shared__ __align__(8) uint64_t s_bars[kStages];
   const SellView& A = P.A;
@@ -378,6 +379,25 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
         s_sum[0][threadIdx.x] = o;
       }
 #endif
+    } else if (s_na <= 4) {
+      // few active segments (the tail of a batched solve): every CTA sums their partials directly,
+      // saving the second barrier of the two-stage form; inactive segments' sums are never read
+      for (int ai = 0; ai < s_na; ++ai) {
+        const int g = s_act[ai];
+        double a0 = 0.0, a1 = 0.0;
+        for (int64_t c = threadIdx.x; c < nCTA; c += kPT) {
+          a0 += P.part[(c * G + g) * 2]; a1 += P.part[(c * G + g) * 2 + 1];
+        }
+        a0 = warp_sum(a0); a1 = warp_sum(a1);
+        if (lane == 0) { s_red[warp][0] = a0; s_red[warp][1] = a1; }
+        __syncthreads();
+        if (threadIdx.x < 2) {
+          double o = 0.0;
+          for (int w = 0; w < kPW; ++w) o += s_red[w][threadIdx.x];
+          s_sum[g][threadIdx.x] = o;
+        }
+        __syncthreads();
+      }
     } else {
       for (int g = (int)bid; g < G; g += (int)nCTA) {       // stage 1: CTA g reduces segment g
         double a0 = 0.0, a1 = 0.0;
@@ -423,6 +443,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       }
       s_actj[na] = J;
       s_act[na] = G;
+      s_na = na;
     }
     __syncthreads();
     int na = 0;
@@ -721,7 +742,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   const size_t vec = sizeof(double) * (size_t)n;
   const size_t vbytes = (vec + 255) & ~(size_t)255;
   const bool own_x = job.x_init != nullptr;
-  const size_t bytes = vbytes * (own_x ? 6 : 5) + sizeof(double) * 2 * G * (nCTA + 1) + 16 * G + 512;
+  const size_t bytes = vbytes * (own_x ? 6 : 5) + sizeof(double) * 2 * G * (nCTA + 1) + 16 * G + sizeof(GridBar) + 640;
   lc_status st = dalloc(&ws, bytes, s);
   if (st) return st;
   char* w = (char*)ws;
@@ -743,7 +764,8 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   if (job.omega && e == cudaSuccess) e = cudaMemsetAsync(a.r, 0, vbytes * 5, s);   // zero outside Omega
   a.part = (double*)w; w += sizeof(double) * 2 * G * nCTA;
   a.red = (double*)w; w += sizeof(double) * 2 * G;
-  a.bar = (GridBar*)w; w += 64;
+  w = (char*)((((uintptr_t)w) + 127) & ~(uintptr_t)127);
+  a.bar = (GridBar*)w; w += sizeof(GridBar);
   a.out_iters = (int*)w; w += 4 * G;
   a.out_status = (int*)w; w += 4 * G;
   a.out_relres = (double*)((((uintptr_t)w) + 7) & ~(uintptr_t)7);
@@ -764,7 +786,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   a.vec2 = (G == 1 && !job.slist &&
             ((((uintptr_t)a.x) | ((uintptr_t)a.r) | ((uintptr_t)a.z) | ((uintptr_t)a.q) | ((uintptr_t)a.p0) |
               ((uintptr_t)a.p1) | ((uintptr_t)M.dinv)) & 15) == 0) ? 1 : 0;
-  if (e == cudaSuccess) e = cudaMemsetAsync(a.bar, 0, 64, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(a.bar, 0, sizeof(GridBar), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(a.out_iters, 0, 8 * G, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(a.out_relres, 0, 8 * G, s);
   cudaEvent_t e0, e1;
