@@ -86,6 +86,16 @@ typedef struct lc_sub_s* lc_sub;
 lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, const int64_t* row_ptr, const int32_t* col_idx,
                         const double* values, int32_t inputs_on_device, int32_t fmt, void* stream, lc_matrix* A);
 
+/*
+ * New values for the SAME pattern A was created with (the systems of a time-step / Picard sequence share
+ * their mesh): row_ptr / col_idx must equal the creation arrays (not re-validated), values
+ * are copied into A's layout in place (host or device inputs as in lc_create_csr).  A zero diagonal ->
+ * LC_ERR_ZERO_DIAGONAL; values that are no longer symmetric under the symmetric stencil layout ->
+ * LC_ERR_PATTERN (recreate the matrix).  Syncs `stream`.
+ */
+lc_status lc_update_values(lc_matrix A, const int64_t* row_ptr, const int32_t* col_idx, const double* values,
+                           int32_t inputs_on_device, void* stream);
+
 typedef struct {
   int32_t criterion;     /* LC_CRIT_* */
   int32_t threshold;     /* LC_THR_* */

@@ -130,6 +130,7 @@ extern "C" lc_status lc_heat_run(const lc_heat_params* hp, double* T, int32_t* p
   if (hp->method == 1) dp = lc_domain_params{LC_CRIT_GRADIENT, LC_THR_REL_MAX, hp->alpha, 0, 0};
   if (hp->method == 2) dp = lc_domain_params{LC_CRIT_RESIDUAL, LC_THR_PAPER, hp->rel_tol, hp->e_max, 0};
   const unsigned nbr = (unsigned)std::min<int64_t>(kNB, (n + kNT - 1) / kNT);
+  lc_matrix A = nullptr;
 #define CKH(x) do { st = (x); if (st < 0) goto done; } while (0)
 #define CKHC(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { st = cuda_fail(_e, #x); goto done; } } while (0)
   for (int step = 0; step < hp->steps; ++step) {
@@ -139,15 +140,15 @@ extern "C" lc_status lc_heat_run(const lc_heat_params* hp, double* T, int32_t* p
     bool conv = false;
     while (sit < hp->picard_max && !conv) {
       CKH(lc_heat_assemble(nx, ny, hp->dt, hp->khalf, hp->t_left, hp->t_right, Ts, T, rp, ci, val, b, s));
-      lc_matrix A = nullptr;
-      CKH(lc_create_csr(n, 1, 1, rp, ci, val, 1, LC_FMT_SELL32, s, &A));
+      if (!A) CKH(lc_create_csr(n, 1, 1, rp, ci, val, 1, LC_FMT_SELL32, s, &A));   // pattern fixed for the run
+      else CKH(lc_update_values(A, rp, ci, val, 1, s));
       CKHC(cudaMemcpyAsync(Tn, Ts, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));  // x0 = previous iterate
       lc_solve_info info;
       if (hp->method > 0) {                                                           // Alg. 1 l.2-7
         lc_domain D = nullptr;
         int64_t K = 0;
         st = lc_select_domain(A, b, Tn, &dp, s, &D, &K);
-        if (st < 0) { lc_destroy_matrix(A); goto done; }
+        if (st < 0) goto done;
         eta_step += (double)K / n;
         R.eta_sum += (double)K / n;
         if (K > 0) {
@@ -158,14 +159,13 @@ extern "C" lc_status lc_heat_run(const lc_heat_params* hp, double* T, int32_t* p
           lc_destroy_sub(S);
         }
         lc_destroy_domain(D);
-        if (st < 0) { lc_destroy_matrix(A); goto done; }
+        if (st < 0) goto done;
         if (hp->gs_sweeps > 0) {
           st = lc_smooth_gs(A, b, Tn, hp->gs_sweeps, s);
-          if (st < 0) { lc_destroy_matrix(A); goto done; }
+          if (st < 0) goto done;
         }
       }
       st = lc_solve_global(A, b, Tn, &sp, s, &info);                                 // Alg. 1 l.8-11
-      lc_destroy_matrix(A);
       if (st < 0) goto done;
       R.it_global += info.iterations;
       // Picard test ||T^{n+1,s+1} - T^{n+1,s}||_2 < tol
@@ -189,6 +189,7 @@ extern "C" lc_status lc_heat_run(const lc_heat_params* hp, double* T, int32_t* p
   }
   st = LC_OK;
 done:
+  lc_destroy_matrix(A);
   dfree(ws, s);
   cudaStreamSynchronize(s);
   R.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -26,6 +26,7 @@
 // stencil SpMV restricted to rows in Omega on vectors that are zero outside
 // Omega, over the slices that contain Omega rows.  The dropped couplings
 // multiply exact zeros, so each row's fma chain equals B's chain (R22).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -70,6 +71,8 @@ struct PcgArgs {
   int spg;
   int vec2;                     // flat double2 update pass (G = 1, no list, aligned)
   int tma;                      // pass A values staged by TMA (G = 1, no list, stencil layout)
+  int cluster;                  // launched as ONE thread-block cluster (small G = 1 systems): cluster
+                                // barriers and DSMEM partial exchange instead of the global grid barrier
 };
 
 struct SegState {
@@ -324,6 +327,8 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   __shared__ int s_act[kMaxSeg + 1];           // active segments of the current pass (+ sentinel)
   __shared__ long long s_actj[kMaxSeg + 1];    // their runs concatenated
   __shared__ int s_na;                         // number of active segments of the current pass
+  __shared__ double s_cpart[2][2];             // cluster mode: this CTA's partials, double-buffered by pass
+  int cpar = 0;
   extern __shared__ __align__(128) double dsm[];   // TMA stages (P.tma): kStages x 8 slices x 32 x vw values
   __shared__ __align__(8) uint64_t s_bars[kStages];
   const SellView& A = P.A;
@@ -354,6 +359,24 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   // per-CTA partials -> part[bid][g][j]; then every CTA obtains s_sum[g][j] for all g (fixed order)
   auto reduce_all = [&]() {
     __syncthreads();
+    if (P.cluster) {
+      // one cluster (G = 1): partials stay in shared memory and are read across the cluster (DSMEM)
+      cg::cluster_group cl = cg::this_cluster();
+      if (threadIdx.x < 2) {
+        double v = 0.0;
+        for (int w = 0; w < kPW; ++w) v += s_acc[w][0][threadIdx.x];
+        s_cpart[cpar][threadIdx.x] = v;
+      }
+      cl.sync();
+      if (threadIdx.x < 2) {
+        double o = 0.0;
+        for (int r = 0; r < (int)nCTA; ++r) o += cl.map_shared_rank(&s_cpart[cpar][0], r)[threadIdx.x];
+        s_sum[0][threadIdx.x] = o;
+      }
+      cpar ^= 1;
+      __syncthreads();
+      return;
+    }
     for (int t = threadIdx.x; t < G * 2; t += kPT) {
       double v = 0.0;
       for (int w = 0; w < kPW; ++w) v += s_acc[w][t >> 1][t & 1];
@@ -736,6 +759,8 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   }
   const int64_t n = M.nunits;
   const int64_t work = job.slist ? job.nlist_max : M.nslices;
+  // small single-segment solves: one cluster of <= 16 CTAs (<= 512 slices = 4 per warp)
+  const bool clus = G == 1 && work <= 16 * kPW * 4 && getenv("LC_NO_CLUSTER") == nullptr;
   int64_t nCTA = std::min<int64_t>(g_pcg_max_ctas[ci], (std::max<int64_t>(work, 1) + kPW - 1) / kPW);
   if (nCTA < 1) nCTA = 1;
   void* ws = nullptr;
@@ -781,7 +806,8 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   a.G = G;
   a.reg_units = job.reg_units;
   a.spg = job.spg;
-  a.tma = tma ? 1 : 0;
+  a.tma = tma && !clus ? 1 : 0;
+  a.cluster = clus ? 1 : 0;
   // (masked solves qualify too: rows outside Omega hold p = q = r = z = 0 and x = 0, the update keeps them 0)
   a.vec2 = (G == 1 && !job.slist &&
             ((((uintptr_t)a.x) | ((uintptr_t)a.r) | ((uintptr_t)a.z) | ((uintptr_t)a.q) | ((uintptr_t)a.p0) |
@@ -793,7 +819,36 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0, s);
   void* args[] = {&a};
-  if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kPT), args, dsmem, s);
+  if (clus) {
+    static bool nonportable_set[9] = {false};
+    if (!nonportable_set[wi]) {
+      cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      nonportable_set[wi] = true;
+    }
+    unsigned csz = (unsigned)std::min<int64_t>(16, std::max<int64_t>(1, (work + 4 * kPW - 1) / (4 * kPW)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(csz);
+    cfg.blockDim = dim3(kPT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csz;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (e == cudaSuccess) e = cudaLaunchKernelExC(&cfg, fn, args);
+    if (e != cudaSuccess && csz > 8) {           // non-portable size refused: fall back to 8
+      cudaGetLastError();
+      csz = 8;
+      cfg.gridDim = dim3(csz);
+      attr[0].val.clusterDim.x = csz;
+      e = cudaLaunchKernelExC(&cfg, fn, args);
+    }
+  } else if (e == cudaSuccess) {
+    e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kPT), args, dsmem, s);
+  }
   count_launch();
   cudaEventRecord(e1, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(it.data(), a.out_iters, 4 * G, cudaMemcpyDeviceToHost, s);

@@ -450,3 +450,93 @@ extern "C" void lc_destroy_matrix(lc_matrix A) {
   cudaStreamSynchronize(0);
   delete A;
 }
+
+// New values for the pattern A was created with (the systems of a time-step / Picard sequence share their
+// mesh): refills the layout in place, skipping pattern validation and layout detection.
+extern "C" lc_status lc_update_values(lc_matrix M, const int64_t* row_ptr, const int32_t* col_idx,
+                                      const double* values, int32_t inputs_on_device, void* stream) {
+  if (!M || !row_ptr || !col_idx || !values) { set_error("lc_update_values: null argument"); return LC_ERR_INVALID_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  Sell& A = M->A;
+  const int64_t n = M->n;
+  const int bb = M->block * M->block;
+  const int spg = (M->seg_units + 31) / 32;
+  const int64_t nnz = M->nnz;
+  const int64_t* d_rp = row_ptr;
+  const int32_t* d_ci = col_idx;
+  const double* d_va = values;
+  void *t_rp = nullptr, *t_ci = nullptr, *t_va = nullptr, *t_err = nullptr, *t_full = nullptr;
+  lc_status st = LC_OK;
+  unsigned h_err = 0;
+#define CK(x) do { st = (x); if (st) goto fail; } while (0)
+#define CKC(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { st = cuda_fail(_e, #x); goto fail; } } while (0)
+  if (!inputs_on_device) {
+    CK(dalloc(&t_rp, sizeof(int64_t) * (n + 1), s));
+    CK(dalloc(&t_ci, sizeof(int32_t) * nnz, s));
+    CK(dalloc(&t_va, sizeof(double) * nnz * bb, s));
+    CKC(cudaMemcpyAsync(t_rp, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+    CKC(cudaMemcpyAsync(t_ci, col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+    CKC(cudaMemcpyAsync(t_va, values, sizeof(double) * nnz * bb, cudaMemcpyHostToDevice, s));
+    d_rp = (const int64_t*)t_rp; d_ci = (const int32_t*)t_ci; d_va = (const double*)t_va;
+  }
+  CK(dalloc(&t_err, 16, s));
+  CKC(cudaMemsetAsync(t_err, 0, 16, s));
+  {
+    const unsigned nb = (unsigned)((n + 255) / 256);
+    if (A.stencil) {
+      Offsets O;
+      O.W = A.maxw;
+      for (int k = 0; k < kMaxOff; ++k) O.off[k] = A.off[k];
+      double* dst = A.val;
+      if (A.sym) {                                  // refill a full-width buffer, check symmetry, compact
+        CK(dalloc(&t_full, sizeof(double) * 32ll * A.maxw * A.nslices, s));
+        CKC(cudaMemsetAsync(t_full, 0, sizeof(double) * 32ll * A.maxw * A.nslices, s));
+        dst = (double*)t_full;
+      }
+      if (M->block == 1)
+        k_fill_stencil<1><<<nb, 256, 0, s>>>(n, M->seg_units, spg, d_rp, d_ci, d_va, O, dst, A.mask, A.dinv,
+                                             (unsigned*)t_err);
+      else
+        k_fill_stencil<3><<<nb, 256, 0, s>>>(n, M->seg_units, spg, d_rp, d_ci, d_va, O, dst, A.mask, A.dinv,
+                                             (unsigned*)t_err);
+      count_launch();
+      CKC(cudaGetLastError());
+      if (A.sym) {
+        k_check_sym<<<nb, 256, 0, s>>>(n, M->seg_units, spg, O, A.kd, dst, (unsigned*)((char*)t_err + 4));
+        count_launch();
+        const int64_t tot = 32ll * A.vw * A.nslices;
+        k_compact_upper<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(A.nslices, A.maxw, A.kd, dst, A.val);
+        count_launch();
+        CKC(cudaGetLastError());
+      }
+    } else {
+      const unsigned blocks = (unsigned)((A.nslices * 32 + 255) / 256);
+      if (M->block == 1)
+        k_fill<1><<<blocks, 256, 0, s>>>(A.nslices, M->seg_units, spg, d_rp, d_ci, d_va, A.slice_ptr, A.col, A.val,
+                                         A.dinv, (unsigned*)t_err);
+      else
+        k_fill<3><<<blocks, 256, 0, s>>>(A.nslices, M->seg_units, spg, d_rp, d_ci, d_va, A.slice_ptr, A.col, A.val,
+                                         A.dinv, (unsigned*)t_err);
+      count_launch();
+      CKC(cudaGetLastError());
+    }
+  }
+  {
+    unsigned e2[2] = {0, 0};
+    CKC(cudaMemcpyAsync(e2, t_err, 8, cudaMemcpyDeviceToHost, s));
+    CKC(cudaStreamSynchronize(s));
+    h_err = e2[0] | (e2[1] ? kErrNotStencil : 0u);
+  }
+  if (h_err & kErrZeroDiag) { st = LC_ERR_ZERO_DIAGONAL; set_error("lc_update_values: zero diagonal"); goto fail; }
+  if (h_err & kErrNotStencil) {
+    st = LC_ERR_PATTERN;
+    set_error("lc_update_values: values no longer symmetric (symmetric stencil layout); recreate the matrix");
+    goto fail;
+  }
+fail:
+  dfree(t_rp, s); dfree(t_ci, s); dfree(t_va, s); dfree(t_err, s); dfree(t_full, s);
+  if (st) cudaStreamSynchronize(s);
+  return st;
+#undef CK
+#undef CKC
+}

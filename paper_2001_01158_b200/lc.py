@@ -27,7 +27,7 @@ _STATUS = {0: "LC_OK", 1: "LC_NOT_CONVERGED", -1: "LC_ERR_INVALID_ARG", -2: "LC_
            -3: "LC_ERR_PATTERN", -4: "LC_ERR_ZERO_DIAGONAL", -5: "LC_ERR_BREAKDOWN", -6: "LC_ERR_NONFINITE",
            -7: "LC_ERR_CUDA", -8: "LC_ERR_OOM"}
 
-EXPORTED = ["lc_create_csr", "lc_select_domain", "lc_domain_export", "lc_extract_sub", "lc_solve_local",
+EXPORTED = ["lc_create_csr", "lc_update_values", "lc_select_domain", "lc_domain_export", "lc_extract_sub", "lc_solve_local",
             "lc_solve_global", "lc_smooth_gs", "lc_heat_assemble", "lc_heat_run", "lc_matrix_info", "lc_destroy_matrix", "lc_destroy_domain",
             "lc_destroy_sub",
             "lc_last_error", "lc_kernel_launches"]
@@ -88,10 +88,12 @@ def load_library(path: str = LIB_PATH):
     lib.lc_solve_global.argtypes = [P, P, P, ctypes.POINTER(SolverParams), P, P]
     lib.lc_matrix_info.argtypes = [P, P, P, P, P, P, P, P]
     lib.lc_smooth_gs.argtypes = [P, P, P, I32, P]
+    lib.lc_update_values.argtypes = [P, P, P, P, I32, P]
     lib.lc_heat_assemble.argtypes = [I32, I32, D, I32, D, D, P, P, P, P, P, P, P]
     lib.lc_heat_run.argtypes = [ctypes.POINTER(HeatParams), P, P, P, P, ctypes.POINTER(HeatReport)]
     for f in ("lc_create_csr", "lc_select_domain", "lc_domain_export", "lc_extract_sub", "lc_solve_local",
-              "lc_solve_global", "lc_matrix_info", "lc_smooth_gs", "lc_heat_assemble", "lc_heat_run"):
+              "lc_solve_global", "lc_matrix_info", "lc_smooth_gs", "lc_heat_assemble", "lc_heat_run",
+              "lc_update_values"):
         getattr(lib, f).restype = ctypes.c_int
     for f in ("lc_destroy_matrix", "lc_destroy_domain", "lc_destroy_sub"):
         getattr(lib, f).argtypes = [P]
@@ -147,6 +149,20 @@ class Matrix:
                                    s, ctypes.byref(h))
         _check(st, "lc_create_csr", ok=(LC_OK,))
         self.h = h
+
+    def update_values(self, row_ptr, col_idx, values):
+        """New values for the pattern the matrix was created with (lc_update_values)."""
+        s = _stream()
+        if isinstance(row_ptr, torch.Tensor) and row_ptr.is_cuda:
+            st = load_library().lc_update_values(self.h, _dptr(row_ptr, torch.int64), _dptr(col_idx, torch.int32),
+                                                 _dptr(values, torch.float64), 1, s)
+        else:
+            import numpy as np
+            rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+            ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+            va = np.ascontiguousarray(values, dtype=np.float64)
+            st = load_library().lc_update_values(self.h, rp.ctypes.data, ci.ctypes.data, va.ctypes.data, 0, s)
+        _check(st, "lc_update_values", ok=(LC_OK,))
 
     @property
     def N(self):

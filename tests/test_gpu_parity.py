@@ -586,3 +586,25 @@ def test_gmres_cgs2_variants(variant, monkeypatch):
     xo, it, st, _ = orc.gmres_bj(Ao, sy.b, sy.x0, bs=3)
     assert info[0]["status"] == 0 and abs(info[0]["iterations"] - it) <= 1
     assert np.linalg.norm(x.cpu().numpy() - xo) / np.linalg.norm(xo) <= 1e-9
+
+
+@pytest.mark.parametrize("layout", ["stencil", "sell", "symstencil"])
+def test_update_values_equals_fresh_create(layout, monkeypatch):
+    """lc_update_values (same mesh, new values: the next system of the sequence) gives exactly the matrix a
+    fresh lc_create_csr would: identical residual criterion and identical solve."""
+    if layout == "sell":
+        monkeypatch.setenv("LC_DISABLE_STENCIL", "1")
+    if layout == "symstencil":
+        monkeypatch.setenv("LC_SYMMETRIC", "1")
+    s1, s2 = synth.system(5, 3, n=20), synth.system(5, 4, n=20)
+    A = gpu_matrix(s1)
+    A.update_values(s2.rp, s2.ci, s2.val)
+    B = gpu_matrix(s2)
+    b, x0 = to_dev(s2.b), to_dev(s2.x0)
+    ca = lc.select_domain(A, b, x0).export(want_crit=True)[2]
+    cb = lc.select_domain(B, b, x0).export(want_crit=True)[2]
+    assert torch.equal(ca, cb)
+    xa, xb = x0.clone(), x0.clone()
+    lc.solve_global(A, b, xa)
+    lc.solve_global(B, b, xb)
+    assert torch.equal(xa, xb)
