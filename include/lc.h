@@ -228,6 +228,87 @@ typedef struct {
 lc_status lc_heat_run(const lc_heat_params* p, double* T, int32_t* picard_per_step, double* eta_per_step,
                       void* stream, lc_heat_report* rep);
 
+/* ---- NEXT-4: the row-partitioned multi-GPU form (Sec. 2.4, Alg. 4/5) ----
+ *
+ * A, b, x are partitioned by rows over p ranks: rank l owns the contiguous slab
+ * I_l = [row0_l, row0_l + n_l), slabs ascending by rank and covering [0, N).  One lc_dist handle = one
+ * rank's slab (its rows of A in the stencil layout, offsets relative to the slab) plus a workspace whose
+ * iterate vectors and exchange block are PEER-VISIBLE (plain cudaMalloc, exportable by CUDA IPC).
+ * The kernels read the neighbour slabs' halo rows directly from peer memory ("communicate all adjacency
+ * components", Alg. 4 l.4 / Alg. 5 l.4, l.17) and perform every global reduction (Alg. 4 l.9, l.15,
+ * Alg. 5 l.11, l.27, the Krylov dot products) as a fixed-order exchange through each rank's exchange block:
+ * no NCCL call and no host round trip inside a phase; every rank obtains bitwise identical scalars.
+ *
+ * Two ways to run p ranks:
+ *   - one process per GPU: each process creates its rank's handle, exports it (lc_dist_export_handle),
+ *     the caller all-gathers the handles (e.g. torch.distributed) and calls lc_dist_connect; every compute
+ *     call then takes ranks = &own handle, nr = 1, and all p processes must make the same calls in the same
+ *     order (each rank's kernel waits for its peers' contributions);
+ *   - emulation (p ranks on ONE device, one process): lc_dist_connect_local wires the handles together and
+ *     every compute call takes all p handles (nr = p): ONE cooperative launch runs all ranks' CTAs, so the
+ *     ranks' mutual waits are between co-resident CTAs (never separate launches waiting on each other).
+ * Restrictions: block = 1, a constant-offset stencil (<= 8 offsets) in every slab (LC_ERR_PATTERN
+ * otherwise), p <= 8, each slab at least as long as the stencil reach into it (checked at connect),
+ * Jacobi-PCG solves, residual or gradient criterion with the paper / rel-max thresholds.
+ */
+typedef struct lc_dist_s* lc_dist;
+enum { LC_DIST_MAX_RANKS = 8, LC_DIST_HANDLE_BYTES = 64 };
+
+/*
+ * Rank `rank` of `nranks`: rows [row0, row0 + n_local) of the n_global-row matrix A.  row_ptr [n_local + 1]
+ * (int64, row_ptr[0] = 0), col_idx (int32, GLOBAL column numbers, strictly ascending per row, diagonal
+ * stored) and values (f64); host arrays, or device arrays if inputs_on_device.  Copied.  Allocates the
+ * rank's workspace (about 6 vectors of n_local f64 + n_local bytes).  Syncs `stream`.
+ */
+lc_status lc_dist_create(int64_t n_global, int64_t row0, int64_t n_local, int32_t rank, int32_t nranks,
+                         const int64_t* row_ptr, const int32_t* col_idx, const double* values,
+                         int32_t inputs_on_device, void* stream, lc_dist* D);
+
+/* CUDA IPC handle (LC_DIST_HANDLE_BYTES bytes, host) of the rank's peer-visible workspace */
+lc_status lc_dist_export_handle(lc_dist D, void* handle);
+
+/*
+ * One process per rank: open every peer's workspace.  handles: host, nranks x LC_DIST_HANDLE_BYTES in rank
+ * order (the own entry is ignored); n_local_all: host [nranks] slab lengths.  LC_ERR_DIMENSION when a
+ * neighbour slab is shorter than the stencil reach into it.
+ */
+lc_status lc_dist_connect(lc_dist D, const void* handles, const int64_t* n_local_all);
+
+/* Emulation: all nranks handles of this process (rank order, one device) see each other directly. */
+lc_status lc_dist_connect_local(lc_dist* ranks, int32_t nranks);
+
+/*
+ * Alg. 4 (gradient) / Alg. 5 (residual) on the partition, followed by the masked
+ * extraction of Eq. 3 (b_sub on Omega rows, x_B0 = x0 on Omega) for lc_dist_solve_local.  ranks: the nr
+ * handles this call drives (see above); b, x0: host arrays of nr device pointers to each rank's slab
+ * [n_local].  The threshold uses the GLOBAL ||b||_2 (double-double, R23) and N, or the global max of the
+ * criterion; an expansion round stops when the GLOBAL admission count is 0 (R40), so Omega equals
+ * the one lc_select_domain finds on the whole matrix.  Dilation hops as in lc_select_domain; the percentile
+ * threshold is not supported here.  K_global (host, optional): |Omega| over all ranks.  Syncs `stream`.
+ */
+lc_status lc_dist_select_domain(lc_dist* ranks, int32_t nr, const double* const* b, const double* const* x0,
+                                const lc_domain_params* p, void* stream, int64_t* K_global);
+
+/* The rank's domain flags: flag_dev (device, optional, [n_local]) = stage at which row row0 + i entered
+   Omega (0 = criterion, 1.. = expansion / dilation round) or 255 = outside; tau_host (host, optional). */
+lc_status lc_dist_domain_export(lc_dist D, uint8_t* flag_dev, double* tau_host, void* stream);
+
+/*
+ * Alg. 1 l.5-6 on the partition: Jacobi-PCG on B xbar = b_sub from x_B0 (the state lc_dist_select_domain
+ * left in the handles), tolerance eps ||b_sub||_2 (global), then x~[Omega] = xbar (Eq. 4).  x: host array of
+ * nr device pointers (in = x0 slab, out = x~ slab).  info (host, optional): the global iteration count,
+ * status and relative residual (identical on every rank).  K = 0: no-op with 0 iterations.  Syncs `stream`.
+ */
+lc_status lc_dist_solve_local(lc_dist* ranks, int32_t nr, const lc_solver_params* p, double* const* x, void* stream,
+                              lc_solve_info* info);
+
+/* Alg. 1 l.8-11 / method0 on the partition: Jacobi-PCG on A x = b from x (b, x: host arrays of nr device
+   pointers to the slabs; x in/out).  p->method must be LC_PCG.  Syncs `stream`. */
+lc_status lc_dist_solve_global(lc_dist* ranks, int32_t nr, const double* const* b, double* const* x,
+                               const lc_solver_params* p, void* stream, lc_solve_info* info);
+
+void lc_dist_destroy(lc_dist D);
+
 /* introspection (host outputs, each optional): unknowns n*block, stored scalars, batch, SELL slices, max row
    length (slots), layout (LC_LAYOUT_*), bytes one SpMV streams for the matrix (values + columns + metadata) */
 lc_status lc_matrix_info(lc_matrix A, int64_t* n_unknowns, int64_t* nnz, int32_t* batch, int64_t* nslices,

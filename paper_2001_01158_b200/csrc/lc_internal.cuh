@@ -338,5 +338,8 @@ lc_status compact_flags(const uint8_t* flag, int64_t m, int32_t* idx, int32_t* i
                         cudaStream_t s);
 // build slice_row0/slice_seg from seg_unit0/seg_slice0 (device)
 lc_status build_slice_map(Sell& M, cudaStream_t s);
+// NEXT-4: stencil layout of the rank slab [row0, row0 + n) of an nglob-row matrix (sell.cu)
+lc_status build_slab(int64_t nglob, int64_t row0, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                     const double* values, int on_device, cudaStream_t s, Sell& A, int64_t* nnz_out);
 
 }  // namespace lc

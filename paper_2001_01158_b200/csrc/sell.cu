@@ -226,6 +226,132 @@ __global__ void k_fill(int64_t nslices, int seg_units, int spg, const int64_t* _
   }
 }
 
+// ------------------------------------------------------------------ slabs ----
+// NEXT-4 (Alg. 4/5): rank slab = rows [row0, row0 + n) of an nglob-row matrix.  Each row must be
+// ascending, inside [0, nglob), with its diagonal and at most kMaxOff entries; cs = ci - row0 (slab-relative
+// columns, may leave [0, n): the halo owned by the neighbour slabs).
+__global__ void k_slab_check(int64_t n, int64_t row0, int64_t nglob, const int64_t* __restrict__ rp,
+                             const int32_t* __restrict__ ci, int32_t* __restrict__ cs, unsigned* err, int* maxw) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const int64_t k0 = rp[u], k1 = rp[u + 1], l = k1 - k0;
+  unsigned e = 0;
+  if (l < 1 || l > kMaxOff) e |= kErrRowLen;
+  bool diag = false;
+  int64_t prev = -1;
+  for (int64_t k = k0; k < k1 && !(e & kErrRowLen); ++k) {
+    const int64_t c = ci[k];
+    if (c <= prev || c >= nglob) e |= kErrPattern;
+    if (c == row0 + u) diag = true;
+    prev = c;
+    cs[k] = (int32_t)(c - row0);
+  }
+  if (!diag) e |= kErrPattern;
+  if (e) atomicOr(err, e);
+  atomicMax(maxw, (int)(l > 255 ? 255 : l));
+}
+
+lc_status build_slab(int64_t nglob, int64_t row0, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                     const double* values, int on_device, cudaStream_t s, Sell& A, int64_t* nnz_out) {
+  lc_status st = LC_OK;
+  int64_t nnz = 0, rp0 = 0;
+  if (on_device) {
+    LC_CUDA(cudaMemcpyAsync(&rp0, row_ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    LC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    LC_CUDA(cudaStreamSynchronize(s));
+  } else {
+    rp0 = row_ptr[0];
+    nnz = row_ptr[n];
+  }
+  if (rp0 != 0 || nnz < n || nnz > (int64_t)kMaxOff * n) {
+    set_error("lc_dist_create: row_ptr must start at 0 with 1..8 entries per row");
+    return LC_ERR_PATTERN;
+  }
+  *nnz_out = nnz;
+  void *t_rp = nullptr, *t_ci = nullptr, *t_va = nullptr, *t_cs = nullptr, *t_err = nullptr;
+  const int64_t* d_rp = row_ptr;
+  const int32_t* d_ci = col_idx;
+  const double* d_va = values;
+  unsigned h_err = 0;
+  int h_maxw = 0, best = 0;
+  int64_t k0 = 0;
+  int32_t cols[kMaxOff];
+  Offsets O;
+  const unsigned nb = (unsigned)((n + 255) / 256);
+#define CK(x) do { st = (x); if (st) goto done; } while (0)
+#define CKC(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { st = cuda_fail(_e, #x); goto done; } } while (0)
+  if (!on_device) {
+    CK(dalloc(&t_rp, sizeof(int64_t) * (n + 1), s));
+    CK(dalloc(&t_ci, sizeof(int32_t) * nnz, s));
+    CK(dalloc(&t_va, sizeof(double) * nnz, s));
+    CKC(cudaMemcpyAsync(t_rp, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+    CKC(cudaMemcpyAsync(t_ci, col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+    CKC(cudaMemcpyAsync(t_va, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+    d_rp = (const int64_t*)t_rp; d_ci = (const int32_t*)t_ci; d_va = (const double*)t_va;
+  }
+  CK(dalloc(&t_cs, sizeof(int32_t) * nnz, s));
+  CK(dalloc(&t_err, 16, s));
+  CKC(cudaMemsetAsync(t_err, 0, 16, s));
+  k_slab_check<<<nb, 256, 0, s>>>(n, row0, nglob, d_rp, d_ci, (int32_t*)t_cs, (unsigned*)t_err,
+                                  (int*)((char*)t_err + 8));
+  count_launch();
+  CKC(cudaGetLastError());
+  CKC(cudaMemcpyAsync(&h_err, t_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  CKC(cudaMemcpyAsync(&h_maxw, (char*)t_err + 8, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CKC(cudaStreamSynchronize(s));
+  if (h_err) {
+    st = LC_ERR_PATTERN;
+    set_error("lc_dist_create: rows need 1..8 strictly ascending columns in [0, n_global) with the diagonal");
+    goto done;
+  }
+  // stencil offsets: those of the slab's first longest row; every entry must match one (else not a stencil)
+  {
+    int big = INT32_MAX;
+    CKC(cudaMemcpyAsync((char*)t_err + 12, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+    k_first_maxrow<<<nb, 256, 0, s>>>(n, d_rp, h_maxw, (int*)((char*)t_err + 12));
+    count_launch();
+    CKC(cudaMemcpyAsync(&best, (char*)t_err + 12, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CKC(cudaStreamSynchronize(s));
+    CKC(cudaMemcpyAsync(&k0, d_rp + best, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CKC(cudaStreamSynchronize(s));
+    CKC(cudaMemcpyAsync(cols, (int32_t*)t_cs + k0, sizeof(int32_t) * h_maxw, cudaMemcpyDeviceToHost, s));
+    CKC(cudaStreamSynchronize(s));
+  }
+  O.W = h_maxw;
+  for (int k = 0; k < kMaxOff; ++k) O.off[k] = k < h_maxw ? cols[k] - best : 0;
+  k_check_stencil<<<nb, 256, 0, s>>>(n, d_rp, (const int32_t*)t_cs, O, (unsigned*)t_err);
+  count_launch();
+  CKC(cudaMemcpyAsync(&h_err, t_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  CKC(cudaStreamSynchronize(s));
+  if (h_err & kErrNotStencil) {
+    st = LC_ERR_PATTERN;
+    set_error("lc_dist_create: the slab is not a constant-offset stencil (<= 8 offsets); the row-partitioned "
+              "path needs the stencil layout");
+    goto done;
+  }
+  A.block = 1; A.nunits = n; A.nseg = 1; A.maxw = h_maxw; A.stencil = 1;
+  A.spg = (int)((n + 31) / 32); A.nslices = A.spg; A.reg_units = (int)n;
+  for (int k = 0; k < kMaxOff; ++k) A.off[k] = O.off[k];
+  A.nslots = 32ll * h_maxw * A.nslices;
+  CK(dalloc((void**)&A.val, sizeof(double) * A.nslots, s));
+  CK(dalloc((void**)&A.mask, n, s));
+  CK(dalloc((void**)&A.dinv, sizeof(double) * n, s));
+  CKC(cudaMemsetAsync(A.val, 0, sizeof(double) * A.nslots, s));
+  k_fill_stencil<1><<<nb, 256, 0, s>>>(n, (int)n, A.spg, d_rp, (const int32_t*)t_cs, d_va, O, A.val, A.mask, A.dinv,
+                                       (unsigned*)t_err);
+  count_launch();
+  CKC(cudaGetLastError());
+  CKC(cudaMemcpyAsync(&h_err, t_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  CKC(cudaStreamSynchronize(s));
+  if (h_err & kErrZeroDiag) { st = LC_ERR_ZERO_DIAGONAL; set_error("lc_dist_create: zero diagonal"); }
+done:
+  dfree(t_rp, s); dfree(t_ci, s); dfree(t_va, s); dfree(t_cs, s); dfree(t_err, s);
+  if (st) { A.release(s); cudaStreamSynchronize(s); }
+  return st;
+#undef CK
+#undef CKC
+}
+
 }  // namespace lc
 
 using namespace lc;

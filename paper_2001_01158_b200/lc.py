@@ -29,8 +29,10 @@ _STATUS = {0: "LC_OK", 1: "LC_NOT_CONVERGED", -1: "LC_ERR_INVALID_ARG", -2: "LC_
 
 EXPORTED = ["lc_create_csr", "lc_update_values", "lc_select_domain", "lc_domain_export", "lc_extract_sub", "lc_solve_local",
             "lc_solve_global", "lc_smooth_gs", "lc_heat_assemble", "lc_heat_run", "lc_matrix_info", "lc_destroy_matrix", "lc_destroy_domain",
-            "lc_destroy_sub",
-            "lc_last_error", "lc_kernel_launches"]
+            "lc_destroy_sub", "lc_dist_create", "lc_dist_export_handle", "lc_dist_connect", "lc_dist_connect_local",
+            "lc_dist_select_domain", "lc_dist_domain_export", "lc_dist_solve_local", "lc_dist_solve_global",
+            "lc_dist_destroy", "lc_last_error", "lc_kernel_launches"]
+DIST_HANDLE_BYTES = 64
 
 
 class LcError(RuntimeError):
@@ -95,6 +97,20 @@ def load_library(path: str = LIB_PATH):
               "lc_solve_global", "lc_matrix_info", "lc_smooth_gs", "lc_heat_assemble", "lc_heat_run",
               "lc_update_values"):
         getattr(lib, f).restype = ctypes.c_int
+    PP = ctypes.POINTER(P)
+    lib.lc_dist_create.argtypes = [I64, I64, I64, I32, I32, P, P, P, I32, P, PP]
+    lib.lc_dist_export_handle.argtypes = [P, P]
+    lib.lc_dist_connect.argtypes = [P, P, P]
+    lib.lc_dist_connect_local.argtypes = [PP, I32]
+    lib.lc_dist_select_domain.argtypes = [PP, I32, PP, PP, ctypes.POINTER(DomainParams), P, P]
+    lib.lc_dist_domain_export.argtypes = [P, P, P, P]
+    lib.lc_dist_solve_local.argtypes = [PP, I32, ctypes.POINTER(SolverParams), PP, P, ctypes.POINTER(SolveInfo)]
+    lib.lc_dist_solve_global.argtypes = [PP, I32, PP, PP, ctypes.POINTER(SolverParams), P, ctypes.POINTER(SolveInfo)]
+    for f in ("lc_dist_create", "lc_dist_export_handle", "lc_dist_connect", "lc_dist_connect_local",
+              "lc_dist_select_domain", "lc_dist_domain_export", "lc_dist_solve_local", "lc_dist_solve_global"):
+        getattr(lib, f).restype = ctypes.c_int
+    lib.lc_dist_destroy.argtypes = [P]
+    lib.lc_dist_destroy.restype = None
     for f in ("lc_destroy_matrix", "lc_destroy_domain", "lc_destroy_sub"):
         getattr(lib, f).argtypes = [P]
         getattr(lib, f).restype = None
@@ -329,3 +345,106 @@ def heat_run(nx, ny, T0: torch.Tensor, steps, method=0, alpha=1e-4, e_max=1, gs_
     _check(load_library().lc_heat_run(ctypes.byref(p), _dptr(T, torch.float64, nx * ny), per.ctypes.data, eta.ctypes.data,
                             _stream(), ctypes.byref(rep)), "lc_heat_run", ok=(LC_OK,))
     return T, per[:steps], eta[:steps], rep
+
+
+# ---- NEXT-4: row-partitioned multi-GPU form (include/lc.h "lc_dist_*", Alg. 4/5) ----
+
+class DistRank:
+    """One rank's row slab [row0, row0 + n_local) of an n_global-row stencil system (lc_dist_create).
+    row_ptr (0-based, n_local + 1), col_idx (GLOBAL columns) and values: host numpy arrays or CUDA tensors."""
+
+    def __init__(self, n_global, row0, n_local, rank, nranks, row_ptr, col_idx, values):
+        lib = load_library()
+        s = _stream()
+        self.n_global, self.row0, self.n_local = int(n_global), int(row0), int(n_local)
+        self.rank, self.nranks = int(rank), int(nranks)
+        h = ctypes.c_void_p()
+        if isinstance(row_ptr, torch.Tensor) and row_ptr.is_cuda:
+            st = lib.lc_dist_create(n_global, row0, n_local, rank, nranks, _dptr(row_ptr, torch.int64),
+                                    _dptr(col_idx, torch.int32), _dptr(values, torch.float64), 1, s, ctypes.byref(h))
+        else:
+            import numpy as np
+            rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+            ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+            va = np.ascontiguousarray(values, dtype=np.float64)
+            st = lib.lc_dist_create(n_global, row0, n_local, rank, nranks, rp.ctypes.data, ci.ctypes.data,
+                                    va.ctypes.data, 0, s, ctypes.byref(h))
+        _check(st, "lc_dist_create", ok=(LC_OK,))
+        self.h = h
+
+    def export_handle(self) -> bytes:
+        buf = (ctypes.c_char * DIST_HANDLE_BYTES)()
+        _check(load_library().lc_dist_export_handle(self.h, buf), "lc_dist_export_handle", ok=(LC_OK,))
+        return bytes(buf)
+
+    def connect(self, handles, n_local_all):
+        """One process per rank: handles = every rank's export_handle() bytes in rank order."""
+        import numpy as np
+        blob = b"".join(handles)
+        nl = np.ascontiguousarray(n_local_all, dtype=np.int64)
+        _check(load_library().lc_dist_connect(self.h, blob, nl.ctypes.data), "lc_dist_connect", ok=(LC_OK,))
+
+    def domain_flags(self):
+        """-> (uint8 CUDA tensor [n_local]: stage or 255, tau)"""
+        f = torch.empty(self.n_local, dtype=torch.uint8, device="cuda")
+        tau = ctypes.c_double()
+        _check(load_library().lc_dist_domain_export(self.h, _dptr(f, torch.uint8), ctypes.byref(tau), _stream()),
+               "lc_dist_domain_export", ok=(LC_OK,))
+        return f, tau.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.lc_dist_destroy(self.h)
+            self.h = None
+
+
+def _handles(ranks):
+    return (ctypes.c_void_p * len(ranks))(*[r.h.value for r in ranks])
+
+
+def _ptrs(ts, ranks):
+    return (ctypes.c_void_p * len(ts))(*[_dptr(t, torch.float64, r.n_local).value for t, r in zip(ts, ranks)])
+
+
+def dist_connect_local(ranks):
+    """Emulation: all ranks of the partition in this process (one device)."""
+    _check(load_library().lc_dist_connect_local(_handles(ranks), len(ranks)), "lc_dist_connect_local", ok=(LC_OK,))
+
+
+def dist_select_domain(ranks, b, x0, criterion=CRIT_RESIDUAL, threshold=THR_PAPER, param=1e-10, expand_rounds=0,
+                       dilate_hops=0) -> int:
+    """Alg. 4 / 5 on the partition (+ the masked extraction); returns the global K."""
+    p = DomainParams(criterion, threshold, param, expand_rounds, dilate_hops)
+    K = ctypes.c_int64()
+    _check(load_library().lc_dist_select_domain(_handles(ranks), len(ranks), _ptrs(b, ranks), _ptrs(x0, ranks),
+                                                ctypes.byref(p), _stream(), ctypes.byref(K)),
+           "lc_dist_select_domain", ok=(LC_OK,))
+    return K.value
+
+
+def dist_solve_local(ranks, x, rel_tol=1e-10, max_iters=20000):
+    p = _solver(PCG, rel_tol, max_iters, 30)
+    info = SolveInfo()
+    _check(load_library().lc_dist_solve_local(_handles(ranks), len(ranks), ctypes.byref(p), _ptrs(x, ranks),
+                                              _stream(), ctypes.byref(info)), "lc_dist_solve_local")
+    return _infos([info])[0]
+
+
+def dist_solve_global(ranks, b, x, rel_tol=1e-10, max_iters=20000):
+    p = _solver(PCG, rel_tol, max_iters, 30)
+    info = SolveInfo()
+    _check(load_library().lc_dist_solve_global(_handles(ranks), len(ranks), _ptrs(b, ranks), _ptrs(x, ranks),
+                                               ctypes.byref(p), _stream(), ctypes.byref(info)), "lc_dist_solve_global")
+    return _infos([info])[0]
+
+
+def dist_local_method(ranks, b, x0, domain: dict | None, rel_tol=1e-10, max_iters=20000):
+    """Alg. 1 on the partition: domain (Alg. 4/5) + masked extraction, local solve + assembly, global solve.
+    b, x0: per-rank slab tensors.  Returns (x slabs, report)."""
+    x = [t.clone() for t in x0]
+    rep = {"K": 0}
+    if domain is not None:
+        rep["K"] = dist_select_domain(ranks, b, x0, **domain)
+        rep["local"] = dist_solve_local(ranks, x, rel_tol, max_iters)
+    rep["global"] = dist_solve_global(ranks, b, x, rel_tol, max_iters)
+    return x, rep
