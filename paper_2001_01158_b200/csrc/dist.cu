@@ -10,7 +10,7 @@
 //   - every global reduction (||b||, max c, K, the admission counts, the Krylov dots) is a fixed-order
 //     exchange: after the rank's grid barrier its CTA 0 combines the per-CTA partials, stores the rank's
 //     4-vector into slot [seq & 1][rank] of EVERY rank's exchange block and raises flag[rank] = seq there
-//     (st.release.sys after a system fence); every CTA of every rank waits for all flags >= seq and combines
+//     (st.release.sys); every CTA of every rank waits for all flags >= seq and combines
 //     the p slots in rank order, so all ranks hold bitwise identical scalars and take identical decisions.
 //     Slots are double-buffered by seq parity: a rank can publish seq + 2 only after every rank published
 //     seq + 1, which each did after all of its CTAs had read seq.
@@ -19,6 +19,7 @@
 // between co-resident CTAs (B200_PROFILING: never separate launches that wait on each other).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -68,6 +69,12 @@ struct DArgs {
   // d[1] global K
   int* out_i;
   double* out_d;
+};
+
+// every rank slot's arguments travel in the launch's parameter space (constant bank: loop-invariant fields
+// stay in registers, no aliasing with the stores of the passes)
+struct DPack {
+  DArgs a[kMaxRanks];
 };
 
 // ---------------------------------------------------------------- memory ops ----
@@ -150,6 +157,7 @@ __device__ void xreduce(const DArgs& P, unsigned bid, unsigned nCTA, int op, dou
     for (int j = 0; j < 4; ++j) P.part[4 * bid + j] = c[j];
   }
   rank_barrier(P.bar, nCTA, bid);
+  const int par = (int)(seq & 1);
   if (bid == 0) {
     double c[4] = {0.0, 0.0, 0.0, 0.0};
     for (unsigned i = threadIdx.x; i < nCTA; i += kDT) comb(op, c, P.part + 4 * i);
@@ -161,24 +169,29 @@ __device__ void xreduce(const DArgs& P, unsigned bid, unsigned nCTA, int op, dou
     if (threadIdx.x == 0) {
       double t[4] = {s_w[0][0], s_w[0][1], s_w[0][2], s_w[0][3]};
       for (int w = 1; w < kDW; ++w) comb(op, t, s_w[w]);
-      const int par = (int)(seq & 1);
-      for (int q = 0; q < P.nranks; ++q)
-        for (int j = 0; j < 4; ++j) P.xpeer[q]->slot[par][P.rank][j] = t[j];
-      __threadfence_system();
-      for (int q = 0; q < P.nranks; ++q) st_rel_sys(&P.xpeer[q]->flag[P.rank], seq);
+      for (int j = 0; j < 4; ++j) s_out[j] = t[j];
+    }
+    __syncthreads();
+    // thread q publishes the rank's value to rank q (in parallel over the ranks)
+    if (threadIdx.x < (unsigned)P.nranks) {
+      DXch* X = P.xpeer[threadIdx.x];
+      for (int j = 0; j < 4; ++j) X->slot[par][P.rank][j] = s_out[j];
+      st_rel_sys(&X->flag[P.rank], seq);          // release at system scope: the slot and (cumulatively)
+                                                  // the rank's pass writes observed through its barrier
     }
   }
-  if (threadIdx.x == 0) {
-    const int par = (int)(seq & 1);
-    double t[4];
-    for (int q = 0; q < P.nranks; ++q) {
-      while (ld_acq_sys(&P.xch->flag[q]) < seq) {
-      }
-      double v[4];
-      for (int j = 0; j < 4; ++j) v[j] = __ldcv(&P.xch->slot[par][q][j]);
-      if (q == 0) { for (int j = 0; j < 4; ++j) t[j] = v[j]; }
-      else comb(op, t, v);
+  // thread q waits for rank q's value; thread 0 then combines the ranks in order
+  __shared__ double s_v[kMaxRanks][4];
+  if (threadIdx.x < (unsigned)P.nranks) {
+    const int q = threadIdx.x;
+    while (ld_acq_sys(&P.xch->flag[q]) < seq) {
     }
+    for (int j = 0; j < 4; ++j) s_v[q][j] = __ldcv(&P.xch->slot[par][q][j]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t[4] = {s_v[0][0], s_v[0][1], s_v[0][2], s_v[0][3]};
+    for (int q = 1; q < P.nranks; ++q) comb(op, t, s_v[q]);
     for (int j = 0; j < 4; ++j) s_out[j] = t[j];
   }
   __syncthreads();
@@ -224,73 +237,178 @@ __device__ __forceinline__ bool slice_edge(const DArgs& P, int64_t s) {
 // ---------------------------------------------------------------- PCG ----
 enum DMode : int { D_INIT = 0, D_RESET, D_FIRST, D_NORMAL, D_UPDATE, D_CONFIRM, D_DONE };
 
-// pass A over the rank's slices: OP 0: r = b - A x (+ r^T r, b^T b); OP 1/2: q = A p with p = z (+ beta p_old)
-// written for own rows (+ p^T q).  Masked solves skip rows outside Omega (their vectors stay 0).
+// one slice of pass A.  EDGE: the slice reaches a neighbour slab (operands of rows outside [0, n) are
+// peer loads); else every column is clamped into [0, n) (only zero holes at the global boundary clamp).
+template <int WM, int OP, bool EDGE>
+__device__ __forceinline__ void dslice_body(const DArgs& P, int64_t s, int lane, bool init, double beta, int par,
+                                       const double* __restrict__ pold, double* __restrict__ pnew, double* a) {
+  const SellView& A = P.A;
+  const int n = (int)P.n;
+  const int u = (int)(32 * s) + lane;
+  if (u >= n) return;
+  const double* vp = A.val + 32ll * A.vw * s + lane;
+  double v[WM], y[WM];
+#pragma unroll
+  for (int k = 0; k < WM; ++k) {
+    const bool use = WM != 8 || k < A.W;     // WM 5 / 7: exactly that width
+    v[k] = use ? __ldg(vp + 32 * k) : 0.0;
+    int c = u + A.off[k];
+    if (!EDGE) c = c < 0 ? 0 : (c >= n ? n - 1 : c);
+    y[k] = use ? opnd<OP>(P, c, EDGE, beta, pold, par) : 0.0;
+  }
+  double acc = 0.0, own = 0.0;
+#pragma unroll
+  for (int k = 0; k < WM; ++k) {
+    acc = __fma_rn(v[k], y[k], acc);
+    if (A.off[k] == 0 && (WM != 8 || k < A.W)) own = y[k];
+  }
+  if (P.masked && P.om[u] == kOutD) return;
+  if (OP == 0) {
+    const double bi = P.b[u];
+    const double ri = bi - acc;
+    P.r[u] = ri;
+    a[0] = __fma_rn(ri, ri, a[0]);
+    if (init) a[1] = __fma_rn(bi, bi, a[1]);
+  } else {
+    pnew[u] = own;
+    P.q[u] = acc;
+    a[0] = __fma_rn(own, acc, a[0]);
+  }
+}
+
+template <int WM, int OP, bool EDGE>
+__device__ __forceinline__ void dslice(const DArgs& P, int64_t s, int lane, bool init, double beta, int par,
+                                       const double* __restrict__ pold, double* __restrict__ pnew, double* a) {
+  dslice_body<WM, OP, EDGE>(P, s, lane, init, beta, par, pold, pnew, a);
+}
+// the few slab-edge slices: out of line, so their peer-load code does not raise the hot loop's registers
 template <int WM, int OP>
-__device__ __forceinline__ void dpass_a(const DArgs& P, int64_t w0, int64_t wst, int lane, bool init, double beta,
-                                        int par, double* a) {
+__device__ __noinline__ void dslice_edge(const DArgs& P, int64_t s, int lane, bool init, double beta, int par,
+                                         const double* pold, double* pnew, double* a) {
+  dslice_body<WM, OP, true>(P, s, lane, init, beta, par, pold, pnew, a);
+}
+
+// pass A over the rank's slices: OP 0: r = b - A x (+ r^T r, b^T b); OP 1/2: q = A p with p = z (+ beta p_old)
+// written for own rows (+ p^T q).  Interior slices [sa, sb) first (no halo code), then the few edge slices.
+// Masked solves skip rows outside Omega (their vectors stay 0).
+template <int WM, int OP>
+__device__ __forceinline__ void dpass_a(const DArgs& P, int64_t sa, int64_t sb, int64_t w0, int64_t wst, int lane,
+                                        bool init, double beta, int par, double* a) {
+  const double* pold = par ? P.p1 : P.p0;
+  double* pnew = par ? P.p0 : P.p1;
+#pragma unroll 1
+  for (int64_t s = sa + w0; s < sb; s += wst) dslice<WM, OP, false>(P, s, lane, init, beta, par, pold, pnew, a);
+  const int64_t ne = sa + (P.A.nslices - sb);
+#pragma unroll 1
+  for (int64_t j = w0; j < ne; j += wst)
+    dslice_edge<WM, OP>(P, j < sa ? j : sb + (j - sa), lane, init, beta, par, pold, pnew, a);
+}
+
+// pass A with the interior value stream staged by TMA (as k_pcg's pass_a_tma): CTA b owns the chunks
+// c = b + t nCTA of 8 consecutive slices, thread 0 keeps kDStages chunks in flight (cp.async.bulk +
+// mbarrier complete_tx) and each warp reads its slice's values from shared memory; a slab-edge slice takes
+// the out-of-line path (values from L2, operands from the neighbour slab).
+constexpr int kDStages = 2;
+template <int WM, int OP>
+__device__ __forceinline__ void dpass_a_tma(const DArgs& P, double* stg, uint64_t* bars, unsigned bid, unsigned nCTA,
+                                            int warp, int lane, bool init, double beta, int par, double* a) {
   const SellView& A = P.A;
   const double* pold = par ? P.p1 : P.p0;
   double* pnew = par ? P.p0 : P.p1;
-  const int n = (int)P.n;
+  const int64_t ns = A.nslices, nch = (ns + kDW - 1) / kDW;
+  const int64_t chd = (int64_t)kDW * 32 * WM;
+  const int n = (int)P.n, nu1 = n - 1;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kDStages; ++st) mbar_init(&bars[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int64_t t) {
+    const int64_t c = bid + t * nCTA;
+    if (c >= nch) return;
+    const int st = (int)(t % kDStages);
+    const int64_t j0c = (int64_t)kDW * c;
+    const int nsl = (int)((ns - j0c) < kDW ? (ns - j0c) : kDW);
+    const unsigned bytes = (unsigned)(32 * WM * 8) * nsl;
+    mbar_expect_tx(&bars[st], bytes);
+    tma_bulk_g2s(stg + st * chd, A.val + j0c * 32 * WM, bytes, &bars[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int t = 0; t < kDStages; ++t) issue(t);
 #pragma unroll 1
-  for (int64_t s = w0; s < A.nslices; s += wst) {
+  for (int64_t t = 0;; ++t) {
+    const int64_t c = bid + t * nCTA;
+    if (c >= nch) break;
+    const int st = (int)(t % kDStages);
+    mbar_wait(&bars[st], (unsigned)((t / kDStages) & 1));
+    const int64_t s = (int64_t)kDW * c + warp;
     const int u = (int)(32 * s) + lane;
-    if (u >= n) continue;
-    const bool edge = slice_edge(P, s);
-    const double* vp = A.val + 32ll * A.vw * s + lane;
-    double v[WM], y[WM];
+    if (s < ns && u < n) {
+      const bool edge = (P.lo.n && 32 * s + P.minoff < 0) || (P.hi.n && 32 * s + 31 + P.maxoff >= P.n);
+      if (edge) {
+        dslice_edge<WM, OP>(P, s, lane, init, beta, par, pold, pnew, a);
+      } else {
+        const double* sp = stg + st * chd + (int64_t)warp * 32 * WM + lane;
+        double v[WM], y[WM];
 #pragma unroll
-    for (int k = 0; k < WM; ++k) {
-      const bool use = k < A.W;
-      v[k] = use ? __ldg(vp + 32 * k) : 0.0;
-      int c = u + A.off[k];
-      if (!edge) c = c < 0 ? 0 : (c >= n ? n - 1 : c);
-      y[k] = use ? opnd<OP>(P, c, edge, beta, pold, par) : 0.0;
-    }
-    double acc = 0.0, own = 0.0;
+        for (int k = 0; k < WM; ++k) {
+          int cc = u + A.off[k];
+          cc = cc < 0 ? 0 : (cc > nu1 ? nu1 : cc);
+          v[k] = sp[32 * k];
+          y[k] = opl<OP>(P, cc, beta, pold);
+        }
+        double acc = 0.0, own = 0.0;
 #pragma unroll
-    for (int k = 0; k < WM; ++k) {
-      if (k < A.W) acc = __fma_rn(v[k], y[k], acc);
-      if (k < A.W && A.off[k] == 0) own = y[k];
+        for (int k = 0; k < WM; ++k) {
+          acc = __fma_rn(v[k], y[k], acc);
+          if (A.off[k] == 0) own = y[k];
+        }
+        if (!P.masked || P.om[u] != kOutD) {
+          if (OP == 0) {
+            const double bi = P.b[u];
+            const double ri = bi - acc;
+            P.r[u] = ri;
+            a[0] = __fma_rn(ri, ri, a[0]);
+            if (init) a[1] = __fma_rn(bi, bi, a[1]);
+          } else {
+            pnew[u] = own;
+            P.q[u] = acc;
+            a[0] = __fma_rn(own, acc, a[0]);
+          }
+        }
+      }
     }
-    const bool in = !P.masked || P.om[u] != kOutD;
-    if (!in) continue;
-    if (OP == 0) {
-      const double bi = P.b[u];
-      const double ri = bi - acc;
-      P.r[u] = ri;
-      a[0] = __fma_rn(ri, ri, a[0]);
-      if (init) a[1] = __fma_rn(bi, bi, a[1]);
-    } else {
-      pnew[u] = own;
-      P.q[u] = acc;
-      a[0] = __fma_rn(own, acc, a[0]);
+    __syncthreads();                               // every warp is done with stage st
+    if (threadIdx.x == 0) {
+      fence_proxy_async_smem();
+      issue(t + kDStages);
     }
   }
 }
 
 template <int WM>
-__global__ void __launch_bounds__(kDT, 3) k_dpcg(const DArgs* __restrict__ args, int nCTA) {
-  __shared__ __align__(16) DArgs sP;
+__global__ void __launch_bounds__(kDT, 3) k_dpcg(const __grid_constant__ DPack pk, int nCTA, int tma) {
   __shared__ double s_w[kDW][4], s_out[4];
+  extern __shared__ __align__(128) double dsm[];   // TMA stages: kDStages x 8 slices x 32 x WM values
+  __shared__ __align__(8) uint64_t s_bars[kDStages];
   __shared__ int s_mode, s_par, s_it, s_final, s_exit;
   __shared__ double s_rho, s_alpha, s_beta, s_tgt, s_nb;
   const unsigned slot = blockIdx.x / nCTA, bid = blockIdx.x % nCTA;
-  {
-    const int* src = reinterpret_cast<const int*>(args + slot);
-    int* dst = reinterpret_cast<int*>(&sP);
-    for (int i = threadIdx.x; i < (int)(sizeof(DArgs) / 4); i += kDT) dst[i] = src[i];
-  }
   if (threadIdx.x == 0) {
     s_mode = D_INIT; s_par = 0; s_it = 0; s_final = 0; s_exit = 0;
     s_rho = s_alpha = s_beta = 0.0; s_tgt = s_nb = 0.0;
   }
   __syncthreads();
-  const DArgs& P = sP;
+  const DArgs& P = pk.a[slot];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t w0 = (int64_t)bid * kDW + warp, wst = (int64_t)nCTA * kDW;
   unsigned long long seq = P.seq0;
+  // interior slices: every column of every row inside the slab (or a zero hole at the global boundary)
+  const int64_t nsl = P.A.nslices;
+  int64_t sa = P.lo.n ? (-P.minoff + 31) / 32 : 0;
+  int64_t sb = P.hi.n ? (P.n - 32 - P.maxoff >= 0 ? (P.n - 32 - P.maxoff) / 32 + 1 : 0) : nsl;
+  sa = sa < nsl ? sa : nsl;
+  sb = sb > sa ? sb : sa;
   auto finish = [&](int status, double rn) {
     s_mode = D_DONE;
     if (bid == 0) {
@@ -303,9 +421,18 @@ __global__ void __launch_bounds__(kDT, 3) k_dpcg(const DArgs* __restrict__ args,
     // ---- pass A
     double a[4] = {0.0, 0.0, 0.0, 0.0};
     const int mode = s_mode;
-    if (mode == D_INIT || mode == D_CONFIRM) dpass_a<WM, 0>(P, w0, wst, lane, mode == D_INIT, 0.0, s_par, a);
-    else if (mode == D_FIRST) dpass_a<WM, 1>(P, w0, wst, lane, false, 0.0, s_par, a);
-    else if (mode == D_NORMAL) dpass_a<WM, 2>(P, w0, wst, lane, false, s_beta, s_par, a);
+    if (WM != 8 && tma) {
+      if (mode == D_INIT || mode == D_CONFIRM)
+        dpass_a_tma<WM, 0>(P, dsm, s_bars, bid, nCTA, warp, lane, mode == D_INIT, 0.0, s_par, a);
+      else if (mode == D_FIRST) dpass_a_tma<WM, 1>(P, dsm, s_bars, bid, nCTA, warp, lane, false, 0.0, s_par, a);
+      else if (mode == D_NORMAL) dpass_a_tma<WM, 2>(P, dsm, s_bars, bid, nCTA, warp, lane, false, s_beta, s_par, a);
+    } else if (mode == D_INIT || mode == D_CONFIRM) {
+      dpass_a<WM, 0>(P, sa, sb, w0, wst, lane, mode == D_INIT, 0.0, s_par, a);
+    } else if (mode == D_FIRST) {
+      dpass_a<WM, 1>(P, sa, sb, w0, wst, lane, false, 0.0, s_par, a);
+    } else if (mode == D_NORMAL) {
+      dpass_a<WM, 2>(P, sa, sb, w0, wst, lane, false, s_beta, s_par, a);
+    }
     xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq);
     if (threadIdx.x == 0) {
       const double s0 = s_out[0], s1 = s_out[1];
@@ -332,13 +459,42 @@ __global__ void __launch_bounds__(kDT, 3) k_dpcg(const DArgs* __restrict__ args,
     const int modeb = s_mode;
     a[0] = a[1] = a[2] = a[3] = 0.0;
     if (modeb == D_UPDATE || modeb == D_RESET) {
+      // own rows as 16-byte pairs (the slab vectors are 256-byte aligned); rows outside Omega of a masked
+      // solve hold p = q = r = 0 and stay 0
       const double alpha = s_alpha;
-      const double* pp = s_par ? P.p1 : P.p0;
-      const double* dinv = P.A.dinv;
-      for (int64_t u = (int64_t)bid * kDT + threadIdx.x; u < P.n; u += (int64_t)nCTA * kDT) {
-        const double di = dinv[u];
+      const double2* pp = reinterpret_cast<const double2*>(s_par ? P.p1 : P.p0);
+      double2* x2 = reinterpret_cast<double2*>(P.x);
+      double2* r2 = reinterpret_cast<double2*>(P.r);
+      double2* z2 = reinterpret_cast<double2*>(P.z);
+      const double2* q2 = reinterpret_cast<const double2*>(P.q);
+      const double2* d2 = reinterpret_cast<const double2*>(P.A.dinv);
+      const int64_t npair = P.n >> 1, gt = (int64_t)bid * kDT + threadIdx.x, gs = (int64_t)nCTA * kDT;
+      if (modeb == D_UPDATE) {
+#pragma unroll 2
+        for (int64_t i = gt; i < npair; i += gs) {
+          double2 xv = x2[i], pv = pp[i], rv = r2[i], qv = q2[i], dv = d2[i];
+          xv.x = __fma_rn(alpha, pv.x, xv.x); xv.y = __fma_rn(alpha, pv.y, xv.y);
+          rv.x = __fma_rn(-alpha, qv.x, rv.x); rv.y = __fma_rn(-alpha, qv.y, rv.y);
+          const double2 zv = make_double2(rv.x * dv.x, rv.y * dv.y);
+          x2[i] = xv; r2[i] = rv; z2[i] = zv;
+          a[0] = __fma_rn(rv.x, zv.x, a[0]); a[0] = __fma_rn(rv.y, zv.y, a[0]);
+          a[1] = __fma_rn(rv.x, rv.x, a[1]); a[1] = __fma_rn(rv.y, rv.y, a[1]);
+        }
+      } else {
+#pragma unroll 2
+        for (int64_t i = gt; i < npair; i += gs) {
+          const double2 rv = r2[i], dv = d2[i];
+          const double2 zv = make_double2(rv.x * dv.x, rv.y * dv.y);
+          z2[i] = zv;
+          a[0] = __fma_rn(rv.x, zv.x, a[0]); a[0] = __fma_rn(rv.y, zv.y, a[0]);
+        }
+      }
+      if ((P.n & 1) && gt == 0) {
+        const int64_t u = P.n - 1;
+        const double* p1 = s_par ? P.p1 : P.p0;
+        const double di = P.A.dinv[u];
         if (modeb == D_UPDATE) {
-          const double xi = __fma_rn(alpha, pp[u], P.x[u]);
+          const double xi = __fma_rn(alpha, p1[u], P.x[u]);
           const double ri = __fma_rn(-alpha, P.q[u], P.r[u]);
           const double zi = ri * di;
           P.x[u] = xi; P.r[u] = ri; P.z[u] = zi;
@@ -383,17 +539,10 @@ __global__ void __launch_bounds__(kDT, 3) k_dpcg(const DArgs* __restrict__ args,
 // ---------------------------------------------------------------- domain ----
 // Alg. 4 / Alg. 5 on the partition, then the masked extraction (Eq. 3) and the masked-solve start state.
 template <int WM>
-__global__ void __launch_bounds__(kDT, 2) k_ddomain(const DArgs* __restrict__ args, int nCTA) {
-  __shared__ __align__(16) DArgs sP;
+__global__ void __launch_bounds__(kDT, 2) k_ddomain(const __grid_constant__ DPack pk, int nCTA, int) {
   __shared__ double s_w[kDW][4], s_out[4];
   const unsigned slot = blockIdx.x / nCTA, bid = blockIdx.x % nCTA;
-  {
-    const int* src = reinterpret_cast<const int*>(args + slot);
-    int* dst = reinterpret_cast<int*>(&sP);
-    for (int i = threadIdx.x; i < (int)(sizeof(DArgs) / 4); i += kDT) dst[i] = src[i];
-  }
-  __syncthreads();
-  const DArgs& P = sP;
+  const DArgs& P = pk.a[slot];
   const SellView& A = P.A;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t w0 = (int64_t)bid * kDW + warp, wst = (int64_t)nCTA * kDW;
@@ -588,7 +737,7 @@ DPeer peer_of(char* base, int64_t n) {
 int g_dmax[6] = {0};    // cached co-resident CTAs per SM x SMs per kernel variant
 
 void* kernel_of(int which, int W) {
-  const int wi = W <= 5 ? 0 : W <= 7 ? 1 : 2;
+  const int wi = W == 5 ? 0 : W == 7 ? 1 : 2;      // 5- / 7-point stencils, else the generic width
   void* const f[6] = {(void*)k_dpcg<5>, (void*)k_dpcg<7>, (void*)k_dpcg<8>,
                       (void*)k_ddomain<5>, (void*)k_ddomain<7>, (void*)k_ddomain<8>};
   return f[which * 3 + wi];
@@ -625,13 +774,16 @@ DArgs base_args(lc_dist D) {
 
 // one cooperative launch over the nr ranks driven by this call (nCTA CTAs each); syncs, reads back seq
 lc_status launch(lc_dist* R, int nr, int which, std::vector<DArgs>& args, cudaStream_t s, float* ms) {
-  int W = 0;
-  for (int i = 0; i < nr; ++i) W = std::max(W, R[i]->A.maxw);
+  int W = R[0]->A.maxw;
+  for (int i = 1; i < nr; ++i)
+    if (R[i]->A.maxw != W) W = 8;                      // mixed widths: the generic variant
   void* fn = kernel_of(which, W);
-  const int ki = which * 3 + (W <= 5 ? 0 : W <= 7 ? 1 : 2);
+  const int ki = which * 3 + (W == 5 ? 0 : W == 7 ? 1 : 2);
+  int tma = (which == 0 && (W == 5 || W == 7) && getenv("LC_NO_TMA") == nullptr) ? 1 : 0;
+  const size_t dsmem = tma ? (size_t)kDStages * kDW * 32 * W * sizeof(double) : 0;
   if (!g_dmax[ki]) {
     int per_sm = 0;
-    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kDT, 0));
+    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kDT, dsmem));
     if (per_sm < 1) { set_error("dist kernel does not fit on an SM"); return LC_ERR_CUDA; }
     g_dmax[ki] = per_sm * num_sms();
   }
@@ -639,17 +791,16 @@ lc_status launch(lc_dist* R, int nr, int which, std::vector<DArgs>& args, cudaSt
   for (int i = 0; i < nr; ++i) ns = std::max<int64_t>(ns, R[i]->A.nslices);
   int nCTA = (int)std::min<int64_t>(g_dmax[ki] / nr, (ns + kDW - 1) / kDW);
   if (nCTA < 1) nCTA = 1;
-  void* d_args = nullptr;
-  lc_status st = dalloc(&d_args, sizeof(DArgs) * nr, s);
-  if (st) return st;
-  cudaError_t e = cudaMemcpyAsync(d_args, args.data(), sizeof(DArgs) * nr, cudaMemcpyHostToDevice, s);
+  DPack pk;
+  memset(&pk, 0, sizeof(pk));
+  for (int i = 0; i < nr; ++i) pk.a[i] = args[i];
+  cudaError_t e = cudaSuccess;
   for (int i = 0; i < nr && e == cudaSuccess; ++i) e = cudaMemsetAsync(R[i]->bar, 0, sizeof(GridBar), s);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0, s);
-  const DArgs* dp = (const DArgs*)d_args;
-  void* kargs[] = {(void*)&dp, (void*)&nCTA};
-  if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)(nr * nCTA)), dim3(kDT), kargs, 0, s);
+  void* kargs[] = {(void*)&pk, (void*)&nCTA, (void*)&tma};
+  if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)(nr * nCTA)), dim3(kDT), kargs, dsmem, s);
   if (e == cudaSuccess) count_launch();
   cudaEventRecord(e1, s);
   std::vector<unsigned long long> sq(nr, 0);
@@ -658,7 +809,6 @@ lc_status launch(lc_dist* R, int nr, int which, std::vector<DArgs>& args, cudaSt
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e == cudaSuccess && ms) cudaEventElapsedTime(ms, e0, e1);
   cudaEventDestroy(e0); cudaEventDestroy(e1);
-  dfree(d_args, s);
   if (e != cudaSuccess) return cuda_fail(e, "dist kernel");
   for (int i = 0; i < nr; ++i) R[i]->seq = sq[i];
   return LC_OK;
