@@ -188,3 +188,73 @@ def test_dist_rejects_non_stencil_and_short_slabs():
         ranks.append(lc.DistRank(N, R[l], R[l + 1] - R[l], l, 2, rp, ci, va))
     with pytest.raises(lc.LcError, match="LC_ERR_DIMENSION"):
         lc.dist_connect_local(ranks)
+
+
+# ---------------------------------------------------------------- one process per rank (IPC plumbing) ----
+
+def test_dist_multiprocess_api_world1():
+    """tools/dist_mp.py through the one-process-per-GPU API (export / all-gather / lc_dist_connect, nr = 1)
+    at world size 1 (the only size one GPU can run without ranks waiting on each other across launches)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), RANK="0", WORLD_SIZE="1",
+               LOCAL_RANK="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "dist_mp.py"), "--config", "1", "--align", "32"],
+                         env=env, capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    sy = synth.system(1, 10)
+    Ao = orc.Csr(sy.rp, sy.ci, sy.val)
+    d = orc.select_domain(Ao, sy.b, sy.x0, 0, 0, 1e-10, 1, 0, 1)
+    assert r["K"] == r["K_gathered"] == d.K
+    assert r["rel_residual"] <= 1e-10 * (1 + 1e-6)
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _ipc_worker(rank, port, q):
+    import os
+    import torch.distributed as tdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE="2")
+    tdist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        from paper_2001_01158_b200 import dist as ld
+        from paper_2001_01158_b200 import lc as llc
+        sy = synth.system(1, 0)
+        R = ld.split_rows(sy.nrows, 2, 32)
+        rp, ci, va = ld.slab_csr(sy.rp, sy.ci, sy.val, R[rank], R[rank + 1])
+        me = llc.DistRank(sy.nrows, R[rank], R[rank + 1] - R[rank], rank, 2, rp, ci, va)
+        hs = ld.exchange_handles(me.export_handle())
+        me.connect(hs, ld.exchange_sizes(R[rank + 1] - R[rank]))   # opens the other process's workspace
+        tdist.barrier()                                                # both mapped before either unmaps
+        del me
+        q.put((rank, "ok"))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
+    tdist.destroy_process_group()
+
+
+def test_dist_ipc_connect_two_processes():
+    """Two processes (one device): each exports its workspace and opens the other's through CUDA IPC.  No
+    kernel runs (cross-process waits need one GPU per rank)."""
+    import torch.multiprocessing as tmp
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_ipc_worker, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res
