@@ -53,6 +53,7 @@ struct PcgArgs {
   double* p1;
   double* part;                 // [nCTA][G][2]
   double* red;                  // [G][2]  (G > 1)
+  double* subred;               // [kBarSub][G][2]  (G > 1: per-sub-group sums of the arrival tree)
   GridBar* bar;                 // zeroed at launch
   int* out_iters;               // [G]
   int* out_status;
@@ -209,6 +210,14 @@ __device__ __forceinline__ void tl_mark(int& k) {
   ++k;
 }
 #define TL(k) tl_mark(k)
+__device__ unsigned long long g_tlx[8192];      // tree barrier: [last sub-group arrival, top release] pairs
+__device__ unsigned g_tlx_n;
+__device__ __forceinline__ void tlx_mark(int which) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  unsigned i = which == 0 ? atomicAdd(&g_tlx_n, 1u) : g_tlx_n - 1;
+  if (i < 4096) g_tlx[2 * i + which] = t;
+}
 #else
 #define TL(k) (void)0
 #endif
@@ -316,17 +325,98 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
   }
 }
 
+// out[t] = sum over the members m_i = first + i step (i < count, ascending) of part[m_i T + t], t < T <= 128:
+// warp w sums a contiguous range of members, then the 8 warp sums are added in warp order (fixed order)
+__device__ __forceinline__ void sum_members(const double* part, int T, unsigned first, unsigned step, unsigned count,
+                                            double* out, double (*s_tmp)[2 * kMaxSeg]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned per = (count + kPW - 1) / kPW;
+  const unsigned i0 = warp * per, i1 = min(count, i0 + per);
+  for (int t = lane; t < T; t += 32) {
+    double a = 0.0;
+    for (unsigned i = i0; i < i1; ++i) a += __ldcg(part + (size_t)(first + i * step) * T + t);
+    s_tmp[warp][t] = a;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < T; t += kPT) {
+    double a = 0.0;
+    for (int w = 0; w < kPW; ++w) a += s_tmp[w][t];
+    out[t] = a;
+  }
+}
+
+// Grid barrier whose arrival tree also reduces the per-CTA partials part[b][0..T) (batched solves, G > 1):
+// the last arriver of each of the kBarSub sub-groups sums its members' partials (by CTA index) into
+// subred[k], the last of those sums the sub-groups (by index) into red and releases the generation.  Every
+// CTA then reads only the T sums, instead of a second barrier plus a per-segment stage (profiles/r01_m).
+__device__ void tree_reduce_barrier(GridBar* gb, const double* part, double* subred, double* red, int T,
+                                    double (*s_tmp)[2 * kMaxSeg], int* s_flag) {
+  const unsigned nb = gridDim.x, b = blockIdx.x;
+  __syncthreads();
+  unsigned g0 = 0;
+  if (threadIdx.x == 0) {
+    g0 = ld_acquire_u32(&gb->gen);
+    __threadfence();
+    int f;
+    if (nb <= 64) {
+      f = atomicAdd(&gb->top, 1u) == nb - 1 ? 2 : 0;
+    } else {
+      const unsigned k = b % kBarSub, nk = (nb - k + kBarSub - 1) / kBarSub;
+      f = atomicAdd(&gb->sub[k][0], 1u) == nk - 1 ? 1 : 0;
+    }
+    if (f) __threadfence();
+    s_flag[0] = f;
+  }
+  __syncthreads();
+  int f = s_flag[0];
+  if (f == 1) {
+    const unsigned k = b % kBarSub, nk = (nb - k + kBarSub - 1) / kBarSub;
+    sum_members(part, T, k, kBarSub, nk, subred + (size_t)k * T, s_tmp);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      gb->sub[k][0] = 0;
+      __threadfence();
+      const bool last = atomicAdd(&gb->top, 1u) == (unsigned)kBarSub - 1;
+      if (last) __threadfence();
+      s_flag[0] = last ? 2 : 1;
+    }
+    __syncthreads();
+    f = s_flag[0];
+#ifdef LC_DEBUG_TIMELINE
+    if (f == 2 && threadIdx.x == 0) tlx_mark(0);
+#endif
+    if (f == 2) sum_members(subred, T, 0, 1, kBarSub, red, s_tmp);
+  } else if (f == 2) {
+    sum_members(part, T, 0, 1, nb, red, s_tmp);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (f == 2) {
+      __threadfence();
+      gb->top = 0;
+#ifdef LC_DEBUG_TIMELINE
+      if (nb > 64) tlx_mark(1);
+#endif
+      st_release_u32(&gb->gen, g0 + 1);
+    } else {
+      while (ld_acquire_u32(&gb->gen) == g0) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 template <int WM, int ST>
 __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   __shared__ SegState S[kMaxSeg];
   __shared__ double s_acc[kPW][kMaxSeg][2];
   __shared__ double s_red[kPW][2];
   __shared__ double s_sum[kMaxSeg][2];
-  __shared__ int s_exit;
+  __shared__ int s_tflag[1];
   __shared__ long long s_segj0[kMaxSeg + 1];   // segment runs in slice space
   __shared__ int s_act[kMaxSeg + 1];           // active segments of the current pass (+ sentinel)
   __shared__ long long s_actj[kMaxSeg + 1];    // their runs concatenated
-  __shared__ int s_na;                         // number of active segments of the current pass
   __shared__ double s_cpart[2][2];             // cluster mode: this CTA's partials, double-buffered by pass
   int cpar = 0;
   extern __shared__ __align__(128) double dsm[];   // TMA stages (P.tma): kStages x 8 slices x 32 x vw values
@@ -382,8 +472,8 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       for (int w = 0; w < kPW; ++w) v += s_acc[w][t >> 1][t & 1];
       P.part[(bid * G) * 2 + t] = v;
     }
-    grid_barrier(P.bar);
     if (G == 1) {
+      grid_barrier(P.bar);
       double a0 = 0.0, a1 = 0.0;
       for (int64_t c = threadIdx.x; c < nCTA; c += kPT) { a0 += P.part[2 * c]; a1 += P.part[2 * c + 1]; }
       a0 = warp_sum(a0); a1 = warp_sum(a1);
@@ -402,43 +492,10 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
         s_sum[0][threadIdx.x] = o;
       }
 #endif
-    } else if (s_na <= 4) {
-      // few active segments (the tail of a batched solve): every CTA sums their partials directly,
-      // saving the second barrier of the two-stage form; inactive segments' sums are never read
-      for (int ai = 0; ai < s_na; ++ai) {
-        const int g = s_act[ai];
-        double a0 = 0.0, a1 = 0.0;
-        for (int64_t c = threadIdx.x; c < nCTA; c += kPT) {
-          a0 += P.part[(c * G + g) * 2]; a1 += P.part[(c * G + g) * 2 + 1];
-        }
-        a0 = warp_sum(a0); a1 = warp_sum(a1);
-        if (lane == 0) { s_red[warp][0] = a0; s_red[warp][1] = a1; }
-        __syncthreads();
-        if (threadIdx.x < 2) {
-          double o = 0.0;
-          for (int w = 0; w < kPW; ++w) o += s_red[w][threadIdx.x];
-          s_sum[g][threadIdx.x] = o;
-        }
-        __syncthreads();
-      }
     } else {
-      for (int g = (int)bid; g < G; g += (int)nCTA) {       // stage 1: CTA g reduces segment g
-        double a0 = 0.0, a1 = 0.0;
-        for (int64_t c = threadIdx.x; c < nCTA; c += kPT) {
-          a0 += P.part[(c * G + g) * 2]; a1 += P.part[(c * G + g) * 2 + 1];
-        }
-        a0 = warp_sum(a0); a1 = warp_sum(a1);
-        if (lane == 0) { s_red[warp][0] = a0; s_red[warp][1] = a1; }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          double o0 = 0.0, o1 = 0.0;
-          for (int w = 0; w < kPW; ++w) { o0 += s_red[w][0]; o1 += s_red[w][1]; }
-          P.red[2 * g] = o0; P.red[2 * g + 1] = o1;
-        }
-        __syncthreads();
-      }
-      grid_barrier(P.bar);
-      for (int t = threadIdx.x; t < G * 2; t += kPT) s_sum[t >> 1][t & 1] = P.red[t];   // stage 2
+      tree_reduce_barrier(P.bar, P.part, P.subred, P.red, 2 * G,
+                          reinterpret_cast<double (*)[2 * kMaxSeg]>(&s_acc[0][0][0]), s_tflag);
+      for (int t = threadIdx.x; t < G * 2; t += kPT) s_sum[t >> 1][t & 1] = __ldcg(P.red + t);
     }
     __syncthreads();
   };
@@ -466,7 +523,6 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       }
       s_actj[na] = J;
       s_act[na] = G;
-      s_na = na;
     }
     __syncthreads();
     int na = 0;
@@ -558,28 +614,27 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
     reduce_all();
     TL(tlk);
     // ---------------------------------------------------- pass A scalars ----
-    if (threadIdx.x == 0) {
-      for (int g = 0; g < G; ++g) {
-        SegState& T = S[g];
-        double s0 = s_sum[g][0], s1 = s_sum[g][1];
-        if (T.mode == M_INIT) {
-          T.nb = sqrt(s1);
-          T.tgt = T.nb > 0 ? P.eps * T.nb : P.eps;
-          double rn = sqrt(s0);
-          if (!isfinite(rn)) finish(g, LC_ERR_NONFINITE, rn);
-          else if (rn <= T.tgt) finish(g, LC_OK, rn);
-          else T.mode = M_RESET;
-        } else if (T.mode == M_FIRST || T.mode == M_NORMAL) {
-          double pq = s0;
-          if (!(pq > 0)) finish(g, isfinite(pq) ? LC_ERR_BREAKDOWN : LC_ERR_NONFINITE, NAN);
-          else { T.alpha = T.rho / pq; T.mode = M_UPDATE; T.par ^= 1; }
-        } else if (T.mode == M_CONFIRM) {
-          double rn = sqrt(s0);
-          if (!isfinite(rn)) finish(g, LC_ERR_NONFINITE, rn);
-          else if (rn <= T.tgt) finish(g, LC_OK, rn);
-          else if (T.final_) finish(g, LC_NOT_CONVERGED, rn);
-          else T.mode = M_RESET;
-        }
+    // segments are independent: thread g updates segment g's state
+    for (int g = threadIdx.x; g < G; g += kPT) {
+      SegState& T = S[g];
+      double s0 = s_sum[g][0], s1 = s_sum[g][1];
+      if (T.mode == M_INIT) {
+        T.nb = sqrt(s1);
+        T.tgt = T.nb > 0 ? P.eps * T.nb : P.eps;
+        double rn = sqrt(s0);
+        if (!isfinite(rn)) finish(g, LC_ERR_NONFINITE, rn);
+        else if (rn <= T.tgt) finish(g, LC_OK, rn);
+        else T.mode = M_RESET;
+      } else if (T.mode == M_FIRST || T.mode == M_NORMAL) {
+        double pq = s0;
+        if (!(pq > 0)) finish(g, isfinite(pq) ? LC_ERR_BREAKDOWN : LC_ERR_NONFINITE, NAN);
+        else { T.alpha = T.rho / pq; T.mode = M_UPDATE; T.par ^= 1; }
+      } else if (T.mode == M_CONFIRM) {
+        double rn = sqrt(s0);
+        if (!isfinite(rn)) finish(g, LC_ERR_NONFINITE, rn);
+        else if (rn <= T.tgt) finish(g, LC_OK, rn);
+        else if (T.final_) finish(g, LC_NOT_CONVERGED, rn);
+        else T.mode = M_RESET;
       }
     }
     __syncthreads();
@@ -687,32 +742,28 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
     reduce_all();
     TL(tlk);
     // ---------------------------------------------------- pass B scalars ----
-    if (threadIdx.x == 0) {
-      int active = 0;
-      for (int g = 0; g < G; ++g) {
-        SegState& T = S[g];
-        double s0 = s_sum[g][0], s1 = s_sum[g][1];
-        if (T.mode == M_UPDATE) {
-          T.it += 1;
-          double rz = s0, rr = s1;
-          if (!isfinite(rr) || sqrt(rr) <= T.tgt || T.it >= P.max_iters) {
-            T.mode = M_CONFIRM;
-            T.final_ = (T.it >= P.max_iters) || !isfinite(rr);
-          } else {
-            T.beta = rz / T.rho;
-            T.rho = rz;
-            T.mode = M_NORMAL;
-          }
-        } else if (T.mode == M_RESET) {
-          T.rho = s0;
-          T.mode = M_FIRST;
+    int active = 0;
+    for (int g = threadIdx.x; g < G; g += kPT) {
+      SegState& T = S[g];
+      double s0 = s_sum[g][0], s1 = s_sum[g][1];
+      if (T.mode == M_UPDATE) {
+        T.it += 1;
+        double rz = s0, rr = s1;
+        if (!isfinite(rr) || sqrt(rr) <= T.tgt || T.it >= P.max_iters) {
+          T.mode = M_CONFIRM;
+          T.final_ = (T.it >= P.max_iters) || !isfinite(rr);
+        } else {
+          T.beta = rz / T.rho;
+          T.rho = rz;
+          T.mode = M_NORMAL;
         }
-        active += (T.mode != M_DONE);
+      } else if (T.mode == M_RESET) {
+        T.rho = s0;
+        T.mode = M_FIRST;
       }
-      s_exit = (active == 0);
+      active += (T.mode != M_DONE);
     }
-    __syncthreads();
-    if (s_exit) break;
+    if (!__syncthreads_or(active)) break;
   }
   // a8: x~[Omega] = xbar_B (Eq. 4), fused into the local solve's exit
   if (P.scatter_idx || P.x_user) {
@@ -767,7 +818,8 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   const size_t vec = sizeof(double) * (size_t)n;
   const size_t vbytes = (vec + 255) & ~(size_t)255;
   const bool own_x = job.x_init != nullptr;
-  const size_t bytes = vbytes * (own_x ? 6 : 5) + sizeof(double) * 2 * G * (nCTA + 1) + 16 * G + sizeof(GridBar) + 640;
+  const size_t bytes = vbytes * (own_x ? 6 : 5) + sizeof(double) * 2 * G * (nCTA + 1 + kBarSub) + 16 * G +
+                       sizeof(GridBar) + 640;
   lc_status st = dalloc(&ws, bytes, s);
   if (st) return st;
   char* w = (char*)ws;
@@ -789,6 +841,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   if (job.omega && e == cudaSuccess) e = cudaMemsetAsync(a.r, 0, vbytes * 5, s);   // zero outside Omega
   a.part = (double*)w; w += sizeof(double) * 2 * G * nCTA;
   a.red = (double*)w; w += sizeof(double) * 2 * G;
+  a.subred = (double*)w; w += sizeof(double) * 2 * G * kBarSub;
   w = (char*)((((uintptr_t)w) + 127) & ~(uintptr_t)127);
   a.bar = (GridBar*)w; w += sizeof(GridBar);
   a.out_iters = (int*)w; w += 4 * G;
@@ -879,5 +932,11 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
 #ifdef LC_DEBUG_TIMELINE
 extern "C" int lc_debug_timeline(unsigned long long* out, int n) {
   return cudaMemcpyFromSymbol(out, lc::g_tl, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -1;
+}
+extern "C" int lc_debug_timeline_tree(unsigned long long* out, int n) {
+  unsigned z = 0;
+  int r = cudaMemcpyFromSymbol(out, lc::g_tlx, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -1;
+  cudaMemcpyToSymbol(lc::g_tlx_n, &z, sizeof(z));
+  return r;
 }
 #endif
