@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--impl", default="lc", choices=["lc", "reference"])
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--n", type=int, default=None, help="grid override (testing only)")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gs", type=int, default=0, help="Gauss-Seidel sweeps of Alg. 1 l.7 (paper: 1; parity path: 0)")
     return ap.parse_args()
@@ -300,16 +300,39 @@ def run_lc(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        # H2D of step i+1 runs on a copy stream while step i computes (the copies stay inside the timed
+        # region; the first one is not hidden), results go back D2H on another stream behind each step
+        h2d_stream, d2h_stream = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
+        def prefetch(i):
+            p = pins[i % len(pins)]
+            with torch.cuda.stream(h2d_stream):
+                inp = {k: v.to(dev, non_blocking=True) for k, v in p.items()}
+                ev = torch.cuda.Event()
+                ev.record(h2d_stream)
+            return inp, ev
+
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        h2d_stream.wait_event(e0)
         sol = 0
+        nxt = prefetch(0)
+        keep_alive = []
         for i in range(args.e2e_steps):
-            p = pins[i % len(pins)]
-            inp = {k: v.to(dev, non_blocking=True) for k, v in p.items()}
+            inp, ev = nxt
+            stream.wait_event(ev)
+            if i + 1 < args.e2e_steps:
+                nxt = prefetch(i + 1)
             xs = []
             sol += one_step(inp, out_x=xs)
-            for xo, xh in zip(xs, outs_host):
-                xh.copy_(xo, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(stream)
+            d2h_stream.wait_event(done)
+            with torch.cuda.stream(d2h_stream):
+                for xo, xh in zip(xs, outs_host):
+                    xh.copy_(xo, non_blocking=True)
+            keep_alive.append((inp, xs))
+        stream.wait_stream(d2h_stream)
         e1.record(stream)
         torch.cuda.synchronize()
         _, evalue = aggregate(e0.elapsed_time(e1), sol, world, dist, dev)
