@@ -43,7 +43,6 @@ __global__ void __launch_bounds__(kTB) k_extract(SellView A, SellView B, int W, 
     for (int a = 0; a < BS; ++a) acc[a] = 0.0;
     for (int k = 0; k < len; ++k) {
       if (!sv_real(A, k, i)) continue;                 // padding / stencil holes
-      int64_t slotA = pA + 32ll * k + laneA;
       int64_t c = sv_col(A, pA + laneA, k, i);
       int ic = inv[c];
       if (ic >= 0) {                                   // B block: column in local numbering
