@@ -24,6 +24,7 @@ constexpr int kGT = 512;
 constexpr int kGW = kGT / 32;
 constexpr int kMaxM = 40;
 constexpr int kMaxQ = 2 * (kMaxM + 1) + 2;   // reduced quantities per phase
+constexpr int kIB = 4;                       // basis vectors per unrolled block of the dot / update loops
 
 struct GmresArgs {
   SellView A;
@@ -229,21 +230,40 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
           }
         }
         const double* Vj = P.V + (size_t)j * n;
-        for (int i = 0; i <= j; ++i) {
-          const double* Vi = P.V + (size_t)i * n;
-          double d = 0.0, gq = 0.0;
+        double vj[2][BS];
 #pragma unroll
-          for (int cc = 0; cc < 2; ++cc)
-            if (ok[cc]) {
+        for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
-              for (int a = 0; a < BS; ++a) {
-                const double vi = Vi[BS * uu[cc] + a];
-                d = __fma_rn(vi, wv[cc][a], d);
-                if (!P.exact_cgs2) gq = __fma_rn(vi, Vj[BS * uu[cc] + a], gq);
-              }
+          for (int a = 0; a < BS; ++a) vj[cc][a] = (ok[cc] && !P.exact_cgs2) ? Vj[BS * uu[cc] + a] : 0.0;
+        // i in blocks of kIB with compile-time indices: the block's V loads issue together (one DRAM
+        // latency per block instead of one per basis vector)
+        for (int i0 = 0; i0 <= j; i0 += kIB) {
+          double d[kIB], gq[kIB];
+#pragma unroll
+          for (int ii = 0; ii < kIB; ++ii) {
+            d[ii] = 0.0;
+            gq[ii] = 0.0;
+            const int i = i0 + ii;
+            if (i <= j) {
+              const double* Vi = P.V + (size_t)i * n;
+#pragma unroll
+              for (int cc = 0; cc < 2; ++cc)
+                if (ok[cc]) {
+#pragma unroll
+                  for (int a = 0; a < BS; ++a) {
+                    const double vi = Vi[BS * uu[cc] + a];
+                    d[ii] = __fma_rn(vi, wv[cc][a], d[ii]);
+                    gq[ii] = __fma_rn(vi, vj[cc][a], gq[ii]);
+                  }
+                }
             }
-          lane_flush(i, d);
-          if (!P.exact_cgs2) lane_flush(j + 1 + i, gq);
+          }
+#pragma unroll
+          for (int ii = 0; ii < kIB; ++ii) {
+            if (i0 + ii > j) break;
+            lane_flush(i0 + ii, d[ii]);
+            if (!P.exact_cgs2) lane_flush(j + 1 + i0 + ii, gq[ii]);
+          }
         }
       }
       if (!P.exact_cgs2) {
@@ -279,11 +299,19 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
             double ww[BS];
 #pragma unroll
             for (int a = 0; a < BS; ++a) ww[a] = P.w[BS * u + a];
-            for (int i = 0; i <= j; ++i) {
-              const double* Vi = P.V + (size_t)i * n;
-              const double hi = hh[i];
+            for (int i0 = 0; i0 <= j; i0 += kIB) {
+              double vv[kIB][BS];
 #pragma unroll
-              for (int a = 0; a < BS; ++a) ww[a] = __fma_rn(-hi, Vi[BS * u + a], ww[a]);
+              for (int ii = 0; ii < kIB; ++ii)
+#pragma unroll
+                for (int a = 0; a < BS; ++a) vv[ii][a] = i0 + ii <= j ? P.V[(size_t)(i0 + ii) * n + BS * u + a] : 0.0;
+#pragma unroll
+              for (int ii = 0; ii < kIB; ++ii) {
+                if (i0 + ii > j) break;
+                const double hi = hh[i0 + ii];
+#pragma unroll
+                for (int a = 0; a < BS; ++a) ww[a] = __fma_rn(-hi, vv[ii][a], ww[a]);
+              }
             }
 #pragma unroll
             for (int a = 0; a < BS; ++a) { P.w[BS * u + a] = ww[a]; a0 = __fma_rn(ww[a], ww[a], a0); }

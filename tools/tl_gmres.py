@@ -1,19 +1,31 @@
-import ctypes, sys
+"""GMRES timeline (debug build -DLC_DEBUG_TIMELINE): CTA 0's phase durations per Arnoldi step of the Gram-form
+(R39) step: 1a | sync 1a | 1b (SpMV + dots) | sync+red 1b | H/Gram + update pass | sync+red.
+usage: python tools/tl_gmres.py paper_2001_01158_b200/liblc_tl.so"""
+import ctypes
+import sys
+
+import numpy as np
+import torch
+
 sys.path.insert(0, ".")
-import numpy as np, torch, synth
-from paper_2001_01158_b200 import lc
+import synth  # noqa: E402
+from paper_2001_01158_b200 import lc  # noqa: E402
+
 lc.load_library(sys.argv[1])
 sy = synth.system(4, 3)
 A = lc.Matrix(sy.nrows, sy.rp, sy.ci, sy.val, block=3)
-b = torch.from_numpy(sy.b).cuda(); x = torch.from_numpy(sy.x0).cuda()
+b = torch.from_numpy(sy.b).cuda()
+x = torch.from_numpy(sy.x0).cuda()
 for i in range(2):
-    xx = x.clone(); info = lc.solve_global(A, b, xx, method=lc.GMRES)
+    xx = x.clone()
+    info = lc.solve_global(A, b, xx, method=lc.GMRES)
 print(info)
+K = 7
 buf = (ctypes.c_ulonglong * 16384)()
 lc._lib.lc_debug_timeline_gmres(buf, 16384)
-t = np.array(buf[:9 * 40], dtype=np.int64).reshape(-1, 9)
+t = np.array(buf[:K * 30], dtype=np.int64).reshape(-1, K)      # first cycle: steps 0..29
 d = np.diff(t, axis=1)
-print("per step (ns): 1a | sync1a | 1b | sync+red1b | hstore+2 | sync+red2 | 3 | sync+red3")
-for j in (1, 5, 15, 25):
-    print(j, d[j])
-print("median", np.median(d[1:30], axis=0), "step total", np.median(np.diff(t[1:30, 0])))
+print("per step (ns): 1a | sync1a | 1b | sync+red1b | hstore+update | sync+red")
+for j in (1, 5, 15, 25, 29):
+    print(j, d[j], "step", t[j + 1, 0] - t[j, 0] if j + 1 < len(t) else None)
+print("median", np.median(d[1:29], axis=0), "step total", np.median(np.diff(t[1:29, 0])))
