@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
   const int m = P.m;
   __shared__ double H[(kMaxM + 1) * kMaxM];
   __shared__ double gv[kMaxM + 1], cs[kMaxM], sn[kMaxM], yv[kMaxM];
+  __shared__ double sig[kMaxM + 1];   // basis scales: V_i = sig_i U_i (U stored; all 1 in the exact-CGS2 mode)
   __shared__ double red[kMaxQ];
   __shared__ double s_acc[kGW][kMaxQ];
   __shared__ double Gm[(kMaxM + 1) * (kMaxM + 1)];   // Gram matrix V^T V (low-sync CGS2, R39)
@@ -146,13 +147,23 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
             }
           }
         }
+        double rv[BS];
 #pragma unroll
         for (int a = 0; a < BS; ++a) {
           double bi = P.b[BS * u + a];
           double ri = bi - acc[a];
-          P.r[BS * u + a] = ri;
+          rv[a] = ri;
           a0 = __fma_rn(ri, ri, a0);
           a1 = __fma_rn(bi, bi, a1);
+        }
+        if (P.exact_cgs2) {
+#pragma unroll
+          for (int a = 0; a < BS; ++a) P.r[BS * u + a] = rv[a];
+        } else {                                   // scaled basis: U_0 = r, t = M^-1 U_0 (cell-local)
+          double tt[BS];
+          block_apply<BS>(A.dinv + BS * BS * u, rv, tt);
+#pragma unroll
+          for (int a = 0; a < BS; ++a) { P.V[BS * u + a] = rv[a]; P.t[BS * u + a] = tt[a]; }
         }
       }
       lane_flush(0, a0);
@@ -168,9 +179,9 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
     if (beta <= tgt) { status = LC_OK; break; }
     if (it >= P.max_iters) { status = LC_NOT_CONVERGED; break; }
     first = false;
-    if (threadIdx.x <= m) gv[threadIdx.x] = 0.0;
+    if (threadIdx.x <= m) { gv[threadIdx.x] = 0.0; sig[threadIdx.x] = 1.0; }
     __syncthreads();
-    if (threadIdx.x == 0) gv[0] = beta;
+    if (threadIdx.x == 0) { gv[0] = beta; if (!P.exact_cgs2) sig[0] = 1.0 / beta; }
     __syncthreads();
     double hnorm = beta;
     const double* src = P.r;
@@ -178,7 +189,9 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
     for (int j = 0; j < m; ++j) {
       TLG(tk);
       double* Vj = P.V + (size_t)j * n;
-      // ---- 1a: v_j = src / h, t = M^-1 v_j
+      // ---- 1a (exact-CGS2 mode): v_j = src / h, t = M^-1 v_j.  The scaled-basis (Gram) mode has t = M^-1 U_j
+      // from the previous update pass (or the residual pass) and skips this pass and its barrier.
+      if (P.exact_cgs2) {
       for (int64_t s = s_begin; s < A.nslices; s += s_step) {
         int64_t u = A.slice_row0[s] + lane;
         if (u >= nunits) continue;
@@ -189,8 +202,9 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
 #pragma unroll
         for (int a = 0; a < BS; ++a) P.t[BS * u + a] = tt[a];
       }
-      TLG(tk);
       grid_barrier(P.bar);
+      }
+      TLG(tk);
       TLG(tk);
       // ---- 1b: w = A t, h_i = V_i . w.  A warp owns 1-2 slices per chunk: their w values stay in registers
       // and the (j+1) dots are formed i by i (no per-thread accumulator array in local memory).
@@ -274,10 +288,12 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
         grid_barrier(P.bar);
         reduce(2 * (j + 1));
         TLG(tk);
-        if (threadIdx.x <= j) {
-          Gm[threadIdx.x * (kMaxM + 1) + j] = red[j + 1 + threadIdx.x];
-          Gm[j * (kMaxM + 1) + threadIdx.x] = red[j + 1 + threadIdx.x];
-          H[threadIdx.x * m + j] = red[threadIdx.x];
+        if (threadIdx.x <= j) {                     // dots of the stored U_i: V_i = sig_i U_i, w = sig_j A t
+          const double sc = sig[threadIdx.x] * sig[j];
+          const double gij = sc * red[j + 1 + threadIdx.x];
+          Gm[threadIdx.x * (kMaxM + 1) + j] = gij;
+          Gm[j * (kMaxM + 1) + threadIdx.x] = gij;
+          H[threadIdx.x * m + j] = sc * red[threadIdx.x];
         }
         __syncthreads();
         __shared__ double hh[kMaxM + 1];
@@ -288,8 +304,12 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
           hh[i] = H[i * m + j] + (H[i * m + j] - gh);        // h + h2, h2 = h - G h
         }
         __syncthreads();
-        if (threadIdx.x <= j) H[threadIdx.x * m + j] = hh[threadIdx.x];
+        if (threadIdx.x <= j) {
+          H[threadIdx.x * m + j] = hh[threadIdx.x];
+          hh[threadIdx.x] *= sig[threadIdx.x];                // coefficient of the stored U_i
+        }
         __syncthreads();
+        const double sj = sig[j];
         clear(1);
         {
           double a0 = 0.0;
@@ -298,7 +318,7 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
             if (u >= nunits) continue;
             double ww[BS];
 #pragma unroll
-            for (int a = 0; a < BS; ++a) ww[a] = P.w[BS * u + a];
+            for (int a = 0; a < BS; ++a) ww[a] = sj * P.w[BS * u + a];
             for (int i0 = 0; i0 <= j; i0 += kIB) {
               double vv[kIB][BS];
 #pragma unroll
@@ -313,8 +333,16 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
                 for (int a = 0; a < BS; ++a) ww[a] = __fma_rn(-hi, vv[ii][a], ww[a]);
               }
             }
+            // U_{j+1} = w (normalised lazily through sig_{j+1}) and t = M^-1 U_{j+1} for the next step
+            double tt[BS];
+            block_apply<BS>(A.dinv + BS * BS * u, ww, tt);
+            double* Un = P.V + (size_t)(j + 1) * n;
 #pragma unroll
-            for (int a = 0; a < BS; ++a) { P.w[BS * u + a] = ww[a]; a0 = __fma_rn(ww[a], ww[a], a0); }
+            for (int a = 0; a < BS; ++a) {
+              Un[BS * u + a] = ww[a];
+              P.t[BS * u + a] = tt[a];
+              a0 = __fma_rn(ww[a], ww[a], a0);
+            }
           }
           lane_flush(0, a0);
         }
@@ -422,6 +450,7 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
         gv[j + 1] = -sn[j] * gv[j];
         gv[j] = cs[j] * gv[j];
         red[kMaxQ - 1] = hn;
+        if (!P.exact_cgs2 && j + 1 <= m) sig[j + 1] = 1.0 / hn;
       }
       __syncthreads();
       hnorm = red[kMaxQ - 1];
@@ -450,7 +479,7 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
       for (int a = 0; a < BS; ++a) acc[a] = 0.0;
       for (int i = 0; i < jend; ++i) {
         const double* Vi = P.V + (size_t)i * n;
-        double yi = yv[i];
+        double yi = yv[i] * sig[i];
 #pragma unroll
         for (int a = 0; a < BS; ++a) acc[a] = __fma_rn(yi, Vi[BS * u + a], acc[a]);
       }
