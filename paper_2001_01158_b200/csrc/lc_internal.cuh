@@ -309,6 +309,85 @@ __device__ __forceinline__ void grid_barrier(GridBar* gb) {
   __syncthreads();
 }
 
+// out[t] = sum over the members m_i = first + i step (i < count, ascending) of part[m_i T + t], t < T <= 128:
+// warp w sums a contiguous range of members, then the NW warp sums are added in warp order (fixed order);
+// the block has NW warps
+template <int NW, int TMAX>
+__device__ __forceinline__ void sum_members(const double* part, int T, unsigned first, unsigned step, unsigned count,
+                                            double* out, double (*s_tmp)[TMAX]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned per = (count + NW - 1) / NW;
+  const unsigned i0 = warp * per, i1 = min(count, i0 + per);
+  for (int t = lane; t < T; t += 32) {
+    double a = 0.0;
+    for (unsigned i = i0; i < i1; ++i) a += __ldcg(part + (size_t)(first + i * step) * T + t);
+    s_tmp[warp][t] = a;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < T; t += NW * 32) {
+    double a = 0.0;
+    for (int w = 0; w < NW; ++w) a += s_tmp[w][t];
+    out[t] = a;
+  }
+}
+
+// Grid barrier whose arrival tree also reduces the per-CTA partials part[b][0..T) (batched solves, G > 1):
+// the last arriver of each of the kBarSub sub-groups sums its members' partials (by CTA index) into
+// subred[k], the last of those sums the sub-groups (by index) into red and releases the generation.  Every
+// CTA then reads only the T sums, instead of a second barrier plus a per-segment stage (profiles/r01_m).
+template <int NW, int TMAX>
+__device__ void tree_reduce_barrier(GridBar* gb, const double* part, double* subred, double* red, int T,
+                                    double (*s_tmp)[TMAX], int* s_flag) {
+  const unsigned nb = gridDim.x, b = blockIdx.x;
+  __syncthreads();
+  unsigned g0 = 0;
+  if (threadIdx.x == 0) {
+    g0 = ld_acquire_u32(&gb->gen);
+    __threadfence();
+    int f;
+    if (nb <= 64) {
+      f = atomicAdd(&gb->top, 1u) == nb - 1 ? 2 : 0;
+    } else {
+      const unsigned k = b % kBarSub, nk = (nb - k + kBarSub - 1) / kBarSub;
+      f = atomicAdd(&gb->sub[k][0], 1u) == nk - 1 ? 1 : 0;
+    }
+    if (f) __threadfence();
+    s_flag[0] = f;
+  }
+  __syncthreads();
+  int f = s_flag[0];
+  if (f == 1) {
+    const unsigned k = b % kBarSub, nk = (nb - k + kBarSub - 1) / kBarSub;
+    sum_members<NW, TMAX>(part, T, k, kBarSub, nk, subred + (size_t)k * T, s_tmp);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      gb->sub[k][0] = 0;
+      __threadfence();
+      const bool last = atomicAdd(&gb->top, 1u) == (unsigned)kBarSub - 1;
+      if (last) __threadfence();
+      s_flag[0] = last ? 2 : 1;
+    }
+    __syncthreads();
+    f = s_flag[0];
+    if (f == 2) sum_members<NW, TMAX>(subred, T, 0, 1, kBarSub, red, s_tmp);
+  } else if (f == 2) {
+    sum_members<NW, TMAX>(part, T, 0, 1, nb, red, s_tmp);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (f == 2) {
+      __threadfence();
+      gb->top = 0;
+      st_release_u32(&gb->gen, g0 + 1);
+    } else {
+      while (ld_acquire_u32(&gb->gen) == g0) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 // ---- TMA (bulk async copy) + mbarrier helpers (sm_90+ PTX; SASS UBLKCP / SYNCS) ----
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {

@@ -210,14 +210,6 @@ __device__ __forceinline__ void tl_mark(int& k) {
   ++k;
 }
 #define TL(k) tl_mark(k)
-__device__ unsigned long long g_tlx[8192];      // tree barrier: [last sub-group arrival, top release] pairs
-__device__ unsigned g_tlx_n;
-__device__ __forceinline__ void tlx_mark(int which) {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  unsigned i = which == 0 ? atomicAdd(&g_tlx_n, 1u) : g_tlx_n - 1;
-  if (i < 4096) g_tlx[2 * i + which] = t;
-}
 #else
 #define TL(k) (void)0
 #endif
@@ -325,88 +317,6 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
   }
 }
 
-// out[t] = sum over the members m_i = first + i step (i < count, ascending) of part[m_i T + t], t < T <= 128:
-// warp w sums a contiguous range of members, then the 8 warp sums are added in warp order (fixed order)
-__device__ __forceinline__ void sum_members(const double* part, int T, unsigned first, unsigned step, unsigned count,
-                                            double* out, double (*s_tmp)[2 * kMaxSeg]) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned per = (count + kPW - 1) / kPW;
-  const unsigned i0 = warp * per, i1 = min(count, i0 + per);
-  for (int t = lane; t < T; t += 32) {
-    double a = 0.0;
-    for (unsigned i = i0; i < i1; ++i) a += __ldcg(part + (size_t)(first + i * step) * T + t);
-    s_tmp[warp][t] = a;
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < T; t += kPT) {
-    double a = 0.0;
-    for (int w = 0; w < kPW; ++w) a += s_tmp[w][t];
-    out[t] = a;
-  }
-}
-
-// Grid barrier whose arrival tree also reduces the per-CTA partials part[b][0..T) (batched solves, G > 1):
-// the last arriver of each of the kBarSub sub-groups sums its members' partials (by CTA index) into
-// subred[k], the last of those sums the sub-groups (by index) into red and releases the generation.  Every
-// CTA then reads only the T sums, instead of a second barrier plus a per-segment stage (profiles/r01_m).
-__device__ void tree_reduce_barrier(GridBar* gb, const double* part, double* subred, double* red, int T,
-                                    double (*s_tmp)[2 * kMaxSeg], int* s_flag) {
-  const unsigned nb = gridDim.x, b = blockIdx.x;
-  __syncthreads();
-  unsigned g0 = 0;
-  if (threadIdx.x == 0) {
-    g0 = ld_acquire_u32(&gb->gen);
-    __threadfence();
-    int f;
-    if (nb <= 64) {
-      f = atomicAdd(&gb->top, 1u) == nb - 1 ? 2 : 0;
-    } else {
-      const unsigned k = b % kBarSub, nk = (nb - k + kBarSub - 1) / kBarSub;
-      f = atomicAdd(&gb->sub[k][0], 1u) == nk - 1 ? 1 : 0;
-    }
-    if (f) __threadfence();
-    s_flag[0] = f;
-  }
-  __syncthreads();
-  int f = s_flag[0];
-  if (f == 1) {
-    const unsigned k = b % kBarSub, nk = (nb - k + kBarSub - 1) / kBarSub;
-    sum_members(part, T, k, kBarSub, nk, subred + (size_t)k * T, s_tmp);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      gb->sub[k][0] = 0;
-      __threadfence();
-      const bool last = atomicAdd(&gb->top, 1u) == (unsigned)kBarSub - 1;
-      if (last) __threadfence();
-      s_flag[0] = last ? 2 : 1;
-    }
-    __syncthreads();
-    f = s_flag[0];
-#ifdef LC_DEBUG_TIMELINE
-    if (f == 2 && threadIdx.x == 0) tlx_mark(0);
-#endif
-    if (f == 2) sum_members(subred, T, 0, 1, kBarSub, red, s_tmp);
-  } else if (f == 2) {
-    sum_members(part, T, 0, 1, nb, red, s_tmp);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (f == 2) {
-      __threadfence();
-      gb->top = 0;
-#ifdef LC_DEBUG_TIMELINE
-      if (nb > 64) tlx_mark(1);
-#endif
-      st_release_u32(&gb->gen, g0 + 1);
-    } else {
-      while (ld_acquire_u32(&gb->gen) == g0) {
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 template <int WM, int ST>
 __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   __shared__ SegState S[kMaxSeg];
@@ -493,8 +403,8 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       }
 #endif
     } else {
-      tree_reduce_barrier(P.bar, P.part, P.subred, P.red, 2 * G,
-                          reinterpret_cast<double (*)[2 * kMaxSeg]>(&s_acc[0][0][0]), s_tflag);
+      tree_reduce_barrier<kPW, 2 * kMaxSeg>(P.bar, P.part, P.subred, P.red, 2 * G,
+                                            reinterpret_cast<double (*)[2 * kMaxSeg]>(&s_acc[0][0][0]), s_tflag);
       for (int t = threadIdx.x; t < G * 2; t += kPT) s_sum[t >> 1][t & 1] = __ldcg(P.red + t);
     }
     __syncthreads();
@@ -932,11 +842,5 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
 #ifdef LC_DEBUG_TIMELINE
 extern "C" int lc_debug_timeline(unsigned long long* out, int n) {
   return cudaMemcpyFromSymbol(out, lc::g_tl, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -1;
-}
-extern "C" int lc_debug_timeline_tree(unsigned long long* out, int n) {
-  unsigned z = 0;
-  int r = cudaMemcpyFromSymbol(out, lc::g_tlx, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -1;
-  cudaMemcpyToSymbol(lc::g_tlx_n, &z, sizeof(z));
-  return r;
 }
 #endif
