@@ -14,6 +14,7 @@
 // x_i = (b_i - acc) / a_ii.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "lc_internal.cuh"
 
@@ -134,6 +135,124 @@ __global__ void __launch_bounds__(kGST) k_gs_levels(SellView A, int reg_units, i
     }
 }
 
+// Line-pipelined sweep for 2-D five-point grids (offsets {-nx, -1, 0, 1, nx}; the paper's heat model):
+// lane l of warp w of CTA c owns grid line L = c kLB + 32 w + l (iy of segment g = L / ny) and walks it in
+// natural order, skewed one step behind line L - 1: at warp step tau it updates ix = tau - l, whose NEW
+// lower neighbour x(ix, iy - 1) line L - 1 produced one step earlier (a register shuffle inside the warp;
+// across warps a shared-memory ring with progress counters; across CTAs global memory behind a progress
+// word published with release semantics), whose NEW left neighbour is the lane's own previous value, and
+// whose right / upper neighbours are still OLD.  The critical path is the nx + ny - 1 wavefront of
+// natural-order GS; no block-wide barrier sits on it (a barrier per step would also wait for the
+// prefetches).  Matrix values, b and the old neighbours are prefetched kPF steps ahead into registers.  Per
+// row the oracle's expression in the slot (ascending column) order, so the sweep is bit-exact.
+constexpr int kLB = 128;        // lines per CTA (4 warps)
+constexpr int kLW = kLB / 32;
+constexpr int kPF = 8;          // prefetch depth (steps)
+constexpr int kPub = 16;        // cross-CTA progress publication period (steps), a multiple of kPF
+constexpr int kRing = 256;      // cross-warp ring of boundary values (per warp)
+__global__ void __launch_bounds__(kLB) k_gs_lines(SellView A, int reg_units, int spg, int nx, int ny, int G,
+                                                  const double* __restrict__ b, double* x, unsigned* prog) {
+  // warp w's lane-31 outputs, slot ix % kRing = (value, ix) written and read as one 16-byte shared access,
+  // so the consumer validates the slot by its tag without a fence on the producer's critical path
+  __shared__ __align__(16) double2 s_ring[kLW][kRing];
+  __shared__ volatile int s_cons[kLW];         // warp w: its lane 0 has consumed ix < s_cons[w]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, c = blockIdx.x;
+  if (lane == 0) s_cons[w] = 0;
+  for (int i = threadIdx.x; i < kLW * kRing; i += kLB) (&s_ring[0][0])[i] = make_double2(0.0, __longlong_as_double(-1ll));
+  __syncthreads();
+  const int64_t L = (int64_t)c * kLB + threadIdx.x;
+  const bool line_ok = L < (int64_t)ny * G;
+  const int g = line_ok ? (int)(L / ny) : 0;
+  const int iy = line_ok ? (int)(L - (int64_t)g * ny) : 0;
+  const int64_t base = (int64_t)g * reg_units + (int64_t)nx * iy;      // row of (0, iy) in segment g
+  double pa[kPF][5], pb[kPF], p3[kPF], p4[kPF];
+  unsigned pm[kPF];
+  const int64_t nu1 = (int64_t)reg_units * G - 1;
+  // loads independent of each other and of the mask (holes hold 0, neighbour indices clamped), so nothing
+  // in a step waits on a prefetch issued for a later step (in-order issue would stall at the first use)
+  auto load = [&](int q, int ix) {                       // branch-free: out-of-range steps load row base
+    const int ixc = (line_ok && ix >= 0 && ix < nx) ? ix : 0;
+    const int64_t lu = (int64_t)nx * iy + ixc, u = base + ixc;
+    const int64_t sl = (int64_t)g * spg + (lu >> 5);
+    const int64_t pl = 32ll * A.vw * sl + (lu & 31);
+    pm[q] = A.mask[u];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) pa[q][k] = __ldg(A.val + pl + 32 * k);
+    pb[q] = b[u];
+    p3[q] = __ldcg(x + (u + 1 <= nu1 ? u + 1 : nu1));       // old right neighbour
+    p4[q] = __ldcg(x + (u + nx <= nu1 ? u + nx : nu1));     // old upper neighbour (not updated yet)
+  };
+#pragma unroll
+  for (int q = 0; q < kPF; ++q) load(q, q - lane);
+  // warp 0 of CTA c > 0: the previous CTA's last line, fetched 32 values at a time once published
+  double bv = 0.0;
+  int bnd_lo = 0, bnd_hi = 0;                              // x(ix, iy0 - 1) for ix in [bnd_lo, bnd_hi) held by lane ix - bnd_lo
+  const int64_t prev_row0 = __shfl_sync(0xffffffffu, base, 0) - nx;   // lane 0's lower line (if any)
+  double xl = 0.0, last = 0.0;                              // own new value at ix - 1; output of the step
+  const int nsteps = nx + 31;
+  for (int tau0 = 0; tau0 < nsteps; tau0 += kPF) {
+#pragma unroll
+    for (int q = 0; q < kPF; ++q) {
+      const int tau = tau0 + q;
+      const int ix = tau - lane;
+      const bool act = line_ok && ix >= 0 && ix < nx;
+      double y0 = __shfl_up_sync(0xffffffffu, last, 1);   // line L - 1 at ix (lanes 1..31)
+      if (w == 0) {                                        // previous CTA's last line (same segment)
+        const bool need = __shfl_sync(0xffffffffu, act && (pm[q] & 1u) && ix >= bnd_hi, 0);
+        if (need) {                                        // warp-uniform refill of the boundary window
+          int pr = 0;
+          if (lane == 0) {                                 // relaxed polling, one acquire fence after it
+            while ((pr = (int)*(volatile unsigned*)(prog + c - 1)) <= tau) {
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          }
+          pr = __shfl_sync(0xffffffffu, pr, 0);
+          bnd_lo = tau;
+          bnd_hi = min(tau + 32, pr);
+          bv = tau + lane < bnd_hi ? __ldcg(x + prev_row0 + tau + lane) : 0.0;
+        }
+        const double bw = __shfl_sync(0xffffffffu, bv, (tau - bnd_lo) & 31);
+        if (lane == 0 && act && (pm[q] & 1u)) y0 = bw;
+      } else if (lane == 0 && act && (pm[q] & 1u)) {       // previous warp's lane 31
+        const unsigned a = (unsigned)__cvta_generic_to_shared(&s_ring[w - 1][ix % kRing]);
+        long long vb, tg;
+        do {
+          asm volatile("ld.volatile.shared.v2.b64 {%0, %1}, [%2];" : "=l"(vb), "=l"(tg) : "r"(a));
+        } while (tg != ix);
+        y0 = __longlong_as_double(vb);
+      }
+      // the row update with selects instead of branches (the warp stays converged for the shuffles)
+      const unsigned m = act ? pm[q] : 0u;
+      double acc = 0.0;
+      acc = (m & 1u) ? __fma_rn(pa[q][0], y0, acc) : acc;
+      acc = (m & 2u) ? __fma_rn(pa[q][1], xl, acc) : acc;
+      acc = (m & 8u) ? __fma_rn(pa[q][3], p3[q], acc) : acc;
+      acc = (m & 16u) ? __fma_rn(pa[q][4], p4[q], acc) : acc;
+      const double xn = act ? (pb[q] - acc) / pa[q][2] : 0.0;
+      if (act) x[base + ix] = xn;
+      xl = act ? xn : xl;
+      if (lane == 31 && w < kLW - 1 && act) {              // hand the value to the next warp's lane 0
+        while (ix - s_cons[w + 1] >= kRing) {
+        }
+        const unsigned a = (unsigned)__cvta_generic_to_shared(&s_ring[w][ix % kRing]);
+        asm volatile("st.volatile.shared.v2.b64 [%0], {%1, %2};" ::"r"(a), "l"(__double_as_longlong(xn)),
+                     "l"((long long)ix) : "memory");
+      }
+      last = xn;
+      if (lane == 0) s_cons[w] = tau + 1;                  // (every step: a line that needs no values never blocks)
+      load(q, tau + kPF - lane);                           // ring slot q now serves step tau + kPF
+      __syncwarp();
+    }
+    // the CTA's last line publishes its progress for the next CTA's first line
+    if (w == kLW - 1 && lane == 31 && ((tau0 / kPF) % (kPub / kPF) == kPub / kPF - 1 || tau0 + kPF >= nsteps)) {
+      int done = tau0 + kPF - 31;                          // ix < done are written
+      done = done < 0 ? 0 : (done > nx ? nx : done);
+      __threadfence();
+      st_release_u32(prog + c, (unsigned)done);
+    }
+  }
+}
+
 // every stored coupling of a stencil row must be a true grid neighbour (else the level schedule is invalid)
 __global__ void k_check_grid(SellView A, int reg_units, Grid3 gr, int64_t n, unsigned* bad) {
   const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -194,6 +313,28 @@ extern "C" lc_status lc_smooth_gs(lc_matrix M, const double* b, double* x, int32
     LC_CUDA(cudaStreamSynchronize(s));
     dfree(ws, s);
     if (bad) gr.nx = 0;
+  }
+  if (gr.nx > 0 && gr.nz == 1 && getenv("LC_GS_LEVELS") == nullptr) {
+    // 2-D five-point grid: line-pipelined sweep (one CTA-local barrier per wavefront step)
+    const int64_t lines = (int64_t)gr.ny * M->batch;
+    const int nCTA = (int)((lines + kLB - 1) / kLB);
+    void* ws = nullptr;
+    lc_status st = dalloc(&ws, sizeof(unsigned) * (size_t)nCTA * sweeps + 64, s);
+    if (st) return st;
+    LC_CUDA(cudaMemsetAsync(ws, 0, sizeof(unsigned) * (size_t)nCTA * sweeps + 64, s));
+    SellView V = view(A);
+    const int spg = (M->seg_units + 31) / 32;
+    int ru = M->seg_units, G = M->batch, nx = gr.nx, ny = gr.ny;
+    for (int sw = 0; sw < sweeps; ++sw) {
+      unsigned* prog = (unsigned*)ws + (size_t)nCTA * sw;
+      void* args[] = {&V, &ru, (void*)&spg, &nx, &ny, &G, (void*)&b, &x, &prog};
+      // cooperative: CTA c spins on CTA c - 1's progress, so all CTAs must be co-resident
+      LC_CUDA(cudaLaunchCooperativeKernel((void*)k_gs_lines, dim3((unsigned)nCTA), dim3(kLB), args, 0, s));
+      count_launch();
+    }
+    dfree(ws, s);
+    LC_CUDA(cudaStreamSynchronize(s));
+    return LC_OK;
   }
   if (gr.nx > 0) {
     void* ws = nullptr;
