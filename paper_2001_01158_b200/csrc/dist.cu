@@ -92,32 +92,18 @@ __device__ __forceinline__ uint8_t ldcv_u8(const uint8_t* p) {
   return (uint8_t)v;
 }
 
-// grid barrier over the nb CTAs of one rank (b = CTA index within the rank); see grid_barrier
-__device__ __forceinline__ void rank_barrier(GridBar* gb, unsigned nb, unsigned b) {
+// barrier over the nb CTAs of one rank: the counter form of grid_barrier (lc_internal.cuh) on the rank's own
+// GridBar; `epoch` counts this CTA's rank barriers
+__device__ __forceinline__ void rank_barrier(GridBar* gb, unsigned nb, unsigned long long& epoch) {
   __syncthreads();
+  epoch += nb;
   if (threadIdx.x == 0) {
-    const unsigned g0 = ld_acquire_u32(&gb->gen);
-    __threadfence();
-    bool last = false;
-    if (nb <= 64) {
-      last = atomicAdd(&gb->top, 1u) == nb - 1;
-    } else {
-      const unsigned k = b % kBarSub;
-      const unsigned nk = (nb - k + kBarSub - 1) / kBarSub;
-      if (atomicAdd(&gb->sub[k][0], 1u) == nk - 1) {
-        gb->sub[k][0] = 0;
-        __threadfence();
-        last = atomicAdd(&gb->top, 1u) == (unsigned)kBarSub - 1;
-      }
-    }
-    if (last) {
-      gb->top = 0;
-      st_release_u32(&gb->gen, g0 + 1);
-    } else {
-      while (ld_acquire_u32(&gb->gen) == g0) {
-      }
-    }
-    __threadfence();
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&gb->ctr) : "memory");
+    unsigned long long v;
+    do {
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&gb->ctr) : "memory");
+    } while (v < epoch);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
 }
@@ -145,7 +131,7 @@ __device__ __forceinline__ void warp_comb(int op, double* a) {
 
 // Global (all ranks) combination of the threads' 4-vectors `a`; result in s_out[4] for every thread.
 __device__ void xreduce(const DArgs& P, unsigned bid, unsigned nCTA, int op, double* a, double (*s_w)[4],
-                        double* s_out, unsigned long long seq) {
+                        double* s_out, unsigned long long seq, unsigned long long& bep) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   warp_comb(op, a);
   if (lane == 0)
@@ -156,7 +142,7 @@ __device__ void xreduce(const DArgs& P, unsigned bid, unsigned nCTA, int op, dou
     for (int w = 1; w < kDW; ++w) comb(op, c, s_w[w]);
     for (int j = 0; j < 4; ++j) P.part[4 * bid + j] = c[j];
   }
-  rank_barrier(P.bar, nCTA, bid);
+  rank_barrier(P.bar, nCTA, bep);
   const int par = (int)(seq & 1);
   if (bid == 0) {
     double c[4] = {0.0, 0.0, 0.0, 0.0};
@@ -402,7 +388,7 @@ __global__ void __launch_bounds__(kDT, 3) k_dpcg(const __grid_constant__ DPack p
   const DArgs& P = pk.a[slot];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t w0 = (int64_t)bid * kDW + warp, wst = (int64_t)nCTA * kDW;
-  unsigned long long seq = P.seq0;
+  unsigned long long seq = P.seq0, bep = 0;
   // interior slices: every column of every row inside the slab (or a zero hole at the global boundary)
   const int64_t nsl = P.A.nslices;
   int64_t sa = P.lo.n ? (-P.minoff + 31) / 32 : 0;
@@ -433,7 +419,7 @@ __global__ void __launch_bounds__(kDT, 3) k_dpcg(const __grid_constant__ DPack p
     } else if (mode == D_NORMAL) {
       dpass_a<WM, 2>(P, sa, sb, w0, wst, lane, false, s_beta, s_par, a);
     }
-    xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq);
+    xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq, bep);
     if (threadIdx.x == 0) {
       const double s0 = s_out[0], s1 = s_out[1];
       if (mode == D_INIT) {
@@ -508,7 +494,7 @@ __global__ void __launch_bounds__(kDT, 3) k_dpcg(const __grid_constant__ DPack p
         }
       }
     }
-    xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq);
+    xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq, bep);
     if (threadIdx.x == 0) {
       const double s0 = s_out[0], s1 = s_out[1];
       if (modeb == D_UPDATE) {
@@ -547,7 +533,7 @@ __global__ void __launch_bounds__(kDT, 2) k_ddomain(const __grid_constant__ DPac
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t w0 = (int64_t)bid * kDW + warp, wst = (int64_t)nCTA * kDW;
   const int n = (int)P.n;
-  unsigned long long seq = P.seq0;
+  unsigned long long seq = P.seq0, bep = 0;
   double* crit = P.q;
   // ---- criterion (Alg. 5 l.3-5 residual / Alg. 4 l.3-8 gradient) + ||b||^2 (double-double) + max c
   double a[4] = {0.0, 0.0, 0.0, 0.0};
@@ -584,7 +570,7 @@ __global__ void __launch_bounds__(kDT, 2) k_ddomain(const __grid_constant__ DPac
     crit[u] = c;
     a[2] = fmax(a[2], c);
   }
-  xreduce(P, bid, nCTA, 1, a, s_w, s_out, ++seq);
+  xreduce(P, bid, nCTA, 1, a, s_w, s_out, ++seq, bep);
   double tau, tc;
   if (P.thr == LC_THR_PAPER) {
     const double nb = sqrt(s_out[0] + s_out[1]);
@@ -601,7 +587,7 @@ __global__ void __launch_bounds__(kDT, 2) k_ddomain(const __grid_constant__ DPac
     P.om[u] = in ? 0 : kOutD;
     a[0] += in ? 1.0 : 0.0;
   }
-  xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq);                           // also: flags visible to peers
+  xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq, bep);                           // also: flags visible to peers
   int stage = 1, rounds = 0;
   // ---- Alg. 5 l.15-34: expansion rounds; stop when the GLOBAL admission count is 0 (R40)
   for (int rd = 0; rd < P.rounds; ++rd, ++stage) {
@@ -628,7 +614,7 @@ __global__ void __launch_bounds__(kDT, 2) k_ddomain(const __grid_constant__ DPac
         a[0] += 1.0;
       }
     }
-    xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq);
+    xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq, bep);
     ++rounds;
     if (s_out[0] == 0.0) { stage = 1 + P.rounds; break; }
   }
@@ -647,7 +633,7 @@ __global__ void __launch_bounds__(kDT, 2) k_ddomain(const __grid_constant__ DPac
         if (flag_at(P, u + A.off[k], edge) < stage) { P.om[u] = (uint8_t)stage; break; }
       }
     }
-    xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq);
+    xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq, bep);
   }
   // ---- Eq. 3 on Omega rows: b_sub = b - (fma chain over stored columns outside Omega, ascending);
   //      masked-solve start: x = x0 on Omega, 0 elsewhere; r, z, q, p0, p1 = 0
@@ -675,7 +661,7 @@ __global__ void __launch_bounds__(kDT, 2) k_ddomain(const __grid_constant__ DPac
     P.x[u] = xu;
     P.r[u] = 0.0; P.z[u] = 0.0; P.q[u] = 0.0; P.p0[u] = 0.0; P.p1[u] = 0.0;
   }
-  xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq);
+  xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq, bep);
   if (bid == 0 && threadIdx.x == 0) {
     P.out_d[0] = tau;
     P.out_d[1] = s_out[0];

@@ -68,6 +68,7 @@ __device__ unsigned long long g_tlg[16384];
 
 template <int BS>
 __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
+  unsigned long long bar_epoch = 0;
 #ifdef LC_DEBUG_TIMELINE
   int tk = 0;
 #endif
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
       lane_flush(1, a1);
     }
     publish(2);
-    grid_barrier(P.bar);
+    grid_barrier(P.bar, bar_epoch);
     reduce(2);
     double beta = sqrt(red[0]);
     if (first) { nb = sqrt(red[1]); tgt = nb > 0 ? P.eps * nb : P.eps; }
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
 #pragma unroll
         for (int a = 0; a < BS; ++a) P.t[BS * u + a] = tt[a];
       }
-      grid_barrier(P.bar);
+      grid_barrier(P.bar, bar_epoch);
       }
       TLG(tk);
       TLG(tk);
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
         // h2 = V^T (w - V h) = h - G h comes from scalars, and both updates merge into one pass.
         publish(2 * (j + 1));
         TLG(tk);
-        grid_barrier(P.bar);
+        grid_barrier(P.bar, bar_epoch);
         reduce(2 * (j + 1));
         TLG(tk);
         if (threadIdx.x <= j) {                     // dots of the stored U_i: V_i = sig_i U_i, w = sig_j A t
@@ -348,13 +349,13 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
         }
         publish(1);
         TLG(tk);
-        grid_barrier(P.bar);
+        grid_barrier(P.bar, bar_epoch);
         reduce(1);
         TLG(tk);
       } else {
       publish(j + 1);
       TLG(tk);
-      grid_barrier(P.bar);
+      grid_barrier(P.bar, bar_epoch);
       reduce(j + 1);
       TLG(tk);
       // keep h in smem column j of H (pass-1 part)
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
       }
       publish(j + 1);
       TLG(tk);
-      grid_barrier(P.bar);
+      grid_barrier(P.bar, bar_epoch);
       reduce(j + 1);
       TLG(tk);
       // ---- 3: w -= V h2, ||w||^2
@@ -430,7 +431,7 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
       }
       publish(1);
       TLG(tk);
-      grid_barrier(P.bar);
+      grid_barrier(P.bar, bar_epoch);
       reduce(1);
       TLG(tk);
       }
@@ -487,7 +488,7 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
 #pragma unroll
       for (int a = 0; a < BS; ++a) P.x[BS * u + a] += tt[a];
     }
-    grid_barrier(P.bar);
+    grid_barrier(P.bar, bar_epoch);
   }
   if (bid == 0 && threadIdx.x == 0) { P.out[0] = it; P.out[1] = status; *P.out_relres = relres; }
   if (P.scatter_idx) {

@@ -104,6 +104,7 @@ struct Grid3 { int nx, ny, nz; };
 __global__ void __launch_bounds__(kGST) k_gs_levels(SellView A, int reg_units, int spg, Grid3 gr, int G,
                                                     const double* __restrict__ b, double* x, int sweeps,
                                                     GridBar* bar) {
+  unsigned long long bar_epoch = 0;
   const int64_t plane = (int64_t)gr.nx * gr.ny;
   const int64_t pairs = (int64_t)gr.ny * gr.nz;         // (iy, iz) candidates per level and segment
   const int nlev = gr.nx + gr.ny + gr.nz - 2;
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(kGST) k_gs_levels(SellView A, int reg_units, i
         x[u] = (b[u] - acc) / d;
       }
       if (gridDim.x == 1) __syncthreads();
-      else grid_barrier(bar);
+      else grid_barrier(bar, bar_epoch);
     }
 }
 

@@ -257,19 +257,28 @@ __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long 
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Grid-wide barrier for cooperative (co-resident) launches: arrivals on counters, the last arriver resets
-// them and bumps a generation word with release semantics; the others spin on the generation with acquire
-// loads (no sleep back-off, unlike cooperative_groups' grid sync, whose wake-up latency measured 2-7 us
-// per barrier on small grids: profiles/r01_d).  The whole struct must be zero at launch.
-// Two-level arrival: CTA b arrives on sub-counter b % kBarSub (each on its own 128-B line, so the arrivals
-// spread over L2 slices instead of serialising on one address: a single counter cost ~3 us with 592 CTAs),
-// the last arriver of each sub-group arrives on the top counter, the last of those releases the generation.
+// Grid-wide barriers for cooperative (co-resident) launches.  The whole struct must be zero at launch.
+//
+// grid_barrier: a counter barrier.  Each CTA adds 1 to one 64-bit counter with a fire-and-forget
+// red.release (no round trip) and polls it with relaxed loads until it reaches epoch x gridDim.x, then one
+// acquire fence: one one-way trip plus one poll on the critical path.  Measured on B200 (tools/micro/
+// barrier_bench.cu): 2.2 us per barrier at 592 CTAs, 1.4 us at 296, 1.3 us at 148, against 3.3-3.6 us for
+// the arrival-tree + generation-word form below, whose last arriver needs its atomic's result back before
+// it can release the others.  `epoch` is the caller's per-CTA barrier count (start at 0, same sequence of
+// barriers in every CTA).
+//
+// The arrival tree (sub-counters, top counter, generation word) is kept for tree_reduce_barrier, which
+// reduces partials inside it.  Two-level arrival: CTA b arrives on sub-counter b % kBarSub (each on its own
+// 128-B line), the last arriver of each sub-group arrives on the top counter, the last of those releases
+// the generation.
 constexpr int kBarSub = 16;
 struct GridBar {
   unsigned sub[kBarSub][32];
   unsigned top;
   unsigned gen;
   unsigned pad[30];
+  unsigned long long ctr;       // counter barrier
+  unsigned long long pad2[15];
 };
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -279,32 +288,16 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void grid_barrier(GridBar* gb) {
-  __syncthreads();
+__device__ __forceinline__ void grid_barrier(GridBar* gb, unsigned long long& epoch) {
+  __syncthreads();                                    // the CTA's writes precede thread 0's release (bar.sync)
+  epoch += gridDim.x;
   if (threadIdx.x == 0) {
-    const unsigned nb = gridDim.x, b = blockIdx.x;
-    const unsigned g0 = ld_acquire_u32(&gb->gen);
-    __threadfence();                                    // publish this CTA's writes (cumulative via bar.sync)
-    bool last = false;
-    if (nb <= 64) {                                     // small grids: one counter (one round trip)
-      last = atomicAdd(&gb->top, 1u) == nb - 1;
-    } else {
-      const unsigned k = b % kBarSub;
-      const unsigned nk = (nb - k + kBarSub - 1) / kBarSub;        // CTAs in sub-group k
-      if (atomicAdd(&gb->sub[k][0], 1u) == nk - 1) {
-        gb->sub[k][0] = 0;
-        __threadfence();
-        last = atomicAdd(&gb->top, 1u) == (unsigned)kBarSub - 1;
-      }
-    }
-    if (last) {
-      gb->top = 0;
-      st_release_u32(&gb->gen, g0 + 1);
-    } else {
-      while (ld_acquire_u32(&gb->gen) == g0) {
-      }
-    }
-    __threadfence();
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&gb->ctr) : "memory");
+    unsigned long long v;
+    do {
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&gb->ctr) : "memory");
+    } while (v < epoch);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
 }

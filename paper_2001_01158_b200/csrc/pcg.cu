@@ -319,6 +319,7 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
 
 template <int WM, int ST>
 __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
+  unsigned long long bar_epoch = 0;
   __shared__ SegState S[kMaxSeg];
   __shared__ double s_acc[kPW][kMaxSeg][2];
   __shared__ double s_red[kPW][2];
@@ -383,7 +384,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       P.part[(bid * G) * 2 + t] = v;
     }
     if (G == 1) {
-      grid_barrier(P.bar);
+      grid_barrier(P.bar, bar_epoch);
       double a0 = 0.0, a1 = 0.0;
       for (int64_t c = threadIdx.x; c < nCTA; c += kPT) { a0 += P.part[2 * c]; a1 += P.part[2 * c + 1]; }
       a0 = warp_sum(a0); a1 = warp_sum(a1);
