@@ -303,25 +303,31 @@ extern "C" lc_status lc_smooth_gs(lc_matrix M, const double* b, double* x, int32
     }
   }
   if (gr.nx > 0) {
-    void* ws = nullptr;
-    lc_status st = dalloc(&ws, 64, s);
+    DevBuf ws(s);
+    lc_status st = ws.alloc(64);
     if (st) return st;
-    LC_CUDA(cudaMemsetAsync(ws, 0, 64, s));
+    LC_CUDA(cudaMemsetAsync(ws.p, 0, 64, s));
     unsigned bad = 0;
-    k_check_grid<<<(unsigned)((M->n + 255) / 256), 256, 0, s>>>(view(A), M->seg_units, gr, M->n, (unsigned*)ws);
+    k_check_grid<<<(unsigned)((M->n + 255) / 256), 256, 0, s>>>(view(A), M->seg_units, gr, M->n, (unsigned*)ws.p);
     count_launch();
-    LC_CUDA(cudaMemcpyAsync(&bad, ws, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    LC_CUDA(cudaMemcpyAsync(&bad, ws.p, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     LC_CUDA(cudaStreamSynchronize(s));
-    dfree(ws, s);
     if (bad) gr.nx = 0;
   }
+  // 2-D five-point grid: line-pipelined sweep (lines of 128 per CTA, all CTAs co-resident)
+  const int64_t glines = (int64_t)gr.ny * M->batch;
+  int lines_ok = 0;
   if (gr.nx > 0 && gr.nz == 1 && getenv("LC_GS_LEVELS") == nullptr) {
-    // 2-D five-point grid: line-pipelined sweep (one CTA-local barrier per wavefront step)
-    const int64_t lines = (int64_t)gr.ny * M->batch;
-    const int nCTA = (int)((lines + kLB - 1) / kLB);
-    void* ws = nullptr;
-    lc_status st = dalloc(&ws, sizeof(unsigned) * (size_t)nCTA * sweeps + 64, s);
+    int per_sm = 0;
+    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_lines, kLB, 0));
+    lines_ok = (glines + kLB - 1) / kLB <= (int64_t)per_sm * num_sms();
+  }
+  if (lines_ok) {
+    const int nCTA = (int)((glines + kLB - 1) / kLB);
+    DevBuf wsb(s);
+    lc_status st = wsb.alloc(sizeof(unsigned) * (size_t)nCTA * sweeps + 64);
     if (st) return st;
+    void* ws = wsb.p;
     LC_CUDA(cudaMemsetAsync(ws, 0, sizeof(unsigned) * (size_t)nCTA * sweeps + 64, s));
     SellView V = view(A);
     const int spg = (M->seg_units + 31) / 32;
@@ -333,14 +339,14 @@ extern "C" lc_status lc_smooth_gs(lc_matrix M, const double* b, double* x, int32
       LC_CUDA(cudaLaunchCooperativeKernel((void*)k_gs_lines, dim3((unsigned)nCTA), dim3(kLB), args, 0, s));
       count_launch();
     }
-    dfree(ws, s);
     LC_CUDA(cudaStreamSynchronize(s));
     return LC_OK;
   }
   if (gr.nx > 0) {
-    void* ws = nullptr;
-    lc_status st = dalloc(&ws, sizeof(GridBar), s);
+    DevBuf wsb(s);
+    lc_status st = wsb.alloc(sizeof(GridBar));
     if (st) return st;
+    void* ws = wsb.p;
     LC_CUDA(cudaMemsetAsync(ws, 0, sizeof(GridBar), s));
     const int64_t work = (int64_t)gr.ny * gr.nz * M->batch;
     int per_sm = 0;
@@ -354,14 +360,14 @@ extern "C" lc_status lc_smooth_gs(lc_matrix M, const double* b, double* x, int32
     void* args[] = {&V, &ru, (void*)&spg, &gr, &G, (void*)&b, &x, &sweeps, &bar};
     LC_CUDA(cudaLaunchCooperativeKernel((void*)k_gs_levels, dim3((unsigned)nCTA), dim3(kGST), args, 0, s));
     count_launch();
-    dfree(ws, s);
     LC_CUDA(cudaStreamSynchronize(s));
     return LC_OK;
   }
-  void* ws = nullptr;
+  DevBuf wsb(s);
   const size_t fbytes = sizeof(unsigned) * (size_t)(A.nslices + 1);
-  lc_status st = dalloc(&ws, fbytes + 64 * (sweeps + 1), s);
+  lc_status st = wsb.alloc(fbytes + 64 * (sweeps + 1));
   if (st) return st;
+  void* ws = wsb.p;
   unsigned* flags = (unsigned*)ws;
   unsigned* counters = (unsigned*)((char*)ws + ((fbytes + 63) & ~(size_t)63));
   unsigned* err = counters + 16 * sweeps;
@@ -384,7 +390,6 @@ extern "C" lc_status lc_smooth_gs(lc_matrix M, const double* b, double* x, int32
   }
   unsigned h_err = 0;
   LC_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-  dfree(ws, s);
   LC_CUDA(cudaStreamSynchronize(s));
   if (h_err) { set_error("lc_smooth_gs: dependency wait timed out"); return LC_ERR_CUDA; }
   return LC_OK;

@@ -67,6 +67,16 @@ struct PcgJob {
 lc_status dalloc(void** p, size_t bytes, cudaStream_t s);
 void dfree(void* p, cudaStream_t s);
 int num_sms();
+// scoped stream-ordered workspace: freed on every return path (also the early LC_CUDA error returns)
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t s;
+  explicit DevBuf(cudaStream_t st) : s(st) {}
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { dfree(p, s); }
+  lc_status alloc(size_t bytes) { return dalloc(&p, bytes, s); }
+};
 
 // ------------------------------------------------------------------ SELL ----
 struct Sell {
