@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
             const int64_t u = uu[cc];
             const int64_t p0 = A.slice_ptr[s];
             const int wd = A.stencil ? A.W : (int)((A.slice_ptr[s + 1] - p0) >> 5);
+#pragma unroll 5
             for (int k = 0; k < wd; ++k) {
               const int64_t c = sv_col(A, p0 + lane, k, u);
               if (BS == 1) {
