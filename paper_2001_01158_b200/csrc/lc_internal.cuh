@@ -63,6 +63,10 @@ struct PcgJob {
   int reg_units = 0, spg = 0;     // equal segments of reg_units units with spg slices each (A), else 0
 };
 
+// small single-segment stencil systems: the cluster-resident PCG (pcg_dsmem.cu)
+bool pcg_dsmem_eligible(const PcgJob& job);
+lc_status run_pcg_dsmem(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info);
+
 // stream-ordered device allocation (pool with unlimited release threshold)
 lc_status dalloc(void** p, size_t bytes, cudaStream_t s);
 void dfree(void* p, cudaStream_t s);

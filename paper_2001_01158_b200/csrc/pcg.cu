@@ -699,6 +699,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   const int G = M.nseg;
   if (G > kMaxSeg) { set_error("PCG: at most 64 segments"); return LC_ERR_DIMENSION; }
   if (M.block != 1) { set_error("PCG: needs block = 1 (use LC_GMRES for block systems)"); return LC_ERR_INVALID_ARG; }
+  if (pcg_dsmem_eligible(job)) return run_pcg_dsmem(job, p, s, info);     // fits one cluster's shared memory
   std::vector<int> it(G, 0), stt(G, LC_OK);
   std::vector<double> rr(G, 0.0);
   float ms = 0.f;

@@ -1,0 +1,313 @@
+// pcg_dsmem.cu -- Jacobi-PCG for small single-segment stencil systems held entirely on chip
+// ("small systems: one thread-block cluster of <= 16 CTAs holds the Krylov vectors in
+// DSMEM, and the matrix too where it fits").
+//
+// One thread-block cluster of nq <= 16 CTAs; CTA q owns the rows [q R, min(n, (q+1) R)) and keeps their
+// stencil values, 1/a_ii, b and every Krylov vector (x, r, z, q, p, p_old) in its shared memory for the
+// whole solve.  A gathered neighbour row owned by another CTA of the cluster is read from that CTA's shared
+// memory (distributed shared memory, ld.shared::cluster through map_shared_rank).  One cluster barrier per
+// pass (two per iteration); the per-CTA partial dots are double-buffered by pass and read across the cluster
+// in rank order (fixed-order, bitwise deterministic).  The step order and the recursive/true residual
+// protocol are those of k_pcg (pcg.cu, or_pcg): INIT/CONFIRM r = b - A x, FIRST/NORMAL q = A p with
+// p = z + beta p_old formed on the fly, UPDATE x, r, z.  Device memory is touched only to load the system
+// and to write x back, so an iteration costs shared-memory latencies instead of L2 round trips.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "lc_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace lc {
+
+constexpr int kST = 512;                 // threads per CTA
+constexpr int kSW = kST / 32;
+constexpr int kMaxCluster = 16;
+constexpr size_t kSmemBudget = 200 * 1024;   // dynamic shared memory per CTA
+
+struct DsArgs {
+  SellView A;                    // stencil layout (values + dinv read once)
+  const double* b;
+  const double* x_in;            // initial guess
+  double* x_out;                 // result: all rows (global solve) or the Omega rows (masked local solve)
+  const uint8_t* omega;          // masked solve: row u is in the subsystem iff omega[u] != 255
+  int n, R;                      // rows, rows per CTA
+  double eps;
+  int max_iters;
+  int* out_iters;
+  int* out_status;
+  double* out_relres;
+};
+
+enum DsMode : int { S_INIT = 0, S_RESET, S_FIRST, S_NORMAL, S_UPDATE, S_CONFIRM, S_DONE };
+
+template <int W>
+__global__ void __launch_bounds__(kST, 1) k_pcg_ds(DsArgs P) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double s_part[2][2], s_w[kSW][2], s_sum[2];
+  __shared__ int s_mode, s_par, s_it, s_final, s_exit;
+  __shared__ double s_rho, s_alpha, s_beta, s_tgt, s_nb;
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank(), nq = (int)cl.num_blocks();
+  const int R = P.R, n = P.n;
+  const int r0 = q * R, nr = max(0, min(n, r0 + R) - r0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const SellView& A = P.A;
+  double* val = sm;                       // [W][R]
+  double* x = val + (size_t)W * R;
+  double* r = x + R;
+  double* z = r + R;
+  double* qv = z + R;
+  double* p0 = qv + R;
+  double* p1 = p0 + R;
+  double* dv = p1 + R;
+  double* bv = dv + R;
+  uint8_t* om = reinterpret_cast<uint8_t*>(bv + R);
+  // ---- load the CTA's rows
+  for (int i = threadIdx.x; i < nr; i += kST) {
+    const int u = r0 + i;
+    const int64_t pl = 32ll * W * (u >> 5) + (u & 31);
+#pragma unroll
+    for (int k = 0; k < W; ++k) val[(size_t)k * R + i] = A.val[pl + 32 * k];
+    x[i] = P.x_in[u];
+    bv[i] = P.b[u];
+    dv[i] = A.dinv[u];
+    om[i] = P.omega ? P.omega[u] : 0;
+    r[i] = 0.0; z[i] = 0.0; qv[i] = 0.0; p0[i] = 0.0; p1[i] = 0.0;
+  }
+  if (threadIdx.x == 0) {
+    s_mode = S_INIT; s_par = 0; s_it = 0; s_final = 0; s_exit = 0;
+    s_rho = s_alpha = s_beta = s_tgt = s_nb = 0.0;
+  }
+  cl.sync();
+  // value of vector v (an array of this CTA's layout) at global row c, from the owning CTA
+  auto at = [&](double* v, int c) -> double {
+    const int owner = c / R;
+    const int li = c - owner * R;
+    if (owner == q) return v[li];
+    return cl.map_shared_rank(v, owner)[li];
+  };
+  int ppar = 0;                           // partial buffer parity
+  auto reduce = [&](double a0, double a1) {
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    if (lane == 0) { s_w[warp][0] = a0; s_w[warp][1] = a1; }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+      double t = 0.0;
+      for (int w = 0; w < kSW; ++w) t += s_w[w][threadIdx.x];
+      s_part[ppar][threadIdx.x] = t;
+    }
+    cl.sync();
+    if (threadIdx.x < 2) {
+      double t = 0.0;
+      for (int o = 0; o < nq; ++o) t += cl.map_shared_rank(&s_part[ppar][0], o)[threadIdx.x];
+      s_sum[threadIdx.x] = t;
+    }
+    ppar ^= 1;
+    __syncthreads();
+  };
+  auto finish = [&](int status, double rn) {
+    s_mode = S_DONE;
+    if (q == 0) {
+      *P.out_iters = s_it;
+      *P.out_status = status;
+      *P.out_relres = s_nb > 0 ? rn / s_nb : rn;
+    }
+  };
+  const int nu1 = n - 1;
+  for (;;) {
+    // ---------------------------------------------------------------- pass A
+    const int mode = s_mode;
+    double a0 = 0.0, a1 = 0.0;
+    if (mode == S_INIT || mode == S_CONFIRM || mode == S_FIRST || mode == S_NORMAL) {
+      const double beta = s_beta;
+      double* pold = s_par ? p1 : p0;
+      double* pnew = s_par ? p0 : p1;
+      for (int i = threadIdx.x; i < nr; i += kST) {
+        const int u = r0 + i;
+        double acc = 0.0, own = 0.0;
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+          int c = u + A.off[k];
+          c = c < 0 ? 0 : (c > nu1 ? nu1 : c);
+          double y;
+          if (mode == S_INIT || mode == S_CONFIRM) y = at(x, c);
+          else if (mode == S_FIRST) y = at(z, c);
+          else y = __fma_rn(beta, at(pold, c), at(z, c));
+          acc = __fma_rn(val[(size_t)k * R + i], y, acc);
+          if (A.off[k] == 0) own = y;
+        }
+        if (om[i] == 255) continue;                // masked solve: rows outside Omega stay 0
+        if (mode == S_INIT || mode == S_CONFIRM) {
+          const double bi = bv[i];
+          const double ri = bi - acc;
+          r[i] = ri;
+          a0 = __fma_rn(ri, ri, a0);
+          if (mode == S_INIT) a1 = __fma_rn(bi, bi, a1);
+        } else {
+          pnew[i] = own;
+          qv[i] = acc;
+          a0 = __fma_rn(own, acc, a0);
+        }
+      }
+    }
+    reduce(a0, a1);
+    if (threadIdx.x == 0) {
+      const double s0 = s_sum[0], s1 = s_sum[1];
+      if (mode == S_INIT) {
+        s_nb = sqrt(s1);
+        s_tgt = s_nb > 0 ? P.eps * s_nb : P.eps;
+        const double rn = sqrt(s0);
+        if (!isfinite(rn)) finish(LC_ERR_NONFINITE, rn);
+        else if (rn <= s_tgt) finish(LC_OK, rn);
+        else s_mode = S_RESET;
+      } else if (mode == S_FIRST || mode == S_NORMAL) {
+        if (!(s0 > 0)) finish(isfinite(s0) ? LC_ERR_BREAKDOWN : LC_ERR_NONFINITE, NAN);
+        else { s_alpha = s_rho / s0; s_mode = S_UPDATE; s_par ^= 1; }
+      } else if (mode == S_CONFIRM) {
+        const double rn = sqrt(s0);
+        if (!isfinite(rn)) finish(LC_ERR_NONFINITE, rn);
+        else if (rn <= s_tgt) finish(LC_OK, rn);
+        else if (s_final) finish(LC_NOT_CONVERGED, rn);
+        else s_mode = S_RESET;
+      }
+    }
+    __syncthreads();
+    // ---------------------------------------------------------------- pass B (own rows only)
+    const int modeb = s_mode;
+    a0 = a1 = 0.0;
+    if (modeb == S_UPDATE || modeb == S_RESET) {
+      const double alpha = s_alpha;
+      const double* pp = s_par ? p1 : p0;
+      for (int i = threadIdx.x; i < nr; i += kST) {
+        if (modeb == S_UPDATE) {
+          const double xi = __fma_rn(alpha, pp[i], x[i]);
+          const double ri = __fma_rn(-alpha, qv[i], r[i]);
+          const double zi = ri * dv[i];
+          x[i] = xi; r[i] = ri; z[i] = zi;
+          a0 = __fma_rn(ri, zi, a0);
+          a1 = __fma_rn(ri, ri, a1);
+        } else {
+          const double zi = r[i] * dv[i];
+          z[i] = zi;
+          a0 = __fma_rn(r[i], zi, a0);
+        }
+      }
+    }
+    reduce(a0, a1);
+    if (threadIdx.x == 0) {
+      const double s0 = s_sum[0], s1 = s_sum[1];
+      if (modeb == S_UPDATE) {
+        s_it += 1;
+        if (!isfinite(s1) || sqrt(s1) <= s_tgt || s_it >= P.max_iters) {
+          s_mode = S_CONFIRM;
+          s_final = (s_it >= P.max_iters) || !isfinite(s1);
+        } else {
+          s_beta = s0 / s_rho;
+          s_rho = s0;
+          s_mode = S_NORMAL;
+        }
+      } else if (modeb == S_RESET) {
+        s_rho = s0;
+        s_mode = S_FIRST;
+      }
+      s_exit = s_mode == S_DONE;
+    }
+    __syncthreads();
+    if (s_exit) break;
+  }
+  // a8 (Eq. 4) / the global solve's result back to device memory
+  for (int i = threadIdx.x; i < nr; i += kST)
+    if (om[i] != 255) P.x_out[r0 + i] = x[i];
+  cl.sync();                                       // no CTA leaves while others may still read its memory
+}
+
+static size_t ds_row_bytes(int W) { return (size_t)8 * W + 8 * 8 + 1; }
+
+// true: the system fits the cluster-resident kernel (single segment, 5- or 7-point stencil, <= 16 CTAs)
+bool pcg_dsmem_eligible(const PcgJob& job) {
+  const Sell& M = *job.M;
+  if (M.nseg != 1 || !M.stencil || M.sym || M.block != 1 || (M.maxw != 5 && M.maxw != 7)) return false;
+  if (job.scatter_idx || getenv("LC_NO_DSMEM")) return false;
+  const int64_t rmax = (int64_t)((kSmemBudget - 64) / ds_row_bytes(M.maxw));
+  return M.nunits <= rmax * kMaxCluster;
+}
+
+lc_status run_pcg_dsmem(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
+  const Sell& M = *job.M;
+  const int W = M.maxw;
+  const int n = (int)M.nunits;
+  void* fn = W == 5 ? (void*)k_pcg_ds<5> : (void*)k_pcg_ds<7>;
+  static bool attr_set[2] = {false, false};
+  const int wi = W == 5 ? 0 : 1;
+  if (!attr_set[wi]) {
+    LC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+    LC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr_set[wi] = true;
+  }
+  DevBuf ws(s);
+  lc_status st = ws.alloc(64);
+  if (st) return st;
+  DsArgs a;
+  a.A = view(M);
+  a.b = job.b;
+  a.x_in = job.x_init ? job.x_init : job.x;
+  a.x_out = job.x_user ? job.x_user : job.x;
+  a.omega = job.omega;
+  a.n = n;
+  a.eps = p->rel_tol;
+  a.max_iters = p->max_iters;
+  a.out_iters = (int*)ws.p;
+  a.out_status = (int*)ws.p + 1;
+  a.out_relres = (double*)((char*)ws.p + 8);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaError_t e = cudaMemsetAsync(ws.p, 0, 64, s);
+  cudaEventRecord(e0, s);
+  // the largest cluster the device accepts (16 non-portable, else 8), rows split evenly
+  for (int nq : {kMaxCluster, 8}) {
+    a.R = (n + nq - 1) / nq;
+    const size_t dsm = (size_t)a.R * ds_row_bytes(W) + 16;
+    if (dsm > kSmemBudget) { e = cudaErrorInvalidValue; continue; }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nq);
+    cfg.blockDim = dim3(kST);
+    cfg.dynamicSmemBytes = dsm;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = nq;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* args[] = {&a};
+    e = cudaLaunchKernelExC(&cfg, fn, args);
+    if (e == cudaSuccess) break;
+    cudaGetLastError();
+  }
+  if (e == cudaSuccess) count_launch();
+  cudaEventRecord(e1, s);
+  int it = 0, stt = LC_OK;
+  double rr = 0.0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&it, a.out_iters, 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&stt, a.out_status, 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&rr, a.out_relres, 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  float ms = 0.f;
+  if (e == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  if (e != cudaSuccess) return cuda_fail(e, "PCG (cluster-resident) kernel");
+  if (info) {
+    info[0].iterations = it;
+    info[0].status = stt;
+    info[0].rel_residual = rr;
+    info[0].seconds = ms * 1e-3;
+  }
+  if (stt < 0) { set_error("PCG: breakdown or non-finite value (see lc_solve_info.status)"); return (lc_status)stt; }
+  return stt == LC_NOT_CONVERGED ? LC_NOT_CONVERGED : LC_OK;
+}
+
+}  // namespace lc
