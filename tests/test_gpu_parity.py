@@ -374,6 +374,35 @@ def test_other_layouts_parity(cfg, n, s, rule, layout, monkeypatch):
     check_system(sy, RULES[cfg][rule])
 
 
+@pytest.mark.parametrize("cfg,n,s,rule", [(1, 64, 4, 0), (1, 64, 8, 0), (5, 20, 6, 0), (2, 96, 5, 0)])
+def test_grid_kernel_path_parity(cfg, n, s, rule, monkeypatch):
+    """Small stencil systems run the cluster-resident PCG (k_pcg_ds) by default; LC_NO_DSMEM=1 sends them
+    through the grid-wide kernel (k_pcg, its cluster form for <= 512 slices) instead: both against the oracle."""
+    monkeypatch.setenv("LC_NO_DSMEM", "1")
+    check_system(synth.system(cfg, s, n=n), RULES[cfg][rule])
+
+
+def test_dsmem_and_grid_kernels_agree():
+    """The cluster-resident kernel and the grid kernel: same iteration counts (the same reductions in a
+    different fixed order may differ by one), solutions within the 1e-9 bar, on configs 1 and 5."""
+    import os
+    for cfg, n in ((1, 64), (5, 20)):
+        sy = synth.system(cfg, 3, n=n)
+        A = gpu_matrix(sy)
+        b, x0 = to_dev(sy.b), to_dev(sy.x0)
+        xa = x0.clone()
+        ia = lc.solve_global(A, b, xa)[0]
+        os.environ["LC_NO_DSMEM"] = "1"
+        try:
+            xb = x0.clone()
+            ib = lc.solve_global(A, b, xb)[0]
+        finally:
+            del os.environ["LC_NO_DSMEM"]
+        assert abs(ia["iterations"] - ib["iterations"]) <= 1
+        xa, xb = xa.cpu().numpy(), xb.cpu().numpy()
+        assert np.linalg.norm(xa - xb) / np.linalg.norm(xb) <= 1e-9
+
+
 def test_default_layouts():
     """All five configs are stencils: the default layout is the stencil layout."""
     for cfg, n, expect in [(1, 64, "stencil"), (5, 12, "stencil"), (3, 16, "stencil"), (4, 16, "stencil")]:
