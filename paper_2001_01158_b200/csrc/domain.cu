@@ -73,6 +73,47 @@ __global__ void __launch_bounds__(kTB) k_residual_crit(SellView A, const double*
   if (lane == 0) { p_max[s] = cmax; p_hi[s] = hi; p_lo[s] = lo; }
 }
 
+// a1 for the (non-symmetric-storage) stencil layout, block 1, width WM known at compile time: the same
+// per-row fma chain over slots k = 0..W-1 (holes add exact zeros), with every value load and gather of a
+// row issued before the chain (no runtime slot loop), so the kernel streams at the HBM rate.
+template <int WM>
+__global__ void __launch_bounds__(kTB) k_residual_stencil(SellView A, const double* __restrict__ b,
+                                                          const double* __restrict__ x, double* __restrict__ r,
+                                                          double* __restrict__ crit, double* __restrict__ p_max,
+                                                          double* __restrict__ p_hi, double* __restrict__ p_lo) {
+  const int64_t s = (blockIdx.x * (int64_t)kTB + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= A.nslices) return;
+  const int g = A.slice_seg[s];
+  const int64_t u = A.slice_row0[s] + lane;
+  const bool valid = u < A.seg_unit0[g + 1];
+  const int n1 = (int)A.nunits - 1, ui = (int)u;
+  const double* vp = A.val + 32ll * WM * s + lane;
+  double v[WM], y[WM];
+#pragma unroll
+  for (int k = 0; k < WM; ++k) {
+    int c = ui + A.off[k];
+    c = c < 0 ? 0 : (c > n1 ? n1 : c);
+    v[k] = __ldg(vp + 32 * k);
+    y[k] = __ldg(x + c);
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < WM; ++k) acc = __fma_rn(v[k], y[k], acc);
+  double cmax = 0.0, hi = 0.0, lo = 0.0;
+  if (valid) {
+    const double bi = b[u];
+    const double ri = bi - acc;
+    r[u] = ri;
+    cmax = fabs(ri);
+    crit[u] = cmax;
+    dd_add_sq(hi, lo, bi);
+  }
+  cmax = warp_max(cmax);
+  warp_dd_sum(hi, lo);
+  if (lane == 0) { p_max[s] = cmax; p_hi[s] = hi; p_lo[s] = lo; }
+}
+
 // ---------------------------------------------------------------- a2 -------
 __global__ void __launch_bounds__(kTB) k_gradient(SellView A, const double* __restrict__ x,
                                                   double* __restrict__ crit, double* __restrict__ p_max) {
@@ -223,6 +264,40 @@ __global__ void k_radix_digit(RadixState* st, unsigned* hist, int shift, double*
   }
 }
 
+// a2 for the stencil layout with a compile-time width: the mask decides which slots are stored neighbours;
+// all gathers of a row issue together.  Same plain adds in slot (ascending column) order as k_gradient.
+template <int WM>
+__global__ void __launch_bounds__(kTB) k_gradient_stencil(SellView A, const double* __restrict__ x,
+                                                          double* __restrict__ crit, double* __restrict__ p_max) {
+  const int64_t s = (blockIdx.x * (int64_t)kTB + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= A.nslices) return;
+  const int g = A.slice_seg[s];
+  const int64_t u = A.slice_row0[s] + lane;
+  const bool valid = u < A.seg_unit0[g + 1];
+  double gmax = 0.0;
+  if (valid) {
+    const int n1 = (int)A.nunits - 1, ui = (int)u;
+    const unsigned m = A.mask[u];
+    const double xi = __ldg(x + u);
+    double y[WM];
+#pragma unroll
+    for (int k = 0; k < WM; ++k) {
+      int c = ui + A.off[k];
+      c = c < 0 ? 0 : (c > n1 ? n1 : c);
+      y[k] = __ldg(x + c);
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < WM; ++k)
+      if (((m >> k) & 1) && A.off[k] != 0) acc = acc + fabs(xi - y[k]);
+    crit[u] = acc;
+    gmax = acc;
+  }
+  gmax = warp_max(gmax);
+  if (lane == 0) p_max[s] = gmax;
+}
+
 // ---------------------------------------------------------------- a4 -------
 __global__ void k_mark(const double* __restrict__ crit, int64_t m, int seg_units, const double* __restrict__ tau_cmp,
                        uint8_t* __restrict__ flag) {
@@ -281,6 +356,46 @@ __global__ void __launch_bounds__(kTB) k_expand(SellView A, const double* __rest
     if (v2 > best) best = v2;
   }
   if (!nb) return;
+  if (adm) adm[u] = best;
+  if (best > tau_cmp[g]) {
+    flag[u] = (uint8_t)stage;
+    atomicAdd(&counters[stage], 1u);
+  }
+}
+
+// a5 expansion round for the stencil layout, block 1, compile-time width (see k_expand): flags, values
+// and x0 of the row's stored neighbours are gathered together; admission sum in slot order.
+template <int WM>
+__global__ void __launch_bounds__(kTB) k_expand_stencil(SellView A, const double* __restrict__ r,
+                                                        const double* __restrict__ x0, uint8_t* __restrict__ flag,
+                                                        const double* __restrict__ tau_cmp, int stage,
+                                                        double* __restrict__ adm, unsigned* counters) {
+  if (stage > 1 && counters[stage - 1] == 0) return;
+  const int64_t s = (blockIdx.x * (int64_t)kTB + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= A.nslices) return;
+  const int g = A.slice_seg[s];
+  const int64_t u = A.slice_row0[s] + lane;
+  if (u >= A.seg_unit0[g + 1]) return;
+  if (flag[u] < stage) return;
+  const unsigned m = A.mask[u];
+  const int n1 = (int)A.nunits - 1, ui = (int)u;
+  const double* vp = A.val + 32ll * WM * s + lane;
+  bool nb = false;
+  double sum = 0.0;
+  uint8_t fl[WM];
+  int cc[WM];
+#pragma unroll
+  for (int k = 0; k < WM; ++k) {
+    int c = ui + A.off[k];
+    cc[k] = c < 0 ? 0 : (c > n1 ? n1 : c);
+    fl[k] = flag[cc[k]];
+  }
+#pragma unroll
+  for (int k = 0; k < WM; ++k)
+    if (((m >> k) & 1) && fl[k] < stage) { nb = true; sum = sum + fabs(__ldg(vp + 32 * k) * x0[cc[k]]); }
+  if (!nb) return;
+  const double best = fabs(r[u]) + sum;
   if (adm) adm[u] = best;
   if (best > tau_cmp[g]) {
     flag[u] = (uint8_t)stage;
@@ -397,13 +512,22 @@ extern "C" lc_status lc_select_domain(lc_matrix M, const double* b, const double
   CK(dalloc((void**)&D->seg_base, sizeof(int32_t) * (G + 1), s));
   if (p->criterion == LC_CRIT_RESIDUAL) {
     CK(dalloc((void**)&D->r, sizeof(double) * m * bs, s));
-    if (bs == 1)
+    if (bs == 1 && A.stencil && !A.sym && A.maxw == 7)
+      k_residual_stencil<7><<<nb_sl, kTB, 0, s>>>(V, b, x0, D->r, D->crit, p_max, p_hi, p_lo);
+    else if (bs == 1 && A.stencil && !A.sym && A.maxw == 5)
+      k_residual_stencil<5><<<nb_sl, kTB, 0, s>>>(V, b, x0, D->r, D->crit, p_max, p_hi, p_lo);
+    else if (bs == 1)
       k_residual_crit<1><<<nb_sl, kTB, 0, s>>>(V, b, x0, D->r, D->crit, p_max, p_hi, p_lo);
     else
       k_residual_crit<3><<<nb_sl, kTB, 0, s>>>(V, b, x0, D->r, D->crit, p_max, p_hi, p_lo);
     CKL();
   } else {
-    k_gradient<<<nb_sl, kTB, 0, s>>>(V, x0, D->crit, p_max);
+    if (A.stencil && !A.sym && A.maxw == 7)
+      k_gradient_stencil<7><<<nb_sl, kTB, 0, s>>>(V, x0, D->crit, p_max);
+    else if (A.stencil && !A.sym && A.maxw == 5)
+      k_gradient_stencil<5><<<nb_sl, kTB, 0, s>>>(V, x0, D->crit, p_max);
+    else
+      k_gradient<<<nb_sl, kTB, 0, s>>>(V, x0, D->crit, p_max);
     CKL();
   }
   k_fill_nan<<<nb_u, 256, 0, s>>>(D->adm, m);
@@ -431,7 +555,11 @@ extern "C" lc_status lc_select_domain(lc_matrix M, const double* b, const double
   {
     int stage = 1;
     for (int rd = 0; rd < p->expand_rounds; ++rd, ++stage) {
-      if (bs == 1)
+      if (bs == 1 && A.stencil && !A.sym && A.maxw == 7)
+        k_expand_stencil<7><<<nb_sl, kTB, 0, s>>>(V, D->r, x0, D->flag, tau_cmp, stage, D->adm, counters);
+      else if (bs == 1 && A.stencil && !A.sym && A.maxw == 5)
+        k_expand_stencil<5><<<nb_sl, kTB, 0, s>>>(V, D->r, x0, D->flag, tau_cmp, stage, D->adm, counters);
+      else if (bs == 1)
         k_expand<1><<<nb_sl, kTB, 0, s>>>(V, D->r, x0, D->flag, tau_cmp, stage, D->adm, counters);
       else
         k_expand<3><<<nb_sl, kTB, 0, s>>>(V, D->r, x0, D->flag, tau_cmp, stage, D->adm, counters);
