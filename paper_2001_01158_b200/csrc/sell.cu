@@ -14,10 +14,14 @@ __device__ bool inv3(const double* A, double* Ai);
 
 struct Offsets { int W; int32_t off[kMaxOff]; };
 
-// first row whose length equals the maximal row length (its offsets are the stencil candidate)
+// first row whose length equals the maximal row length (its offsets are the stencil candidate); one
+// atomic per warp (most rows of a stencil have the maximal length)
 __global__ void k_first_maxrow(int64_t n, const int64_t* __restrict__ rp, int maxw, int* best) {
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (u < n && rp[u + 1] - rp[u] == maxw) atomicMin(best, (int)u);
+  int cand = (u < n && rp[u + 1] - rp[u] == maxw) ? (int)u : INT32_MAX;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
+  if ((threadIdx.x & 31) == 0 && cand != INT32_MAX) atomicMin(best, cand);
 }
 
 // every stored (u, c) must have c - u in the candidate offset set
@@ -119,38 +123,45 @@ __global__ void k_uniform_slice_ptr(int64_t nslices, int W, int64_t* slice_ptr) 
 __global__ void k_slice_width(int64_t nslices, int seg_units, int spg, const int64_t* __restrict__ rp,
                               const int32_t* __restrict__ ci, int64_t* __restrict__ widths,
                               uint8_t* __restrict__ rowlen, unsigned* err, int* maxw) {
-  int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (s >= nslices) return;
-  int64_t g = s / spg;
-  int64_t lu = (s - g * spg) * 32 + lane;
-  int64_t seg0 = g * (int64_t)seg_units, seg1 = seg0 + seg_units;
+  const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   int len = 0;
-  if (lu < seg_units) {
-    int64_t u = seg0 + lu;
-    int64_t k0 = rp[u], k1 = rp[u + 1];
-    int64_t l = k1 - k0;
-    unsigned e = 0;
-    if (l < 1 || l > 255) e |= kErrRowLen;
-    bool diag = false;
-    int prev = -1;
-    for (int64_t k = k0; k < k1 && !(e & kErrRowLen); ++k) {
-      int c = ci[k];
-      if (c <= prev || c < seg0 || c >= seg1) e |= kErrPattern;
-      if (c == u) diag = true;
-      prev = c;
+  if (s < nslices) {
+    const int64_t g = s / spg;
+    const int64_t lu = (s - g * spg) * 32 + lane;
+    const int64_t seg0 = g * (int64_t)seg_units, seg1 = seg0 + seg_units;
+    if (lu < seg_units) {
+      const int64_t u = seg0 + lu;
+      const int64_t k0 = rp[u], k1 = rp[u + 1];
+      const int64_t l = k1 - k0;
+      unsigned e = 0;
+      if (l < 1 || l > 255) e |= kErrRowLen;
+      bool diag = false;
+      int prev = -1;
+      for (int64_t k = k0; k < k1 && !(e & kErrRowLen); ++k) {
+        const int c = ci[k];
+        if (c <= prev || c < seg0 || c >= seg1) e |= kErrPattern;
+        if (c == u) diag = true;
+        prev = c;
+      }
+      if (!diag) e |= kErrPattern;
+      if (e) atomicOr(err, e);
+      len = (l > 255) ? 255 : (int)l;
+      rowlen[u] = (uint8_t)len;
     }
-    if (!diag) e |= kErrPattern;
-    if (e) atomicOr(err, e);
-    len = (l > 255) ? 255 : (int)l;
-    rowlen[u] = (uint8_t)len;
   }
   int w = len;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, o));
-  if (lane == 0) {
-    widths[s] = 32ll * w;
-    atomicMax(maxw, w);
+  if (lane == 0 && s < nslices) widths[s] = 32ll * w;
+  // one atomic per CTA for the maximal width
+  __shared__ int s_w[32];
+  if (lane == 0) s_w[threadIdx.x >> 5] = w;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int mw = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mw = max(mw, s_w[i]);
+    atomicMax(maxw, mw);
   }
 }
 
