@@ -21,7 +21,14 @@ __global__ void k_first_maxrow(int64_t n, const int64_t* __restrict__ rp, int ma
   int cand = (u < n && rp[u + 1] - rp[u] == maxw) ? (int)u : INT32_MAX;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
-  if ((threadIdx.x & 31) == 0 && cand != INT32_MAX) atomicMin(best, cand);
+  __shared__ int s_c[32];
+  if ((threadIdx.x & 31) == 0) s_c[threadIdx.x >> 5] = cand;
+  __syncthreads();
+  if (threadIdx.x == 0) {                    // one candidate per CTA; no atomic once a smaller one is known
+    int c = INT32_MAX;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) c = min(c, s_c[i]);
+    if (c != INT32_MAX && c < *(volatile int*)best) atomicMin(best, c);
+  }
 }
 
 // every stored (u, c) must have c - u in the candidate offset set
