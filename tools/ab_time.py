@@ -20,7 +20,7 @@ for cfg in cfgs:
     best = 1e9
     for rep in range(4):
         x = x0.clone()
-        info = lc.solve_global(A, b, x)
+        info = lc.solve_global(A, b, x, method=lc.GMRES if cfg == 4 else lc.PCG)
         best = min(best, info[0]["seconds"])
         its = max(i["iterations"] for i in info)
     print(f"{os.path.basename(lib)} stencil_off={os.environ.get('LC_DISABLE_STENCIL','0')} config {cfg}: its {its} "
