@@ -373,7 +373,7 @@ __device__ __forceinline__ void dpass_a_tma(const DArgs& P, double* stg, uint64_
 }
 
 template <int WM>
-__global__ void __launch_bounds__(kDT, 3) k_dpcg(const __grid_constant__ DPack pk, int nCTA, int tma) {
+__global__ void __launch_bounds__(kDT, 4) k_dpcg(const __grid_constant__ DPack pk, int nCTA, int tma) {
   __shared__ double s_w[kDW][4], s_out[4];
   extern __shared__ __align__(128) double dsm[];   // TMA stages: kDStages x 8 slices x 32 x WM values
   __shared__ __align__(8) uint64_t s_bars[kDStages];
