@@ -25,3 +25,14 @@ for n in (99, 1024):
         lc.smooth_gs(A, b, x, 1)
         best = min(best, time.perf_counter() - t0)
     print(f"heat {n}^2: {best * 1e3:.3f} ms per sweep", flush=True)
+sy = synth.system(5, 3)
+A = lc.Matrix(sy.nrows, sy.rp, sy.ci, sy.val)
+b = torch.from_numpy(sy.b).cuda()
+best = 1e9
+for _ in range(3):
+    x = torch.from_numpy(sy.x0).cuda()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    lc.smooth_gs(A, b, x, 1)
+    best = min(best, time.perf_counter() - t0)
+print(f"config 5 (256^3): {best * 1e3:.3f} ms per sweep", flush=True)
