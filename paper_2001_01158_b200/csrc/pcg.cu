@@ -703,14 +703,17 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   std::vector<int> it(G, 0), stt(G, LC_OK);
   std::vector<double> rr(G, 0.0);
   float ms = 0.f;
-  const int wi = (M.maxw <= 5 ? 0 : M.maxw <= 7 ? 1 : 2) + (M.sym ? 6 : M.stencil ? 3 : 0);
+  // compile-time width: SELL rows guard k < w, so W = 5 / 7 serve rows up to that width; stencil slices hold
+  // exactly maxw slots, so they take W = 5 / 7 only when maxw is exactly that (else the generic loop)
+  const int wi = (M.stencil ? (M.maxw == 5 ? 0 : M.maxw == 7 ? 1 : 2) : (M.maxw <= 5 ? 0 : M.maxw <= 7 ? 1 : 2)) +
+                 (M.sym ? 6 : M.stencil ? 3 : 0);
   void* const fns[9] = {(void*)k_pcg<5, 0>, (void*)k_pcg<7, 0>, (void*)k_pcg<0, 0>,
                         (void*)k_pcg<5, 1>, (void*)k_pcg<7, 1>, (void*)k_pcg<0, 1>,
                         (void*)k_pcg<5, 2>, (void*)k_pcg<7, 2>, (void*)k_pcg<0, 2>};
   void* fn = fns[wi];
   // TMA staging for contiguous slice ranges (global solves); slice-list (masked) solves keep plain loads: the
   // per-slice bulk copies were 4% slower there in the bench (profiles/r01_h_tma_ab.txt)
-  const bool tma = M.stencil && M.maxw <= 7 && G == 1 && !job.slist && getenv("LC_NO_TMA") == nullptr;
+  const bool tma = M.stencil && (M.maxw == 5 || M.maxw == 7) && G == 1 && !job.slist && getenv("LC_NO_TMA") == nullptr;
   const size_t dsmem = tma ? (size_t)kStages * kPW * 32 * (M.sym ? M.vw : M.maxw) * sizeof(double) : 0;
   const int ci = wi * 2 + (tma ? 1 : 0);
   if (!g_pcg_max_ctas[ci]) {

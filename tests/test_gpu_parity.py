@@ -289,6 +289,63 @@ def test_random_tiny_systems_vs_dense():
         assert np.linalg.norm(x.cpu().numpy() - xlu) / np.linalg.norm(xlu) <= 1e-8
 
 
+@pytest.mark.parametrize("dsmem", [True, False])
+@pytest.mark.parametrize("n", [1, 2, 31, 33])
+def test_tiny_stencil_systems(n, dsmem, monkeypatch):
+    """Degenerate sizes on both PCG paths (cluster-resident / grid): 1, 2 rows, one slice minus / plus one
+    row.  A tridiagonal (3-offset stencil, generic width) and the oracle's PCG."""
+    if not dsmem:
+        monkeypatch.setenv("LC_NO_DSMEM", "1")
+    M = np.eye(n) * 3.0
+    for i in range(n - 1):
+        M[i, i + 1] = M[i + 1, i] = -1.0
+    Ao = orc.Csr.from_dense(M)
+    rng = np.random.default_rng(n)
+    xs = rng.standard_normal(n)
+    b = M @ xs
+    A = lc.Matrix(n, Ao.rp, Ao.ci, Ao.val)
+    x = to_dev(np.zeros(n))
+    info = lc.solve_global(A, to_dev(b), x)[0]
+    xo, it, st, _ = orc.pcg(Ao, b, np.zeros(n))
+    assert info["status"] == 0 and st == 0 and abs(info["iterations"] - it) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xo) <= 1e-9 * max(np.linalg.norm(xo), 1e-300)
+
+
+@pytest.mark.parametrize("path", ["dsmem", "grid", "gmres"])
+def test_zero_rhs_absolute_tolerance(path, monkeypatch):
+    """b = 0: the tolerance becomes absolute (eps, Eq. 6 with ||b|| = 0); the solution is driven to ~0."""
+    if path == "grid":
+        monkeypatch.setenv("LC_NO_DSMEM", "1")
+    sy = synth.system(1, 2) if path != "gmres" else synth.system(4, 2, n=16)
+    A = gpu_matrix(sy)
+    b = torch.zeros(sy.N, dtype=torch.float64, device=DEV)
+    x = to_dev(sy.x0)
+    info = lc.solve_global(A, b, x, method=method_of(sy.config))[0]
+    assert info["status"] == 0
+    r = orc.residual(oracle_csr(sy), np.zeros(sy.N), x.cpu().numpy())
+    assert np.linalg.norm(r) <= EPS * (1 + 1e-6)
+
+
+@pytest.mark.parametrize("path", ["dsmem", "grid"])
+def test_nonfinite_and_iteration_cap(path, monkeypatch):
+    """NaN in b -> LC_ERR_NONFINITE reported (no hang); max_iters = 3 -> LC_NOT_CONVERGED with the best
+    iterate, iterations = 3 (non-fatal, R18)."""
+    if path == "grid":
+        monkeypatch.setenv("LC_NO_DSMEM", "1")
+    sy = synth.system(1, 4)
+    A = gpu_matrix(sy)
+    b = to_dev(sy.b)
+    b[17] = float("nan")
+    x = to_dev(sy.x0)
+    with pytest.raises(lc.LcError) as e:
+        lc.solve_global(A, b, x)
+    assert e.value.status == -6
+    x = to_dev(sy.x0)
+    info = lc.solve_global(A, to_dev(sy.b), x, max_iters=3)[0]
+    assert info["status"] == 1 and info["iterations"] == 3
+    assert np.isfinite(x.cpu().numpy()).all()
+
+
 def test_gmres_scalar_jacobi():
     """GMRES with block = 1 (Jacobi) on a nonsymmetric random system vs the oracle's GMRES."""
     s = synth.random_system(200, bw=4, spd=False, seed=9)
