@@ -346,6 +346,45 @@ def test_nonfinite_and_iteration_cap(path, monkeypatch):
     assert np.isfinite(x.cpu().numpy()).all()
 
 
+@pytest.mark.parametrize("rule", [0, 1])
+def test_local_method_1d_three_point(rule):
+    """A 1-D three-point operator (stencil width 3, generic-width kernels everywhere) through the whole
+    local method vs the oracle: a moving front, residual (E_max = 2) and gradient domains."""
+    n = 5000
+    xg = np.arange(n) / n
+    xs = 0.1 + 0.9 * 0.5 * (1 - np.tanh((xg - 0.5) / 0.01))
+    x0 = 0.1 + 0.9 * 0.5 * (1 - np.tanh((xg - 0.49) / 0.01))
+    k = (0.5 * (x0[:-1] + x0[1:])) ** 2.5
+    lam = 50.0
+    rp, ci, va = [0], [], []
+    for i in range(n):
+        d = 1.0
+        if i > 0:
+            ci.append(i - 1); va.append(-lam * k[i - 1]); d += lam * k[i - 1]
+        ci.append(i); va.append(0.0); di = len(va) - 1
+        if i < n - 1:
+            ci.append(i + 1); va.append(-lam * k[i]); d += lam * k[i]
+        va[di] = d
+        rp.append(len(ci))
+    Ao = orc.Csr(np.array(rp), np.array(ci, np.int32), np.array(va))
+    b = orc.spmv(Ao, xs)
+    rules = [dict(criterion=0, threshold=0, param=1e-10, expand_rounds=2, dilate_hops=0),
+             dict(criterion=1, threshold=1, param=1e-3, expand_rounds=0, dilate_hops=0)]
+    r = rules[rule]
+    A = lc.Matrix(n, Ao.rp, Ao.ci, Ao.val)
+    assert A.info()["layout"] == "stencil" and A.info()["max_row"] == 3
+    xg_, rep = lc.local_method(A, to_dev(b), to_dev(x0), r)
+    d = orc.select_domain(Ao, b, x0, r["criterion"], r["threshold"], r["param"], r["expand_rounds"], 0, 1)
+    dom = lc.select_domain(A, to_dev(b), to_dev(x0), **r)
+    compare_sets(Ao, dom.export()[0].cpu().numpy(), d, 1)
+    xo, _, ro = orc.local_method(Ao, b, x0, oracle_dp(r, 1), oracle_sp(1))
+    if d.K > 0:
+        assert abs(rep["local"][0]["iterations"] - ro.it_local) <= 1
+    assert abs(rep["global"][0]["iterations"] - ro.it_global) <= 1
+    xn = xg_.cpu().numpy()
+    assert np.linalg.norm(xn - xo) / np.linalg.norm(xo) <= 1e-9
+
+
 def test_gmres_scalar_jacobi():
     """GMRES with block = 1 (Jacobi) on a nonsymmetric random system vs the oracle's GMRES."""
     s = synth.random_system(200, bw=4, spd=False, seed=9)
