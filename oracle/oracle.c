@@ -346,6 +346,7 @@ int or_pcg(int64_t n, const int64_t* rp, const int32_t* ci, const double* a, con
   or_residual(n, rp, ci, a, b, x, r);                         /* 1. r = b - A x */
   double rn = sqrt(dot(n, r, r));
   if (rn <= tgt) { *relres = nb > 0 ? rn / nb : rn; st = OR_OK; goto done; }
+  if (max_iters <= 0) { *relres = nb > 0 ? rn / nb : rn; goto done; }   /* cap 0: the Eq. 6 check only (R34) */
   for (;;) {
     for (int64_t i = 0; i < n; ++i) { z[i] = r[i] * dinv[i]; pp[i] = z[i]; }   /* 2. z = D^-1 r, p = z */
     double rho = dot(n, r, z);

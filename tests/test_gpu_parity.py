@@ -385,6 +385,22 @@ def test_local_method_1d_three_point(rule):
     assert np.linalg.norm(xn - xo) / np.linalg.norm(xo) <= 1e-9
 
 
+@pytest.mark.parametrize("path", ["dsmem", "grid"])
+def test_max_iters_zero_is_the_eq6_check(path, monkeypatch):
+    """max_iters = 0: only the Eq. 6 check at the start (as the oracle): 0 iterations, x untouched, status
+    LC_NOT_CONVERGED when the start does not satisfy Eq. 6 (tools/param_study.py relies on it)."""
+    if path == "grid":
+        monkeypatch.setenv("LC_NO_DSMEM", "1")
+    sy = synth.system(1, 5)
+    A = gpu_matrix(sy)
+    x = to_dev(sy.x0)
+    info = lc.solve_global(A, to_dev(sy.b), x, max_iters=0)[0]
+    assert info["iterations"] == 0 and info["status"] == 1
+    assert torch.equal(x, to_dev(sy.x0))
+    _, it, st, _ = orc.pcg(oracle_csr(sy), sy.b, sy.x0, EPS, 0)
+    assert it == 0 and st == 1
+
+
 def test_gmres_scalar_jacobi():
     """GMRES with block = 1 (Jacobi) on a nonsymmetric random system vs the oracle's GMRES."""
     s = synth.random_system(200, bw=4, spd=False, seed=9)
