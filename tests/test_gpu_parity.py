@@ -401,6 +401,34 @@ def test_max_iters_zero_is_the_eq6_check(path, monkeypatch):
     assert it == 0 and st == 1
 
 
+@pytest.mark.parametrize("restart", [1, 7, 40])
+def test_gmres_restart_lengths(restart):
+    """GMRES(m) for m = 1 (restart every step), 7 and the maximum 40 vs the oracle's GMRES(m)."""
+    sy = synth.system(4, 6, n=20)
+    A = gpu_matrix(sy)
+    x = to_dev(sy.x0)
+    info = lc.solve_global(A, to_dev(sy.b), x, method=lc.GMRES, restart=restart, max_iters=3000)[0]
+    xo, it, st, _ = orc.gmres_bj(oracle_csr(sy), sy.b, sy.x0, bs=3, restart=restart)
+    assert info["status"] == 0 and st == 0
+    assert abs(info["iterations"] - it) <= 1, (info["iterations"], it)
+    assert np.linalg.norm(x.cpu().numpy() - xo) / np.linalg.norm(xo) <= 1e-9
+
+
+def test_batched_64_segments():
+    """The maximum batch (64 segments; 128 reduced quantities in the arrival-tree reduction), ragged
+    segments of 12 x 12 = 144 rows, vs the oracle per segment."""
+    sy = synth.system(3, 5, n=12, G=64)
+    check_system(sy, RULES[3][0])
+
+
+@pytest.mark.parametrize("rule", [dict(criterion=1, threshold=2, param=0.9, expand_rounds=0, dilate_hops=2),
+                                  dict(criterion=0, threshold=1, param=1e-2, expand_rounds=0, dilate_hops=1)])
+def test_batched_percentile_and_dilation(rule):
+    """Per-segment percentile threshold (R14) and dilation (R15) on a batched system vs the oracle."""
+    sy = synth.system(3, 7, n=30, G=4)
+    check_system(sy, rule)
+
+
 def test_gmres_scalar_jacobi():
     """GMRES with block = 1 (Jacobi) on a nonsymmetric random system vs the oracle's GMRES."""
     s = synth.random_system(200, bw=4, spd=False, seed=9)
