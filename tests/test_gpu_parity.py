@@ -429,6 +429,23 @@ def test_batched_percentile_and_dilation(rule):
     check_system(sy, rule)
 
 
+def test_non_default_stream():
+    """Every call enqueues on the caller's (torch current) stream: the local method on a side stream equals
+    the default-stream result bitwise, with the inputs produced on that stream just before."""
+    sy = synth.system(5, 8, n=20)
+    A = gpu_matrix(sy)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    x_ref, rep_ref = lc.local_method(A, b, x0, RULES[5][0])
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        b2 = b * 1.0                      # produced on the side stream
+        x02 = x0 * 1.0
+        x2, rep2 = lc.local_method(A, b2, x02, RULES[5][0])
+    torch.cuda.synchronize()
+    assert torch.equal(x2, x_ref)
+    assert rep2["K"] == rep_ref["K"]
+
+
 def test_gmres_scalar_jacobi():
     """GMRES with block = 1 (Jacobi) on a nonsymmetric random system vs the oracle's GMRES."""
     s = synth.random_system(200, bw=4, spd=False, seed=9)
