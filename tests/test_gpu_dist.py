@@ -165,6 +165,37 @@ def test_dist_matches_single_gpu_path_config5_full():
     assert np.linalg.norm(xg - x1) / np.linalg.norm(x1) <= 1e-9
 
 
+class _Sys:
+    pass
+
+
+def test_dist_1d_three_point_generic_width():
+    """A 1-D three-point operator (generic-width kernels) on 3 emulated ranks through Alg. 5 + the solves."""
+    n = 3000
+    xg = np.arange(n) / n
+    xs = 0.1 + 0.9 * 0.5 * (1 - np.tanh((xg - 0.5) / 0.01))
+    x0 = 0.1 + 0.9 * 0.5 * (1 - np.tanh((xg - 0.49) / 0.01))
+    k = (0.5 * (x0[:-1] + x0[1:])) ** 2.5
+    lam = 50.0
+    rp, ci, va = [0], [], []
+    for i in range(n):
+        d = 1.0
+        if i > 0:
+            ci.append(i - 1); va.append(-lam * k[i - 1]); d += lam * k[i - 1]
+        ci.append(i); va.append(0.0); di = len(va) - 1
+        if i < n - 1:
+            ci.append(i + 1); va.append(-lam * k[i]); d += lam * k[i]
+        va[di] = d
+        rp.append(len(ci))
+    sy = _Sys()
+    sy.nrows = n
+    sy.rp, sy.ci, sy.val = np.array(rp), np.array(ci, np.int32), np.array(va)
+    sy.b = orc.spmv(orc.Csr(sy.rp, sy.ci, sy.val), xs)
+    sy.x0 = x0
+    run_and_check(sy, dict(criterion=0, threshold=0, param=1e-10, expand_rounds=2, dilate_hops=0), 3, align=1,
+                  R=[0, 1001, 1999, n])
+
+
 def test_dist_rejects_non_stencil_and_short_slabs():
     sy = synth.random_system(300, 7, True, 5)   # random band: no constant offset set
     rp, ci, va = ldist.slab_csr(sy.rp, sy.ci, sy.val, 0, 150)
