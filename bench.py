@@ -292,6 +292,30 @@ def run_lc(args):
                 "bytes_rule": (f"{rule} + 96 B/row vectors per PCG iteration" if solver == "pcg"
                                else "8 B/nnz + 80 B/unknown + 16 (j+1) B/unknown per Arnoldi step j")}
 
+    # ---- the FP64 SpMV alone (BASELINE metric "SpMV HBM GB/s"): lc_spmv y = A x on the last system,
+    # 20 calls timed with events on the launching stream (A, x, y = 0.9 GB + 0.27 GB at 256^3, > L2)
+    spmv = None
+    if sy0.batch >= 1:
+        Asp = lc.Matrix(sy0.nrows, dev_in[-1]["rp"], dev_in[-1]["ci"], dev_in[-1]["val"], block=sy0.block,
+                        batch=sy0.batch)
+        xs_, ys_ = dev_in[-1]["x0"], torch.empty_like(dev_in[-1]["x0"])
+        for _ in range(3):
+            lc.spmv(Asp, xs_, ys_)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s0.record(stream)
+        for _ in range(20):
+            lc.spmv(Asp, xs_, ys_)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        t_sp = s0.elapsed_time(s1) / 1e3 / 20
+        sp_bytes = mat_bytes + 16.0 * N
+        spmv = {"kernel": "lc_spmv (k_spmv_stencil / k_spmv)", "bound": "hbm", "achieved": round(sp_bytes / t_sp / 1e9, 1),
+                "peak": hbm_peak, "unit": "GB/s", "frac": round(sp_bytes / t_sp / 1e9 / hbm_peak, 4),
+                "us_per_call": round(t_sp * 1e6, 2), "bytes_per_call": int(sp_bytes),
+                "bytes_rule": f"{rule} + 16 B/row (x, y)"}
+        del Asp
+
     # ---- e2e: host buffers through the C-ABI, H2D + D2H inside the timed region
     e2e = None
     if args.e2e_steps > 0:
@@ -364,7 +388,7 @@ def run_lc(args):
                        "solves_per_step": len(rules) * sy0.batch, "methods": [r[0] for r in rules],
                        "systems": ids[args.warmup:], "rel_tol": EPS, "l2": "inputs > L2 (1.8 GB/system)",
                        "breakdown": breakdown, "gen_seconds": round(gen_s, 1)},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "roofline": roof, "spmv": spmv, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
         print(json.dumps(line))

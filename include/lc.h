@@ -167,6 +167,14 @@ lc_status lc_solve_local(lc_sub sub, const lc_solver_params* p, double* x, void*
 lc_status lc_solve_global(lc_matrix A, const double* b, double* x, const lc_solver_params* p, void* stream,
                           lc_solve_info* info);
 
+/*
+ * y = A x (the operator of Eq. 1; the product inside the residual of Alg. 3 l.4, and inside every
+ * Krylov iteration).  x, y: device [n*block], must not alias.  Per row the canonical chain (R22): stored
+ * entries in ascending column order with explicit fma, so y equals the oracle's or_spmv bitwise.
+ * Enqueued on `stream`, no sync.
+ */
+lc_status lc_spmv(lc_matrix A, const double* x, double* y, void* stream);
+
 /* storage layout chosen by lc_create_csr */
 enum { LC_LAYOUT_SELL = 0     /* SELL-32 with explicit int32 column per slot (12 B per slot) */,
        LC_LAYOUT_STENCIL = 1  /* every row's column offsets lie in one sorted set of <= 8 offsets: values only,

@@ -446,6 +446,32 @@ def test_non_default_stream():
     assert rep2["K"] == rep_ref["K"]
 
 
+@pytest.mark.parametrize("case", ["c5", "c1", "c3", "c4", "sell", "tridiag"])
+def test_spmv_bitexact(case, monkeypatch):
+    """lc_spmv (y = A x) equals the oracle's or_spmv bitwise on every layout / width / block size."""
+    if case == "sell":
+        monkeypatch.setenv("LC_DISABLE_STENCIL", "1")
+    if case == "tridiag":
+        n = 1000
+        M = np.eye(n) * 3.0
+        for i in range(n - 1):
+            M[i, i + 1] = -1.0 - 0.001 * i
+            M[i + 1, i] = -1.0 + 0.0005 * i
+        Ao = orc.Csr.from_dense(M)
+        A = lc.Matrix(n, Ao.rp, Ao.ci, Ao.val)
+        xh = np.sin(np.arange(n) * 0.37)
+    else:
+        cfg, nn = {"c5": (5, 20), "c1": (1, 64), "c3": (3, 30), "c4": (4, 24), "sell": (5, 16)}[case]
+        sy = synth.system(cfg, 3, n=nn, G=4)
+        Ao = oracle_csr(sy)
+        A = gpu_matrix(sy)
+        xh = sy.x0
+    x = to_dev(xh)
+    y = torch.empty_like(x)
+    lc.spmv(A, x, y)
+    np.testing.assert_array_equal(y.cpu().numpy(), orc.spmv(Ao, xh))
+
+
 def test_gmres_scalar_jacobi():
     """GMRES with block = 1 (Jacobi) on a nonsymmetric random system vs the oracle's GMRES."""
     s = synth.random_system(200, bw=4, spd=False, seed=9)
