@@ -175,6 +175,16 @@ lc_status lc_solve_global(lc_matrix A, const double* b, double* x, const lc_solv
  */
 lc_status lc_spmv(lc_matrix A, const double* x, double* y, void* stream);
 
+/*
+ * y = A x straight from CSR device arrays (n rows, row_ptr [n+1] int64, col_idx / values [nnz]): the
+ * row-slab CSR kernel (each warp's 32-row slab copied into shared memory with coalesced loads).
+ * The handles keep the SELL / stencil layouts instead (faster on every config, profiles/
+ * r01_ac); this entry point serves CSR data that is never converted.  Bit-exact with or_spmv (R22).
+ * Enqueued on `stream`, no sync.
+ */
+lc_status lc_spmv_csr(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* values,
+                      const double* x, double* y, void* stream);
+
 /* storage layout chosen by lc_create_csr */
 enum { LC_LAYOUT_SELL = 0     /* SELL-32 with explicit int32 column per slot (12 B per slot) */,
        LC_LAYOUT_STENCIL = 1  /* every row's column offsets lie in one sorted set of <= 8 offsets: values only,

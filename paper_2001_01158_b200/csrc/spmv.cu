@@ -33,6 +33,38 @@ __global__ void __launch_bounds__(kVT) k_spmv_stencil(SellView A, const double* 
   y[u] = acc;
 }
 
+// SELL-32 (explicit columns), block 1: the slots in groups of 4 -- the group's columns and values load
+// together, then its 4 gathers, then the 4 fma of the chain in slot order (padding slots add +0).
+__global__ void __launch_bounds__(kVT) k_spmv_sell(SellView A, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t s = (blockIdx.x * (int64_t)kVT + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= A.nslices) return;
+  const int g = A.slice_seg[s];
+  const int64_t u = A.slice_row0[s] + lane;
+  if (u >= A.seg_unit0[g + 1]) return;
+  const int64_t p0 = A.slice_ptr[s];
+  const int w = (int)((A.slice_ptr[s + 1] - p0) >> 5);
+  const int32_t* cp = A.col + p0 + lane;
+  const double* vp = A.val + p0 + lane;
+  double acc = 0.0;
+  for (int k0 = 0; k0 < w; k0 += 4) {
+    int c[4];
+    double v[4], xv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool ok = k0 + j < w;
+      c[j] = ok ? __ldg(cp + 32 * (k0 + j)) : 0;
+      v[j] = ok ? __ldg(vp + 32 * (k0 + j)) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xv[j] = __ldg(x + c[j]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (k0 + j < w) acc = __fma_rn(v[j], xv[j], acc);
+  }
+  y[u] = acc;
+}
+
 template <int BS>
 __global__ void __launch_bounds__(kVT) k_spmv(SellView A, const double* __restrict__ x, double* __restrict__ y) {
   const int64_t s = (blockIdx.x * (int64_t)kVT + threadIdx.x) >> 5;
@@ -65,6 +97,52 @@ __global__ void __launch_bounds__(kVT) k_spmv(SellView A, const double* __restri
   for (int a = 0; a < BS; ++a) y[BS * u + a] = acc[a];
 }
 
+// ---- CSR row-slab SpMV (SURVEY 8(a) kernel notes; the format the handles do NOT keep -- DESIGN.md s5):
+// a warp owns a slab of 32 consecutive rows; its lanes copy the slab's values and columns
+// [rp[r0], rp[r0 + 32]) into the warp's shared-memory slot with coalesced loads (no block-wide barrier),
+// then lane l walks row r0 + l in stored order (the R22 chain, bit-exact with or_spmv) with the gathers of
+// x issued in groups of 8.  Slabs with more than kCWE entries read their rows straight from global memory.
+constexpr int kCT = 256;        // threads per CTA (8 warps)
+constexpr int kCWE = 256;       // staged entries per warp slab (8 per row on average)
+__global__ void __launch_bounds__(kCT) k_spmv_csr(int64_t n, const int64_t* __restrict__ rp,
+                                                  const int32_t* __restrict__ ci, const double* __restrict__ va,
+                                                  const double* __restrict__ x, double* __restrict__ y) {
+  __shared__ __align__(16) double s_v[kCT / 32][kCWE];
+  __shared__ __align__(16) int32_t s_c[kCT / 32][kCWE];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * (kCT / 32) + warp) * 32;
+  if (r0 >= n) return;
+  const int64_t r1 = r0 + 32 < n ? r0 + 32 : n;
+  const int64_t u = r0 + lane;
+  const int64_t e0 = rp[r0], e1 = rp[r1];
+  const int64_t ne = e1 - e0;
+  double acc = 0.0;
+  if (ne > kCWE) {                                        // dense slab: rows straight from global memory
+    if (u < r1)
+      for (int64_t k = rp[u]; k < rp[u + 1]; ++k) acc = __fma_rn(__ldg(va + k), __ldg(x + ci[k]), acc);
+  } else {
+    double* sv = s_v[warp];
+    int32_t* sc = s_c[warp];
+    for (int64_t k = lane; k < ne; k += 32) {
+      sv[k] = __ldg(va + e0 + k);
+      sc[k] = __ldg(ci + e0 + k);
+    }
+    __syncwarp();
+    if (u < r1) {
+      const int k0 = (int)(rp[u] - e0), k1 = (int)(rp[u + 1] - e0);
+      for (int kb = k0; kb < k1; kb += 8) {
+        double xv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xv[j] = kb + j < k1 ? __ldg(x + sc[kb + j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (kb + j < k1) acc = __fma_rn(sv[kb + j], xv[j], acc);
+      }
+    }
+  }
+  if (u < r1) y[u] = acc;
+}
+
 }  // namespace lc
 
 using namespace lc;
@@ -80,10 +158,26 @@ extern "C" lc_status lc_spmv(lc_matrix M, const double* x, double* y, void* stre
     k_spmv_stencil<7><<<nb, kVT, 0, s>>>(V, x, y);
   else if (M->block == 1 && A.stencil && !A.sym && A.maxw == 5)
     k_spmv_stencil<5><<<nb, kVT, 0, s>>>(V, x, y);
+  else if (M->block == 1 && !A.stencil)
+    k_spmv_sell<<<nb, kVT, 0, s>>>(V, x, y);
   else if (M->block == 1)
     k_spmv<1><<<nb, kVT, 0, s>>>(V, x, y);
   else
     k_spmv<3><<<nb, kVT, 0, s>>>(V, x, y);
+  LC_LAUNCHED();
+  return LC_OK;
+}
+
+extern "C" lc_status lc_spmv_csr(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* values,
+                                 const double* x, double* y, void* stream) {
+  if (n < 0 || (n > 0 && (!row_ptr || !col_idx || !values || !x || !y))) {
+    set_error("lc_spmv_csr: null argument or n < 0");
+    return LC_ERR_INVALID_ARG;
+  }
+  if (x == y) { set_error("lc_spmv_csr: x and y must not alias"); return LC_ERR_INVALID_ARG; }
+  if (n == 0) return LC_OK;
+  const unsigned nb = (unsigned)((n + kCT - 1) / kCT);
+  k_spmv_csr<<<nb, kCT, 0, (cudaStream_t)stream>>>(n, row_ptr, col_idx, values, x, y);
   LC_LAUNCHED();
   return LC_OK;
 }

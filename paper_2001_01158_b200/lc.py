@@ -29,7 +29,7 @@ _STATUS = {0: "LC_OK", 1: "LC_NOT_CONVERGED", -1: "LC_ERR_INVALID_ARG", -2: "LC_
 
 EXPORTED = ["lc_create_csr", "lc_update_values", "lc_select_domain", "lc_domain_export", "lc_extract_sub", "lc_solve_local",
             "lc_solve_global", "lc_smooth_gs", "lc_heat_assemble", "lc_heat_run", "lc_matrix_info", "lc_destroy_matrix", "lc_destroy_domain",
-            "lc_destroy_sub", "lc_spmv", "lc_dist_create", "lc_dist_export_handle", "lc_dist_connect", "lc_dist_connect_local",
+            "lc_destroy_sub", "lc_spmv", "lc_spmv_csr", "lc_dist_create", "lc_dist_export_handle", "lc_dist_connect", "lc_dist_connect_local",
             "lc_dist_select_domain", "lc_dist_domain_export", "lc_dist_solve_local", "lc_dist_solve_global",
             "lc_dist_destroy", "lc_last_error", "lc_kernel_launches"]
 DIST_HANDLE_BYTES = 64
@@ -92,6 +92,8 @@ def load_library(path: str = LIB_PATH):
     lib.lc_smooth_gs.argtypes = [P, P, P, I32, P]
     lib.lc_spmv.argtypes = [P, P, P, P]
     lib.lc_spmv.restype = ctypes.c_int
+    lib.lc_spmv_csr.argtypes = [I64, P, P, P, P, P, P]
+    lib.lc_spmv_csr.restype = ctypes.c_int
     lib.lc_update_values.argtypes = [P, P, P, P, I32, P]
     lib.lc_heat_assemble.argtypes = [I32, I32, D, I32, D, D, P, P, P, P, P, P, P]
     lib.lc_heat_run.argtypes = [ctypes.POINTER(HeatParams), P, P, P, P, ctypes.POINTER(HeatReport)]
@@ -297,6 +299,15 @@ def spmv(A: Matrix, x: torch.Tensor, y: torch.Tensor):
     """y = A x on the current stream (lc_spmv)."""
     _check(load_library().lc_spmv(A.h, _dptr(x, torch.float64, A.N), _dptr(y, torch.float64, A.N), _stream()),
            "lc_spmv", ok=(LC_OK,))
+    return y
+
+
+def spmv_csr(row_ptr: torch.Tensor, col_idx: torch.Tensor, values: torch.Tensor, x: torch.Tensor, y: torch.Tensor):
+    """y = A x from CSR device tensors (lc_spmv_csr, the row-slab CSR kernel)."""
+    n = row_ptr.numel() - 1
+    _check(load_library().lc_spmv_csr(n, _dptr(row_ptr, torch.int64), _dptr(col_idx, torch.int32),
+                                      _dptr(values, torch.float64), _dptr(x, torch.float64, n),
+                                      _dptr(y, torch.float64, n), _stream()), "lc_spmv_csr", ok=(LC_OK,))
     return y
 
 

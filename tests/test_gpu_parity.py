@@ -472,6 +472,35 @@ def test_spmv_bitexact(case, monkeypatch):
     np.testing.assert_array_equal(y.cpu().numpy(), orc.spmv(Ao, xh))
 
 
+@pytest.mark.parametrize("case", ["c5", "c2", "c4blocks", "random", "dense_rows"])
+def test_spmv_csr_bitexact(case):
+    """lc_spmv_csr (the row-slab CSR kernel) equals or_spmv bitwise: staged x window (2-D), unstaged (3-D),
+    a scalar view of the 3T BSR matrix, a random band, and slabs too dense to stage (rows of 40 entries)."""
+    if case == "dense_rows":
+        n = 700
+        rng = np.random.default_rng(3)
+        rp, ci, va = [0], [], []
+        for i in range(n):
+            cols = sorted(set(rng.choice(n, 39, replace=False).tolist()) | {i})
+            ci += cols
+            va += rng.standard_normal(len(cols)).tolist()
+            rp.append(len(ci))
+        Ao = orc.Csr(np.array(rp), np.array(ci, np.int32), np.array(va))
+    elif case == "random":
+        s_ = synth.random_system(3001, bw=6, spd=False, seed=4)
+        Ao = orc.Csr(s_.rp, s_.ci, s_.val)
+    elif case == "c4blocks":
+        Ao = oracle_csr(synth.system(4, 2, n=16))
+    else:
+        sy = synth.system(5 if case == "c5" else 2, 3, n=20 if case == "c5" else 96)
+        Ao = oracle_csr(sy)
+    n = Ao.n
+    xh = np.cos(np.arange(n) * 0.11)
+    y = torch.empty(n, dtype=torch.float64, device=DEV)
+    lc.spmv_csr(to_dev(Ao.rp.astype(np.int64)), to_dev(Ao.ci.astype(np.int32)), to_dev(Ao.val), to_dev(xh), y)
+    np.testing.assert_array_equal(y.cpu().numpy(), orc.spmv(Ao, xh))
+
+
 def test_gmres_scalar_jacobi():
     """GMRES with block = 1 (Jacobi) on a nonsymmetric random system vs the oracle's GMRES."""
     s = synth.random_system(200, bw=4, spd=False, seed=9)
