@@ -269,12 +269,6 @@ def heat_run(nx, ny, T0, steps, domain: DomainParams | None, solver: SolverParam
     return T, per[:steps], rep
 
 
-def heat_initial(nx, ny, Tl=1.0, Tr=1e-4):
-    """T_0(x, y) = e^{-100 x} T_l + T_r at the interior nodes x_p = (p+1)/(nx+1)."""
-    x = (np.arange(nx) + 1.0) / (nx + 1)
-    return np.tile(np.exp(-100.0 * x) * Tl + Tr, ny)
-
-
 def local_method(A: Csr, b, x0, domain: DomainParams | None, solver: SolverParams):
     """Alg. 1 (domain given) or method0 (domain None).  Returns (x, flag, Report)."""
     b = _c(b, np.float64); x = np.array(x0, dtype=np.float64, copy=True)

@@ -106,3 +106,10 @@ def random_system(n: int, bw: int = 2, spd: bool = True, seed: int = 1) -> Syste
     b = np.empty(n); x0 = np.empty(n); xs = np.empty(n)
     lib.synth_random(n, bw, 1 if spd else 0, seed, _p(rp), _p(ci), _p(val), _p(b), _p(x0), _p(xs))
     return System(0, n, 0, n, 1, 1, rp, ci, val, b, x0, xs)
+
+
+def heat_initial(nx: int, ny: int, Tl: float = 1.0, Tr: float = 1e-4) -> np.ndarray:
+    """The paper's heat-model initial field T_0(x, y) = e^{-100 x} T_l + T_r at the interior nodes
+    x_p = (p+1)/(nx+1), row i = p + nx q (an input of Alg. 6, shared by the oracle and the device driver)."""
+    x = (np.arange(nx) + 1.0) / (nx + 1)
+    return np.tile(np.exp(-100.0 * x) * Tl + Tr, ny)

@@ -773,7 +773,7 @@ def test_heat_run_vs_oracle(method):
     the final fields within 1e-8 relative (the Picard stop ||dT|| < 1e-8 bounds the difference one extra
     or missing Picard iteration can make; ||T|| >= 1 here)."""
     nx = ny = 20
-    T0 = orc.heat_initial(nx, ny)
+    T0 = synth.heat_initial(nx, ny)
     dp = {0: None, 1: orc.DomainParams(1, 1, 1e-4, 0, 0, 1), 2: orc.DomainParams(0, 0, 1e-10, 1, 0, 1)}[method]
     To, per_o, rep_o = orc.heat_run(nx, ny, T0, 6, dp, orc.SolverParams(0, 1, 30, 1e-10, 20000, 1 if method else 0))
     Tg, per_g, eta_g, rep_g = lc.heat_run(nx, ny, to_dev(T0), 6, method=method, gs_sweeps=1 if method else 0)
@@ -787,7 +787,7 @@ def test_heat_fig2_agreement_on_gpu():
     """Fig. 2 on the device, 99 x 99 for 5 steps: methods 1 and 2 (alpha = 1e-4, E_max = 1,
     one GS sweep) agree with method0 to the paper's 7.6e-9 relative."""
     nx = ny = 99
-    T0 = to_dev(orc.heat_initial(nx, ny))
+    T0 = to_dev(synth.heat_initial(nx, ny))
     T0m = lc.heat_run(nx, ny, T0, 5, method=0)[0]
     for m in (1, 2):
         Tm, per, eta, rep = lc.heat_run(nx, ny, T0, 5, method=m)

@@ -541,7 +541,7 @@ def test_heat_run_maximum_principle_and_y_symmetry():
     y-uniform; each solve is only accurate to ||x - x*|| <= ||r|| <= 1e-10 ||b|| (R31, lambda_min >= 1), so
     rows may differ by up to 2e-10 ||b|| (||b|| <= ||T|| + lam kf T_l sqrt(ny) bounded by 2 ||T|| + 1e3 here)."""
     nx, ny = 15, 7
-    T0 = orc.heat_initial(nx, ny)
+    T0 = synth.heat_initial(nx, ny)
     T, per, rep = orc.heat_run(nx, ny, T0, 5, None, orc.SolverParams(0, 1, 30, 1e-10, 20000, 0))
     lo, hi = min(1e-4, T0.min()), max(1.0, T0.max())
     assert T.min() >= lo - 1e-12 and T.max() <= hi + 1e-12
@@ -554,7 +554,7 @@ def test_heat_methods_agree_like_fig2():
     """Fig. 2 / P:1106-1107: the local methods' fields agree with method0's (the paper reports <= 7.6e-9
     relative); here after 4 steps of the 99x99 problem, methods 1 and 2 with one GS sweep."""
     nx = ny = 99
-    T0 = orc.heat_initial(nx, ny)
+    T0 = synth.heat_initial(nx, ny)
     sp = orc.SolverParams(0, 1, 30, 1e-10, 20000, 1)
     T0m, _, _ = orc.heat_run(nx, ny, T0, 4, None, orc.SolverParams(0, 1, 30, 1e-10, 20000, 0))
     T1m, _, r1 = orc.heat_run(nx, ny, T0, 4, orc.DomainParams(1, 1, 1e-4, 0, 0, 1), sp)

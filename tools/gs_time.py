@@ -6,7 +6,6 @@ import time
 import torch
 
 sys.path.insert(0, ".")
-import oracle as orc  # noqa: E402
 import synth  # noqa: E402
 from paper_2001_01158_b200 import lc  # noqa: E402
 
@@ -14,7 +13,7 @@ if len(sys.argv) > 1:
     lc.load_library(sys.argv[1])
     lc._lib.lc_matrix_info.argtypes = None
 for n in (99, 1024):
-    T = torch.from_numpy(orc.heat_initial(n, n)).cuda()
+    T = torch.from_numpy(synth.heat_initial(n, n)).cuda()
     rp, ci, va, b = lc.heat_assemble(n, n, 1e-2, T, T)
     A = lc.Matrix(n * n, rp, ci, va)
     best = 1e9

@@ -4,23 +4,23 @@
 99 x 99, dt = 1e-2, 100 steps, Picard (||dT|| < 1e-8), linear eps = 1e-10; method0 (global Jacobi-PCG),
 method1 (Alg. 2, alpha = 1e-4) and method2 (Alg. 3, E_max = 1), one GS sweep for the local methods.
 Reports total time per method (device driver wall time), S = t0 / t_m, eta per step, Picard counts and the
-Fig. 2 differences max_n ||T_m - T_0|| / ||T_0||; optionally the oracle's totals on the host (--oracle).
+Fig. 2 differences max_n ||T_m - T_0|| / ||T_0||.  (The device driver against the CPU oracle's driver is a
+GPU test, tests/test_gpu_parity.py::test_heat_run_vs_oracle; tools never run the oracle.)
 The paper's numbers (E5-2620, BoomerAMG-GMRES): 39.19 / 28.09 / 29.76 s, S 1.40 / 1.32, e 7.6e-9 / 7.0e-9.
 """
 import json
 import sys
-import time
 
 import numpy as np
 import torch
 
 sys.path.insert(0, ".")
-import oracle as orc  # noqa: E402  (only for the optional CPU comparison and T0)
+import synth  # noqa: E402
 from paper_2001_01158_b200 import lc  # noqa: E402
 
 nx = ny = int(dict(a.split("=") for a in sys.argv[1:] if "=" in a).get("n", 99))
 steps = int(dict(a.split("=") for a in sys.argv[1:] if "=" in a).get("steps", 100))
-T0 = torch.from_numpy(orc.heat_initial(nx, ny)).cuda()
+T0 = torch.from_numpy(synth.heat_initial(nx, ny)).cuda()
 res = {"grid": f"{nx}x{ny}", "steps": steps, "methods": {}}
 fields = {}
 for m in (0, 1, 2):
@@ -41,12 +41,4 @@ for m in (1, 2):
     d = [(torch.linalg.norm(a - b) / torch.linalg.norm(b)).item() for a, b in zip(fields[m], fields[0])]
     res["methods"][f"method{m}"]["fig2_max_rel_diff"] = max(d)
     res["methods"][f"method{m}"]["speedup"] = res["methods"]["method0"]["seconds"] / res["methods"][f"method{m}"]["seconds"]
-if "--oracle" in sys.argv:
-    for m, dp, gs in ((0, None, 0), (1, orc.DomainParams(1, 1, 1e-4, 0, 0, 1), 1),
-                      (2, orc.DomainParams(0, 0, 1e-10, 1, 0, 1), 1)):
-        t = time.perf_counter()
-        To, per, rep = orc.heat_run(nx, ny, orc.heat_initial(nx, ny), steps, dp, orc.SolverParams(0, 1, 30, 1e-10, 20000, gs))
-        res["methods"][f"method{m}"]["oracle_seconds_1core"] = time.perf_counter() - t
-        res["methods"][f"method{m}"]["oracle_vs_gpu_rel_diff"] = float(
-            np.linalg.norm(To - fields[m][-1].cpu().numpy()) / np.linalg.norm(To))
 print(json.dumps(res))

@@ -9,12 +9,12 @@ import time
 import torch
 
 sys.path.insert(0, ".")
-import oracle as orc  # noqa: E402  (initial field only)
+import synth  # noqa: E402
 from paper_2001_01158_b200 import lc  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 pre = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-T0 = torch.from_numpy(orc.heat_initial(n, n)).cuda()
+T0 = torch.from_numpy(synth.heat_initial(n, n)).cuda()
 T, _, _, _ = lc.heat_run(n, n, T0, pre, method=0)          # advance a few steps (a front has formed)
 rp, ci, va, b = lc.heat_assemble(n, n, 1e-2, T, T)
 A = lc.Matrix(n * n, rp, ci, va)
