@@ -162,9 +162,25 @@ __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_
                                             bool init, double beta, const double* __restrict__ pold,
                                             double* __restrict__ pnew, double& a0, double& a1) {
   const SellView& A = P.A;
+  // the slice list entry and the row's Omega flag are loaded one slice ahead (masked solves walk a list of
+  // slices; without the prefetch every slice starts with two dependent load latencies)
+  int64_t s_next = j0 < jlim ? (P.slist ? (int64_t)P.slist[j0] : j0) : 0;
+  uint8_t om_next = 0;
+  auto om_of = [&](int64_t s_) -> uint8_t {
+    int g_;
+    int64_t r0_, e_;
+    slice_map(P, s_, g_, r0_, e_);
+    return r0_ + lane < e_ ? P.omega[r0_ + lane] : (uint8_t)0;
+  };
+  if (P.omega && j0 < jlim) om_next = om_of(s_next);
 #pragma unroll 1
   for (int64_t j = j0; j < jlim; j += jstep) {
-    const int64_t s = P.slist ? (int64_t)P.slist[j] : j;
+    const int64_t s = s_next;
+    const uint8_t om_cur = om_next;
+    if (j + jstep < jlim) {
+      s_next = P.slist ? (int64_t)P.slist[j + jstep] : j + jstep;
+      if (P.omega) om_next = om_of(s_next);
+    }
     int g;
     int64_t row0, end;
     slice_map(P, s, g, row0, end);
@@ -173,7 +189,7 @@ __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_
     const int64_t pl = (ST ? 32ll * A.vw * s : A.slice_ptr[s]) + lane;
     const int w = ST ? A.W : (int)((A.slice_ptr[s + 1] - (pl - lane)) >> 5);
     double own = 0.0;
-    const bool in = !P.omega || P.omega[u] != 255;
+    const bool in = !P.omega || om_cur != 255;
     if (MODE == 0) {
       const double* xx = P.x;
       double acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return xx[c]; }, &own);
@@ -258,17 +274,26 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
   };
   if (threadIdx.x == 0)
     for (int t = 0; t < kStages; ++t) issue(t);
+  // masked solves: the Omega flag of the row is loaded one chunk ahead, so no row waits on its flag load
+  auto om_at = [&](int64_t c) -> uint8_t {
+    const int64_t js = (int64_t)kPW * c + warp;
+    const int64_t u = 32 * (P.slist ? (js < njs ? (int64_t)P.slist[js] : 0) : js) + lane;
+    return (c < nch && js < njs && u < n) ? P.omega[u] : (uint8_t)0;
+  };
+  uint8_t om_next = P.omega ? om_at(bid) : (uint8_t)0;
 #pragma unroll 1
   for (int64_t t = 0;; ++t) {
     const int64_t c = bid + t * nCTA;
     if (c >= nch) break;
+    const uint8_t om_cur = om_next;
+    if (P.omega) om_next = om_at(c + nCTA);
     const int st = (int)(t % kStages);
     mbar_wait(&bars[st], (unsigned)((t / kStages) & 1));
     const int64_t js = (int64_t)kPW * c + warp;
     const int64_t s = js < njs ? (P.slist ? (int64_t)P.slist[js] : js) : 0;
     const int u = (int)(32 * s) + lane;
     if (js < njs && u < n) {
-      const bool in = !P.omega || P.omega[u] != 255;
+      const bool in = !P.omega || om_cur != 255;
       const double* sp = stg + st * chd + (int64_t)warp * 32 * vw + lane;
       double v[W], y[W];
 #pragma unroll
@@ -535,6 +560,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
         double rn = sqrt(s0);
         if (!isfinite(rn)) finish(g, LC_ERR_NONFINITE, rn);
         else if (rn <= T.tgt) finish(g, LC_OK, rn);
+        else if (P.max_iters == 0) finish(g, LC_NOT_CONVERGED, rn);   // Eq. 6 check only
         else T.mode = M_RESET;
       } else if (T.mode == M_FIRST || T.mode == M_NORMAL) {
         double pq = s0;
