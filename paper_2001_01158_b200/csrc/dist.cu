@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(kDT, 4) k_dpcg(const __grid_constant__ DPack p
         const double rn = sqrt(s0);
         if (!isfinite(rn)) finish(LC_ERR_NONFINITE, rn);
         else if (rn <= s_tgt) finish(LC_OK, rn);
+        else if (P.max_iters == 0) finish(LC_NOT_CONVERGED, rn);       // Eq. 6 check only
         else s_mode = D_RESET;
       } else if (mode == D_FIRST || mode == D_NORMAL) {
         if (!(s0 > 0)) finish(isfinite(s0) ? LC_ERR_BREAKDOWN : LC_ERR_NONFINITE, NAN);

@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(kST, 1) k_pcg_ds(DsArgs P) {
         const double rn = sqrt(s0);
         if (!isfinite(rn)) finish(LC_ERR_NONFINITE, rn);
         else if (rn <= s_tgt) finish(LC_OK, rn);
+        else if (P.max_iters == 0) finish(LC_NOT_CONVERGED, rn);       // Eq. 6 check only
         else s_mode = S_RESET;
       } else if (mode == S_FIRST || mode == S_NORMAL) {
         if (!(s0 > 0)) finish(isfinite(s0) ? LC_ERR_BREAKDOWN : LC_ERR_NONFINITE, NAN);
