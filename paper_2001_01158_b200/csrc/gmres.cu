@@ -93,19 +93,25 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
     __syncthreads();
     (void)nq;
   };
+  // the partials are double-buffered by reduction (ppar): a CTA leaving a barrier early may publish its next
+  // partials before a slower CTA has read these (short passes)
+  int ppar = 0;
   auto publish = [&](int nq) {
     __syncthreads();
+    double* pt = P.part + (size_t)ppar * kMaxQ * nCTA;
     for (int q = threadIdx.x; q < nq; q += kGT) {
       double v = 0.0;
       for (int w = 0; w < kGW; ++w) v += s_acc[w][q];
-      P.part[q * nCTA + bid] = v;
+      pt[q * nCTA + bid] = v;
     }
   };
   // fixed-order reduction of nq quantities over all CTAs into red[]
   auto reduce = [&](int nq) {
+    const double* pt = P.part + (size_t)ppar * kMaxQ * nCTA;
+    ppar ^= 1;
     for (int q = warp; q < nq; q += kGW) {
       double v = 0.0;
-      for (int64_t c = lane; c < nCTA; c += 32) v += P.part[q * nCTA + c];
+      for (int64_t c = lane; c < nCTA; c += 32) v += pt[q * nCTA + c];
       v = warp_sum(v);
       if (lane == 0) red[q] = v;
     }
@@ -523,7 +529,7 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   int64_t nCTA = std::min<int64_t>(g_gm_ctas[ci], (M.nslices + kGW - 1) / kGW);
   if (nCTA < 1) nCTA = 1;
   size_t vbytes = ((sizeof(double) * (size_t)n) + 255) & ~(size_t)255;
-  size_t bytes = vbytes * (3 + (m + 1) + (scatter_idx ? 1 : 0)) + sizeof(double) * kMaxQ * nCTA + sizeof(GridBar) + 384;
+  size_t bytes = vbytes * (3 + (m + 1) + (scatter_idx ? 1 : 0)) + sizeof(double) * 2 * kMaxQ * nCTA + sizeof(GridBar) + 384;
   void* ws = nullptr;
   lc_status st = dalloc(&ws, bytes, s);
   if (st) return st;
@@ -542,7 +548,7 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   } else {
     a.x = x;
   }
-  a.part = (double*)w; w += sizeof(double) * kMaxQ * nCTA;
+  a.part = (double*)w; w += sizeof(double) * 2 * kMaxQ * nCTA;
   w = (char*)((((uintptr_t)w) + 127) & ~(uintptr_t)127);
   a.bar = (GridBar*)w; w += sizeof(GridBar);
   a.out = (int*)w;

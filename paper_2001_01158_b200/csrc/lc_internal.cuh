@@ -61,6 +61,7 @@ struct PcgJob {
   double* x_full = nullptr;
   double* x_user = nullptr;       // masked local solve: x_user[u] = x[u] on Omega
   int reg_units = 0, spg = 0;     // equal segments of reg_units units with spg slices each (A), else 0
+  int64_t rows_hint = -1;         // rows the solve works on (masked: K), -1 = all; picks team mode for G > 1
 };
 
 // small single-segment stencil systems: the cluster-resident PCG (pcg_dsmem.cu)
@@ -310,6 +311,21 @@ __device__ __forceinline__ void grid_barrier(GridBar* gb, unsigned long long& ep
     unsigned long long v;
     do {
       asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&gb->ctr) : "memory");
+    } while (v < epoch);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+// the same counter barrier over `count` co-resident CTAs of a team (its own counter; epoch as above)
+__device__ __forceinline__ void team_barrier(unsigned long long* ctr, unsigned long long& epoch, unsigned count) {
+  __syncthreads();
+  epoch += count;
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+    unsigned long long v;
+    do {
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
     } while (v < epoch);
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }

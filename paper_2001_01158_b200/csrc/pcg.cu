@@ -74,6 +74,9 @@ struct PcgArgs {
   int tma;                      // pass A values staged by TMA (G = 1, no list, stencil layout)
   int cluster;                  // launched as ONE thread-block cluster (small G = 1 systems): cluster
                                 // barriers and DSMEM partial exchange instead of the global grid barrier
+  int teams;                    // > 0 (G > 1): the CTAs form `teams` contiguous teams; team t solves segments
+                                // t, t + teams, ... one after another as G = 1 systems with its own barrier
+  unsigned long long* tctr;     // [teams][16] team barrier counters (zeroed at launch)
 };
 
 struct SegState {
@@ -342,7 +345,7 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
   }
 }
 
-template <int WM, int ST>
+template <int WM, int ST, bool TEAM>
 __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   unsigned long long bar_epoch = 0;
   __shared__ SegState S[kMaxSeg];
@@ -360,10 +363,20 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   const SellView& A = P.A;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nCTA = gridDim.x, bid = blockIdx.x;
-  const int G = P.G;
-  const int64_t j0 = bid * kPW + warp, jstep = nCTA * kPW;
-  const int64_t jlim = P.slist ? *P.nlist : A.nslices;
-  for (int g = threadIdx.x; g <= G; g += kPT) s_segj0[g] = P.seg_j0[g];
+  // team mode: CTAs [tb0, tb1) form team `team`; every pass below runs over the team's current segment only
+  const int TM = TEAM ? P.teams : 0;           // compile-time 0 in the single-grid kernels
+  int team = 0;
+  const int TD = TM > 0 ? TM : 1;
+  if (TM)
+    while (team < TM - 1 && bid >= (int64_t)(team + 1) * nCTA / TD) ++team;
+  const int64_t tb0 = TM ? (int64_t)team * nCTA / TD : 0;
+  const int64_t tn = TM ? (int64_t)(team + 1) * nCTA / TD - tb0 : nCTA;
+  const int G = TEAM ? 1 : P.G;                 // the team kernels run only with P.teams >= 1
+  int gseg = TM ? team : 0;                     // segment being solved (team mode)
+  int64_t j0 = (bid - tb0) * kPW + warp;
+  const int64_t jstep = tn * kPW;
+  int64_t jlim = P.slist ? *P.nlist : A.nslices;
+  for (int g = threadIdx.x; g <= P.G; g += kPT) s_segj0[g] = P.seg_j0[g];
   if (threadIdx.x < kMaxSeg) {
     S[threadIdx.x].mode = M_INIT; S[threadIdx.x].par = 0; S[threadIdx.x].it = 0; S[threadIdx.x].final_ = 0;
     S[threadIdx.x].beta = 0.0; S[threadIdx.x].alpha = 0.0; S[threadIdx.x].rho = 0.0;
@@ -403,15 +416,20 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       __syncthreads();
       return;
     }
+    // G = 1: the partials are double-buffered by pass, since a CTA that leaves the barrier early may finish its
+    // next pass and store its next partial before a slower CTA has read this one (short passes)
+    double* const pt = P.part + (G == 1 ? (size_t)cpar * 2 * nCTA : 0);
     for (int t = threadIdx.x; t < G * 2; t += kPT) {
       double v = 0.0;
       for (int w = 0; w < kPW; ++w) v += s_acc[w][t >> 1][t & 1];
-      P.part[(bid * G) * 2 + t] = v;
+      pt[(bid * G) * 2 + t] = v;
     }
     if (G == 1) {
-      grid_barrier(P.bar, bar_epoch);
+      cpar ^= 1;
+      if (TM) team_barrier(P.tctr + 16 * team, bar_epoch, (unsigned)tn);
+      else grid_barrier(P.bar, bar_epoch);
       double a0 = 0.0, a1 = 0.0;
-      for (int64_t c = threadIdx.x; c < nCTA; c += kPT) { a0 += P.part[2 * c]; a1 += P.part[2 * c + 1]; }
+      for (int64_t c = tb0 + threadIdx.x; c < tb0 + tn; c += kPT) { a0 += pt[2 * c]; a1 += pt[2 * c + 1]; }
       a0 = warp_sum(a0); a1 = warp_sum(a1);
       if (lane == 0) { s_red[warp][0] = a0; s_red[warp][1] = a1; }
       __syncthreads();
@@ -438,10 +456,11 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   auto finish = [&](int g, int status, double rn) {
     SegState& T = S[g];
     T.mode = M_DONE;
-    if (bid == g % nCTA) {
-      P.out_iters[g] = T.it;
-      P.out_status[g] = status;
-      P.out_relres[g] = T.nb > 0 ? rn / T.nb : rn;
+    const int go = TM ? gseg : g;
+    if (bid == (TM ? tb0 : g % nCTA)) {
+      P.out_iters[go] = T.it;
+      P.out_status[go] = status;
+      P.out_relres[go] = T.nb > 0 ? rn / T.nb : rn;
     }
   };
   auto in_omega = [&](int64_t u) -> bool { return !P.omega || P.omega[u] != 255; };
@@ -469,6 +488,17 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
 #ifdef LC_DEBUG_TIMELINE
   int tlk = 0;
 #endif
+  for (; gseg < (TM ? P.G : 1); gseg += (TM ? TM : 1)) {
+  if (TM) {                                     // next segment of this team: a fresh G = 1 solve on its run
+    __syncthreads();
+    j0 = s_segj0[gseg] + (bid - tb0) * kPW + warp;
+    jlim = s_segj0[gseg + 1];
+    if (threadIdx.x == 0) {
+      S[0].mode = M_INIT; S[0].par = 0; S[0].it = 0; S[0].final_ = 0;
+      S[0].beta = 0.0; S[0].alpha = 0.0; S[0].rho = 0.0;
+    }
+    __syncthreads();
+  }
   for (;;) {
     // ------------------------------------------------------------ pass A ----
     TL(tlk);
@@ -646,6 +676,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
         int g;
         int64_t row0, end;
         slice_map(P, s, g, row0, end);
+        if (TEAM) g = 0;                          // the team's current segment lives in S[0]
         if (g != gcur) {
           if (gcur >= 0) flush(gcur, a0, a1);
           a0 = a1 = 0.0;
@@ -715,10 +746,11 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       else if (in_omega(u)) P.x_user[u] = P.x[u];
     }
   }
+  }                                             // segments of the team
 }
 
 // ---------------------------------------------------------------- host ----
-static int g_pcg_max_ctas[18] = {0};
+static int g_pcg_max_ctas[36] = {0};
 
 lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
   const Sell& M = *job.M;
@@ -733,15 +765,41 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   // exactly maxw slots, so they take W = 5 / 7 only when maxw is exactly that (else the generic loop)
   const int wi = (M.stencil ? (M.maxw == 5 ? 0 : M.maxw == 7 ? 1 : 2) : (M.maxw <= 5 ? 0 : M.maxw <= 7 ? 1 : 2)) +
                  (M.sym ? 6 : M.stencil ? 3 : 0);
-  void* const fns[9] = {(void*)k_pcg<5, 0>, (void*)k_pcg<7, 0>, (void*)k_pcg<0, 0>,
-                        (void*)k_pcg<5, 1>, (void*)k_pcg<7, 1>, (void*)k_pcg<0, 1>,
-                        (void*)k_pcg<5, 2>, (void*)k_pcg<7, 2>, (void*)k_pcg<0, 2>};
-  void* fn = fns[wi];
+  void* const fns[18] = {(void*)k_pcg<5, 0, false>, (void*)k_pcg<7, 0, false>, (void*)k_pcg<0, 0, false>,
+                         (void*)k_pcg<5, 1, false>, (void*)k_pcg<7, 1, false>, (void*)k_pcg<0, 1, false>,
+                         (void*)k_pcg<5, 2, false>, (void*)k_pcg<7, 2, false>, (void*)k_pcg<0, 2, false>,
+                         (void*)k_pcg<5, 0, true>,  (void*)k_pcg<7, 0, true>,  (void*)k_pcg<0, 0, true>,
+                         (void*)k_pcg<5, 1, true>,  (void*)k_pcg<7, 1, true>,  (void*)k_pcg<0, 1, true>,
+                         (void*)k_pcg<5, 2, true>,  (void*)k_pcg<7, 2, true>,  (void*)k_pcg<0, 2, true>};
+  // batched systems (G > 1), two schedules:
+  //  - lock step: the whole grid sweeps the runs of all segments still active, pass by pass (every SM keeps
+  //    streaming until the last segment converges);
+  //  - teams: the CTAs form min(G, nCTA) contiguous teams, team t solves segments t, t + teams, ... one after
+  //    another as G = 1 systems with its own counter barrier (no arrival-tree reduction over all segments).
+  // A team's warps walk their slices one after another, so teams pay once each warp has only a few slices:
+  // chosen when the rows worked on are <= 4 slices per warp of the grid (config 3: the masked local solves,
+  // eta ~ 9%, 9.2 -> 4.9 ms; the global solves stay in lock step, 55 vs 80 ms with teams).  LC_TEAMS=0/1 forces.
+  const char* tenv = getenv("LC_TEAMS");
+  const int64_t rows_work = job.rows_hint >= 0 ? job.rows_hint : M.nunits;
+  bool team_k = G > 1;
+  if (team_k) {
+    if (tenv) team_k = tenv[0] == '1';
+    else {
+      // the team kernels' occupancy equals the lock-step kernels' (same launch bounds, 64 registers)
+      if (!g_pcg_max_ctas[wi * 2]) {
+        int per_sm = 0;
+        LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[wi], kPT, 0));
+        g_pcg_max_ctas[wi * 2] = std::max(per_sm, 1) * num_sms();
+      }
+      team_k = rows_work <= (int64_t)4 * 32 * kPW * g_pcg_max_ctas[wi * 2];
+    }
+  }
+  void* fn = fns[wi + (team_k ? 9 : 0)];
   // TMA staging for contiguous slice ranges (global solves); slice-list (masked) solves keep plain loads: the
   // per-slice bulk copies were 4% slower there in the bench (profiles/r01_h_tma_ab.txt)
   const bool tma = M.stencil && (M.maxw == 5 || M.maxw == 7) && G == 1 && !job.slist && getenv("LC_NO_TMA") == nullptr;
   const size_t dsmem = tma ? (size_t)kStages * kPW * 32 * (M.sym ? M.vw : M.maxw) * sizeof(double) : 0;
-  const int ci = wi * 2 + (tma ? 1 : 0);
+  const int ci = wi * 2 + (tma ? 1 : 0) + (team_k ? 18 : 0);
   if (!g_pcg_max_ctas[ci]) {
     if (dsmem > 48 * 1024) LC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
     int per_sm = 0;
@@ -759,8 +817,9 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   const size_t vec = sizeof(double) * (size_t)n;
   const size_t vbytes = (vec + 255) & ~(size_t)255;
   const bool own_x = job.x_init != nullptr;
-  const size_t bytes = vbytes * (own_x ? 6 : 5) + sizeof(double) * 2 * G * (nCTA + 1 + kBarSub) + 16 * G +
-                       sizeof(GridBar) + 640;
+  const int teams = team_k ? (int)std::min<int64_t>(G, nCTA) : 0;
+  const size_t bytes = vbytes * (own_x ? 6 : 5) + sizeof(double) * 2 * G * (2 * nCTA + 1 + kBarSub) + 16 * G +
+                       sizeof(GridBar) + 640 + 128 * (size_t)kMaxSeg;
   lc_status st = dalloc(&ws, bytes, s);
   if (st) return st;
   char* w = (char*)ws;
@@ -780,7 +839,11 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
     a.x = job.x;
   }
   if (job.omega && e == cudaSuccess) e = cudaMemsetAsync(a.r, 0, vbytes * 5, s);   // zero outside Omega
-  a.part = (double*)w; w += sizeof(double) * 2 * G * nCTA;
+  // batched (G > 1): a boundary row's stencil holes gather z / p of the neighbouring segment (times an exact 0),
+  // which may not have been written yet (its team has not started it, or it converged at INIT): start them at 0
+  if (G > 1 && !job.omega && e == cudaSuccess) e = cudaMemsetAsync(a.z, 0, vbytes, s);
+  if (G > 1 && !job.omega && e == cudaSuccess) e = cudaMemsetAsync(a.p0, 0, vbytes * 2, s);
+  a.part = (double*)w; w += sizeof(double) * 2 * G * 2 * nCTA;   // G = 1: two buffers (by pass)
   a.red = (double*)w; w += sizeof(double) * 2 * G;
   a.subred = (double*)w; w += sizeof(double) * 2 * G * kBarSub;
   w = (char*)((((uintptr_t)w) + 127) & ~(uintptr_t)127);
@@ -788,6 +851,8 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   a.out_iters = (int*)w; w += 4 * G;
   a.out_status = (int*)w; w += 4 * G;
   a.out_relres = (double*)((((uintptr_t)w) + 7) & ~(uintptr_t)7);
+  a.tctr = (unsigned long long*)((((uintptr_t)(a.out_relres + G)) + 127) & ~(uintptr_t)127);
+  a.teams = teams;
   a.slist = job.slist;
   a.nlist = job.nlist_dev;
   a.omega = job.omega;
@@ -807,6 +872,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
             ((((uintptr_t)a.x) | ((uintptr_t)a.r) | ((uintptr_t)a.z) | ((uintptr_t)a.q) | ((uintptr_t)a.p0) |
               ((uintptr_t)a.p1) | ((uintptr_t)M.dinv)) & 15) == 0) ? 1 : 0;
   if (e == cudaSuccess) e = cudaMemsetAsync(a.bar, 0, sizeof(GridBar), s);
+  if (e == cudaSuccess && teams) e = cudaMemsetAsync(a.tctr, 0, 128 * (size_t)teams, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(a.out_iters, 0, 8 * G, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(a.out_relres, 0, 8 * G, s);
   cudaEvent_t e0, e1;

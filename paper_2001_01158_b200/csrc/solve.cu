@@ -62,6 +62,7 @@ extern "C" lc_status lc_solve_local(lc_sub S, const lc_solver_params* p, double*
     job.nlist_max = std::min<int64_t>(A->A.nslices, S->K_units);
     job.omega = S->omega; job.x_user = x;
     job.reg_units = A->seg_units; job.spg = (A->seg_units + 31) / 32;
+    job.rows_hint = S->K_units;
     return run_pcg(job, p, (cudaStream_t)stream, info);
   }
   return run(S->B, S->bsub, nullptr, S->idx, x, S->xB0, p, (cudaStream_t)stream, info, 0, 0);

@@ -172,6 +172,16 @@ def test_config3_reduced_batched(n, G, s):
     check_system(sy, RULES[3][0])
 
 
+@pytest.mark.parametrize("sched", ["0", "1"])
+@pytest.mark.parametrize("n,G,s", [(30, 4, 0), (64, 20, 3)])
+def test_config3_batched_schedules(n, G, s, sched, monkeypatch):
+    """Both batched PCG schedules (LC_TEAMS=0: the grid sweeps all active groups in lock step; 1: one team of
+    CTAs per group) against the oracle; the automatic choice is exercised by test_config3_reduced_batched."""
+    monkeypatch.setenv("LC_TEAMS", sched)
+    sy = synth.system(3, s, n=n, G=G)
+    check_system(sy, RULES[3][0])
+
+
 @pytest.mark.parametrize("n,s", [(20, 0), (45, 4), (64, 29)])
 def test_config4_reduced_gmres(n, s):
     sy = synth.system(4, s, n=n)
