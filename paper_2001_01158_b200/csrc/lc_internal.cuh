@@ -294,6 +294,8 @@ struct GridBar {
   unsigned pad[30];
   unsigned long long ctr;       // counter barrier
   unsigned long long pad2[15];
+  unsigned long long done;      // tree_reduce_barrier: sub-group sums published
+  unsigned long long pad3[15];
 };
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -334,7 +336,8 @@ __device__ __forceinline__ void team_barrier(unsigned long long* ctr, unsigned l
 
 // out[t] = sum over the members m_i = first + i step (i < count, ascending) of part[m_i T + t], t < T <= 128:
 // warp w sums a contiguous range of members, then the NW warp sums are added in warp order (fixed order);
-// the block has NW warps
+// the block has NW warps.  A lane issues the loads of up to 8 members at once and then adds them in order, so
+// a range costs one L2 round trip instead of one per member (on the barrier's critical path).
 template <int NW, int TMAX>
 __device__ __forceinline__ void sum_members(const double* part, int T, unsigned first, unsigned step, unsigned count,
                                             double* out, double (*s_tmp)[TMAX]) {
@@ -343,7 +346,15 @@ __device__ __forceinline__ void sum_members(const double* part, int T, unsigned 
   const unsigned i0 = warp * per, i1 = min(count, i0 + per);
   for (int t = lane; t < T; t += 32) {
     double a = 0.0;
-    for (unsigned i = i0; i < i1; ++i) a += __ldcg(part + (size_t)(first + i * step) * T + t);
+    for (unsigned ib = i0; ib < i1; ib += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        v[q] = ib + q < i1 ? __ldcg(part + (size_t)(first + (ib + q) * step) * T + t) : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (ib + q < i1) a += v[q];
+    }
     s_tmp[warp][t] = a;
   }
   __syncthreads();
@@ -354,59 +365,62 @@ __device__ __forceinline__ void sum_members(const double* part, int T, unsigned 
   }
 }
 
-// Grid barrier whose arrival tree also reduces the per-CTA partials part[b][0..T) (batched solves, G > 1):
-// the last arriver of each of the kBarSub sub-groups sums its members' partials (by CTA index) into
-// subred[k], the last of those sums the sub-groups (by index) into red and releases the generation.  Every
-// CTA then reads only the T sums, instead of a second barrier plus a per-segment stage (profiles/r01_m).
+// Grid barrier that also reduces the per-CTA partials part[b][0..T) (batched solves, G > 1), with no atomic
+// round trip on its critical path: CTA b announces its arrival on sub-group counter k = b % kBarSub with a
+// fire-and-forget red.release; CTA k (the sub-group's reducer) polls that counter until all its members arrived,
+// sums their partials in CTA order into subred[epoch & 1][k] and announces it on the `done` counter; every CTA
+// polls `done` until all reducers finished and sums the kBarSub sub-group sums in order itself, into s_out[t]
+// (shared memory).  Counters are monotonic (epoch = the caller's count of these barriers, from 0); subred is
+// double-buffered by epoch (a reducer can only start epoch e + 2 after every CTA has left epoch e + 1, hence read
+// epoch e).  Fixed order everywhere, so every CTA holds bitwise identical sums.  The earlier form (last arriver
+// of each sub-group found by an atomicAdd, a second atomic level, a generation word) took 7.8 us from the last
+// arrival to the first CTA out on config 3 (per-CTA timeline, tools/tl_cta.py); see DESIGN s6.
 template <int NW, int TMAX>
-__device__ void tree_reduce_barrier(GridBar* gb, const double* part, double* subred, double* red, int T,
-                                    double (*s_tmp)[TMAX], int* s_flag) {
+__device__ void tree_reduce_barrier(GridBar* gb, const double* part, double* subred, double* s_out, int T,
+                                    double (*s_tmp)[TMAX], unsigned& epoch) {
   const unsigned nb = gridDim.x, b = blockIdx.x;
-  __syncthreads();
-  unsigned g0 = 0;
+  const unsigned nsub = nb < (unsigned)kBarSub ? nb : (unsigned)kBarSub;
+  const unsigned e = ++epoch;
+  double* sr = subred + (size_t)(e & 1) * kBarSub * T;
+  __syncthreads();                                    // the CTA's partials precede thread 0's release (bar.sync)
   if (threadIdx.x == 0) {
-    g0 = ld_acquire_u32(&gb->gen);
-    __threadfence();
-    int f;
-    if (nb <= 64) {
-      f = atomicAdd(&gb->top, 1u) == nb - 1 ? 2 : 0;
-    } else {
-      const unsigned k = b % kBarSub, nk = (nb - k + kBarSub - 1) / kBarSub;
-      f = atomicAdd(&gb->sub[k][0], 1u) == nk - 1 ? 1 : 0;
-    }
-    if (f) __threadfence();
-    s_flag[0] = f;
+    unsigned long long* c = reinterpret_cast<unsigned long long*>(&gb->sub[b % kBarSub][0]);
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(c) : "memory");
   }
-  __syncthreads();
-  int f = s_flag[0];
-  if (f == 1) {
-    const unsigned k = b % kBarSub, nk = (nb - k + kBarSub - 1) / kBarSub;
-    sum_members<NW, TMAX>(part, T, k, kBarSub, nk, subred + (size_t)k * T, s_tmp);
-    __syncthreads();
+  if (b < nsub) {                                     // reducer of sub-group b
+    const unsigned nk = (nb - b + kBarSub - 1) / kBarSub;
     if (threadIdx.x == 0) {
-      gb->sub[k][0] = 0;
-      __threadfence();
-      const bool last = atomicAdd(&gb->top, 1u) == (unsigned)kBarSub - 1;
-      if (last) __threadfence();
-      s_flag[0] = last ? 2 : 1;
+      const unsigned long long* c = reinterpret_cast<const unsigned long long*>(&gb->sub[b][0]);
+      const unsigned long long want = (unsigned long long)e * nk;
+      unsigned long long v;
+      do {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
+      } while (v < want);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
-    f = s_flag[0];
-    if (f == 2) sum_members<NW, TMAX>(subred, T, 0, 1, kBarSub, red, s_tmp);
-  } else if (f == 2) {
-    sum_members<NW, TMAX>(part, T, 0, 1, nb, red, s_tmp);
+    sum_members<NW, TMAX>(part, T, b, kBarSub, nk, sr + (size_t)b * T, s_tmp);
+    __syncthreads();                                  // the sums precede thread 0's release
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&gb->done) : "memory");
+  }
+  if (threadIdx.x == 0) {
+    const unsigned long long want = (unsigned long long)e * nsub;
+    unsigned long long v;
+    do {
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&gb->done) : "memory");
+    } while (v < want);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (f == 2) {
-      __threadfence();
-      gb->top = 0;
-      st_release_u32(&gb->gen, g0 + 1);
-    } else {
-      while (ld_acquire_u32(&gb->gen) == g0) {
-      }
-    }
-    __threadfence();
+  for (int t = threadIdx.x; t < T; t += NW * 32) {
+    double v[kBarSub];
+#pragma unroll
+    for (int k = 0; k < kBarSub; ++k) v[k] = k < (int)nsub ? __ldcg(sr + (size_t)k * T + t) : 0.0;
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < kBarSub; ++k)
+      if (k < (int)nsub) a += v[k];
+    s_out[t] = a;
   }
   __syncthreads();
 }

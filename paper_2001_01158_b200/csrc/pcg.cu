@@ -53,7 +53,7 @@ struct PcgArgs {
   double* p1;
   double* part;                 // [nCTA][G][2]
   double* red;                  // [G][2]  (G > 1)
-  double* subred;               // [kBarSub][G][2]  (G > 1: per-sub-group sums of the arrival tree)
+  double* subred;               // [2][kBarSub][G][2]  (G > 1: per-sub-group sums, double-buffered)
   GridBar* bar;                 // zeroed at launch
   int* out_iters;               // [G]
   int* out_status;
@@ -229,8 +229,21 @@ __device__ __forceinline__ void tl_mark(int& k) {
   ++k;
 }
 #define TL(k) tl_mark(k)
+// per-CTA pass timeline: [pass - g_cta_pass0][bid][0: pass start, 1: pass end, 2: reduction/barrier out]
+__device__ unsigned long long g_cta[64][1024][3];
+__device__ int g_cta_pass0;
+__device__ __forceinline__ void cta_mark(int pc, int slot) {
+  const int k = pc - g_cta_pass0;
+  if (threadIdx.x == 0 && k >= 0 && k < 64 && blockIdx.x < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_cta[k][blockIdx.x][slot] = t;
+  }
+}
+#define CT(pc, slot) cta_mark(pc, slot)
 #else
 #define TL(k) (void)0
+#define CT(pc, slot) (void)0
 #endif
 #ifndef LCV_MINB
 #define LCV_MINB 4
@@ -348,11 +361,11 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
 template <int WM, int ST, bool TEAM>
 __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   unsigned long long bar_epoch = 0;
+  unsigned tree_gen = 0;                        // tree barriers passed (G > 1)
   __shared__ SegState S[kMaxSeg];
   __shared__ double s_acc[kPW][kMaxSeg][2];
   __shared__ double s_red[kPW][2];
   __shared__ double s_sum[kMaxSeg][2];
-  __shared__ int s_tflag[1];
   __shared__ long long s_segj0[kMaxSeg + 1];   // segment runs in slice space
   __shared__ int s_act[kMaxSeg + 1];           // active segments of the current pass (+ sentinel)
   __shared__ long long s_actj[kMaxSeg + 1];    // their runs concatenated
@@ -447,9 +460,8 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       }
 #endif
     } else {
-      tree_reduce_barrier<kPW, 2 * kMaxSeg>(P.bar, P.part, P.subred, P.red, 2 * G,
-                                            reinterpret_cast<double (*)[2 * kMaxSeg]>(&s_acc[0][0][0]), s_tflag);
-      for (int t = threadIdx.x; t < G * 2; t += kPT) s_sum[t >> 1][t & 1] = __ldcg(P.red + t);
+      tree_reduce_barrier<kPW, 2 * kMaxSeg>(P.bar, P.part, P.subred, &s_sum[0][0], 2 * G,
+                                            reinterpret_cast<double (*)[2 * kMaxSeg]>(&s_acc[0][0][0]), tree_gen);
     }
     __syncthreads();
   };
@@ -488,6 +500,8 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
 #ifdef LC_DEBUG_TIMELINE
   int tlk = 0;
 #endif
+  int pc = 0;                                   // pass counter (debug timeline)
+  (void)pc;
   for (; gseg < (TM ? P.G : 1); gseg += (TM ? TM : 1)) {
   if (TM) {                                     // next segment of this team: a fresh G = 1 solve on its run
     __syncthreads();
@@ -502,6 +516,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   for (;;) {
     // ------------------------------------------------------------ pass A ----
     TL(tlk);
+    CT(pc, 0);
     clear_acc();
     if (G == 1) {
       const int mode = S[0].mode;
@@ -577,7 +592,10 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       if (gcur >= 0) flush(gcur, a0, a1);
     }
     TL(tlk);
+    CT(pc, 1);
     reduce_all();
+    CT(pc, 2);
+    ++pc;
     TL(tlk);
     // ---------------------------------------------------- pass A scalars ----
     // segments are independent: thread g updates segment g's state
@@ -607,6 +625,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
     __syncthreads();
     // ------------------------------------------------------------ pass B ----
     TL(tlk);
+    CT(pc, 0);
     clear_acc();
     if (P.vec2) {
       // single segment over all rows: flat grid-stride over row pairs with 16-byte loads/stores
@@ -707,7 +726,10 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       if (gcur >= 0) flush(gcur, a0, a1);
     }
     TL(tlk);
+    CT(pc, 1);
     reduce_all();
+    CT(pc, 2);
+    ++pc;
     TL(tlk);
     // ---------------------------------------------------- pass B scalars ----
     int active = 0;
@@ -812,13 +834,14 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   // small single-segment solves: one cluster of <= 16 CTAs (<= 512 slices = 4 per warp)
   const bool clus = G == 1 && work <= 16 * kPW * 4 && getenv("LC_NO_CLUSTER") == nullptr;
   int64_t nCTA = std::min<int64_t>(g_pcg_max_ctas[ci], (std::max<int64_t>(work, 1) + kPW - 1) / kPW);
+  if (const char* cap = getenv("LC_PCG_MAX_CTAS")) nCTA = std::max<int64_t>(1, std::min<int64_t>(nCTA, atoll(cap)));
   if (nCTA < 1) nCTA = 1;
   void* ws = nullptr;
   const size_t vec = sizeof(double) * (size_t)n;
   const size_t vbytes = (vec + 255) & ~(size_t)255;
   const bool own_x = job.x_init != nullptr;
   const int teams = team_k ? (int)std::min<int64_t>(G, nCTA) : 0;
-  const size_t bytes = vbytes * (own_x ? 6 : 5) + sizeof(double) * 2 * G * (2 * nCTA + 1 + kBarSub) + 16 * G +
+  const size_t bytes = vbytes * (own_x ? 6 : 5) + sizeof(double) * 2 * G * (2 * nCTA + 1 + 2 * kBarSub) + 16 * G +
                        sizeof(GridBar) + 640 + 128 * (size_t)kMaxSeg;
   lc_status st = dalloc(&ws, bytes, s);
   if (st) return st;
@@ -845,7 +868,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   if (G > 1 && !job.omega && e == cudaSuccess) e = cudaMemsetAsync(a.p0, 0, vbytes * 2, s);
   a.part = (double*)w; w += sizeof(double) * 2 * G * 2 * nCTA;   // G = 1: two buffers (by pass)
   a.red = (double*)w; w += sizeof(double) * 2 * G;
-  a.subred = (double*)w; w += sizeof(double) * 2 * G * kBarSub;
+  a.subred = (double*)w; w += sizeof(double) * 2 * G * 2 * kBarSub;
   w = (char*)((((uintptr_t)w) + 127) & ~(uintptr_t)127);
   a.bar = (GridBar*)w; w += sizeof(GridBar);
   a.out_iters = (int*)w; w += 4 * G;
@@ -939,5 +962,11 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
 #ifdef LC_DEBUG_TIMELINE
 extern "C" int lc_debug_timeline(unsigned long long* out, int n) {
   return cudaMemcpyFromSymbol(out, lc::g_tl, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -1;
+}
+extern "C" int lc_debug_cta_window(int pass0) {
+  return cudaMemcpyToSymbol(lc::g_cta_pass0, &pass0, sizeof(int)) == cudaSuccess ? 0 : -1;
+}
+extern "C" int lc_debug_cta(unsigned long long* out) {   // [64][1024][3]
+  return cudaMemcpyFromSymbol(out, lc::g_cta, sizeof(unsigned long long) * 64 * 1024 * 3) == cudaSuccess ? 0 : -1;
 }
 #endif
