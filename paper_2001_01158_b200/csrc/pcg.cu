@@ -358,7 +358,8 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
   }
 }
 
-template <int WM, int ST, bool TEAM>
+// KIND: 0 = one segment (G = 1), 1 = batched lock step (G > 1), 2 = batched teams (each team a G = 1 solve)
+template <int WM, int ST, int KIND>
 __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   unsigned long long bar_epoch = 0;
   unsigned tree_gen = 0;                        // tree barriers passed (G > 1)
@@ -377,6 +378,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nCTA = gridDim.x, bid = blockIdx.x;
   // team mode: CTAs [tb0, tb1) form team `team`; every pass below runs over the team's current segment only
+  constexpr bool TEAM = KIND == 2;
   const int TM = TEAM ? P.teams : 0;           // compile-time 0 in the single-grid kernels
   int team = 0;
   const int TD = TM > 0 ? TM : 1;
@@ -384,7 +386,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
     while (team < TM - 1 && bid >= (int64_t)(team + 1) * nCTA / TD) ++team;
   const int64_t tb0 = TM ? (int64_t)team * nCTA / TD : 0;
   const int64_t tn = TM ? (int64_t)(team + 1) * nCTA / TD - tb0 : nCTA;
-  const int G = TEAM ? 1 : P.G;                 // the team kernels run only with P.teams >= 1
+  const int G = KIND == 1 ? P.G : 1;            // compile-time 1 except in the lock-step kernels
   int gseg = TM ? team : 0;                     // segment being solved (team mode)
   int64_t j0 = (bid - tb0) * kPW + warp;
   const int64_t jstep = tn * kPW;
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   // per-CTA partials -> part[bid][g][j]; then every CTA obtains s_sum[g][j] for all g (fixed order)
   auto reduce_all = [&]() {
     __syncthreads();
-    if (P.cluster) {
+    if (KIND == 0 && P.cluster) {
       // one cluster (G = 1): partials stay in shared memory and are read across the cluster (DSMEM)
       cg::cluster_group cl = cg::this_cluster();
       if (threadIdx.x < 2) {
@@ -524,7 +526,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       const double beta = S[0].beta;
       const double* pold = S[0].par ? P.p1 : P.p0;
       double* pnew = S[0].par ? P.p0 : P.p1;
-      if (ST && WM > 0 && P.tma) {
+      if (KIND == 0 && ST && WM > 0 && P.tma) {
         if (mode == M_INIT || mode == M_CONFIRM)
           pass_a_tma<WM, ST, 0>(P, dsm, s_bars, bid, nCTA, warp, lane, mode == M_INIT, beta, pold, pnew, a0, a1);
         else if (mode == M_FIRST)
@@ -627,7 +629,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
     TL(tlk);
     CT(pc, 0);
     clear_acc();
-    if (P.vec2) {
+    if (KIND == 0 && P.vec2) {
       // single segment over all rows: flat grid-stride over row pairs with 16-byte loads/stores
       const int mode = S[0].mode;
       double a0 = 0.0, a1 = 0.0;
@@ -772,7 +774,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
 }
 
 // ---------------------------------------------------------------- host ----
-static int g_pcg_max_ctas[36] = {0};
+static int g_pcg_max_ctas[54] = {0};
 
 lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
   const Sell& M = *job.M;
@@ -787,12 +789,11 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   // exactly maxw slots, so they take W = 5 / 7 only when maxw is exactly that (else the generic loop)
   const int wi = (M.stencil ? (M.maxw == 5 ? 0 : M.maxw == 7 ? 1 : 2) : (M.maxw <= 5 ? 0 : M.maxw <= 7 ? 1 : 2)) +
                  (M.sym ? 6 : M.stencil ? 3 : 0);
-  void* const fns[18] = {(void*)k_pcg<5, 0, false>, (void*)k_pcg<7, 0, false>, (void*)k_pcg<0, 0, false>,
-                         (void*)k_pcg<5, 1, false>, (void*)k_pcg<7, 1, false>, (void*)k_pcg<0, 1, false>,
-                         (void*)k_pcg<5, 2, false>, (void*)k_pcg<7, 2, false>, (void*)k_pcg<0, 2, false>,
-                         (void*)k_pcg<5, 0, true>,  (void*)k_pcg<7, 0, true>,  (void*)k_pcg<0, 0, true>,
-                         (void*)k_pcg<5, 1, true>,  (void*)k_pcg<7, 1, true>,  (void*)k_pcg<0, 1, true>,
-                         (void*)k_pcg<5, 2, true>,  (void*)k_pcg<7, 2, true>,  (void*)k_pcg<0, 2, true>};
+#define LC_PCG_FNS(K) (void*)k_pcg<5, 0, K>, (void*)k_pcg<7, 0, K>, (void*)k_pcg<0, 0, K>, \
+                      (void*)k_pcg<5, 1, K>, (void*)k_pcg<7, 1, K>, (void*)k_pcg<0, 1, K>, \
+                      (void*)k_pcg<5, 2, K>, (void*)k_pcg<7, 2, K>, (void*)k_pcg<0, 2, K>
+  void* const fns[27] = {LC_PCG_FNS(0), LC_PCG_FNS(1), LC_PCG_FNS(2)};
+#undef LC_PCG_FNS
   // batched systems (G > 1), two schedules:
   //  - lock step: the whole grid sweeps the runs of all segments still active, pass by pass (every SM keeps
   //    streaming until the last segment converges);
@@ -808,20 +809,21 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
     if (tenv) team_k = tenv[0] == '1';
     else {
       // the team kernels' occupancy equals the lock-step kernels' (same launch bounds, 64 registers)
-      if (!g_pcg_max_ctas[wi * 2]) {
+      if (!g_pcg_max_ctas[36 + wi * 2]) {
         int per_sm = 0;
-        LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[wi], kPT, 0));
-        g_pcg_max_ctas[wi * 2] = std::max(per_sm, 1) * num_sms();
+        LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[9 + wi], kPT, 0));
+        g_pcg_max_ctas[36 + wi * 2] = std::max(per_sm, 1) * num_sms();
       }
-      team_k = rows_work <= (int64_t)4 * 32 * kPW * g_pcg_max_ctas[wi * 2];
+      team_k = rows_work <= (int64_t)4 * 32 * kPW * g_pcg_max_ctas[36 + wi * 2];
     }
   }
-  void* fn = fns[wi + (team_k ? 9 : 0)];
+  const int kind = G == 1 ? 0 : team_k ? 2 : 1;
+  void* fn = fns[wi + 9 * kind];
   // TMA staging for contiguous slice ranges (global solves); slice-list (masked) solves keep plain loads: the
   // per-slice bulk copies were 4% slower there in the bench (profiles/r01_h_tma_ab.txt)
   const bool tma = M.stencil && (M.maxw == 5 || M.maxw == 7) && G == 1 && !job.slist && getenv("LC_NO_TMA") == nullptr;
   const size_t dsmem = tma ? (size_t)kStages * kPW * 32 * (M.sym ? M.vw : M.maxw) * sizeof(double) : 0;
-  const int ci = wi * 2 + (tma ? 1 : 0) + (team_k ? 18 : 0);
+  const int ci = wi * 2 + (tma ? 1 : 0) + 18 * kind;
   if (!g_pcg_max_ctas[ci]) {
     if (dsmem > 48 * 1024) LC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
     int per_sm = 0;
