@@ -817,6 +817,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
       team_k = rows_work <= (int64_t)4 * 32 * kPW * g_pcg_max_ctas[36 + wi * 2];
     }
   }
+  // (larger batched solves: lock step; two task-flow schedules measured slower, profiles/r01_aj)
   const int kind = G == 1 ? 0 : team_k ? 2 : 1;
   void* fn = fns[wi + 9 * kind];
   // TMA staging for contiguous slice ranges (global solves); slice-list (masked) solves keep plain loads: the
