@@ -100,6 +100,18 @@ __device__ __forceinline__ void slice_map(const PcgArgs& P, int64_t s, int& g, i
   }
 }
 
+// slice_map for a slice whose segment g is already known (the batched loops know it from the active-run
+// table): no 64-bit division by the slices per segment on the path to the slice's loads
+__device__ __forceinline__ void slice_map_g(const PcgArgs& P, int64_t s, int g, int64_t& row0, int64_t& end) {
+  if (P.reg_units > 0) {
+    row0 = (int64_t)g * P.reg_units + 32 * (s - (int64_t)g * P.spg);
+    end = (int64_t)(g + 1) * P.reg_units;
+  } else {
+    row0 = P.A.slice_row0[s];
+    end = P.A.seg_unit0[g + 1];
+  }
+}
+
 // One row of a slice times an operand y(c).  WM > 0: slice width bound known at compile time; the
 // loop is fully unrolled so all value loads and gathers issue together (stencil: columns are
 // u + off[k], no column loads at all).  Returns the fma chain; *own = y at the diagonal slot when
@@ -163,8 +175,9 @@ __device__ __forceinline__ double row_dot(const SellView& A, int64_t pl, int w, 
 template <int WM, int ST, int MODE>
 __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_t jlim, int64_t jstep, int lane,
                                             bool init, double beta, const double* __restrict__ pold,
-                                            double* __restrict__ pnew, double& a0, double& a1) {
+                                            double* __restrict__ pnew, double& a0, double& a1, int gk = -1) {
   const SellView& A = P.A;
+  // (gk >= 0: every slice belongs to segment gk)
   // the slice list entry and the row's Omega flag are loaded one slice ahead (masked solves walk a list of
   // slices; without the prefetch every slice starts with two dependent load latencies)
   int64_t s_next = j0 < jlim ? (P.slist ? (int64_t)P.slist[j0] : j0) : 0;
@@ -172,7 +185,8 @@ __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_
   auto om_of = [&](int64_t s_) -> uint8_t {
     int g_;
     int64_t r0_, e_;
-    slice_map(P, s_, g_, r0_, e_);
+    if (gk >= 0) slice_map_g(P, s_, gk, r0_, e_);
+    else slice_map(P, s_, g_, r0_, e_);
     return r0_ + lane < e_ ? P.omega[r0_ + lane] : (uint8_t)0;
   };
   if (P.omega && j0 < jlim) om_next = om_of(s_next);
@@ -186,7 +200,8 @@ __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_
     }
     int g;
     int64_t row0, end;
-    slice_map(P, s, g, row0, end);
+    if (gk >= 0) slice_map_g(P, s, gk, row0, end);
+    else slice_map(P, s, g, row0, end);
     const int64_t u = row0 + lane;
     if (u >= end) continue;
     const int64_t pl = (ST ? 32ll * A.vw * s : A.slice_ptr[s]) + lane;
@@ -534,11 +549,11 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
         else if (mode == M_NORMAL)
           pass_a_tma<WM, ST, 2>(P, dsm, s_bars, bid, nCTA, warp, lane, false, beta, pold, pnew, a0, a1);
       } else if (mode == M_INIT || mode == M_CONFIRM)
-        pass_a_loop<WM, ST, 0>(P, j0, jlim, jstep, lane, mode == M_INIT, beta, pold, pnew, a0, a1);
+        pass_a_loop<WM, ST, 0>(P, j0, jlim, jstep, lane, mode == M_INIT, beta, pold, pnew, a0, a1, TEAM ? gseg : -1);
       else if (mode == M_FIRST)
-        pass_a_loop<WM, ST, 1>(P, j0, jlim, jstep, lane, false, beta, pold, pnew, a0, a1);
+        pass_a_loop<WM, ST, 1>(P, j0, jlim, jstep, lane, false, beta, pold, pnew, a0, a1, TEAM ? gseg : -1);
       else if (mode == M_NORMAL)
-        pass_a_loop<WM, ST, 2>(P, j0, jlim, jstep, lane, false, beta, pold, pnew, a0, a1);
+        pass_a_loop<WM, ST, 2>(P, j0, jlim, jstep, lane, false, beta, pold, pnew, a0, a1, TEAM ? gseg : -1);
       flush(0, a0, a1);
     } else {
       const int64_t J = build_active(0);
@@ -548,11 +563,11 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       double* pnew = nullptr;
       for (int64_t j = j0; j < J; j += jstep) {
         while (s_actj[ka + 1] <= j) ++ka;
-        const int64_t jj = s_segj0[s_act[ka]] + (j - s_actj[ka]);
+        const int g = s_act[ka];
+        const int64_t jj = s_segj0[g] + (j - s_actj[ka]);
         const int64_t s = P.slist ? (int64_t)P.slist[jj] : jj;
-        int g;
         int64_t row0, end;
-        slice_map(P, s, g, row0, end);
+        slice_map_g(P, s, g, row0, end);
         if (g != gcur) {
           if (gcur >= 0) flush(gcur, a0, a1);
           a0 = a1 = 0.0;
@@ -687,17 +702,20 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       const double* pp = nullptr;
       for (int64_t j = j0; j < J; j += jstep) {
         int64_t s;
-        if (G == 1) {
-          s = P.slist ? (int64_t)P.slist[j] : j;
-        } else {
-          while (s_actj[ka + 1] <= j) ++ka;
-          const int64_t jj = s_segj0[s_act[ka]] + (j - s_actj[ka]);
-          s = P.slist ? (int64_t)P.slist[jj] : jj;
-        }
         int g;
         int64_t row0, end;
-        slice_map(P, s, g, row0, end);
-        if (TEAM) g = 0;                          // the team's current segment lives in S[0]
+        if (G == 1) {
+          s = P.slist ? (int64_t)P.slist[j] : j;
+          if (TEAM) slice_map_g(P, s, gseg, row0, end);
+          else slice_map(P, s, g, row0, end);
+          g = 0;                                  // (a team's current segment lives in S[0])
+        } else {
+          while (s_actj[ka + 1] <= j) ++ka;
+          g = s_act[ka];
+          const int64_t jj = s_segj0[g] + (j - s_actj[ka]);
+          s = P.slist ? (int64_t)P.slist[jj] : jj;
+          slice_map_g(P, s, g, row0, end);
+        }
         if (g != gcur) {
           if (gcur >= 0) flush(gcur, a0, a1);
           a0 = a1 = 0.0;
