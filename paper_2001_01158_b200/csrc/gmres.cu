@@ -110,8 +110,16 @@ __global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
     const double* pt = P.part + (size_t)ppar * kMaxQ * nCTA;
     ppar ^= 1;
     for (int q = warp; q < nq; q += kGW) {
+      // a lane's partials (CTAs lane, lane + 32, ...) are loaded 8 at a time and added in that order
       double v = 0.0;
-      for (int64_t c = lane; c < nCTA; c += 32) v += pt[q * nCTA + c];
+      for (int64_t c0 = lane; c0 < nCTA; c0 += 32 * 8) {
+        double t[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t[k] = c0 + 32 * k < nCTA ? pt[q * nCTA + c0 + 32 * k] : 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (c0 + 32 * k < nCTA) v += t[k];
+      }
       v = warp_sum(v);
       if (lane == 0) red[q] = v;
     }
