@@ -274,6 +274,41 @@ def test_determinism_bitwise():
     assert [i["iterations"] for i in r1["global"]] == [i["iterations"] for i in r2["global"]]
 
 
+@pytest.mark.parametrize("path", ["grid", "lock", "team", "gmres"])
+def test_determinism_short_passes(path, monkeypatch):
+    """Repeated solves with very short passes (tiny systems on the multi-CTA kernels, where a CTA leaving a
+    barrier early races ahead of slower CTAs) are bitwise identical: guards the per-CTA partial buffers and
+    the barrier/reduction protocols (a partial overwritten before it was read showed up here as breakdowns
+    or run-to-run differences)."""
+    if path == "grid":
+        monkeypatch.setenv("LC_NO_DSMEM", "1")
+        monkeypatch.setenv("LC_NO_CLUSTER", "1")
+        sy = synth.system(1, 4, n=40)
+    elif path == "gmres":
+        sy = synth.system(4, 4, n=16)
+    else:
+        monkeypatch.setenv("LC_TEAMS", "1" if path == "team" else "0")
+        sy = synth.system(3, 5, n=30, G=6)
+    A = gpu_matrix(sy)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    method = method_of(sy.config)
+    ref = None
+    for _ in range(12):
+        x = x0.clone()
+        info = lc.solve_global(A, b, x, method=method)
+        its = [i["iterations"] for i in info]
+        assert all(i["status"] == 0 for i in info), info
+        if ref is None:
+            ref = (x.clone(), its)
+        else:
+            assert its == ref[1]
+            assert torch.equal(x, ref[0])
+    xo, _, ro = orc.local_method(oracle_csr(sy), sy.b, sy.x0, None, oracle_sp(sy.config)) if sy.batch == 1 else (None, None, None)
+    if xo is not None:
+        assert abs(ref[1][0] - ro.it_global) <= 1
+        assert np.linalg.norm(ref[0].cpu().numpy() - xo) <= 1e-9 * np.linalg.norm(xo)
+
+
 def test_errors_zero_diagonal_and_pattern():
     with pytest.raises(lc.LcError) as e:
         lc.Matrix(2, [0, 1, 2], [0, 1], [1.0, 0.0])
