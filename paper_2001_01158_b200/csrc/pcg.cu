@@ -72,6 +72,7 @@ struct PcgArgs {
   int spg;
   int vec2;                     // flat double2 update pass (G = 1, no list, aligned)
   int tma;                      // pass A values staged by TMA (G = 1, no list, stencil layout)
+  int lazyx;                    // (vec2 solves) x is updated every second iteration: see pass B
   int cluster;                  // launched as ONE thread-block cluster (small G = 1 systems): cluster
                                 // barriers and DSMEM partial exchange instead of the global grid barrier
   int teams;                    // > 0 (G > 1): the CTAs form `teams` contiguous teams; team t solves segments
@@ -82,6 +83,8 @@ struct PcgArgs {
 struct SegState {
   int mode, par, it, final_;
   double rho, alpha, beta, tgt, nb;
+  int pend, pbuf;               // lazy x (P.lazyx): x lacks palpha * p[pbuf] (p0 / p1) while pend
+  double palpha;
 };
 
 __device__ __forceinline__ void slice_map(const PcgArgs& P, int64_t s, int& g, int64_t& row0, int64_t& end) {
@@ -175,7 +178,8 @@ __device__ __forceinline__ double row_dot(const SellView& A, int64_t pl, int w, 
 template <int WM, int ST, int MODE>
 __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_t jlim, int64_t jstep, int lane,
                                             bool init, double beta, const double* __restrict__ pold,
-                                            double* __restrict__ pnew, double& a0, double& a1, int gk = -1) {
+                                            double* __restrict__ pnew, double& a0, double& a1, int gk = -1,
+                                            const double* __restrict__ xp = nullptr, double xa = 0.0) {
   const SellView& A = P.A;
   // (gk >= 0: every slice belongs to segment gk)
   // the slice list entry and the row's Omega flag are loaded one slice ahead (masked solves walk a list of
@@ -210,7 +214,8 @@ __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_
     const bool in = !P.omega || om_cur != 255;
     if (MODE == 0) {
       const double* xx = P.x;
-      double acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return xx[c]; }, &own);
+      double acc = xp ? row_dot<WM, ST>(A, pl, w, u, [&](int c) { return __fma_rn(xa, xp[c], xx[c]); }, &own)
+                      : row_dot<WM, ST>(A, pl, w, u, [&](int c) { return xx[c]; }, &own);
       if (in) {
         double bi = P.b[u];
         double ri = bi - acc;
@@ -273,7 +278,7 @@ template <int WM, int ST, int MODE>
 __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64_t* bars, int64_t bid, int64_t nCTA,
                                            int warp, int lane, bool init, double beta,
                                            const double* __restrict__ pold, double* __restrict__ pnew, double& a0,
-                                           double& a1) {
+                                           double& a1, const double* __restrict__ xp = nullptr, double xa = 0.0) {
   const SellView& A = P.A;
   constexpr int W = WM > 0 ? WM : 1;
   const int vw = A.vw;
@@ -340,7 +345,7 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
         } else {
           v[k] = sp[32 * k];
         }
-        if (MODE == 0) y[k] = P.x[cc];
+        if (MODE == 0) y[k] = xp ? __fma_rn(xa, xp[cc], P.x[cc]) : P.x[cc];   // (x with its pending update)
         else if (MODE == 1) y[k] = P.z[cc];
         else y[k] = __fma_rn(beta, pold[cc], P.z[cc]);
       }
@@ -410,6 +415,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   if (threadIdx.x < kMaxSeg) {
     S[threadIdx.x].mode = M_INIT; S[threadIdx.x].par = 0; S[threadIdx.x].it = 0; S[threadIdx.x].final_ = 0;
     S[threadIdx.x].beta = 0.0; S[threadIdx.x].alpha = 0.0; S[threadIdx.x].rho = 0.0;
+    S[threadIdx.x].pend = 0; S[threadIdx.x].pbuf = 0; S[threadIdx.x].palpha = 0.0;
   }
   __syncthreads();
 
@@ -527,6 +533,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
     if (threadIdx.x == 0) {
       S[0].mode = M_INIT; S[0].par = 0; S[0].it = 0; S[0].final_ = 0;
       S[0].beta = 0.0; S[0].alpha = 0.0; S[0].rho = 0.0;
+      S[0].pend = 0; S[0].pbuf = 0; S[0].palpha = 0.0;
     }
     __syncthreads();
   }
@@ -541,15 +548,20 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       const double beta = S[0].beta;
       const double* pold = S[0].par ? P.p1 : P.p0;
       double* pnew = S[0].par ? P.p0 : P.p1;
+      // lazy x: a CONFIRM pass gathers x with its pending update (x itself is completed by the next pass B)
+      const double* xp = (KIND == 0 && S[0].pend) ? (S[0].pbuf ? P.p1 : P.p0) : nullptr;
+      const double xa = S[0].palpha;
       if (KIND == 0 && ST && WM > 0 && P.tma) {
         if (mode == M_INIT || mode == M_CONFIRM)
-          pass_a_tma<WM, ST, 0>(P, dsm, s_bars, bid, nCTA, warp, lane, mode == M_INIT, beta, pold, pnew, a0, a1);
+          pass_a_tma<WM, ST, 0>(P, dsm, s_bars, bid, nCTA, warp, lane, mode == M_INIT, beta, pold, pnew, a0, a1, xp,
+                                xa);
         else if (mode == M_FIRST)
           pass_a_tma<WM, ST, 1>(P, dsm, s_bars, bid, nCTA, warp, lane, false, beta, pold, pnew, a0, a1);
         else if (mode == M_NORMAL)
           pass_a_tma<WM, ST, 2>(P, dsm, s_bars, bid, nCTA, warp, lane, false, beta, pold, pnew, a0, a1);
       } else if (mode == M_INIT || mode == M_CONFIRM)
-        pass_a_loop<WM, ST, 0>(P, j0, jlim, jstep, lane, mode == M_INIT, beta, pold, pnew, a0, a1, TEAM ? gseg : -1);
+        pass_a_loop<WM, ST, 0>(P, j0, jlim, jstep, lane, mode == M_INIT, beta, pold, pnew, a0, a1, TEAM ? gseg : -1,
+                               xp, xa);
       else if (mode == M_FIRST)
         pass_a_loop<WM, ST, 1>(P, j0, jlim, jstep, lane, false, beta, pold, pnew, a0, a1, TEAM ? gseg : -1);
       else if (mode == M_NORMAL)
@@ -658,7 +670,51 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
         const double2* d2 = reinterpret_cast<const double2*>(A.dinv);
         const int64_t n = A.nunits, npair = n >> 1;
         const int64_t gt = bid * kPT + threadIdx.x, gs = nCTA * kPT;
-        if (mode == M_UPDATE) {
+        // lazy x: every second UPDATE skips x (it stays x_{k-1} + pending alpha_k p_k: 40 instead of 64 B per
+        // row), the next one applies both, x = fma(alpha_k+1, p_k+1, fma(alpha_k, p_k, x)): the same roundings as
+        // two updates; a RESET applies a pending update, and so does the exit
+        const int pend = S[0].pend;
+        const double pa = S[0].palpha;
+        const double2* pq2 = reinterpret_cast<const double2*>(S[0].pbuf ? P.p1 : P.p0);
+        if (mode == M_UPDATE && P.lazyx && !pend) {
+#pragma unroll 2
+          for (int64_t i = gt; i < npair; i += gs) {
+            double2 rv = r2[i], qv = q2[i], dv = d2[i];
+            rv.x = __fma_rn(-alpha, qv.x, rv.x); rv.y = __fma_rn(-alpha, qv.y, rv.y);
+            double2 zv = make_double2(rv.x * dv.x, rv.y * dv.y);
+            r2[i] = rv; z2[i] = zv;
+            a0 = __fma_rn(rv.x, zv.x, a0); a0 = __fma_rn(rv.y, zv.y, a0);
+            a1 = __fma_rn(rv.x, rv.x, a1); a1 = __fma_rn(rv.y, rv.y, a1);
+          }
+          if ((n & 1) && gt == 0) {
+            int64_t u = n - 1;
+            double ri = __fma_rn(-alpha, P.q[u], P.r[u]);
+            double zi = ri * A.dinv[u];
+            P.r[u] = ri; P.z[u] = zi;
+            a0 = __fma_rn(ri, zi, a0); a1 = __fma_rn(ri, ri, a1);
+          }
+        } else if (mode == M_UPDATE && pend) {
+#pragma unroll 2
+          for (int64_t i = gt; i < npair; i += gs) {
+            double2 xv = x2[i], ov = pq2[i], pv = pp[i], rv = r2[i], qv = q2[i], dv = d2[i];
+            xv.x = __fma_rn(alpha, pv.x, __fma_rn(pa, ov.x, xv.x)); xv.y = __fma_rn(alpha, pv.y, __fma_rn(pa, ov.y, xv.y));
+            rv.x = __fma_rn(-alpha, qv.x, rv.x); rv.y = __fma_rn(-alpha, qv.y, rv.y);
+            double2 zv = make_double2(rv.x * dv.x, rv.y * dv.y);
+            x2[i] = xv; r2[i] = rv; z2[i] = zv;
+            a0 = __fma_rn(rv.x, zv.x, a0); a0 = __fma_rn(rv.y, zv.y, a0);
+            a1 = __fma_rn(rv.x, rv.x, a1); a1 = __fma_rn(rv.y, rv.y, a1);
+          }
+          if ((n & 1) && gt == 0) {
+            const double* p1 = S[0].par ? P.p1 : P.p0;
+            const double* po = S[0].pbuf ? P.p1 : P.p0;
+            int64_t u = n - 1;
+            double xi = __fma_rn(alpha, p1[u], __fma_rn(pa, po[u], P.x[u]));
+            double ri = __fma_rn(-alpha, P.q[u], P.r[u]);
+            double zi = ri * A.dinv[u];
+            P.x[u] = xi; P.r[u] = ri; P.z[u] = zi;
+            a0 = __fma_rn(ri, zi, a0); a1 = __fma_rn(ri, ri, a1);
+          }
+        } else if (mode == M_UPDATE) {
 #pragma unroll 2
           for (int64_t i = gt; i < npair; i += gs) {
             double2 xv = x2[i], pv = pp[i], rv = r2[i], qv = q2[i], dv = d2[i];
@@ -685,12 +741,18 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
             double2 zv = make_double2(rv.x * dv.x, rv.y * dv.y);
             z2[i] = zv;
             a0 = __fma_rn(rv.x, zv.x, a0); a0 = __fma_rn(rv.y, zv.y, a0);
+            if (pend) {
+              double2 xv = x2[i], ov = pq2[i];
+              xv.x = __fma_rn(pa, ov.x, xv.x); xv.y = __fma_rn(pa, ov.y, xv.y);
+              x2[i] = xv;
+            }
           }
           if ((n & 1) && gt == 0) {
             int64_t u = n - 1;
             double zi = P.r[u] * A.dinv[u];
             P.z[u] = zi;
             a0 = __fma_rn(P.r[u], zi, a0);
+            if (pend) P.x[u] = __fma_rn(pa, (S[0].pbuf ? P.p1 : P.p0)[u], P.x[u]);
           }
         }
       }
@@ -758,6 +820,10 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       double s0 = s_sum[g][0], s1 = s_sum[g][1];
       if (T.mode == M_UPDATE) {
         T.it += 1;
+        if (KIND == 0 && P.lazyx) {               // the update just done left alpha p pending / applied both
+          if (T.pend) T.pend = 0;
+          else { T.pend = 1; T.pbuf = T.par; T.palpha = T.alpha; }
+        }
         double rz = s0, rr = s1;
         if (!isfinite(rr) || sqrt(rr) <= T.tgt || T.it >= P.max_iters) {
           T.mode = M_CONFIRM;
@@ -770,11 +836,24 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       } else if (T.mode == M_RESET) {
         T.rho = s0;
         T.mode = M_FIRST;
+        T.pend = 0;                               // (the RESET pass applied a pending x update)
       }
       active += (T.mode != M_DONE);
     }
     if (!__syncthreads_or(active)) break;
   }
+  if (KIND == 0 && S[0].pend) {
+    // lazy x: the last update is still pending (the solve ended after a CONFIRM or a breakdown); apply it and
+    // do a8 in the same loop (every row is completed and scattered by the same thread)
+    const double* po = S[0].pbuf ? P.p1 : P.p0;
+    const double pa = S[0].palpha;
+    for (int64_t u = bid * kPT + threadIdx.x; u < A.nunits; u += nCTA * kPT) {
+      const double xi = __fma_rn(pa, po[u], P.x[u]);
+      P.x[u] = xi;
+      if (P.scatter_idx) P.x_full[P.scatter_idx[u]] = xi;
+      else if (P.x_user && in_omega(u)) P.x_user[u] = xi;
+    }
+  } else
   // a8: x~[Omega] = xbar_B (Eq. 4), fused into the local solve's exit
   if (P.scatter_idx || P.x_user) {
     for (int64_t j = j0; j < jlim; j += jstep) {
@@ -915,6 +994,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   a.vec2 = (G == 1 && !job.slist &&
             ((((uintptr_t)a.x) | ((uintptr_t)a.r) | ((uintptr_t)a.z) | ((uintptr_t)a.q) | ((uintptr_t)a.p0) |
               ((uintptr_t)a.p1) | ((uintptr_t)M.dinv)) & 15) == 0) ? 1 : 0;
+  a.lazyx = (kind == 0 && a.vec2 && getenv("LC_NO_LAZY_X") == nullptr) ? 1 : 0;
   if (e == cudaSuccess) e = cudaMemsetAsync(a.bar, 0, sizeof(GridBar), s);
   if (e == cudaSuccess && teams) e = cudaMemsetAsync(a.tctr, 0, 128 * (size_t)teams, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(a.out_iters, 0, 8 * G, s);

@@ -1,5 +1,6 @@
-# quick A/B: GPU tests, config 3 global solve device time, config 5 and 3 bench lines
+# quick A/B: GPU tests, config 5 global solve (lazy x vs not), config 5 and 2 bench lines
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/t_pytest.log 2>&1; echo PYTEST_EXIT $? >> gpurun_out/t_pytest.log
-python tools/c3_ideal.py 3 > gpurun_out/t_c3_3.json 2>&1
+timeout 300 python tools/time_pcg.py 5 2 > gpurun_out/t_pcg_c5.txt 2>&1
+LC_NO_LAZY_X=1 timeout 300 python tools/time_pcg.py 5 2 > gpurun_out/t_pcg_c5_nolazy.txt 2>&1
 timeout 600 python bench.py --no-cpu-baseline > gpurun_out/t_bench_c5.log 2>&1
-timeout 600 python bench.py --config 3 --no-cpu-baseline > gpurun_out/t_bench_c3.log 2>&1
+timeout 600 python bench.py --config 2 --no-cpu-baseline > gpurun_out/t_bench_c2.log 2>&1
