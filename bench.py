@@ -226,10 +226,11 @@ def run_lc(args):
         mat_bytes, rule = 8.0 * nnz, "8 B/nnz stencil values"
     else:
         mat_bytes, rule = 12.0 * nnz, "12 B/nnz SELL values + columns"
-    # matrix once + pass A 32 B/row + pass B 64 B/row; single-segment solves update x every second
-    # iteration (lazy x: pass B 40 / 72 B/row alternately, 56 on average)
-    lazy = solver == "pcg" and sy0.batch == 1 and not os.environ.get("LC_NO_LAZY_X")
-    vec_bytes = 88.0 if lazy else 96.0
+    # matrix once + pass A 32 B/row + pass B 64 B/row; single-segment solves update x every L-th
+    # iteration (lazy x of depth L = 3: pass B 40, 40, 80 B/row, i.e. (40 (L - 1) + 56 + 8 L) / L on average)
+    L = int(os.environ.get("LC_LAZY_X_DEPTH", "3"))
+    lazy = solver == "pcg" and sy0.batch == 1 and not os.environ.get("LC_NO_LAZY_X") and L > 1
+    vec_bytes = 32.0 + (40.0 * (L - 1) + 56.0 + 8.0 * L) / L if lazy else 96.0
     it_bytes = mat_bytes + vec_bytes * N
     try:
         trafficdb = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -293,7 +294,7 @@ def run_lc(args):
                 "traffic": tr, "algorithmic_bytes_per_launch": int(pcg_bytes / max(nlaunch, 1)),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650",
                 "layout": Ainfo["layout"],
-                "bytes_rule": (f"{rule} + {vec_bytes:.0f} B/row vectors per PCG iteration" if solver == "pcg"
+                "bytes_rule": (f"{rule} + {vec_bytes:.2f} B/row vectors per PCG iteration" if solver == "pcg"
                                else "8 B/nnz + 80 B/unknown + 16 (j+1) B/unknown per Arnoldi step j")}
 
     # ---- the FP64 SpMV alone (BASELINE metric "SpMV HBM GB/s"): lc_spmv y = A x on the last system,

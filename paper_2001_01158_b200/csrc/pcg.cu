@@ -51,6 +51,8 @@ struct PcgArgs {
   double* q;
   double* p0;
   double* p1;
+  double* p2;                   // third search-direction buffer (np3: lazy x of depth 3)
+  int np3;                      // 1: p rotates over p0, p1, p2; 0: over p0, p1
   double* part;                 // [nCTA][G][2]
   double* red;                  // [G][2]  (G > 1)
   double* subred;               // [2][kBarSub][G][2]  (G > 1: per-sub-group sums, double-buffered)
@@ -72,7 +74,7 @@ struct PcgArgs {
   int spg;
   int vec2;                     // flat double2 update pass (G = 1, no list, aligned)
   int tma;                      // pass A values staged by TMA (G = 1, no list, stencil layout)
-  int lazyx;                    // (vec2 solves) x is updated every second iteration: see pass B
+  int lazyx;                    // (vec2 solves) x is updated every lazyx-th iteration (0: every one): pass B
   int cluster;                  // launched as ONE thread-block cluster (small G = 1 systems): cluster
                                 // barriers and DSMEM partial exchange instead of the global grid barrier
   int teams;                    // > 0 (G > 1): the CTAs form `teams` contiguous teams; team t solves segments
@@ -83,8 +85,8 @@ struct PcgArgs {
 struct SegState {
   int mode, par, it, final_;
   double rho, alpha, beta, tgt, nb;
-  int pend, pbuf;               // lazy x (P.lazyx): x lacks palpha * p[pbuf] (p0 / p1) while pend
-  double palpha;
+  int pend, pbuf, pbuf2;        // lazy x (P.lazyx): x lacks palpha p[pbuf] (pend >= 1), then palpha2 p[pbuf2]
+  double palpha, palpha2;       // (pend = 2), p[i] = p0 / p1 / p2
 };
 
 __device__ __forceinline__ void slice_map(const PcgArgs& P, int64_t s, int& g, int64_t& row0, int64_t& end) {
@@ -102,6 +104,10 @@ __device__ __forceinline__ void slice_map(const PcgArgs& P, int64_t s, int& g, i
     end = P.A.seg_unit0[g + 1];
   }
 }
+
+// search-direction buffer i and its successor in the rotation
+__device__ __forceinline__ double* pvec(const PcgArgs& P, int i) { return i == 0 ? P.p0 : (i == 1 ? P.p1 : P.p2); }
+__device__ __forceinline__ int pnext(const PcgArgs& P, int i) { return P.np3 ? (i == 2 ? 0 : i + 1) : (i ^ 1); }
 
 // slice_map for a slice whose segment g is already known (the batched loops know it from the active-run
 // table): no 64-bit division by the slices per segment on the path to the slice's loads
@@ -179,7 +185,8 @@ template <int WM, int ST, int MODE>
 __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_t jlim, int64_t jstep, int lane,
                                             bool init, double beta, const double* __restrict__ pold,
                                             double* __restrict__ pnew, double& a0, double& a1, int gk = -1,
-                                            const double* __restrict__ xp = nullptr, double xa = 0.0) {
+                                            const double* __restrict__ xp = nullptr, double xa = 0.0,
+                                            const double* __restrict__ xp2 = nullptr, double xa2 = 0.0) {
   const SellView& A = P.A;
   // (gk >= 0: every slice belongs to segment gk)
   // the slice list entry and the row's Omega flag are loaded one slice ahead (masked solves walk a list of
@@ -214,7 +221,9 @@ __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_
     const bool in = !P.omega || om_cur != 255;
     if (MODE == 0) {
       const double* xx = P.x;
-      double acc = xp ? row_dot<WM, ST>(A, pl, w, u, [&](int c) { return __fma_rn(xa, xp[c], xx[c]); }, &own)
+      double acc = xp ? row_dot<WM, ST>(A, pl, w, u, [&](int c) {
+                          const double t = __fma_rn(xa, xp[c], xx[c]);
+                          return xp2 ? __fma_rn(xa2, xp2[c], t) : t; }, &own)
                       : row_dot<WM, ST>(A, pl, w, u, [&](int c) { return xx[c]; }, &own);
       if (in) {
         double bi = P.b[u];
@@ -278,7 +287,8 @@ template <int WM, int ST, int MODE>
 __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64_t* bars, int64_t bid, int64_t nCTA,
                                            int warp, int lane, bool init, double beta,
                                            const double* __restrict__ pold, double* __restrict__ pnew, double& a0,
-                                           double& a1, const double* __restrict__ xp = nullptr, double xa = 0.0) {
+                                           double& a1, const double* __restrict__ xp = nullptr, double xa = 0.0,
+                                           const double* __restrict__ xp2 = nullptr, double xa2 = 0.0) {
   const SellView& A = P.A;
   constexpr int W = WM > 0 ? WM : 1;
   const int vw = A.vw;
@@ -345,7 +355,11 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
         } else {
           v[k] = sp[32 * k];
         }
-        if (MODE == 0) y[k] = xp ? __fma_rn(xa, xp[cc], P.x[cc]) : P.x[cc];   // (x with its pending update)
+        if (MODE == 0) {                                            // (x with its pending updates)
+          y[k] = P.x[cc];
+          if (xp) y[k] = __fma_rn(xa, xp[cc], y[k]);
+          if (xp2) y[k] = __fma_rn(xa2, xp2[cc], y[k]);
+        }
         else if (MODE == 1) y[k] = P.z[cc];
         else y[k] = __fma_rn(beta, pold[cc], P.z[cc]);
       }
@@ -416,6 +430,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
     S[threadIdx.x].mode = M_INIT; S[threadIdx.x].par = 0; S[threadIdx.x].it = 0; S[threadIdx.x].final_ = 0;
     S[threadIdx.x].beta = 0.0; S[threadIdx.x].alpha = 0.0; S[threadIdx.x].rho = 0.0;
     S[threadIdx.x].pend = 0; S[threadIdx.x].pbuf = 0; S[threadIdx.x].palpha = 0.0;
+    S[threadIdx.x].pbuf2 = 0; S[threadIdx.x].palpha2 = 0.0;
   }
   __syncthreads();
 
@@ -533,7 +548,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
     if (threadIdx.x == 0) {
       S[0].mode = M_INIT; S[0].par = 0; S[0].it = 0; S[0].final_ = 0;
       S[0].beta = 0.0; S[0].alpha = 0.0; S[0].rho = 0.0;
-      S[0].pend = 0; S[0].pbuf = 0; S[0].palpha = 0.0;
+      S[0].pend = 0; S[0].pbuf = 0; S[0].palpha = 0.0; S[0].pbuf2 = 0; S[0].palpha2 = 0.0;
     }
     __syncthreads();
   }
@@ -546,22 +561,23 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       const int mode = S[0].mode;
       double a0 = 0.0, a1 = 0.0;
       const double beta = S[0].beta;
-      const double* pold = S[0].par ? P.p1 : P.p0;
-      double* pnew = S[0].par ? P.p0 : P.p1;
-      // lazy x: a CONFIRM pass gathers x with its pending update (x itself is completed by the next pass B)
-      const double* xp = (KIND == 0 && S[0].pend) ? (S[0].pbuf ? P.p1 : P.p0) : nullptr;
-      const double xa = S[0].palpha;
+      const double* pold = pvec(P, S[0].par);
+      double* pnew = pvec(P, pnext(P, S[0].par));
+      // lazy x: a CONFIRM pass gathers x with its pending updates (x itself is completed by the next pass B)
+      const double* xp = (KIND == 0 && S[0].pend >= 1) ? pvec(P, S[0].pbuf) : nullptr;
+      const double* xp2 = (KIND == 0 && S[0].pend >= 2) ? pvec(P, S[0].pbuf2) : nullptr;
+      const double xa = S[0].palpha, xa2 = S[0].palpha2;
       if (KIND == 0 && ST && WM > 0 && P.tma) {
         if (mode == M_INIT || mode == M_CONFIRM)
           pass_a_tma<WM, ST, 0>(P, dsm, s_bars, bid, nCTA, warp, lane, mode == M_INIT, beta, pold, pnew, a0, a1, xp,
-                                xa);
+                                xa, xp2, xa2);
         else if (mode == M_FIRST)
           pass_a_tma<WM, ST, 1>(P, dsm, s_bars, bid, nCTA, warp, lane, false, beta, pold, pnew, a0, a1);
         else if (mode == M_NORMAL)
           pass_a_tma<WM, ST, 2>(P, dsm, s_bars, bid, nCTA, warp, lane, false, beta, pold, pnew, a0, a1);
       } else if (mode == M_INIT || mode == M_CONFIRM)
         pass_a_loop<WM, ST, 0>(P, j0, jlim, jstep, lane, mode == M_INIT, beta, pold, pnew, a0, a1, TEAM ? gseg : -1,
-                               xp, xa);
+                               xp, xa, xp2, xa2);
       else if (mode == M_FIRST)
         pass_a_loop<WM, ST, 1>(P, j0, jlim, jstep, lane, false, beta, pold, pnew, a0, a1, TEAM ? gseg : -1);
       else if (mode == M_NORMAL)
@@ -642,7 +658,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       } else if (T.mode == M_FIRST || T.mode == M_NORMAL) {
         double pq = s0;
         if (!(pq > 0)) finish(g, isfinite(pq) ? LC_ERR_BREAKDOWN : LC_ERR_NONFINITE, NAN);
-        else { T.alpha = T.rho / pq; T.mode = M_UPDATE; T.par ^= 1; }
+        else { T.alpha = T.rho / pq; T.mode = M_UPDATE; T.par = pnext(P, T.par); }
       } else if (T.mode == M_CONFIRM) {
         double rn = sqrt(s0);
         if (!isfinite(rn)) finish(g, LC_ERR_NONFINITE, rn);
@@ -662,7 +678,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       double a0 = 0.0, a1 = 0.0;
       if (mode == M_UPDATE || mode == M_RESET) {
         const double alpha = S[0].alpha;
-        const double2* pp = reinterpret_cast<const double2*>(S[0].par ? P.p1 : P.p0);
+        const double2* pp = reinterpret_cast<const double2*>(pvec(P, S[0].par));
         double2* x2 = reinterpret_cast<double2*>(P.x);
         double2* r2 = reinterpret_cast<double2*>(P.r);
         double2* z2 = reinterpret_cast<double2*>(P.z);
@@ -670,13 +686,15 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
         const double2* d2 = reinterpret_cast<const double2*>(A.dinv);
         const int64_t n = A.nunits, npair = n >> 1;
         const int64_t gt = bid * kPT + threadIdx.x, gs = nCTA * kPT;
-        // lazy x: every second UPDATE skips x (it stays x_{k-1} + pending alpha_k p_k: 40 instead of 64 B per
-        // row), the next one applies both, x = fma(alpha_k+1, p_k+1, fma(alpha_k, p_k, x)): the same roundings as
-        // two updates; a RESET applies a pending update, and so does the exit
+        // lazy x (depth L = P.lazyx): L - 1 UPDATE passes leave x alone (r, z only: 40 instead of 64 B per row;
+        // x lacks the pending alpha_i p_i), the L-th applies them all in order, x = fma(alpha_k, p_k, fma(...,
+        // fma(alpha_k-L+1, p_k-L+1, x))): the same roundings as updating every pass.  p_k-L+1 .. p_k survive until
+        // then (L = 3 rotates p over three buffers).  A RESET applies the pending updates, and so does the exit.
         const int pend = S[0].pend;
-        const double pa = S[0].palpha;
-        const double2* pq2 = reinterpret_cast<const double2*>(S[0].pbuf ? P.p1 : P.p0);
-        if (mode == M_UPDATE && P.lazyx && !pend) {
+        const double pa = S[0].palpha, pa2 = S[0].palpha2;
+        const double2* t1 = reinterpret_cast<const double2*>(pvec(P, S[0].pbuf));
+        const double2* t2 = reinterpret_cast<const double2*>(pvec(P, S[0].pbuf2));
+        if (mode == M_UPDATE && P.lazyx && pend < P.lazyx - 1) {
 #pragma unroll 2
           for (int64_t i = gt; i < npair; i += gs) {
             double2 rv = r2[i], qv = q2[i], dv = d2[i];
@@ -693,10 +711,31 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
             P.r[u] = ri; P.z[u] = zi;
             a0 = __fma_rn(ri, zi, a0); a1 = __fma_rn(ri, ri, a1);
           }
-        } else if (mode == M_UPDATE && pend) {
+        } else if (mode == M_UPDATE && pend == 2) {
 #pragma unroll 2
           for (int64_t i = gt; i < npair; i += gs) {
-            double2 xv = x2[i], ov = pq2[i], pv = pp[i], rv = r2[i], qv = q2[i], dv = d2[i];
+            double2 xv = x2[i], ov = t1[i], ov2 = t2[i], pv = pp[i], rv = r2[i], qv = q2[i], dv = d2[i];
+            xv.x = __fma_rn(alpha, pv.x, __fma_rn(pa2, ov2.x, __fma_rn(pa, ov.x, xv.x)));
+            xv.y = __fma_rn(alpha, pv.y, __fma_rn(pa2, ov2.y, __fma_rn(pa, ov.y, xv.y)));
+            rv.x = __fma_rn(-alpha, qv.x, rv.x); rv.y = __fma_rn(-alpha, qv.y, rv.y);
+            double2 zv = make_double2(rv.x * dv.x, rv.y * dv.y);
+            x2[i] = xv; r2[i] = rv; z2[i] = zv;
+            a0 = __fma_rn(rv.x, zv.x, a0); a0 = __fma_rn(rv.y, zv.y, a0);
+            a1 = __fma_rn(rv.x, rv.x, a1); a1 = __fma_rn(rv.y, rv.y, a1);
+          }
+          if ((n & 1) && gt == 0) {
+            int64_t u = n - 1;
+            double xi = __fma_rn(alpha, pvec(P, S[0].par)[u],
+                                 __fma_rn(pa2, pvec(P, S[0].pbuf2)[u], __fma_rn(pa, pvec(P, S[0].pbuf)[u], P.x[u])));
+            double ri = __fma_rn(-alpha, P.q[u], P.r[u]);
+            double zi = ri * A.dinv[u];
+            P.x[u] = xi; P.r[u] = ri; P.z[u] = zi;
+            a0 = __fma_rn(ri, zi, a0); a1 = __fma_rn(ri, ri, a1);
+          }
+        } else if (mode == M_UPDATE && pend == 1) {
+#pragma unroll 2
+          for (int64_t i = gt; i < npair; i += gs) {
+            double2 xv = x2[i], ov = t1[i], pv = pp[i], rv = r2[i], qv = q2[i], dv = d2[i];
             xv.x = __fma_rn(alpha, pv.x, __fma_rn(pa, ov.x, xv.x)); xv.y = __fma_rn(alpha, pv.y, __fma_rn(pa, ov.y, xv.y));
             rv.x = __fma_rn(-alpha, qv.x, rv.x); rv.y = __fma_rn(-alpha, qv.y, rv.y);
             double2 zv = make_double2(rv.x * dv.x, rv.y * dv.y);
@@ -705,10 +744,8 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
             a1 = __fma_rn(rv.x, rv.x, a1); a1 = __fma_rn(rv.y, rv.y, a1);
           }
           if ((n & 1) && gt == 0) {
-            const double* p1 = S[0].par ? P.p1 : P.p0;
-            const double* po = S[0].pbuf ? P.p1 : P.p0;
             int64_t u = n - 1;
-            double xi = __fma_rn(alpha, p1[u], __fma_rn(pa, po[u], P.x[u]));
+            double xi = __fma_rn(alpha, pvec(P, S[0].par)[u], __fma_rn(pa, pvec(P, S[0].pbuf)[u], P.x[u]));
             double ri = __fma_rn(-alpha, P.q[u], P.r[u]);
             double zi = ri * A.dinv[u];
             P.x[u] = xi; P.r[u] = ri; P.z[u] = zi;
@@ -726,9 +763,8 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
             a1 = __fma_rn(rv.x, rv.x, a1); a1 = __fma_rn(rv.y, rv.y, a1);
           }
           if ((n & 1) && gt == 0) {
-            const double* p1 = S[0].par ? P.p1 : P.p0;
             int64_t u = n - 1;
-            double xi = __fma_rn(alpha, p1[u], P.x[u]);
+            double xi = __fma_rn(alpha, pvec(P, S[0].par)[u], P.x[u]);
             double ri = __fma_rn(-alpha, P.q[u], P.r[u]);
             double zi = ri * A.dinv[u];
             P.x[u] = xi; P.r[u] = ri; P.z[u] = zi;
@@ -742,8 +778,12 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
             z2[i] = zv;
             a0 = __fma_rn(rv.x, zv.x, a0); a0 = __fma_rn(rv.y, zv.y, a0);
             if (pend) {
-              double2 xv = x2[i], ov = pq2[i];
+              double2 xv = x2[i], ov = t1[i];
               xv.x = __fma_rn(pa, ov.x, xv.x); xv.y = __fma_rn(pa, ov.y, xv.y);
+              if (pend == 2) {
+                const double2 ov2 = t2[i];
+                xv.x = __fma_rn(pa2, ov2.x, xv.x); xv.y = __fma_rn(pa2, ov2.y, xv.y);
+              }
               x2[i] = xv;
             }
           }
@@ -752,7 +792,11 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
             double zi = P.r[u] * A.dinv[u];
             P.z[u] = zi;
             a0 = __fma_rn(P.r[u], zi, a0);
-            if (pend) P.x[u] = __fma_rn(pa, (S[0].pbuf ? P.p1 : P.p0)[u], P.x[u]);
+            if (pend) {
+              double xi = __fma_rn(pa, pvec(P, S[0].pbuf)[u], P.x[u]);
+              if (pend == 2) xi = __fma_rn(pa2, pvec(P, S[0].pbuf2)[u], xi);
+              P.x[u] = xi;
+            }
           }
         }
       }
@@ -821,8 +865,9 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
       if (T.mode == M_UPDATE) {
         T.it += 1;
         if (KIND == 0 && P.lazyx) {               // the update just done left alpha p pending / applied both
-          if (T.pend) T.pend = 0;
-          else { T.pend = 1; T.pbuf = T.par; T.palpha = T.alpha; }
+          if (T.pend == P.lazyx - 1) T.pend = 0;
+          else if (T.pend == 0) { T.pend = 1; T.pbuf = T.par; T.palpha = T.alpha; }
+          else { T.pend = 2; T.pbuf2 = T.par; T.palpha2 = T.alpha; }
         }
         double rz = s0, rr = s1;
         if (!isfinite(rr) || sqrt(rr) <= T.tgt || T.it >= P.max_iters) {
@@ -845,10 +890,13 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
   if (KIND == 0 && S[0].pend) {
     // lazy x: the last update is still pending (the solve ended after a CONFIRM or a breakdown); apply it and
     // do a8 in the same loop (every row is completed and scattered by the same thread)
-    const double* po = S[0].pbuf ? P.p1 : P.p0;
-    const double pa = S[0].palpha;
+    const double* po = pvec(P, S[0].pbuf);
+    const double* po2 = pvec(P, S[0].pbuf2);
+    const double pa = S[0].palpha, pa2 = S[0].palpha2;
+    const bool two = S[0].pend == 2;
     for (int64_t u = bid * kPT + threadIdx.x; u < A.nunits; u += nCTA * kPT) {
-      const double xi = __fma_rn(pa, po[u], P.x[u]);
+      double xi = __fma_rn(pa, po[u], P.x[u]);
+      if (two) xi = __fma_rn(pa2, po2[u], xi);
       P.x[u] = xi;
       if (P.scatter_idx) P.x_full[P.scatter_idx[u]] = xi;
       else if (P.x_user && in_omega(u)) P.x_user[u] = xi;
@@ -941,7 +989,8 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   const size_t vbytes = (vec + 255) & ~(size_t)255;
   const bool own_x = job.x_init != nullptr;
   const int teams = team_k ? (int)std::min<int64_t>(G, nCTA) : 0;
-  const size_t bytes = vbytes * (own_x ? 6 : 5) + sizeof(double) * 2 * G * (2 * nCTA + 1 + 2 * kBarSub) + 16 * G +
+  const int npv = G == 1 ? 3 : 2;                 // search-direction buffers (3: lazy x of depth 3 possible)
+  const size_t bytes = vbytes * (own_x ? 4 + npv : 3 + npv) + sizeof(double) * 2 * G * (2 * nCTA + 1 + 2 * kBarSub) + 16 * G +
                        sizeof(GridBar) + 640 + 128 * (size_t)kMaxSeg;
   lc_status st = dalloc(&ws, bytes, s);
   if (st) return st;
@@ -954,6 +1003,8 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   a.q = (double*)w; w += vbytes;
   a.p0 = (double*)w; w += vbytes;
   a.p1 = (double*)w; w += vbytes;
+  a.p2 = nullptr;
+  if (npv == 3) { a.p2 = (double*)w; w += vbytes; }
   cudaError_t e = cudaSuccess;
   if (own_x) {
     a.x = (double*)w; w += vbytes;
@@ -961,7 +1012,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   } else {
     a.x = job.x;
   }
-  if (job.omega && e == cudaSuccess) e = cudaMemsetAsync(a.r, 0, vbytes * 5, s);   // zero outside Omega
+  if (job.omega && e == cudaSuccess) e = cudaMemsetAsync(a.r, 0, vbytes * (3 + npv), s);   // zero outside Omega
   // batched (G > 1): a boundary row's stencil holes gather z / p of the neighbouring segment (times an exact 0),
   // which may not have been written yet (its team has not started it, or it converged at INIT): start them at 0
   if (G > 1 && !job.omega && e == cudaSuccess) e = cudaMemsetAsync(a.z, 0, vbytes, s);
@@ -993,8 +1044,14 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   // (masked solves qualify too: rows outside Omega hold p = q = r = z = 0 and x = 0, the update keeps them 0)
   a.vec2 = (G == 1 && !job.slist &&
             ((((uintptr_t)a.x) | ((uintptr_t)a.r) | ((uintptr_t)a.z) | ((uintptr_t)a.q) | ((uintptr_t)a.p0) |
-              ((uintptr_t)a.p1) | ((uintptr_t)M.dinv)) & 15) == 0) ? 1 : 0;
-  a.lazyx = (kind == 0 && a.vec2 && getenv("LC_NO_LAZY_X") == nullptr) ? 1 : 0;
+              ((uintptr_t)a.p1) | ((uintptr_t)a.p2) | ((uintptr_t)M.dinv)) & 15) == 0) ? 1 : 0;
+  // lazy x of depth 3 (LC_LAZY_X_DEPTH=2 or 3; LC_NO_LAZY_X=1: x updated every pass)
+  {
+    const char* dz = getenv("LC_LAZY_X_DEPTH");
+    const int depth = dz ? std::min(3, std::max(1, atoi(dz))) : 3;
+    a.lazyx = (kind == 0 && a.vec2 && getenv("LC_NO_LAZY_X") == nullptr && depth > 1) ? depth : 0;
+  }
+  a.np3 = a.lazyx == 3 ? 1 : 0;
   if (e == cudaSuccess) e = cudaMemsetAsync(a.bar, 0, sizeof(GridBar), s);
   if (e == cudaSuccess && teams) e = cudaMemsetAsync(a.tctr, 0, 128 * (size_t)teams, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(a.out_iters, 0, 8 * G, s);

@@ -274,6 +274,29 @@ def test_determinism_bitwise():
     assert [i["iterations"] for i in r1["global"]] == [i["iterations"] for i in r2["global"]]
 
 
+@pytest.mark.parametrize("lazy", ["3", "2", "off"])
+@pytest.mark.parametrize("cfg,n,s,rule", [(5, 33, 4, 0), (5, 30, 9, 1), (2, 100, 7, 0), (1, 64, 2, 0)])
+def test_lazy_x_depths_parity(cfg, n, s, rule, lazy, monkeypatch):
+    """The flat single-segment update pass with x updated every 3rd / 2nd / every iteration (lazy x, DESIGN s6)
+    on the grid-wide k_pcg: the same parity bars, and the solutions of the three variants bitwise equal (the
+    deferred updates apply the same fma roundings in the same order)."""
+    monkeypatch.setenv("LC_NO_DSMEM", "1")
+    monkeypatch.setenv("LC_NO_CLUSTER", "1")
+    if lazy == "off":
+        monkeypatch.setenv("LC_NO_LAZY_X", "1")
+    else:
+        monkeypatch.setenv("LC_LAZY_X_DEPTH", lazy)
+    sy = synth.system(cfg, s, n=n)
+    check_system(sy, RULES[cfg][rule])
+    A = gpu_matrix(sy)
+    x = to_dev(sy.x0)
+    lc.solve_global(A, to_dev(sy.b), x)
+    monkeypatch.setenv("LC_NO_LAZY_X", "1")
+    x_ref = to_dev(sy.x0)
+    lc.solve_global(A, to_dev(sy.b), x_ref)
+    assert torch.equal(x, x_ref)
+
+
 @pytest.mark.parametrize("path", ["grid", "lock", "team", "gmres"])
 def test_determinism_short_passes(path, monkeypatch):
     """Repeated solves with very short passes (tiny systems on the multi-CTA kernels, where a CTA leaving a
