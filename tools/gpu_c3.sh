@@ -1,4 +1,4 @@
-# batched lock step: config 3 global solve device time vs the TMA chunk threshold
-timeout 600 python -m pytest tests -m gpu -x -q -k "batched or determinism" > gpurun_out/t_pytest.log 2>&1; echo PYTEST_EXIT $? >> gpurun_out/t_pytest.log
-for th in 4 8 16 32; do echo "th$th 3 $(LC_TMA_BATCH_CHUNKS=$th timeout 300 python tools/c3_ideal.py 3 2>&1 | tail -1)" >> gpurun_out/t_c3_sched.txt; done
-echo "plain 3 $(LC_NO_TMA_BATCH=1 timeout 300 python tools/c3_ideal.py 3 2>&1 | tail -1)" >> gpurun_out/t_c3_sched.txt
+# batched lock step: parity tests, config 3 global solve device time, bench config 3
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/t_pytest.log 2>&1; echo PYTEST_EXIT $? >> gpurun_out/t_pytest.log
+for s in 3 10; do echo "lock $s $(timeout 300 python tools/c3_ideal.py $s 2>&1 | tail -1)" >> gpurun_out/t_c3_sched.txt; done
+timeout 600 python bench.py --config 3 --no-cpu-baseline > gpurun_out/t_bench_c3.log 2>&1
