@@ -2,7 +2,7 @@
 """Per-CTA pass timeline of k_pcg (debug build, tools/build_debug.sh): for 64 consecutive passes from pass0,
 every CTA's pass start / pass end / reduction-out times.  Prints, per pass, the pass-end spread (first to last
 CTA arrival), the barrier exit spread, and how late CTAs correlate with their index.
-usage: tl_cta.py build_dbg/liblc_dbg.so CONFIG PASS0 [n]"""
+usage: tl_cta.py build_dbg/liblc_dbg.so CONFIG PASS0 [n|0] [local]"""
 import ctypes
 import json
 import sys
@@ -16,18 +16,28 @@ from paper_2001_01158_b200 import lc  # noqa: E402
 
 lc.load_library(sys.argv[1])
 cfg, pass0 = int(sys.argv[2]), int(sys.argv[3])
-n = int(sys.argv[4]) if len(sys.argv) > 4 else None
+n = int(sys.argv[4]) if len(sys.argv) > 4 and int(sys.argv[4]) > 0 else None
 sy = synth.system(cfg, 3, n=n) if n else synth.system(cfg, 3)
 A = lc.Matrix(sy.nrows, sy.rp, sy.ci, sy.val, block=sy.block, batch=sy.batch)
 b = torch.from_numpy(sy.b).cuda()
 x = torch.from_numpy(sy.x0).cuda()
 lib = lc._lib
+local = len(sys.argv) > 5 and sys.argv[5] == "local"      # the method2 local solve (residual domain, E_max = 1)
+if local:
+    dom = lc.select_domain(A, b, x, criterion=0, threshold=0, param=1e-10, expand_rounds=1)
+    sub = lc.extract_sub(A, dom, b, x)
+    print(json.dumps(dict(K=dom.K)))
+
+
+def run():
+    xx = x.clone()
+    return lc.solve_local(sub, xx) if local else lc.solve_global(A, b, xx)
+
+
 lib.lc_debug_cta_window(ctypes.c_int(1 << 30))
-xx = x.clone()
-lc.solve_global(A, b, xx)
+run()
 lib.lc_debug_cta_window(ctypes.c_int(pass0))
-xx = x.clone()
-info = lc.solve_global(A, b, xx)
+info = run()
 buf = np.zeros(64 * 1024 * 3, dtype=np.uint64)
 lib.lc_debug_cta(ctypes.c_void_p(buf.ctypes.data))
 t = buf.reshape(64, 1024, 3).astype(np.int64)
