@@ -24,8 +24,17 @@ constexpr int kGT = 512;
 constexpr int kGW = kGT / 32;
 constexpr int kMaxM = 40;
 constexpr int kMaxQ = 2 * (kMaxM + 1) + 2;   // reduced quantities per phase
-constexpr int kCC = 2;                       // slices per warp chunk in the SpMV + dots pass (1: 83, 3: 84 us/step)
-constexpr int kIB = 4;                       // basis vectors per unrolled block of the dot / update loops
+#ifndef LC_GMRES_CC
+#define LC_GMRES_CC 2
+#endif
+constexpr int kCC = LC_GMRES_CC;             // slices per warp chunk in the SpMV + dots pass (with kIB = 2: 1: 78.2,
+                                             // 2: 69.0, 3: 81.3 us/step)
+#ifndef LC_GMRES_IB
+#define LC_GMRES_IB 1
+#endif
+// basis vectors per unrolled block of the dot / update loops: 1 (config 4 Arnoldi step 67.2 us) beats 2 (69.0),
+// 3 (69.1), 4 (72.3), 8 (81.0): the wider blocks' register arrays spill (tools/build_variant.sh A/B)
+constexpr int kIB = LC_GMRES_IB;
 
 struct GmresArgs {
   SellView A;
