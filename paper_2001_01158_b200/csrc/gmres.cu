@@ -20,7 +20,10 @@ namespace cg = cooperative_groups;
 
 namespace lc {
 
-constexpr int kGT = 512;
+#ifndef LC_GMRES_GT
+#define LC_GMRES_GT 512
+#endif
+constexpr int kGT = LC_GMRES_GT;             // threads per CTA (1024 / kGT CTAs per SM)
 constexpr int kGW = kGT / 32;
 constexpr int kMaxM = 40;
 constexpr int kMaxQ = 2 * (kMaxM + 1) + 2;   // reduced quantities per phase
@@ -77,7 +80,7 @@ __device__ unsigned long long g_tlg[16384];
 #endif
 
 template <int BS>
-__global__ void __launch_bounds__(kGT, 2) k_gmres(GmresArgs P) {
+__global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
   unsigned long long bar_epoch = 0;
 #ifdef LC_DEBUG_TIMELINE
   int tk = 0;
@@ -541,7 +544,7 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
     int per_sm = 0;
     LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGT, 0));
     if (per_sm < 1) { set_error("GMRES kernel does not fit on an SM"); return LC_ERR_CUDA; }
-    g_gm_ctas[ci] = std::min(per_sm, 2) * num_sms();
+    g_gm_ctas[ci] = std::min(per_sm, 1024 / kGT) * num_sms();
   }
   int64_t nCTA = std::min<int64_t>(g_gm_ctas[ci], (M.nslices + kGW - 1) / kGW);
   if (nCTA < 1) nCTA = 1;

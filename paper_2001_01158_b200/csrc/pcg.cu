@@ -282,7 +282,10 @@ __device__ __forceinline__ void cta_mark(int pc, int slot) {
 // interleaved order); thread 0 keeps kStages chunks in flight with cp.async.bulk into a shared-memory
 // ring (mbarrier complete_tx), the warps read their slice's values from shared memory, so the DRAM
 // stream no longer waits on each warp's gather latency.  Gathers and the symmetric mirrors stay loads.
-constexpr int kStages = 2;
+#ifndef LC_PCG_STAGES
+#define LC_PCG_STAGES 2
+#endif
+constexpr int kStages = LC_PCG_STAGES;
 template <int WM, int ST, int MODE>
 __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64_t* bars, int64_t bid, int64_t nCTA,
                                            int warp, int lane, bool init, double beta,
