@@ -36,7 +36,10 @@ namespace cg = cooperative_groups;
 
 namespace lc {
 
-constexpr int kPT = 256;             // threads per CTA
+#ifndef LC_PCG_PT
+#define LC_PCG_PT 256
+#endif
+constexpr int kPT = LC_PCG_PT;        // threads per CTA
 constexpr int kPW = kPT / 32;        // warps per CTA
 constexpr int kMaxSeg = 64;
 
@@ -275,7 +278,7 @@ __device__ __forceinline__ void cta_mark(int pc, int slot) {
 #define CT(pc, slot) (void)0
 #endif
 #ifndef LCV_MINB
-#define LCV_MINB 4
+#define LCV_MINB (1024 / LC_PCG_PT)
 #endif
 // Pass A with the value stream staged by TMA (single segment, stencil layouts, no slice list): CTA b owns
 // the chunks c = b + t nCTA of 8 consecutive slices (exactly the slices its 8 warps take in the
