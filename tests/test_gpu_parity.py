@@ -297,6 +297,36 @@ def test_lazy_x_depths_parity(cfg, n, s, rule, lazy, monkeypatch):
     assert torch.equal(x, x_ref)
 
 
+@pytest.mark.parametrize("depth", ["3", "2"])
+def test_lazy_x_confirm_reset_and_cap(depth, monkeypatch):
+    """A tolerance below what the true residual can reach makes every recursive-residual convergence fail its
+    true-residual confirmation (CONFIRM -> RESET with x updates pending) until the iteration cap: the lazy-x
+    solve ends with the same status, iteration count and bitwise the same x as the every-pass update."""
+    monkeypatch.setenv("LC_NO_DSMEM", "1")
+    monkeypatch.setenv("LC_NO_CLUSTER", "1")
+    sy = synth.system(5, 6, n=24)
+    A = gpu_matrix(sy)
+    b = to_dev(sy.b)
+    res = {}
+    for mode in ("lazy", "off"):
+        if mode == "lazy":
+            monkeypatch.delenv("LC_NO_LAZY_X", raising=False)
+            monkeypatch.setenv("LC_LAZY_X_DEPTH", depth)
+        else:
+            monkeypatch.setenv("LC_NO_LAZY_X", "1")
+        for cap in (301, 302, 303):
+            x = to_dev(sy.x0)
+            try:
+                info = lc.solve_global(A, b, x, rel_tol=1e-17, max_iters=cap)
+                st = [(i["status"], i["iterations"]) for i in info]
+            except lc.LcError as e:
+                st = [e.status]
+            res[(mode, cap)] = (x.clone(), st)
+    for cap in (301, 302, 303):
+        assert res[("lazy", cap)][1] == res[("off", cap)][1]
+        assert torch.equal(res[("lazy", cap)][0], res[("off", cap)][0]), cap
+
+
 @pytest.mark.parametrize("path", ["grid", "lock", "team", "gmres"])
 def test_determinism_short_passes(path, monkeypatch):
     """Repeated solves with very short passes (tiny systems on the multi-CTA kernels, where a CTA leaving a
