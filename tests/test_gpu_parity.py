@@ -297,6 +297,16 @@ def test_lazy_x_depths_parity(cfg, n, s, rule, lazy, monkeypatch):
     assert torch.equal(x, x_ref)
 
 
+@pytest.mark.parametrize("sub", ["LC_EXPLICIT_SUB", "LC_MASKED_SUB"])
+@pytest.mark.parametrize("cfg,n,s,rule", [(5, 33, 4, 0), (5, 40, 12, 1), (2, 128, 30, 0), (1, 64, 5, 0)])
+def test_subsystem_representations(cfg, n, s, rule, sub, monkeypatch):
+    """Both subsystem representations of a stencil matrix (masked on A's layout / explicit SELL B of the Omega
+    rows, chosen by size in lc_extract_sub) against the oracle, on the grid kernels and the small-system ones."""
+    monkeypatch.setenv(sub, "1")
+    sy = synth.system(cfg, s, n=n)
+    check_system(sy, RULES[cfg][rule])
+
+
 @pytest.mark.parametrize("depth", ["3", "2"])
 def test_lazy_x_confirm_reset_and_cap(depth, monkeypatch):
     """A tolerance below what the true residual can reach makes every recursive-residual convergence fail its

@@ -11,5 +11,5 @@ for f in sys.argv[1:]:
     d = json.loads(lines[-1])
     bd = d.get("config", {}).get("breakdown", {})
     parts = [f"{k}: {v['ms_local']:.2f}/{v['ms_global']:.2f}" for k, v in bd.items()]
-    print(f, d["value"], d.get("e2e", {}).get("value"), d.get("roofline", {}).get("frac"),
+    print(f, d["value"], (d.get("e2e") or {}).get("value"), d.get("roofline", {}).get("frac"),
           d.get("clocks", {}).get("sm_mhz"), "; ".join(parts))
