@@ -133,6 +133,13 @@ lc_status lc_domain_export(lc_domain dom, int32_t* idx_dev, double* tau_host, do
  * b_sub = b_B - E x_C^(0) (Eq. 3; per row the fma chain over stored columns
  * outside Omega, ascending, then one subtraction), x_B0 = x0[Omega] and the
  * (block-)Jacobi inverse diagonal of B.  K = 0 gives an empty handle.
+ * Representation (no effect on results): B is either materialised (SELL-32 over
+ * the Omega rows) or, for stencil matrices, applied as A's stencil restricted to
+ * Omega on vectors that vanish outside it ("masked"); a single system with
+ * K <= n/2 and K >= 65536 gets the materialised form, near-full, small and batched
+ * domains the masked one.  A masked handle refers to A's device
+ * layout: destroy the sub handle before A.  Errors: LC_ERR_INVALID_ARG (null
+ * handle / vectors), LC_ERR_OOM, LC_ERR_CUDA.
  */
 lc_status lc_extract_sub(lc_matrix A, lc_domain dom, const double* b, const double* x0, void* stream, lc_sub* sub);
 
