@@ -93,6 +93,10 @@ struct SegState {
 };
 
 __device__ __forceinline__ void slice_map(const PcgArgs& P, int64_t s, int& g, int64_t& row0, int64_t& end) {
+  if (P.G == 1) {                    // one segment: slice s holds units 32 s .. (no table loads on the path)
+    g = 0; row0 = 32 * s; end = P.A.nunits;
+    return;
+  }
   if (P.reg_units > 0) {
     if (P.G == 1) {
       g = 0; row0 = 32 * s; end = P.reg_units;
@@ -204,13 +208,18 @@ __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_
     return r0_ + lane < e_ ? P.omega[r0_ + lane] : (uint8_t)0;
   };
   if (P.omega && j0 < jlim) om_next = om_of(s_next);
+  // SELL: the slice's first slot and width are loaded one slice ahead too (column loads then follow directly)
+  int64_t sp_next = 0, se_next = 0;
+  if (!ST && j0 < jlim) { sp_next = A.slice_ptr[s_next]; se_next = A.slice_ptr[s_next + 1]; }
 #pragma unroll 1
   for (int64_t j = j0; j < jlim; j += jstep) {
     const int64_t s = s_next;
     const uint8_t om_cur = om_next;
+    const int64_t sp_cur = sp_next, se_cur = se_next;
     if (j + jstep < jlim) {
       s_next = P.slist ? (int64_t)P.slist[j + jstep] : j + jstep;
       if (P.omega) om_next = om_of(s_next);
+      if (!ST) { sp_next = A.slice_ptr[s_next]; se_next = A.slice_ptr[s_next + 1]; }
     }
     int g;
     int64_t row0, end;
@@ -218,8 +227,8 @@ __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_
     else slice_map(P, s, g, row0, end);
     const int64_t u = row0 + lane;
     if (u >= end) continue;
-    const int64_t pl = (ST ? 32ll * A.vw * s : A.slice_ptr[s]) + lane;
-    const int w = ST ? A.W : (int)((A.slice_ptr[s + 1] - (pl - lane)) >> 5);
+    const int64_t pl = (ST ? 32ll * A.vw * s : sp_cur) + lane;
+    const int w = ST ? A.W : (int)((se_cur - sp_cur) >> 5);
     double own = 0.0;
     const bool in = !P.omega || om_cur != 255;
     if (MODE == 0) {
