@@ -135,9 +135,9 @@ lc_status lc_domain_export(lc_domain dom, int32_t* idx_dev, double* tau_host, do
  * (block-)Jacobi inverse diagonal of B.  K = 0 gives an empty handle.
  * Representation (no effect on results): B is either materialised (SELL-32 over
  * the Omega rows) or, for stencil matrices, applied as A's stencil restricted to
- * Omega on vectors that vanish outside it ("masked"); a single system with
- * K <= n/2 and K >= 65536 gets the materialised form, near-full, small and batched
- * domains the masked one.  A masked handle refers to A's device
+ * Omega on vectors that vanish outside it ("masked"); K <= n/2 with K >= 65536
+ * gets the materialised form, near-full and small domains the masked one
+ * (DESIGN.md s5).  A masked handle refers to A's device
  * layout: destroy the sub handle before A.  Errors: LC_ERR_INVALID_ARG (null
  * handle / vectors), LC_ERR_OOM, LC_ERR_CUDA.
  */

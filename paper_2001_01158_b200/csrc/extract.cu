@@ -167,13 +167,13 @@ extern "C" lc_status lc_extract_sub(lc_matrix M, lc_domain D, const double* b, c
 #define CK(x) do { st = (x); if (st) goto fail; } while (0)
 #define CKC(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { st = cuda_fail(_e, #x); goto fail; } } while (0)
   // Stencil layouts: the masked representation (below) sweeps A's slices that hold Omega rows, so its cost
-  // follows the slices' fill; a single system whose Omega is at most half the rows and too large for the
-  // cluster-resident kernel gets the explicit B instead (SELL, 12 B/nnz, only Omega rows): config 5 method2
-  // (eta 0.093, slices 54% filled) local solve 8.70 -> 6.07 ms, config 2 method1 2.31 -> 1.92 ms; near-full
-  // domains (config 5 method1: 44 vs 62 ms), small and batched ones keep the masked form.  LC_EXPLICIT_SUB=1 /
-  // LC_MASKED_SUB=1 force either.
+  // follows the slices' fill; an Omega of at most half the rows that is too large for the cluster-resident
+  // kernel gets the explicit B instead (SELL, 12 B/nnz, only Omega rows): config 5 method2 (eta 0.093, slices
+  // 54% filled) local solve 8.70 -> 6.07 ms, config 2 method1 2.31 -> 1.92 ms, config 3 (20 groups) 4.27 ->
+  // 3.78 ms; near-full domains (config 5 method1: 44 vs 62 ms) and small ones keep the masked form.
+  // LC_EXPLICIT_SUB=1 / LC_MASKED_SUB=1 force either.
   bool masked = M->A.stencil && bs == 1;
-  if (masked && G == 1 && 2 * K <= n && K >= 65536) masked = false;
+  if (masked && 2 * K <= n && K >= 65536) masked = false;
   if (getenv("LC_EXPLICIT_SUB")) masked = false;
   if (getenv("LC_MASKED_SUB") && M->A.stencil && bs == 1) masked = true;
   if (masked) {
