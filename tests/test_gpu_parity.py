@@ -298,7 +298,8 @@ def test_lazy_x_depths_parity(cfg, n, s, rule, lazy, monkeypatch):
 
 
 @pytest.mark.parametrize("sub", ["LC_EXPLICIT_SUB", "LC_MASKED_SUB"])
-@pytest.mark.parametrize("cfg,n,s,rule", [(5, 33, 4, 0), (5, 40, 12, 1), (2, 128, 30, 0), (1, 64, 5, 0)])
+@pytest.mark.parametrize("cfg,n,s,rule", [(5, 33, 4, 0), (5, 40, 12, 1), (2, 128, 30, 0), (1, 64, 5, 0),
+                                          (3, 48, 6, 0), (3, 30, 2, 0)])
 def test_subsystem_representations(cfg, n, s, rule, sub, monkeypatch):
     """Both subsystem representations of a stencil matrix (masked on A's layout / explicit SELL B of the Omega
     rows, chosen by size in lc_extract_sub) against the oracle, on the grid kernels and the small-system ones."""
