@@ -289,6 +289,9 @@ __device__ __forceinline__ void cta_mark(int pc, int slot) {
 #ifndef LCV_MINB
 #define LCV_MINB (1024 / LC_PCG_PT)
 #endif
+#ifndef LCV_MINB_SELL
+#define LCV_MINB_SELL LCV_MINB
+#endif
 // Pass A with the value stream staged by TMA (single segment, stencil layouts, no slice list): CTA b owns
 // the chunks c = b + t nCTA of 8 consecutive slices (exactly the slices its 8 warps take in the
 // interleaved order); thread 0 keeps kStages chunks in flight with cp.async.bulk into a shared-memory
@@ -409,7 +412,7 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
 
 // KIND: 0 = one segment (G = 1), 1 = batched lock step (G > 1), 2 = batched teams (each team a G = 1 solve)
 template <int WM, int ST, int KIND>
-__global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg(PcgArgs P) {
+__global__ void __launch_bounds__(kPT, ST == 0 ? LCV_MINB_SELL : LCV_MINB) k_pcg(PcgArgs P) {
   unsigned long long bar_epoch = 0;
   unsigned tree_gen = 0;                        // tree barriers passed (G > 1)
   __shared__ SegState S[kMaxSeg];
