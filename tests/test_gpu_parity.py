@@ -678,6 +678,17 @@ def test_full_size_solution_properties(cfg, s):
                 assert np.max(np.abs(xn[r0:r1] - sy.xs[r0:r1])) <= np.max(np.abs(r)) * (1 + 1e-6) + 1e-300
 
 
+@pytest.mark.parametrize("cfg,s,rule", [(3, 10, 0), (4, 15, 0), (5, 10, 0), (2, 25, 0)])
+def test_full_size_local_method_vs_oracle(cfg, s, rule):
+    """BASELINE sizes, in the bench's launch configuration (explicit subsystems, teams / lock step, the TMA
+    and lazy-x global kernels), element by element against the oracle's Alg. 1: domain sets, tau, criterion,
+    local and global iteration counts (+-1) and the solution (1e-9), group by group for config 3.  The oracle
+    side takes ~1-17 s per case (method0's 933-iteration global solves of config 3 are left to the property
+    test above)."""
+    sy = synth.system(cfg, s)
+    check_system(sy, RULES[cfg][rule])
+
+
 # ------------------------------------------------- general (non-stencil) SELL --
 
 @pytest.mark.parametrize("layout", ["sell", "symstencil"])
