@@ -60,6 +60,7 @@ struct DArgs {
   unsigned long long* seq_out;
   // solve
   int masked, max_iters;
+  int lazyx;                      // x updated every second iteration (as k_pcg's lazy x, depth 2)
   double eps;
   double* x_user;                 // exit: x_user[u] = x[u] (all rows, or Omega rows when masked)
   // domain
@@ -184,12 +185,14 @@ __device__ void xreduce(const DArgs& P, unsigned bid, unsigned nCTA, int op, dou
 }
 
 // ---------------------------------------------------------------- operands ----
-// W: 0 x, 1 z, 2 p = z + beta p_old, 3 x0
+// W: 0 x, 1 z, 2 p = z + beta p_old, 3 x0, 4 x with its pending lazy update (beta = its alpha, pold / par =
+// its direction): the CONFIRM pass of a lazy-x solve
 template <int OP>
 __device__ __forceinline__ double opl(const DArgs& P, int c, double beta, const double* pold) {
   if (OP == 0) return P.x[c];
   if (OP == 1) return P.z[c];
   if (OP == 2) return __fma_rn(beta, pold[c], P.z[c]);
+  if (OP == 4) return __fma_rn(beta, pold[c], P.x[c]);
   return P.x0[c];
 }
 template <int OP>
@@ -197,6 +200,7 @@ __device__ __forceinline__ double opp(const DPeer& Q, int i, double beta, int pa
   if (OP == 0) return __ldcv(Q.x + i);
   if (OP == 1) return __ldcv(Q.z + i);
   if (OP == 2) return __fma_rn(beta, __ldcv((par ? Q.p1 : Q.p0) + i), __ldcv(Q.z + i));
+  if (OP == 4) return __fma_rn(beta, __ldcv((par ? Q.p1 : Q.p0) + i), __ldcv(Q.x + i));
   return __ldcv(Q.x0 + i);
 }
 // operand at slab-relative column c (edge slices may leave [0, n): the neighbours' rows; outside the
@@ -249,7 +253,7 @@ __device__ __forceinline__ void dslice_body(const DArgs& P, int64_t s, int lane,
     if (A.off[k] == 0 && (WM != 8 || k < A.W)) own = y[k];
   }
   if (P.masked && P.om[u] == kOutD) return;
-  if (OP == 0) {
+  if (OP == 0 || OP == 4) {
     const double bi = P.b[u];
     const double ri = bi - acc;
     P.r[u] = ri;
@@ -280,7 +284,7 @@ __device__ __noinline__ void dslice_edge(const DArgs& P, int64_t s, int lane, bo
 template <int WM, int OP>
 __device__ __forceinline__ void dpass_a(const DArgs& P, int64_t sa, int64_t sb, int64_t w0, int64_t wst, int lane,
                                         bool init, double beta, int par, double* a) {
-  const double* pold = par ? P.p1 : P.p0;
+  const double* pold = par ? P.p1 : P.p0;        // (OP 4: the pending direction)
   double* pnew = par ? P.p0 : P.p1;
 #pragma unroll 1
   for (int64_t s = sa + w0; s < sb; s += wst) dslice<WM, OP, false>(P, s, lane, init, beta, par, pold, pnew, a);
@@ -350,7 +354,7 @@ __device__ __forceinline__ void dpass_a_tma(const DArgs& P, double* stg, uint64_
           if (A.off[k] == 0) own = y[k];
         }
         if (!P.masked || P.om[u] != kOutD) {
-          if (OP == 0) {
+          if (OP == 0 || OP == 4) {
             const double bi = P.b[u];
             const double ri = bi - acc;
             P.r[u] = ri;
@@ -377,12 +381,12 @@ __global__ void __launch_bounds__(kDT, 4) k_dpcg(const __grid_constant__ DPack p
   __shared__ double s_w[kDW][4], s_out[4];
   extern __shared__ __align__(128) double dsm[];   // TMA stages: kDStages x 8 slices x 32 x WM values
   __shared__ __align__(8) uint64_t s_bars[kDStages];
-  __shared__ int s_mode, s_par, s_it, s_final, s_exit;
-  __shared__ double s_rho, s_alpha, s_beta, s_tgt, s_nb;
+  __shared__ int s_mode, s_par, s_it, s_final, s_exit, s_pend, s_pbuf;
+  __shared__ double s_rho, s_alpha, s_beta, s_tgt, s_nb, s_palpha;
   const unsigned slot = blockIdx.x / nCTA, bid = blockIdx.x % nCTA;
   if (threadIdx.x == 0) {
-    s_mode = D_INIT; s_par = 0; s_it = 0; s_final = 0; s_exit = 0;
-    s_rho = s_alpha = s_beta = 0.0; s_tgt = s_nb = 0.0;
+    s_mode = D_INIT; s_par = 0; s_it = 0; s_final = 0; s_exit = 0; s_pend = 0; s_pbuf = 0;
+    s_rho = s_alpha = s_beta = 0.0; s_tgt = s_nb = 0.0; s_palpha = 0.0;
   }
   __syncthreads();
   const DArgs& P = pk.a[slot];
@@ -407,7 +411,10 @@ __global__ void __launch_bounds__(kDT, 4) k_dpcg(const __grid_constant__ DPack p
     // ---- pass A
     double a[4] = {0.0, 0.0, 0.0, 0.0};
     const int mode = s_mode;
-    if (WM != 8 && tma) {
+    if (mode == D_CONFIRM && s_pend) {            // lazy x: true residual at x + the pending alpha p
+      if (WM != 8 && tma) dpass_a_tma<WM, 4>(P, dsm, s_bars, bid, nCTA, warp, lane, false, s_palpha, s_pbuf, a);
+      else dpass_a<WM, 4>(P, sa, sb, w0, wst, lane, false, s_palpha, s_pbuf, a);
+    } else if (WM != 8 && tma) {
       if (mode == D_INIT || mode == D_CONFIRM)
         dpass_a_tma<WM, 0>(P, dsm, s_bars, bid, nCTA, warp, lane, mode == D_INIT, 0.0, s_par, a);
       else if (mode == D_FIRST) dpass_a_tma<WM, 1>(P, dsm, s_bars, bid, nCTA, warp, lane, false, 0.0, s_par, a);
@@ -456,7 +463,32 @@ __global__ void __launch_bounds__(kDT, 4) k_dpcg(const __grid_constant__ DPack p
       const double2* q2 = reinterpret_cast<const double2*>(P.q);
       const double2* d2 = reinterpret_cast<const double2*>(P.A.dinv);
       const int64_t npair = P.n >> 1, gt = (int64_t)bid * kDT + threadIdx.x, gs = (int64_t)nCTA * kDT;
-      if (modeb == D_UPDATE) {
+      // lazy x (as k_pcg): every second UPDATE leaves x alone, the next applies both updates in order
+      const int pend = s_pend;
+      const double pa = s_palpha;
+      const double2* po2 = reinterpret_cast<const double2*>(s_pbuf ? P.p1 : P.p0);
+      if (modeb == D_UPDATE && P.lazyx && !pend) {
+#pragma unroll 2
+        for (int64_t i = gt; i < npair; i += gs) {
+          double2 rv = r2[i], qv = q2[i], dv = d2[i];
+          rv.x = __fma_rn(-alpha, qv.x, rv.x); rv.y = __fma_rn(-alpha, qv.y, rv.y);
+          const double2 zv = make_double2(rv.x * dv.x, rv.y * dv.y);
+          r2[i] = rv; z2[i] = zv;
+          a[0] = __fma_rn(rv.x, zv.x, a[0]); a[0] = __fma_rn(rv.y, zv.y, a[0]);
+          a[1] = __fma_rn(rv.x, rv.x, a[1]); a[1] = __fma_rn(rv.y, rv.y, a[1]);
+        }
+      } else if (modeb == D_UPDATE && pend) {
+#pragma unroll 2
+        for (int64_t i = gt; i < npair; i += gs) {
+          double2 xv = x2[i], ov = po2[i], pv = pp[i], rv = r2[i], qv = q2[i], dv = d2[i];
+          xv.x = __fma_rn(alpha, pv.x, __fma_rn(pa, ov.x, xv.x)); xv.y = __fma_rn(alpha, pv.y, __fma_rn(pa, ov.y, xv.y));
+          rv.x = __fma_rn(-alpha, qv.x, rv.x); rv.y = __fma_rn(-alpha, qv.y, rv.y);
+          const double2 zv = make_double2(rv.x * dv.x, rv.y * dv.y);
+          x2[i] = xv; r2[i] = rv; z2[i] = zv;
+          a[0] = __fma_rn(rv.x, zv.x, a[0]); a[0] = __fma_rn(rv.y, zv.y, a[0]);
+          a[1] = __fma_rn(rv.x, rv.x, a[1]); a[1] = __fma_rn(rv.y, rv.y, a[1]);
+        }
+      } else if (modeb == D_UPDATE) {
 #pragma unroll 2
         for (int64_t i = gt; i < npair; i += gs) {
           double2 xv = x2[i], pv = pp[i], rv = r2[i], qv = q2[i], dv = d2[i];
@@ -474,17 +506,25 @@ __global__ void __launch_bounds__(kDT, 4) k_dpcg(const __grid_constant__ DPack p
           const double2 zv = make_double2(rv.x * dv.x, rv.y * dv.y);
           z2[i] = zv;
           a[0] = __fma_rn(rv.x, zv.x, a[0]); a[0] = __fma_rn(rv.y, zv.y, a[0]);
+          if (pend) {                               // RESET: apply the pending update
+            double2 xv = x2[i];
+            const double2 ov = po2[i];
+            xv.x = __fma_rn(pa, ov.x, xv.x); xv.y = __fma_rn(pa, ov.y, xv.y);
+            x2[i] = xv;
+          }
         }
       }
       if ((P.n & 1) && gt == 0) {
         const int64_t u = P.n - 1;
         const double* p1 = s_par ? P.p1 : P.p0;
+        const double* po = s_pbuf ? P.p1 : P.p0;
         const double di = P.A.dinv[u];
         if (modeb == D_UPDATE) {
-          const double xi = __fma_rn(alpha, p1[u], P.x[u]);
           const double ri = __fma_rn(-alpha, P.q[u], P.r[u]);
           const double zi = ri * di;
-          P.x[u] = xi; P.r[u] = ri; P.z[u] = zi;
+          if (!P.lazyx) P.x[u] = __fma_rn(alpha, p1[u], P.x[u]);
+          else if (pend) P.x[u] = __fma_rn(alpha, p1[u], __fma_rn(pa, po[u], P.x[u]));
+          P.r[u] = ri; P.z[u] = zi;
           a[0] = __fma_rn(ri, zi, a[0]);
           a[1] = __fma_rn(ri, ri, a[1]);
         } else {
@@ -492,6 +532,7 @@ __global__ void __launch_bounds__(kDT, 4) k_dpcg(const __grid_constant__ DPack p
           const double zi = ri * di;
           P.z[u] = zi;
           a[0] = __fma_rn(ri, zi, a[0]);
+          if (pend) P.x[u] = __fma_rn(pa, po[u], P.x[u]);
         }
       }
     }
@@ -500,6 +541,10 @@ __global__ void __launch_bounds__(kDT, 4) k_dpcg(const __grid_constant__ DPack p
       const double s0 = s_out[0], s1 = s_out[1];
       if (modeb == D_UPDATE) {
         s_it += 1;
+        if (P.lazyx) {
+          if (s_pend) s_pend = 0;
+          else { s_pend = 1; s_pbuf = s_par; s_palpha = s_alpha; }
+        }
         if (!isfinite(s1) || sqrt(s1) <= s_tgt || s_it >= P.max_iters) {
           s_mode = D_CONFIRM;
           s_final = (s_it >= P.max_iters) || !isfinite(s1);
@@ -511,15 +556,17 @@ __global__ void __launch_bounds__(kDT, 4) k_dpcg(const __grid_constant__ DPack p
       } else if (modeb == D_RESET) {
         s_rho = s0;
         s_mode = D_FIRST;
+        s_pend = 0;
       }
       s_exit = s_mode == D_DONE;
     }
     __syncthreads();
     if (s_exit) break;
   }
-  // a8 (Eq. 4) / the global solve's result: back into the caller's slab
+  // a8 (Eq. 4) / the global solve's result: back into the caller's slab (with a still pending lazy update)
+  const double* po = s_pbuf ? P.p1 : P.p0;
   for (int64_t u = (int64_t)bid * kDT + threadIdx.x; u < P.n; u += (int64_t)nCTA * kDT)
-    if (!P.masked || P.om[u] != kOutD) P.x_user[u] = P.x[u];
+    if (!P.masked || P.om[u] != kOutD) P.x_user[u] = s_pend ? __fma_rn(s_palpha, po[u], P.x[u]) : P.x[u];
   if (bid == 0 && threadIdx.x == 0) *P.seq_out = seq;
 }
 
@@ -811,6 +858,7 @@ lc_status run_dpcg(lc_dist* R, int nr, const double* const* b, double* const* xu
     a.x_user = xu[i];
     a.eps = p->rel_tol;
     a.max_iters = p->max_iters;
+    a.lazyx = getenv("LC_NO_LAZY_X") == nullptr ? 1 : 0;
     args[i] = a;
     if (!masked) LC_CUDA(cudaMemcpyAsync(R[i]->x, xu[i], sizeof(double) * R[i]->n, cudaMemcpyDeviceToDevice, s));
   }

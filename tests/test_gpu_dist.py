@@ -165,6 +165,27 @@ def test_dist_matches_single_gpu_path_config5_full():
     assert np.linalg.norm(xg - x1) / np.linalg.norm(x1) <= 1e-9
 
 
+@pytest.mark.parametrize("P", [1, 3])
+def test_dist_lazy_x_bitwise(P, monkeypatch):
+    """Lazy x in the row-partitioned PCG (x updated every second iteration with the same fma roundings, the
+    CONFIRM pass gathering x plus its pending update from the neighbour slabs) gives bitwise the solution
+    of the every-pass update, local and global solves."""
+    sy = synth.system(5, 7, n=28)
+    outs = []
+    for lazy in (True, False):
+        if lazy:
+            monkeypatch.delenv("LC_NO_LAZY_X", raising=False)
+        else:
+            monkeypatch.setenv("LC_NO_LAZY_X", "1")
+        ranks, R = make_ranks(sy, P)
+        b, x0 = slabs(sy.b, R), slabs(sy.x0, R)
+        x, rep = lc.dist_local_method(ranks, b, x0, R_RES, rel_tol=EPS)
+        outs.append((gather(x), rep["local"]["iterations"], rep["global"]["iterations"]))
+        del ranks
+    assert outs[0][1:] == outs[1][1:]
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+
+
 class _Sys:
     pass
 
