@@ -164,7 +164,10 @@ def run_lc(args):
     t0 = time.time()
     host = {}
     dev_in = []
-    keep = set(ids[:2])
+    # host copies: the first system (cpu baseline, shapes) and the first two TIMED systems (the e2e loop feeds
+    # those, so its iteration counts match the device-timed steps')
+    e2e_ids = ids[args.warmup:args.warmup + 2] or ids[:2]
+    keep = set(ids[:1]) | set(e2e_ids)
     for s in ids:
         sy = host[s] if s in host else synth.system(cfg, s, n=n)
         dev_in.append(dict(s=s, rp=torch.from_numpy(sy.rp).to(dev), ci=torch.from_numpy(sy.ci).to(dev),
@@ -325,8 +328,8 @@ def run_lc(args):
     e2e = None
     if args.e2e_steps > 0:
         pins = []
-        for i in range(min(2, len(ids))):
-            sy = host[ids[i]]
+        for i in range(len(e2e_ids)):
+            sy = host[e2e_ids[i]]
             pins.append({k: torch.from_numpy(getattr(sy, k)).pin_memory() for k in ("rp", "ci", "val", "b", "x0")})
         h2d = sum(t.numel() * t.element_size() for t in pins[0].values())
         d2h = len(rules) * N * 8
