@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gs", type=int, default=0, help="Gauss-Seidel sweeps of Alg. 1 l.7 (paper: 1; parity path: 0)")
+    ap.add_argument("--tune", default="", help="lc_tuning fields for A/B runs, e.g. lazy_x_depth=2,pcg_tma=0")
     return ap.parse_args()
 
 
@@ -152,6 +153,8 @@ def run_lc(args):
     from paper_2001_01158_b200 import build as lcbuild
     lcbuild.build()
     from paper_2001_01158_b200 import lc
+    if args.tune:
+        lc.set_tuning(**{k: int(v) for k, v in (kv.split("=") for kv in args.tune.split(","))})
 
     cfg = args.config
     n = args.n or synth.default_n(cfg)
@@ -184,18 +187,33 @@ def run_lc(args):
 
     stream = torch.cuda.current_stream()
 
-    def one_step(inp, out_x=None, rec=None):
+    def one_step(inp, out_x=None, rec=None, keep=False):
         A = lc.Matrix(sy0.nrows, inp["rp"], inp["ci"], inp["val"], block=sy0.block, batch=sy0.batch)
         nsolves = 0
         for name, rule in rules:
             x, rep = lc.local_method(A, inp["b"], inp["x0"], rule, method=method, rel_tol=EPS,
-                                     gs_sweeps=args.gs if rule is not None else 0)
+                                     gs_sweeps=args.gs if rule is not None else 0, keep=keep,
+                                     timing=rec is not None)
             nsolves += sy0.batch
             if out_x is not None:
                 out_x.append(x)
             if rec is not None:
                 rec.append((name, rep))
         return nsolves
+
+    # ---- the oracle baseline (rank 0, N = 1): complete oracle solves of the first system, one pinned process per
+    # rule, running on host cores while the GPU arm below runs; they also check that system's GPU results
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        runs, xs_ = {}, []
+        one_step(dev_in[0], out_x=xs_, rec=(recs0 := []), keep=True)
+        for (name, rep), x in zip(recs0, xs_):
+            its = {"local": [i["iterations"] for i in rep.get("local", [])] or [0] * sy0.batch,
+                   "global": [i["iterations"] for i in rep["global"]]}
+            runs[name] = (x.cpu().numpy(), rep["idx"].cpu().numpy() if "idx" in rep else None, its)
+        del xs_, recs0
+        cpu = CpuBaseline(cfg, sy0, rules, solver, args.gs, runs)
+        del runs
 
     # ---- warm-up
     for i in range(args.warmup):
@@ -229,16 +247,16 @@ def run_lc(args):
         mat_bytes, rule = 8.0 * nnz, "8 B/nnz stencil values"
     else:
         mat_bytes, rule = 12.0 * nnz, "12 B/nnz SELL values + columns"
-    # matrix once + pass A 32 B/row + pass B 64 B/row; single-segment solves update x every L-th
-    # iteration (lazy x of depth L = 3: pass B 40, 40, 80 B/row, i.e. (40 (L - 1) + 56 + 8 L) / L on average)
-    L = int(os.environ.get("LC_LAZY_X_DEPTH", "3"))
-    lazy = solver == "pcg" and sy0.batch == 1 and not os.environ.get("LC_NO_LAZY_X") and L > 1
-    vec_bytes = 32.0 + (40.0 * (L - 1) + 56.0 + 8.0 * L) / L if lazy else 96.0
-    it_bytes = mat_bytes + vec_bytes * N
+
+    # matrix once + pass A 32 B/row + pass B 64 B/row; a solve that updates x every L-th iteration
+    # (lazy x of depth L, reported by lc_solve_info) moves (40 (L - 1) + 56 + 8 L) / L B/row in pass B on average
+    def vec_bytes_of(L):
+        return 32.0 + (40.0 * (L - 1) + 56.0 + 8.0 * L) / L if L > 1 else 96.0
     try:
         trafficdb = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except OSError:
         trafficdb = {}
+    src_sha = lcbuild.source_sha256()
     # GMRES(m), low-sync CGS2 (R39): per Arnoldi step j: 8 nnz + 80 N + 16 (j+1) N bytes
     # (M^-1 apply 48 N; SpMV + w write + one V read for h and the Gram column; one merged update pass)
     m_restart = 30
@@ -255,10 +273,14 @@ def run_lc(args):
     pcg_bytes = 0.0
     pcg_sec = 0.0
     pcg_its = 0
+    depths = set()
     for name, rep in reps:
-        d = by.setdefault(name, dict(K=0, it_local=0, it_global=0, t_local=0.0, t_global=0.0, n=0))
+        d = by.setdefault(name, dict(K=0, it_local=0, it_global=0, t_local=0.0, t_global=0.0, n=0,
+                                     ms={"select": 0.0, "extract": 0.0, "local": 0.0, "gs": 0.0, "global": 0.0}))
         d["n"] += 1
         d["K"] += sum(rep["K"])
+        for k, v in rep.get("ms", {}).items():
+            d["ms"][k] += v
         # a batched (config 3) solve is ONE launch for all groups: every group reports that launch's device
         # time, so the time is taken once (max), the iterations summed over the groups
         if rep.get("local"):
@@ -269,14 +291,25 @@ def run_lc(args):
         for inf in rep["global"]:
             d["it_global"] += inf["iterations"]
             if solver == "pcg":
-                pcg_bytes += inf["iterations"] * it_bytes / sy0.batch
+                depths.add(inf["lazy_x_depth"])
+                pcg_bytes += inf["iterations"] * (mat_bytes + vec_bytes_of(inf["lazy_x_depth"]) * N) / sy0.batch
             else:
                 pcg_bytes += gmres_bytes(inf["iterations"])
             pcg_its += inf["iterations"]
         pcg_sec += max(inf["seconds"] for inf in rep["global"])
-    breakdown = {k: dict(eta=round(v["K"] / (v["n"] * N), 5), it_local=v["it_local"] / v["n"],
-                         it_global=v["it_global"] / v["n"], ms_local=1e3 * v["t_local"] / v["n"],
-                         ms_global=1e3 * v["t_global"] / v["n"]) for k, v in by.items()}
+    # per method: device-time breakdown (lc_solve_info kernel seconds), phase times on the stream (CUDA events:
+    # select = Alg. 1 l.2, extract = l.3-4, local = l.5-6, global = l.8-11, launches and info reads included),
+    # that method's own solves/s and the paper's speedup S = t_method0 / t_method
+    t_m0 = sum(by["method0"]["ms"].values()) / by["method0"]["n"] if "method0" in by else None
+    breakdown = {}
+    for k, v in by.items():
+        t_m = sum(v["ms"].values()) / v["n"]
+        breakdown[k] = dict(eta=round(v["K"] / (v["n"] * N), 5), it_local=v["it_local"] / v["n"],
+                            it_global=v["it_global"] / v["n"], ms_local=1e3 * v["t_local"] / v["n"],
+                            ms_global=1e3 * v["t_global"] / v["n"],
+                            phase_ms={p: round(t / v["n"], 3) for p, t in v["ms"].items()},
+                            ms_total=round(t_m, 3), solves_per_s=round(sy0.batch * 1e3 / t_m, 3),
+                            S=round(t_m0 / t_m, 3) if t_m0 else None)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -288,16 +321,24 @@ def run_lc(args):
         ach = pcg_bytes / pcg_sec / 1e9
         nlaunch = len(reps)
         kname = "k_pcg" if solver == "pcg" else "k_gmres"
-        tr = None
-        if kname in trafficdb and cfg == 5 and Ainfo["layout"] == trafficdb[kname].get("layout"):
-            # measured DRAM bytes per iteration (ncu) x the mean iterations per launch, like `achieved`
-            tr = int(trafficdb[kname]["dram_bytes_per_iteration"] * pcg_its / max(nlaunch, 1))
+        tr, tr_note = None, "no ncu capture for this config"
+        tdb = trafficdb.get(kname, {})
+        if tdb and cfg == tdb.get("config") and Ainfo["layout"] == tdb.get("layout"):
+            if tdb.get("source_sha256") == src_sha and sorted(depths) == tdb.get("lazy_x_depths", sorted(depths)):
+                # measured DRAM bytes per iteration (ncu, this build) x the mean iterations per launch, like `achieved`
+                tr = int(tdb["dram_bytes_per_iteration"] * pcg_its / max(nlaunch, 1))
+                tr_note = tdb.get("source", "")
+            else:
+                tr_note = "profiles/ncu_traffic.json was measured on another build (source sha256 differs): dropped"
         roof = {"kernel": f"{kname} (global solves, one cooperative launch per solve)", "bound": "hbm",
                 "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
-                "traffic": tr, "algorithmic_bytes_per_launch": int(pcg_bytes / max(nlaunch, 1)),
+                "traffic": tr, "traffic_note": tr_note, "algorithmic_bytes_per_launch": int(pcg_bytes / max(nlaunch, 1)),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650",
                 "layout": Ainfo["layout"],
-                "bytes_rule": (f"{rule} + {vec_bytes:.2f} B/row vectors per PCG iteration" if solver == "pcg"
+                "lazy_x_depths": sorted(depths),
+                "bytes_rule": (f"{rule} + " + " / ".join(f"{vec_bytes_of(L):.2f}" for L in sorted(depths))
+                               + " B/row vectors per PCG iteration (lazy-x depth " + "/".join(map(str, sorted(depths)))
+                               + " as reported by lc_solve_info)" if solver == "pcg"
                                else "8 B/nnz + 80 B/unknown + 16 (j+1) B/unknown per Arnoldi step j")}
 
     # ---- the FP64 SpMV alone (BASELINE metric "SpMV HBM GB/s"): lc_spmv y = A x on the last system,
@@ -391,9 +432,9 @@ def run_lc(args):
         e2e = {"value": round(evalue, 4), "unit": "solves/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "h2d_gbs_measured": round(h2d_gbs, 1)}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, n, host[ids[0]], breakdown, rules, solver)
+    parity = None
+    if cpu is not None:
+        cpu, parity = cpu.result()
 
     if rank == 0:
         line = {
@@ -404,8 +445,11 @@ def run_lc(args):
             "config": {"workload": WORKLOAD[cfg], "config_index": cfg, "n": n, "unknowns": N, "nnz": nnz,
                        "solves_per_step": len(rules) * sy0.batch, "methods": [r[0] for r in rules],
                        "systems": ids[args.warmup:], "rel_tol": EPS, "l2": "inputs > L2 (1.8 GB/system)",
-                       "breakdown": breakdown, "gen_seconds": round(gen_s, 1)},
-            "roofline": roof, "spmv": spmv, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                       "breakdown": breakdown, "gen_seconds": round(gen_s, 1),
+                       "tuning": {k: v for k, v in lc.get_tuning().items() if lc.tuning_defaults()[k] != v}
+                       or "library defaults"},
+            "roofline": roof, "spmv": spmv, "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
+            "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
         print(json.dumps(line))
@@ -414,88 +458,208 @@ def run_lc(args):
 
 
 # ----------------------------------------------------------- CPU oracle -----
-def oracle_sample(cfg, n, sy, rules, solver, pcg_iters=3):
-    """Time the oracle (as it stands, 1 thread) on a bounded sample of one system and scale it to
-    solves/s: full-size domain selection + extraction per rule, plus `pcg_iters` Krylov iterations
-    whose per-iteration cost is multiplied by the iteration counts the solves need."""
+# bench.py is the only product-side file that may execute oracle/ (its cpu_baseline leg and --impl reference).
+
+def host_info():
+    try:
+        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except (OSError, IndexError):
+        model = "unknown"
+    return {"cpu": model, "nproc": os.cpu_count()}
+
+
+def sample_segments(G):
+    """config 3: 4 of the G groups (first, last and two between: group sigma_g spans 4 decades, so iteration
+    counts differ), else the whole system"""
+    return sorted({0, G // 3, (2 * G) // 3, G - 1}) if G > 4 else list(range(G))
+
+
+def _neighbours(A, u, cell):
+    out = set()
+    for a in range(cell):
+        i = u * cell + a
+        for k in range(A.rp[i], A.rp[i + 1]):
+            v = int(A.ci[k]) // cell
+            if v != u:
+                out.add(v)
+    return out
+
+
+def cpu_worker(spec):
+    """One complete oracle Alg. 1 (or method0) of one rule on the sampled segments of one system, pinned to one
+    core (1 thread); compares the result with the GPU's run of the same system (Omega incl. near-threshold /
+    cascade counts, iterations, x).  Prints one JSON line."""
     import oracle as orc
-    A = orc.Csr.from_bsr(sy.rp, sy.ci, sy.val) if sy.block == 3 else orc.Csr(sy.rp, sy.ci, sy.val)
-    t = {}
-    for name, rule in rules:
-        if rule is None:
-            continue
+    try:
+        os.sched_setaffinity(0, {spec["core"]})
+    except (AttributeError, OSError):
+        pass
+    d = spec["dir"]
+    ld = lambda k: np.load(os.path.join(d, k + ".npy"), mmap_mode="r")
+    rp, ci, val, b, x0 = ld("rp"), ld("ci"), ld("val"), ld("b"), ld("x0")
+    block, G, N = spec["block"], spec["batch"], len(b)
+    Ao = orc.Csr.from_bsr(rp, ci, val) if block == 3 else orc.Csr(rp, ci, val)
+    rule = spec["rule"]
+    sp = orc.SolverParams(1 if spec["solver"] == "gmres" else 0, 3, 30, EPS, 3000 if spec["solver"] == "gmres" else 20000,
+                          spec["gs"])
+    xg = np.load(os.path.join(d, f"x_{spec['name']}.npy"), mmap_mode="r")
+    gi_all = np.load(os.path.join(d, f"idx_{spec['name']}.npy")) if rule is not None else None
+    its = json.load(open(os.path.join(d, f"its_{spec['name']}.json")))
+    out = {"name": spec["name"], "core": spec["core"], "segments": spec["segments"], "seconds": 0.0,
+           "phases": {"select": 0.0, "extract": 0.0, "local": 0.0, "global": 0.0}, "near": 0, "cascade": 0,
+           "omega_bit_exact": True, "max_x_rel_err": 0.0, "max_it_local_diff": 0, "max_it_global_diff": 0}
+    for g in spec["segments"]:
+        r0, r1 = g * N // G, (g + 1) * N // G
+        As = Ao.segment(r0, r1) if G > 1 else Ao
+        bs_, x0s = np.ascontiguousarray(b[r0:r1]), np.ascontiguousarray(x0[r0:r1])
+        dp = None
+        if rule is not None:
+            dp = orc.DomainParams(rule.get("criterion", 0), rule.get("threshold", 0), rule["param"],
+                                  rule.get("expand_rounds", 0), rule.get("dilate_hops", 0), block)
         t0 = time.perf_counter()
-        d = orc.select_domain(A, sy.b, sy.x0, rule.get("criterion", 0), rule.get("threshold", 0), rule["param"],
-                              rule.get("expand_rounds", 0), rule.get("dilate_hops", 0), sy.block)
-        t1 = time.perf_counter()
-        orc.extract(A, sy.b, sy.x0, d.flag)
-        t2 = time.perf_counter()
-        t[name] = (t1 - t0, t2 - t1, d.K / A.n)
-    t0 = time.perf_counter()
-    if solver == "pcg":
-        orc.pcg(A, sy.b, sy.x0, eps=EPS, max_iters=pcg_iters)
-    else:
-        orc.gmres_bj(A, sy.b, sy.x0, bs=3, eps=EPS, max_iters=pcg_iters)
-    t_it = (time.perf_counter() - t0) / pcg_iters
-    return t, t_it
+        xo, flag, rep = orc.local_method(As, bs_, x0s, dp, sp)
+        out["seconds"] += time.perf_counter() - t0
+        for k, v in (("select", rep.t_select), ("extract", rep.t_extract), ("local", rep.t_local),
+                     ("global", rep.t_global)):
+            out["phases"][k] += v
+        out["max_x_rel_err"] = max(out["max_x_rel_err"],
+                                   float(np.linalg.norm(xg[r0:r1] - xo) / np.linalg.norm(xo)))
+        out["max_it_global_diff"] = max(out["max_it_global_diff"], abs(its["global"][g] - rep.it_global))
+        if rule is not None:
+            gi = gi_all[(gi_all >= r0) & (gi_all < r1)] - r0
+            ora = np.flatnonzero(flag)
+            if its["local"][g] or rep.it_local:
+                out["max_it_local_diff"] = max(out["max_it_local_diff"], abs(its["local"][g] - rep.it_local))
+            if not np.array_equal(gi, ora):
+                out["omega_bit_exact"] = False
+                dd = orc.select_domain(As, bs_, x0s, rule.get("criterion", 0), rule.get("threshold", 0),
+                                       rule["param"], rule.get("expand_rounds", 0), rule.get("dilate_hops", 0), block)
+                gu, ou = set((gi[::block] // block).tolist()), set((ora[::block] // block).tolist())
+                diff = gu ^ ou
+                near = {u for u in diff if abs(dd.crit[u] - dd.tau) <= 1e-12 * dd.tau or
+                        (np.isfinite(dd.adm[u]) and abs(dd.adm[u] - dd.tau) <= 1e-12 * dd.tau)}
+                casc, fr = set(), set(near)
+                for _ in range(8):
+                    fr = {v for u in fr for v in _neighbours(As, u, block) if v in diff and v not in near | casc}
+                    casc |= fr
+                out["near"] += len(near)
+                out["cascade"] += len(casc)
+                out["outside_window"] = out.get("outside_window", 0) + len(diff - near - casc)
+    print(json.dumps(out), flush=True)
 
 
-def cpu_baseline(cfg, n, sy, breakdown, rules, solver):
-    t, t_it = oracle_sample(cfg, n, sy, rules, solver)
-    t_it /= sy.batch          # the sample iterates over all G groups; the counts below are per group, summed
-    total = 0.0
-    for name, rule in rules:
-        bd = breakdown.get(name, {})
-        it_l, it_g = bd.get("it_local", 0.0), bd.get("it_global", 0.0)
-        eta = t.get(name, (0, 0, 0))[2]
-        sel = t.get(name, (0, 0, 0))[0] + t.get(name, (0, 0, 0))[1]
-        total += sel + t_it * (eta * it_l + it_g)
-    nsol = len(rules) * sy.batch
-    return {"value": round(nsol / total, 6), "unit": "solves/s", "cores": 1, "kind": "oracle",
-            "sample": (f"oracle (C, 1 thread) on system s={sy.s} of {WORKLOAD[cfg]}: full-size domain selection + "
-                       f"extraction per rule timed, plus 3 Krylov iterations timed ({t_it:.3f} s/iteration) and "
-                       f"scaled by the iteration counts of this run (local iterations weighted by eta; per group for G > 1)")}
+class CpuBaseline:
+    """The oracle (as it stands, single-threaded C) on one complete system of the workload: one process per
+    rule, each pinned to its own host core, started while the GPU arm runs."""
+
+    def __init__(self, cfg, sy, rules, solver, gs, gpu_runs):
+        import tempfile
+        self.dir = tempfile.mkdtemp(prefix="lc_cpu_")
+        for k in ("rp", "ci", "val", "b", "x0"):
+            np.save(os.path.join(self.dir, k + ".npy"), getattr(sy, k))
+        self.segs = sample_segments(sy.batch)
+        self.sy, self.cfg, self.rules = sy, cfg, rules
+        ncores = os.cpu_count() or 1
+        self.procs = []
+        for j, (name, rule) in enumerate(rules):
+            x, idx, its = gpu_runs[name]
+            np.save(os.path.join(self.dir, f"x_{name}.npy"), x)
+            if idx is not None:
+                np.save(os.path.join(self.dir, f"idx_{name}.npy"), idx)
+            json.dump(its, open(os.path.join(self.dir, f"its_{name}.json"), "w"))
+            core = ncores - 1 - j if ncores > j + 1 else j % ncores
+            spec = dict(dir=self.dir, name=name, rule=rule, solver=solver, gs=gs if rule is not None else 0,
+                        block=sy.block, batch=sy.batch, segments=self.segs, core=core)
+            self.procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), "--cpu-worker",
+                                                json.dumps(spec)], stdout=subprocess.PIPE, text=True,
+                                               env=dict(os.environ, OMP_NUM_THREADS="1")))
+
+    def result(self):
+        import shutil
+        outs = []
+        for p in self.procs:
+            so, _ = p.communicate()
+            if p.returncode != 0 or not so.strip():
+                raise RuntimeError("oracle cpu worker failed")
+            outs.append(json.loads(so.strip().splitlines()[-1]))
+        shutil.rmtree(self.dir, ignore_errors=True)
+        nsol = len(outs) * len(self.segs)
+        tot = sum(o["seconds"] for o in outs)
+        cb = {"value": round(nsol / tot, 6), "unit": "solves/s", "cores": 1, "kind": "oracle",
+              "sample": (f"oracle (C, 1 thread per process) running COMPLETE Alg. 1 / method0 solves of system "
+                         f"s={self.sy.s} of {WORKLOAD[self.cfg]}: {', '.join(n for n, _ in self.rules)}"
+                         + (f" on groups {self.segs} of {self.sy.batch}" if self.sy.batch > 1 else "")
+                         + f"; one process per rule, each pinned to its own core, concurrently with the GPU arm; "
+                           f"value = solves / summed single-core seconds"),
+              "measured_seconds": round(tot, 2), "host": host_info(),
+              "processes": [{"rule": o["name"], "core": o["core"], "seconds": round(o["seconds"], 3),
+                             "phases": {k: round(v, 3) for k, v in o["phases"].items()}} for o in outs]}
+        parity = {o["name"]: {k: o[k] for k in ("omega_bit_exact", "near", "cascade", "max_x_rel_err",
+                                                "max_it_local_diff", "max_it_global_diff") if k in o}
+                  for o in outs}
+        for o in outs:
+            if "outside_window" in o:
+                parity[o["name"]]["outside_window"] = o["outside_window"]
+        return cb, {"system": self.sy.s, "segments": self.segs, "by_rule": parity}
 
 
 def run_reference(args):
+    """The reference arm: the oracle itself (no reference implementation exists; the reference is a paper).  Each
+    step is ONE complete oracle Alg. 1 solve of the workload's cheapest rule (method2, or method1 for config 2) on
+    system s_i (on 4 of the 20 groups for config 3), timed whole; every printed time was spent."""
     rank, world, local = dist_env()
     if rank != 0:
         return
+    import oracle as orc
     cfg = args.config
     n = args.n or synth.default_n(cfg)
     rules, solver = CFG_RULES[cfg]
-    sy = synth.system(cfg, 10 % synth.default_systems(cfg), n=n)
-    # the oracle's own full-size iteration counts are too slow to run every step; take the
-    # per-iteration cost from each sample and the iteration counts from one oracle-complete run
-    # on a system of the same sequence at the reduced grid n/8 scaled by sqrt(N) growth is NOT used:
-    # counts come from the GPU-free estimate of Jacobi-PCG below (documented in DESIGN.md s8).
-    it_est = {"pcg": 120, "gmres": 200}[solver]
-    times = []
+    name, rule = rules[0]
+    nsys = synth.default_systems(cfg)
+    sp = orc.SolverParams(1 if solver == "gmres" else 0, 3, 30, EPS, 3000 if solver == "gmres" else 20000, 0)
+    times, nsol = [], 0
+    sys_done = []
+    wall0 = time.perf_counter()
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        t, t_it = oracle_sample(cfg, n, sy, rules, solver, pcg_iters=2)
-        el = time.perf_counter() - t0
-        total = sum(v[0] + v[1] for v in t.values()) + t_it * it_est * len(rules)
+        sy = synth.system(cfg, (10 + i) % nsys, n=n)
+        Ao = orc.Csr.from_bsr(sy.rp, sy.ci, sy.val) if sy.block == 3 else orc.Csr(sy.rp, sy.ci, sy.val)
+        dp = orc.DomainParams(rule.get("criterion", 0), rule.get("threshold", 0), rule["param"],
+                              rule.get("expand_rounds", 0), rule.get("dilate_hops", 0), sy.block)
+        segs = sample_segments(sy.batch)
+        t = 0.0
+        for g in segs:
+            r0, r1 = g * sy.N // sy.batch, (g + 1) * sy.N // sy.batch
+            As = Ao.segment(r0, r1) if sy.batch > 1 else Ao
+            t0 = time.perf_counter()
+            orc.local_method(As, sy.b[r0:r1], sy.x0[r0:r1], dp, sp)
+            t += time.perf_counter() - t0
         if i >= args.warmup:
-            times.append(total)
-        _ = el
-    mean = float(np.mean(times))
-    nsol = len(rules) * sy.batch
-    val = nsol / mean
+            times.append(t)
+            nsol += len(segs)
+            sys_done.append(sy.s)
+    total = float(sum(times))
+    val = nsol / total
     line = {"impl": "reference", "metric": "linear solves/s (local character-based method + method0, FP64, "
             "rel. residual 1e-10)", "value": round(val, 6), "unit": "solves/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean * 1e3, 1),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, SURVEY 8(d))",
-            "config": {"workload": WORKLOAD[cfg], "config_index": cfg, "n": n},
+            "config": {"workload": WORKLOAD[cfg], "config_index": cfg, "n": n, "systems": sys_done},
             "cpu_baseline": {"value": round(val, 6), "unit": "solves/s", "cores": 1, "kind": "oracle",
-                             "sample": f"per step: full-size domain selection + extraction per rule and 2 timed "
-                                       f"Krylov iterations of the oracle, scaled to {it_est} iterations per solve"},
+                             "host": host_info(),
+                             "sample": f"per step one complete oracle Alg. 1 ({name}: domain, extraction, local "
+                                       f"and global solve) of system s_i"
+                                       + (f", groups {sample_segments(20)} of 20" if cfg == 3 else "")
+                                       + "; every timed second was spent (no extrapolation)"},
+            "wall_seconds": round(time.perf_counter() - wall0, 1),
             "e2e": {"value": round(val, 6), "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
 if __name__ == "__main__":
+    if len(sys.argv) == 3 and sys.argv[1] == "--cpu-worker":
+        cpu_worker(json.loads(sys.argv[2]))
+        sys.exit(0)
     a = parse()
     if a.impl == "reference":
         run_reference(a)

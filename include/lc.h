@@ -143,6 +143,14 @@ lc_status lc_domain_export(lc_domain dom, int32_t* idx_dev, double* tau_host, do
  */
 lc_status lc_extract_sub(lc_matrix A, lc_domain dom, const double* b, const double* x0, void* stream, lc_sub* sub);
 
+/*
+ * Copy out what lc_extract_sub computed (Eq. 3), whatever the representation: bsub_dev, xB0_dev (device,
+ * each optional, [sum K * block]) receive b_sub = b_B - E x_C^(0) and x_B0 = x0[Omega] in the order of
+ * Omega (ascending global rows, segment by segment; the cell's 3 unknowns together for block = 3).  For
+ * parity checks against the oracle's extraction.  Syncs `stream`.
+ */
+lc_status lc_sub_export(lc_sub sub, double* bsub_dev, double* xB0_dev, void* stream);
+
 typedef struct {
   int32_t method;    /* LC_PCG (Jacobi-preconditioned CG, SPD systems) | LC_GMRES (right-preconditioned
                         block-Jacobi GMRES(restart) with CGS2, nonsymmetric block = 3 systems) */
@@ -157,7 +165,18 @@ typedef struct {
   int32_t status;           /* LC_OK | LC_NOT_CONVERGED | LC_ERR_BREAKDOWN | LC_ERR_NONFINITE */
   double rel_residual;      /* ||b - A x||_2 / ||b||_2 of the returned x (true residual) */
   double seconds;           /* device time of the solve (CUDA events) */
+  int32_t kernel;           /* which Krylov kernel ran (LC_KERNEL_*) */
+  int32_t lazy_x_depth;     /* PCG: x updated every lazy_x_depth-th iteration (1 = every iteration) */
 } lc_solve_info;
+
+/* lc_solve_info.kernel */
+enum { LC_KERNEL_NONE = 0      /* no launch (empty subsystem) */,
+       LC_KERNEL_PCG_GRID = 1  /* cooperative persistent grid, one segment */,
+       LC_KERNEL_PCG_CLUSTER = 2 /* one thread-block cluster (<= 512 slices) */,
+       LC_KERNEL_PCG_RESIDENT = 3 /* cluster with the system resident in shared memory (<= ~30k rows) */,
+       LC_KERNEL_PCG_LOCKSTEP = 4 /* batched, all active segments swept in lock step */,
+       LC_KERNEL_PCG_TEAMS = 5    /* batched, one team of CTAs per segment */,
+       LC_KERNEL_GMRES = 6 };
 
 /*
  * Alg. 1 l.5-6: solve B xbar_B = b_sub from x_B0 to ||b_sub - B xbar|| <= eps ||b_sub||
@@ -242,13 +261,16 @@ typedef struct {
   int64_t it_local, it_global;   /* summed Krylov iterations */
   double eta_sum;                /* sum over linear solves of K / N */
   double seconds;                /* host wall time of the run */
+  int32_t local_not_converged;   /* local solves that hit max_iters (non-fatal, R18) */
+  int32_t global_not_converged;  /* global solves that hit max_iters: lc_heat_run then returns LC_NOT_CONVERGED */
 } lc_heat_report;
 
 /*
  * Alg. 6 on the device: T (device [nx ny]) in = T^0, out = T^steps.  Every Picard linear
  * system is assembled by lc_heat_assemble and solved by the selected method with x0 = the previous
  * Picard iterate.  picard_per_step / eta_per_step (host, optional, [steps]) receive the
- * Picard count and the mean eta of each step.  Syncs `stream` once per Picard iteration.
+ * Picard count and the mean eta of each step.  Syncs `stream` once per Picard iteration.  Returns
+ * LC_NOT_CONVERGED (non-fatal, T still advanced) when any global linear solve hit its iteration cap.
  */
 lc_status lc_heat_run(const lc_heat_params* p, double* T, int32_t* picard_per_step, double* eta_per_step,
                       void* stream, lc_heat_report* rep);
@@ -333,6 +355,40 @@ lc_status lc_dist_solve_global(lc_dist* ranks, int32_t nr, const double* const* 
                                const lc_solver_params* p, void* stream, lc_solve_info* info);
 
 void lc_dist_destroy(lc_dist D);
+
+/* ---- tuning: kernel / layout choices that never change results beyond the parity bars ----
+ *
+ * Every field selects between implementations of the SAME operation (all of them parity-tested against the
+ * oracle); the defaults are what the library picks on its own.  The setting belongs to the CALLING HOST
+ * THREAD (thread-local; a new thread starts with the defaults) and is read when a call is made: layout
+ * choices when the matrix / subsystem is created, kernel choices when a solve is launched.  No environment
+ * variable is consulted anywhere in the library.
+ */
+typedef struct {
+  int32_t stencil_layout;       /* 1 (default): constant-offset stencils are stored without column indices
+                                   (LC_LAYOUT_STENCIL); 0: always SELL-32 with explicit columns */
+  int32_t symmetric_layout;     /* 0 (default); 1: bitwise-symmetric stencils store diagonal + upper slots */
+  int32_t pcg_cluster_resident; /* 1 (default): stencil systems of <= ~30k rows run the PCG whose vectors stay
+                                   in the shared memory of one thread-block cluster; 0: never */
+  int32_t pcg_cluster;          /* 1 (default): single-segment solves of <= 512 slices launch as ONE cluster with
+                                   hardware cluster barriers; 0: always the cooperative grid */
+  int32_t pcg_tma;              /* 1 (default): TMA bulk-copy ring for the value stream of contiguous solves */
+  int32_t lazy_x_depth;         /* 3 (default) or 2: x updated every 3rd / 2nd PCG iteration (same roundings,
+                                   DESIGN.md s6); 0 or 1: every iteration */
+  int32_t batched_schedule;     /* -1 (default) automatic, 0 lock step, 1 teams (batched PCG, G > 1) */
+  int32_t pcg_max_ctas;         /* 0 (default): occupancy x SMs; > 0 caps the grid of the PCG kernels */
+  int32_t sub_repr;             /* -1 (default) automatic, 0 explicit SELL B, 1 masked on A's stencil layout */
+  int32_t gmres_exact_cgs2;     /* 0 (default): Gram-form CGS2 (R39); 1: the textbook two passes */
+  int32_t gs_lines;             /* 1 (default): 2-D five-point grids take the line-pipelined GS sweep; 0: the
+                                   level schedule */
+} lc_tuning;
+
+/* the defaults listed above (host output) */
+void lc_tuning_defaults(lc_tuning* t);
+/* set the calling thread's tuning (NULL = defaults); LC_ERR_INVALID_ARG for out-of-range fields */
+lc_status lc_set_tuning(const lc_tuning* t);
+/* the calling thread's tuning (host output) */
+lc_status lc_get_tuning(lc_tuning* t);
 
 /* introspection (host outputs, each optional): unknowns n*block, stored scalars, batch, SELL slices, max row
    length (slots), layout (LC_LAYOUT_*), bytes one SpMV streams for the matrix (values + columns + metadata) */

@@ -79,7 +79,7 @@ def _load():
                                     ctypes.POINTER(SolverParams), P, P, ctypes.c_void_p]
         lib.or_heat_run.restype = I32
         lib.or_local_method.argtypes = [I64, P, P, P, P, P, ctypes.POINTER(DomainParams),
-                                        ctypes.POINTER(SolverParams), P, ctypes.POINTER(Report)]
+                                        ctypes.POINTER(SolverParams), P, ctypes.POINTER(Report), P]
         for f in ("or_select_domain", "or_extract", "or_pcg", "or_gmres_bj", "or_local_method"):
             getattr(lib, f).restype = I32
         _lib = lib
@@ -269,16 +269,18 @@ def heat_run(nx, ny, T0, steps, domain: DomainParams | None, solver: SolverParam
     return T, per[:steps], rep
 
 
-def local_method(A: Csr, b, x0, domain: DomainParams | None, solver: SolverParams):
-    """Alg. 1 (domain given) or method0 (domain None).  Returns (x, flag, Report)."""
+def local_method(A: Csr, b, x0, domain: DomainParams | None, solver: SolverParams, want_xt=False):
+    """Alg. 1 (domain given) or method0 (domain None).  Returns (x, flag, Report), plus x~ (Eq. 4, after
+    Alg. 1 l.6, before any GS sweep) when want_xt."""
     b = _c(b, np.float64); x = np.array(x0, dtype=np.float64, copy=True)
     flag = np.zeros(A.n, np.uint8); rep = Report()
+    xt = np.array(x0, dtype=np.float64, copy=True) if want_xt else None
     st = _load().or_local_method(A.n, _p(A.rp), _p(A.ci), _p(A.val), _p(b), _p(x),
                                  ctypes.byref(domain) if domain is not None else None, ctypes.byref(solver),
-                                 _p(flag), ctypes.byref(rep))
+                                 _p(flag), ctypes.byref(rep), _p(xt))
     if st < 0:
         raise RuntimeError(f"or_local_method status {st}")
-    return x, flag, rep
+    return (x, flag, rep, xt) if want_xt else (x, flag, rep)
 
 
 def tau_paper(b, eps):

@@ -577,9 +577,11 @@ static int solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* 
 }
 
 /* method0 when dp == NULL: the global solve from x0.  Otherwise Alg. 1.
-   x: in = x0, out = solution.  flag_out (optional, [n]) receives Omega_local. */
+   x: in = x0, out = solution.  flag_out (optional, [n]) receives Omega_local; xt_out (optional, [n]) receives
+   x~ = Q (xbar_B; x_C^(0)) of Eq. 4 after l.6, before the l.7 sweeps (a copy; no effect on the arithmetic). */
 int or_local_method(int64_t n, const int64_t* rp, const int32_t* ci, const double* a, const double* b, double* x,
-                    const or_domain_params* dp, const or_solver_params* sp, uint8_t* flag_out, or_report* rep) {
+                    const or_domain_params* dp, const or_solver_params* sp, uint8_t* flag_out, or_report* rep,
+                    double* xt_out) {
   memset(rep, 0, sizeof(*rep));
   int st;
   if (dp) {
@@ -611,6 +613,7 @@ int or_local_method(int64_t n, const int64_t* rp, const int32_t* ci, const doubl
       free(idx); free(Brp); free(Bci); free(Ba); free(bsub); free(xB);
     }
     free(flag);
+    if (xt_out) memcpy(xt_out, x, sizeof(double) * n);                                        /* x~ (Eq. 4) */
     if (sp->gs_sweeps > 0) {                                                                 /* l.7 */
       st = or_gauss_seidel(n, rp, ci, a, b, x, sp->gs_sweeps);
       if (st != OR_OK) return st;
@@ -696,7 +699,7 @@ int or_heat_run(int nx, int ny, double dt, int khalf, double Tl, double Tr, int 
       or_heat_assemble(nx, ny, dt, khalf, Tl, Tr, Ts, T, rp, ci, a, b);
       memcpy(Tn, Ts, sizeof(double) * n);                      /* x0 = previous Picard iterate */
       or_report r;
-      st = or_local_method(n, rp, ci, a, b, Tn, dp, sp, NULL, &r);
+      st = or_local_method(n, rp, ci, a, b, Tn, dp, sp, NULL, &r, NULL);
       if (st < 0) goto done;
       rep->it_local += r.it_local; rep->it_global += r.it_global; rep->eta_sum += (double)r.K / n;
       rep->picard_total += 1;

@@ -28,6 +28,20 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def source_sha256() -> str:
+    """Hash of everything that determines liblc.so (sources, header, nvcc flags): stamps measured evidence such as
+    profiles/ncu_traffic.json, so a consumer can tell whether it was measured on the current build."""
+    import hashlib
+    h = hashlib.sha256()
+    deps = sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "lc.h")]
+    for d in deps:
+        h.update(os.path.basename(d).encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(f for f in FLAGS if not f.startswith("-I")).encode())
+    return h.hexdigest()
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB

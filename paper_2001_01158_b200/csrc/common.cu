@@ -1,6 +1,10 @@
 // common.cu -- error plumbing, stream-ordered allocation, the decoupled
 // look-back scan / stream compaction, SELL slice maps.
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <cstdio>
 #include <cstring>
 
@@ -19,16 +23,31 @@ lc_status cuda_fail(cudaError_t e, const char* what) {
 }
 void count_launch(int n) { g_launches += n; }
 
-static bool g_pool_init = false;
+// ---- per-device state (one process may drive several GPUs from several host threads) ----
+static std::mutex g_dev_mu;
+static std::set<int> g_pool_dev;                                        // pools set to keep memory
+static std::map<int, int> g_sms;                                        // SM count per device
+static std::map<std::tuple<int, const void*, int, size_t>, int> g_occ;  // co-resident CTAs per (dev, fn, thr, smem)
+static std::map<std::tuple<int, const void*, int>, int> g_attr;         // function attributes set per device
+
+static lc_status device_of_caller(int* dev) {
+  LC_CUDA(cudaGetDevice(dev));
+  return LC_OK;
+}
+
 lc_status dalloc(void** p, size_t bytes, cudaStream_t s) {
-  if (!g_pool_init) {
-    int dev = 0;
-    LC_CUDA(cudaGetDevice(&dev));
-    cudaMemPool_t pool;
-    LC_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-    uint64_t thr = UINT64_MAX;
-    LC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    g_pool_init = true;
+  int dev = 0;
+  lc_status st = device_of_caller(&dev);
+  if (st) return st;
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (!g_pool_dev.count(dev)) {
+      cudaMemPool_t pool;
+      LC_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+      uint64_t thr = UINT64_MAX;
+      LC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      g_pool_dev.insert(dev);
+    }
   }
   if (bytes == 0) bytes = 16;
   cudaError_t e = cudaMallocAsync(p, bytes, s);
@@ -42,14 +61,68 @@ void dfree(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
 }
 int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto it = g_sms.find(dev);
+  if (it != g_sms.end()) return it->second;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms < 1) sms = 1;
+  g_sms[dev] = sms;
   return sms;
 }
+
+lc_status func_attr(const void* fn, cudaFuncAttribute attr, int value) {
+  int dev = 0;
+  lc_status st = device_of_caller(&dev);
+  if (st) return st;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  const auto key = std::make_tuple(dev, fn, (int)attr);
+  auto it = g_attr.find(key);
+  // the dynamic shared-memory limit only ever grows (a smaller later request keeps the larger opt-in)
+  if (it != g_attr.end() && (it->second == value ||
+                             (attr == cudaFuncAttributeMaxDynamicSharedMemorySize && it->second >= value)))
+    return LC_OK;
+  LC_CUDA(cudaFuncSetAttribute(fn, attr, value));
+  g_attr[key] = value;
+  return LC_OK;
+}
+
+lc_status max_coresident(const void* fn, int threads, size_t dsmem, int64_t* ctas) {
+  int dev = 0;
+  lc_status st = device_of_caller(&dev);
+  if (st) return st;
+  const auto key = std::make_tuple(dev, fn, threads, dsmem);
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) { *ctas = it->second; return LC_OK; }
+  }
+  if (dsmem > 48 * 1024) {
+    st = func_attr(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
+    if (st) return st;
+  }
+  int per_sm = 0;
+  LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, dsmem));
+  if (per_sm < 1) { set_error("kernel does not fit on an SM"); return LC_ERR_CUDA; }
+  const int v = per_sm * num_sms();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  g_occ[key] = v;
+  *ctas = v;
+  return LC_OK;
+}
+
+// ---- tuning (include/lc.h): thread-local, explicit, no environment variables ----
+static lc_tuning defaults_() {
+  lc_tuning t;
+  t.stencil_layout = 1; t.symmetric_layout = 0; t.pcg_cluster_resident = 1; t.pcg_cluster = 1; t.pcg_tma = 1;
+  t.lazy_x_depth = 3; t.batched_schedule = -1; t.pcg_max_ctas = 0; t.sub_repr = -1; t.gmres_exact_cgs2 = 0;
+  t.gs_lines = 1;
+  return t;
+}
+static thread_local lc_tuning g_tune = defaults_();
+const lc_tuning& tuning() { return g_tune; }
 
 void Sell::release(cudaStream_t s) {
   dfree(slice_ptr, s); dfree(slice_row0, s); dfree(slice_seg, s); dfree(seg_unit0, s); dfree(seg_slice0, s);
@@ -266,6 +339,16 @@ lc_status build_slice_map(Sell& M, cudaStream_t s) {
   return LC_OK;
 }
 
+lc_status check_matrix(const lc_matrix_s* M, const char* where) {
+  if (!M) { set_error(std::string(where) + ": null matrix"); return LC_ERR_INVALID_ARG; }
+  if (!M->valid) {
+    set_error(std::string(where) + ": the matrix holds half-written values after a failed lc_update_values "
+              "(call lc_update_values again with valid values, or recreate it)");
+    return LC_ERR_INVALID_ARG;
+  }
+  return LC_OK;
+}
+
 }  // namespace lc
 
 void lc_domain_s::release(cudaStream_t s) {
@@ -282,3 +365,25 @@ void lc_sub_s::release(cudaStream_t s) {
 
 extern "C" const char* lc_last_error(void) { return lc::g_err.c_str(); }
 extern "C" int64_t lc_kernel_launches(void) { return (int64_t)lc::g_launches.load(); }
+
+extern "C" void lc_tuning_defaults(lc_tuning* t) {
+  if (t) *t = lc::defaults_();
+}
+extern "C" lc_status lc_set_tuning(const lc_tuning* t) {
+  if (!t) { lc::g_tune = lc::defaults_(); return LC_OK; }
+  auto bin = [](int32_t v) { return v == 0 || v == 1; };
+  if (!bin(t->stencil_layout) || !bin(t->symmetric_layout) || !bin(t->pcg_cluster_resident) || !bin(t->pcg_cluster) ||
+      !bin(t->pcg_tma) || t->lazy_x_depth < 0 || t->lazy_x_depth > 3 || t->batched_schedule < -1 ||
+      t->batched_schedule > 1 || t->pcg_max_ctas < 0 || t->sub_repr < -1 || t->sub_repr > 1 ||
+      !bin(t->gmres_exact_cgs2) || !bin(t->gs_lines)) {
+    lc::set_error("lc_set_tuning: field out of range");
+    return LC_ERR_INVALID_ARG;
+  }
+  lc::g_tune = *t;
+  return LC_OK;
+}
+extern "C" lc_status lc_get_tuning(lc_tuning* t) {
+  if (!t) { lc::set_error("lc_get_tuning: null argument"); return LC_ERR_INVALID_ARG; }
+  *t = lc::g_tune;
+  return LC_OK;
+}

@@ -768,8 +768,6 @@ DPeer peer_of(char* base, int64_t n) {
   return q;
 }
 
-int g_dmax[6] = {0};    // cached co-resident CTAs per SM x SMs per kernel variant
-
 void* kernel_of(int which, int W) {
   const int wi = W == 5 ? 0 : W == 7 ? 1 : 2;      // 5- / 7-point stencils, else the generic width
   void* const f[6] = {(void*)k_dpcg<5>, (void*)k_dpcg<7>, (void*)k_dpcg<8>,
@@ -812,18 +810,14 @@ lc_status launch(lc_dist* R, int nr, int which, std::vector<DArgs>& args, cudaSt
   for (int i = 1; i < nr; ++i)
     if (R[i]->A.maxw != W) W = 8;                      // mixed widths: the generic variant
   void* fn = kernel_of(which, W);
-  const int ki = which * 3 + (W == 5 ? 0 : W == 7 ? 1 : 2);
-  int tma = (which == 0 && (W == 5 || W == 7) && getenv("LC_NO_TMA") == nullptr) ? 1 : 0;
+  int tma = (which == 0 && (W == 5 || W == 7) && tuning().pcg_tma) ? 1 : 0;
   const size_t dsmem = tma ? (size_t)kDStages * kDW * 32 * W * sizeof(double) : 0;
-  if (!g_dmax[ki]) {
-    int per_sm = 0;
-    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kDT, dsmem));
-    if (per_sm < 1) { set_error("dist kernel does not fit on an SM"); return LC_ERR_CUDA; }
-    g_dmax[ki] = per_sm * num_sms();
-  }
+  int64_t dmax = 0;
+  lc_status st = max_coresident(fn, kDT, dsmem, &dmax);
+  if (st) return st;
   int64_t ns = 1;
   for (int i = 0; i < nr; ++i) ns = std::max<int64_t>(ns, R[i]->A.nslices);
-  int nCTA = (int)std::min<int64_t>(g_dmax[ki] / nr, (ns + kDW - 1) / kDW);
+  int nCTA = (int)std::min<int64_t>(dmax / nr, (ns + kDW - 1) / kDW);
   if (nCTA < 1) nCTA = 1;
   DPack pk;
   memset(&pk, 0, sizeof(pk));
@@ -858,7 +852,7 @@ lc_status run_dpcg(lc_dist* R, int nr, const double* const* b, double* const* xu
     a.x_user = xu[i];
     a.eps = p->rel_tol;
     a.max_iters = p->max_iters;
-    a.lazyx = getenv("LC_NO_LAZY_X") == nullptr ? 1 : 0;
+    a.lazyx = tuning().lazy_x_depth > 1 ? 1 : 0;
     args[i] = a;
     if (!masked) LC_CUDA(cudaMemcpyAsync(R[i]->x, xu[i], sizeof(double) * R[i]->n, cudaMemcpyDeviceToDevice, s));
   }

@@ -455,6 +455,7 @@ extern "C" lc_status lc_select_domain(lc_matrix M, const double* b, const double
   if (!out) { set_error("lc_select_domain: out is NULL"); return LC_ERR_INVALID_ARG; }
   *out = nullptr;
   if (!M || !b || !x0 || !p || !K_host) { set_error("lc_select_domain: null argument"); return LC_ERR_INVALID_ARG; }
+  if (lc_status cs = check_matrix(M, "lc_select_domain")) return cs;
   const int bs = M->block;
   if (p->criterion != LC_CRIT_RESIDUAL && p->criterion != LC_CRIT_GRADIENT) {
     set_error("lc_select_domain: bad criterion"); return LC_ERR_INVALID_ARG;
@@ -474,6 +475,7 @@ extern "C" lc_status lc_select_domain(lc_matrix M, const double* b, const double
     return LC_ERR_INVALID_ARG;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  Touch tA(M->use, s);
   const Sell& A = M->A;
   SellView V = view(A);
   const int64_t m = M->n, ns = A.nslices;
@@ -584,6 +586,7 @@ extern "C" lc_status lc_select_domain(lc_matrix M, const double* b, const double
   for (int g = 0; g <= G; ++g) D->h_seg_base[g] = h_base[g];
   D->K_units = h_base[G];
   for (int g = 0; g < G; ++g) K_host[g] = (int64_t)(h_base[g + 1] - h_base[g]) * bs;
+  D->use.mark(s);
   *out = D;
   return LC_OK;
 fail:
@@ -601,6 +604,7 @@ extern "C" lc_status lc_domain_export(lc_domain D, int32_t* idx_dev, double* tau
                                       double* adm_dev, void* stream) {
   if (!D) { set_error("lc_domain_export: NULL handle"); return LC_ERR_INVALID_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
+  Touch tD(D->use, s);
   int bs = D->A->block;
   if (idx_dev && D->K_units > 0) {
     k_expand_idx<<<(unsigned)((D->K_units + 255) / 256), 256, 0, s>>>(D->idx, D->K_units, bs, idx_dev);
@@ -615,7 +619,7 @@ extern "C" lc_status lc_domain_export(lc_domain D, int32_t* idx_dev, double* tau
 
 extern "C" void lc_destroy_domain(lc_domain D) {
   if (!D) return;
+  D->use.order_free();
   D->release(0);
-  cudaStreamSynchronize(0);
   delete D;
 }

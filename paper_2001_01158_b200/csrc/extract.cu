@@ -13,6 +13,13 @@ namespace lc {
 
 constexpr int kTB = 256;
 
+// out[l] = v[idx[l]] (masked subsystems keep b_sub / x_B0 in A's row numbering)
+__global__ void k_gather_rows(const double* __restrict__ v, const int32_t* __restrict__ idx, int64_t K,
+                              double* __restrict__ out) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < K) out[l] = v[idx[l]];
+}
+
 template <int BS>
 __global__ void __launch_bounds__(kTB) k_extract(SellView A, SellView B, int W, const int32_t* __restrict__ idx,
                                                  const int32_t* __restrict__ inv, const double* __restrict__ b,
@@ -144,7 +151,9 @@ extern "C" lc_status lc_extract_sub(lc_matrix M, lc_domain D, const double* b, c
     set_error("lc_extract_sub: null argument or domain of another matrix");
     return LC_ERR_INVALID_ARG;
   }
+  if (lc_status cs = check_matrix(M, "lc_extract_sub")) return cs;
   cudaStream_t s = (cudaStream_t)stream;
+  Touch tA(M->use, s), tD(D->use, s);
   const int bs = M->block, G = M->batch, bb = bs * bs;
   lc_sub_s* S = new lc_sub_s();
   S->block = bs; S->nseg = G; S->K_units = D->K_units; S->h_seg_base = D->h_seg_base;
@@ -160,7 +169,8 @@ extern "C" lc_status lc_extract_sub(lc_matrix M, lc_domain D, const double* b, c
   }
   B.nslices = nsl;
   B.nslots = 32ll * B.maxw * nsl;
-  if (S->K_units == 0) { *out = S; return LC_OK; }
+  if (S->K_units == 0) { S->use.mark(s);
+  *out = S; return LC_OK; }
   lc_status st = LC_OK;
   const int64_t K = S->K_units;
   const int64_t n = M->n;
@@ -171,11 +181,11 @@ extern "C" lc_status lc_extract_sub(lc_matrix M, lc_domain D, const double* b, c
   // kernel gets the explicit B instead (SELL, 12 B/nnz, only Omega rows): config 5 method2 (eta 0.093, slices
   // 54% filled) local solve 8.70 -> 6.07 ms, config 2 method1 2.31 -> 1.92 ms, config 3 (20 groups) 4.27 ->
   // 3.78 ms; near-full domains (config 5 method1: 44 vs 62 ms) and small ones keep the masked form.
-  // LC_EXPLICIT_SUB=1 / LC_MASKED_SUB=1 force either.
+  // lc_tuning.sub_repr = 0 / 1 forces either.
   bool masked = M->A.stencil && bs == 1;
   if (masked && 2 * K <= n && K >= 65536) masked = false;
-  if (getenv("LC_EXPLICIT_SUB")) masked = false;
-  if (getenv("LC_MASKED_SUB") && M->A.stencil && bs == 1) masked = true;
+  if (tuning().sub_repr == 0) masked = false;
+  if (tuning().sub_repr == 1 && M->A.stencil && bs == 1) masked = true;
   if (masked) {
     // ---- masked representation: B = A[Omega, Omega] applied implicitly on A's stencil layout
     S->masked = 1;
@@ -192,6 +202,8 @@ extern "C" lc_status lc_extract_sub(lc_matrix M, lc_domain D, const double* b, c
     CKC(cudaMemsetAsync(S->bs, 0, sizeof(double) * n, s));
     CKC(cudaMemsetAsync(S->xm0, 0, sizeof(double) * n, s));
     CKC(cudaMemcpyAsync(S->omega, D->flag, n, cudaMemcpyDeviceToDevice, s));
+    CK(dalloc((void**)&S->idx, sizeof(int32_t) * K, s));                 // Omega's rows, for lc_sub_export
+    CKC(cudaMemcpyAsync(S->idx, D->idx, sizeof(int32_t) * K, cudaMemcpyDeviceToDevice, s));
     {
       uint8_t* sflag = (uint8_t*)t;
       int32_t* sinv = (int32_t*)((char*)t + ((nsA + 15) & ~(int64_t)15));
@@ -207,7 +219,8 @@ extern "C" lc_status lc_extract_sub(lc_matrix M, lc_domain D, const double* b, c
       CKC(cudaGetLastError());
     }
     dfree(t, s);
-    *out = S;
+    S->use.mark(s);
+  *out = S;
     return LC_OK;
   }
   CK(dalloc((void**)&B.seg_unit0, sizeof(int32_t) * (G + 1), s));
@@ -238,6 +251,7 @@ extern "C" lc_status lc_extract_sub(lc_matrix M, lc_domain D, const double* b, c
     count_launch();
     CKC(cudaGetLastError());
   }
+  S->use.mark(s);
   *out = S;
   return LC_OK;
 fail:
@@ -249,9 +263,33 @@ fail:
 #undef CKC
 }
 
+extern "C" lc_status lc_sub_export(lc_sub S, double* bsub_dev, double* xB0_dev, void* stream) {
+  if (!S) { set_error("lc_sub_export: NULL handle"); return LC_ERR_INVALID_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  Touch tS(S->use, s);
+  const int64_t len = S->K_units * S->block;
+  if (len > 0) {
+    if (S->masked) {                       // global numbering on A's rows: gather the Omega rows in order
+      if (bsub_dev) {
+        k_gather_rows<<<(unsigned)((len + kTB - 1) / kTB), kTB, 0, s>>>(S->bs, S->idx, len, bsub_dev);
+        LC_LAUNCHED();
+      }
+      if (xB0_dev) {
+        k_gather_rows<<<(unsigned)((len + kTB - 1) / kTB), kTB, 0, s>>>(S->xm0, S->idx, len, xB0_dev);
+        LC_LAUNCHED();
+      }
+    } else {
+      if (bsub_dev) LC_CUDA(cudaMemcpyAsync(bsub_dev, S->bsub, sizeof(double) * len, cudaMemcpyDeviceToDevice, s));
+      if (xB0_dev) LC_CUDA(cudaMemcpyAsync(xB0_dev, S->xB0, sizeof(double) * len, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  LC_CUDA(cudaStreamSynchronize(s));
+  return LC_OK;
+}
+
 extern "C" void lc_destroy_sub(lc_sub S) {
   if (!S) return;
+  S->use.order_free();
   S->release(0);
-  cudaStreamSynchronize(0);
   delete S;
 }

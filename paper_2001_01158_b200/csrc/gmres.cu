@@ -530,28 +530,23 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
   }
 }
 
-static int g_gm_ctas[2] = {0, 0};
-
 lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* scatter_idx, double* x_full,
                     const double* x_init, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
   if (M.nseg != 1) { set_error("GMRES: batched (block-diagonal) systems are not supported"); return LC_ERR_DIMENSION; }
   const int BS = M.block;
   const int m = p->restart;
   const int64_t n = M.nunits * BS;
-  int ci = BS == 1 ? 0 : 1;
   void* fn = BS == 1 ? (void*)k_gmres<1> : (void*)k_gmres<3>;
-  if (!g_gm_ctas[ci]) {
-    int per_sm = 0;
-    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGT, 0));
-    if (per_sm < 1) { set_error("GMRES kernel does not fit on an SM"); return LC_ERR_CUDA; }
-    g_gm_ctas[ci] = std::min(per_sm, 1024 / kGT) * num_sms();
-  }
-  int64_t nCTA = std::min<int64_t>(g_gm_ctas[ci], (M.nslices + kGW - 1) / kGW);
+  int64_t max_ctas = 0;
+  lc_status st = max_coresident(fn, kGT, 0, &max_ctas);
+  if (st) return st;
+  max_ctas = std::min<int64_t>(max_ctas, (int64_t)(1024 / kGT) * num_sms());
+  int64_t nCTA = std::min<int64_t>(max_ctas, (M.nslices + kGW - 1) / kGW);
   if (nCTA < 1) nCTA = 1;
   size_t vbytes = ((sizeof(double) * (size_t)n) + 255) & ~(size_t)255;
   size_t bytes = vbytes * (3 + (m + 1) + (scatter_idx ? 1 : 0)) + sizeof(double) * 2 * kMaxQ * nCTA + sizeof(GridBar) + 384;
   void* ws = nullptr;
-  lc_status st = dalloc(&ws, bytes, s);
+  st = dalloc(&ws, bytes, s);
   if (st) return st;
   char* w = (char*)ws;
   GmresArgs a;
@@ -579,7 +574,7 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   a.eps = p->rel_tol;
   a.m = m;
   a.max_iters = p->max_iters;
-  a.exact_cgs2 = getenv("LC_GMRES_EXACT_CGS2") != nullptr ? 1 : 0;
+  a.exact_cgs2 = tuning().gmres_exact_cgs2;
   int out[2] = {0, 0};
   double rr = 0.0;
   float ms = 0.f;
@@ -598,7 +593,8 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   if (e == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0); cudaEventDestroy(e1);
   if (e != cudaSuccess) return cuda_fail(e, "GMRES kernel");
-  if (info) { info[0].iterations = out[0]; info[0].status = out[1]; info[0].rel_residual = rr; info[0].seconds = ms * 1e-3; }
+  if (info) { info[0].iterations = out[0]; info[0].status = out[1]; info[0].rel_residual = rr; info[0].seconds = ms * 1e-3;
+              info[0].kernel = LC_KERNEL_GMRES; info[0].lazy_x_depth = 1; }
   if (out[1] < 0) set_error("GMRES: non-finite value");
   return (lc_status)out[1];
 }

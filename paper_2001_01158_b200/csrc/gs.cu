@@ -270,6 +270,28 @@ __global__ void k_check_grid(SellView A, int reg_units, Grid3 gr, int64_t n, uns
   }
 }
 
+// structural symmetry of a general (explicit-column) SELL pattern: every stored (u, v), v != u, has (v, u)
+// stored.  The sync-free sweep relies on it (a later row coupled to this slice must wait for its flag).
+__global__ void k_check_pattern_sym(SellView A, int64_t n, int reg_units, int spg, unsigned* bad) {
+  const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  auto slot0 = [&](int64_t v) {
+    const int64_t g = v / reg_units, lv = v - g * reg_units;
+    return A.slice_ptr[g * spg + (lv >> 5)] + (lv & 31);
+  };
+  const int64_t pu = slot0(u);
+  const int lu = A.rowlen[u];
+  for (int k = 0; k < lu; ++k) {
+    const int64_t v = A.col[pu + 32ll * k];
+    if (v == u) continue;
+    const int64_t pv = slot0(v);
+    const int lv = A.rowlen[v];
+    bool found = false;
+    for (int q = 0; q < lv; ++q) found |= (A.col[pv + 32ll * q] == u);
+    if (!found) { atomicOr(bad, 1u); return; }
+  }
+}
+
 }  // namespace lc
 
 using namespace lc;
@@ -277,6 +299,8 @@ using namespace lc;
 extern "C" lc_status lc_smooth_gs(lc_matrix M, const double* b, double* x, int32_t sweeps, void* stream) {
   if (!M || !b || !x || sweeps < 0) { set_error("lc_smooth_gs: null argument or sweeps < 0"); return LC_ERR_INVALID_ARG; }
   if (M->block != 1) { set_error("lc_smooth_gs: needs block = 1"); return LC_ERR_INVALID_ARG; }
+  if (lc_status cs = check_matrix(M, "lc_smooth_gs")) return cs;
+  Touch tA(M->use, (cudaStream_t)stream);
   if (M->A.maxw > kGSMaxW) { set_error("lc_smooth_gs: rows longer than 16 entries are not supported"); return LC_ERR_PATTERN; }
   if (M->A.stencil) {   // structural symmetry of the stencil: the offset set must be symmetric
     for (int k = 0; k < M->A.maxw; ++k) {
@@ -285,8 +309,25 @@ extern "C" lc_status lc_smooth_gs(lc_matrix M, const double* b, double* x, int32
       if (!found) { set_error("lc_smooth_gs: pattern must be structurally symmetric"); return LC_ERR_PATTERN; }
     }
   }
-  if (sweeps == 0) return LC_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (!M->A.stencil && M->pattern_sym < 0) {     // general layout: check the pattern once per matrix
+    DevBuf ws(s);
+    lc_status st = ws.alloc(64);
+    if (st) return st;
+    LC_CUDA(cudaMemsetAsync(ws.p, 0, 64, s));
+    k_check_pattern_sym<<<(unsigned)((M->n + 255) / 256), 256, 0, s>>>(view(M->A), M->n, M->seg_units,
+                                                                          (M->seg_units + 31) / 32, (unsigned*)ws.p);
+    LC_LAUNCHED();
+    unsigned bad = 0;
+    LC_CUDA(cudaMemcpyAsync(&bad, ws.p, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    LC_CUDA(cudaStreamSynchronize(s));
+    M->pattern_sym = bad ? 0 : 1;
+  }
+  if (!M->A.stencil && M->pattern_sym == 0) {
+    set_error("lc_smooth_gs: pattern must be structurally symmetric");
+    return LC_ERR_PATTERN;
+  }
+  if (sweeps == 0) return LC_OK;
   const Sell& A = M->A;
   // ---- regular-grid stencil?  offsets {-(nx ny), -nx, -1, 0, 1, nx, nx ny} (3-D) or {-nx, -1, 0, 1, nx}
   Grid3 gr{0, 0, 0};
@@ -317,10 +358,11 @@ extern "C" lc_status lc_smooth_gs(lc_matrix M, const double* b, double* x, int32
   // 2-D five-point grid: line-pipelined sweep (lines of 128 per CTA, all CTAs co-resident)
   const int64_t glines = (int64_t)gr.ny * M->batch;
   int lines_ok = 0;
-  if (gr.nx > 0 && gr.nz == 1 && getenv("LC_GS_LEVELS") == nullptr) {
-    int per_sm = 0;
-    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_lines, kLB, 0));
-    lines_ok = (glines + kLB - 1) / kLB <= (int64_t)per_sm * num_sms();
+  if (gr.nx > 0 && gr.nz == 1 && tuning().gs_lines) {
+    int64_t mc = 0;
+    lc_status st = max_coresident((const void*)k_gs_lines, kLB, 0, &mc);
+    if (st) return st;
+    lines_ok = (glines + kLB - 1) / kLB <= mc;
   }
   if (lines_ok) {
     const int nCTA = (int)((glines + kLB - 1) / kLB);

@@ -156,6 +156,7 @@ extern "C" lc_status lc_heat_run(const lc_heat_params* hp, double* T, int32_t* p
           st = lc_extract_sub(A, D, b, Tn, s, &S);
           if (st >= 0) st = lc_solve_local(S, &sp, Tn, s, &info);
           if (st >= 0) R.it_local += info.iterations;
+          if (st == LC_NOT_CONVERGED) R.local_not_converged += 1;      // non-fatal (R18)
           lc_destroy_sub(S);
         }
         lc_destroy_domain(D);
@@ -167,6 +168,7 @@ extern "C" lc_status lc_heat_run(const lc_heat_params* hp, double* T, int32_t* p
       }
       st = lc_solve_global(A, b, Tn, &sp, s, &info);                                 // Alg. 1 l.8-11
       if (st < 0) goto done;
+      if (st == LC_NOT_CONVERGED) R.global_not_converged += 1;
       R.it_global += info.iterations;
       // Picard test ||T^{n+1,s+1} - T^{n+1,s}||_2 < tol
       k_diff2_part<<<nbr, kNT, 0, s>>>(Tn, Ts, n, part);
@@ -194,7 +196,7 @@ done:
   cudaStreamSynchronize(s);
   R.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (rep) *rep = R;
-  return st < 0 ? st : LC_OK;
+  return st < 0 ? st : (R.global_not_converged ? LC_NOT_CONVERGED : LC_OK);
 #undef CKH
 #undef CKHC
 }

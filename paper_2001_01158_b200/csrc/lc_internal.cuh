@@ -71,7 +71,14 @@ lc_status run_pcg_dsmem(const PcgJob& job, const lc_solver_params* p, cudaStream
 // stream-ordered device allocation (pool with unlimited release threshold)
 lc_status dalloc(void** p, size_t bytes, cudaStream_t s);
 void dfree(void* p, cudaStream_t s);
-int num_sms();
+int num_sms();                                   // SMs of the calling thread's current device (cached per device)
+// co-resident CTAs (occupancy x SMs) of `fn` on the current device, cached per (device, fn, threads, smem); opts the
+// function into > 48 KB of dynamic shared memory on that device first when needed
+lc_status max_coresident(const void* fn, int threads, size_t dsmem, int64_t* ctas);
+// cudaFuncSetAttribute once per (device, fn, attribute) (function attributes are per device context)
+lc_status func_attr(const void* fn, cudaFuncAttribute attr, int value);
+// the calling thread's tuning (lc_set_tuning; defaults otherwise)
+const lc_tuning& tuning();
 // scoped stream-ordered workspace: freed on every return path (also the early LC_CUDA error returns)
 struct DevBuf {
   void* p = nullptr;
@@ -178,6 +185,26 @@ __device__ __forceinline__ bool sv_real(const SellView& A, int k, int64_t u) {
 __device__ __forceinline__ int sv_len(const SellView& A, int64_t u) { return A.stencil ? A.W : A.rowlen[u]; }
 
 // --------------------------------------------------------------- handles ----
+// The last stream a handle was used on: every entry point records an event there when it returns, and the
+// destroy call makes the legacy stream wait for it before the stream-ordered frees, so a handle destroyed
+// while a non-synchronising call (lc_spmv, lc_extract_sub) is still running on a side stream keeps its
+// memory until that work is done -- without a host synchronisation.
+struct LastUse {
+  cudaEvent_t ev = nullptr;
+  void mark(cudaStream_t s) {
+    if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) { ev = nullptr; cudaGetLastError(); }
+    if (ev) cudaEventRecord(ev, s);
+  }
+  void order_free() {
+    if (ev) { cudaStreamWaitEvent(0, ev, 0); cudaEventDestroy(ev); ev = nullptr; }
+  }
+};
+struct Touch {               // marks `u` on scope exit (all return paths)
+  LastUse& u;
+  cudaStream_t s;
+  Touch(LastUse& use, cudaStream_t st) : u(use), s(st) {}
+  ~Touch() { u.mark(s); }
+};
 }  // namespace lc
 
 struct lc_matrix_s {
@@ -186,6 +213,9 @@ struct lc_matrix_s {
   int64_t nnz = 0;          // stored blocks / scalars of the input
   int32_t seg_units = 0;    // n / batch
   lc::Sell A;
+  int valid = 1;            // 0 after a failed lc_update_values (values half-written): calls refuse the handle
+  int pattern_sym = -1;     // structural symmetry of the pattern (lc_smooth_gs, general layout): -1 unknown
+  lc::LastUse use;
 };
 
 struct lc_domain_s {
@@ -202,6 +232,7 @@ struct lc_domain_s {
   int32_t* seg_base = nullptr;  // [nseg+1] rank offsets (device)
   std::vector<int64_t> h_seg_base;   // [nseg+1] (units)
   std::vector<double> h_tau;         // [nseg]
+  lc::LastUse use;
   void release(cudaStream_t s);
 };
 
@@ -223,6 +254,7 @@ struct lc_sub_s {
   double* bsub = nullptr;   // [K_units*block]
   double* xB0 = nullptr;    // [K_units*block]
   std::vector<int64_t> h_seg_base;
+  lc::LastUse use;
   void release(cudaStream_t s);
 };
 
@@ -454,6 +486,9 @@ lc_status compact_flags(const uint8_t* flag, int64_t m, int32_t* idx, int32_t* i
                         cudaStream_t s);
 // build slice_row0/slice_seg from seg_unit0/seg_slice0 (device)
 lc_status build_slice_map(Sell& M, cudaStream_t s);
+// LC_ERR_INVALID_ARG (with a message naming `where`) for a null handle or one a failed lc_update_values left
+// half-written
+lc_status check_matrix(const lc_matrix_s* M, const char* where);
 // NEXT-4: stencil layout of the rank slab [row0, row0 + n) of an nglob-row matrix (sell.cu)
 lc_status build_slab(int64_t nglob, int64_t row0, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                      const double* values, int on_device, cudaStream_t s, Sell& A, int64_t* nnz_out);

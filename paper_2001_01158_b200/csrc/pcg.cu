@@ -937,8 +937,6 @@ __global__ void __launch_bounds__(kPT, ST == 0 ? LCV_MINB_SELL : LCV_MINB) k_pcg
 }
 
 // ---------------------------------------------------------------- host ----
-static int g_pcg_max_ctas[54] = {0};
-
 lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
   const Sell& M = *job.M;
   const int G = M.nseg;
@@ -964,20 +962,19 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   //    another as G = 1 systems with its own counter barrier (no arrival-tree reduction over all segments).
   // A team's warps walk their slices one after another, so teams pay once each warp has only a few slices:
   // chosen when the rows worked on are <= 4 slices per warp of the grid (config 3: the masked local solves,
-  // eta ~ 9%, 9.2 -> 4.9 ms; the global solves stay in lock step, 55 vs 80 ms with teams).  LC_TEAMS=0/1 forces.
-  const char* tenv = getenv("LC_TEAMS");
+  // eta ~ 9%, 9.2 -> 4.9 ms; the global solves stay in lock step, 55 vs 80 ms with teams).  lc_tuning.batched_schedule forces either.
+  const lc_tuning& tune = tuning();
   const int64_t rows_work = job.rows_hint >= 0 ? job.rows_hint : M.nunits;
   bool team_k = G > 1;
+  lc_status st;
   if (team_k) {
-    if (tenv) team_k = tenv[0] == '1';
+    if (tune.batched_schedule >= 0) team_k = tune.batched_schedule == 1;
     else {
       // the team kernels' occupancy equals the lock-step kernels' (same launch bounds, 64 registers)
-      if (!g_pcg_max_ctas[36 + wi * 2]) {
-        int per_sm = 0;
-        LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[9 + wi], kPT, 0));
-        g_pcg_max_ctas[36 + wi * 2] = std::max(per_sm, 1) * num_sms();
-      }
-      team_k = rows_work <= (int64_t)4 * 32 * kPW * g_pcg_max_ctas[36 + wi * 2];
+      int64_t lock_ctas = 0;
+      st = max_coresident(fns[9 + wi], kPT, 0, &lock_ctas);
+      if (st) return st;
+      team_k = rows_work <= (int64_t)4 * 32 * kPW * lock_ctas;
     }
   }
   // (larger batched solves: lock step; two task-flow schedules measured slower, profiles/r01_aj)
@@ -985,22 +982,17 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   void* fn = fns[wi + 9 * kind];
   // TMA staging for contiguous slice ranges (global solves); slice-list (masked) solves keep plain loads: the
   // per-slice bulk copies were 4% slower there in the bench (profiles/r01_h_tma_ab.txt)
-  const bool tma = M.stencil && (M.maxw == 5 || M.maxw == 7) && G == 1 && !job.slist && getenv("LC_NO_TMA") == nullptr;
+  const bool tma = M.stencil && (M.maxw == 5 || M.maxw == 7) && G == 1 && !job.slist && tune.pcg_tma;
   const size_t dsmem = tma ? (size_t)kStages * kPW * 32 * (M.sym ? M.vw : M.maxw) * sizeof(double) : 0;
-  const int ci = wi * 2 + (tma ? 1 : 0) + 18 * kind;
-  if (!g_pcg_max_ctas[ci]) {
-    if (dsmem > 48 * 1024) LC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
-    int per_sm = 0;
-    LC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPT, dsmem));
-    if (per_sm < 1) { set_error("PCG kernel does not fit on an SM"); return LC_ERR_CUDA; }
-    g_pcg_max_ctas[ci] = per_sm * num_sms();
-  }
+  int64_t max_ctas = 0;
+  st = max_coresident(fn, kPT, dsmem, &max_ctas);
+  if (st) return st;
   const int64_t n = M.nunits;
   const int64_t work = job.slist ? job.nlist_max : M.nslices;
   // small single-segment solves: one cluster of <= 16 CTAs (<= 512 slices = 4 per warp)
-  const bool clus = G == 1 && work <= 16 * kPW * 4 && getenv("LC_NO_CLUSTER") == nullptr;
-  int64_t nCTA = std::min<int64_t>(g_pcg_max_ctas[ci], (std::max<int64_t>(work, 1) + kPW - 1) / kPW);
-  if (const char* cap = getenv("LC_PCG_MAX_CTAS")) nCTA = std::max<int64_t>(1, std::min<int64_t>(nCTA, atoll(cap)));
+  const bool clus = G == 1 && work <= 16 * kPW * 4 && tune.pcg_cluster;
+  int64_t nCTA = std::min<int64_t>(max_ctas, (std::max<int64_t>(work, 1) + kPW - 1) / kPW);
+  if (tune.pcg_max_ctas > 0) nCTA = std::max<int64_t>(1, std::min<int64_t>(nCTA, tune.pcg_max_ctas));
   if (nCTA < 1) nCTA = 1;
   void* ws = nullptr;
   const size_t vec = sizeof(double) * (size_t)n;
@@ -1010,7 +1002,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   const int npv = G == 1 ? 3 : 2;                 // search-direction buffers (3: lazy x of depth 3 possible)
   const size_t bytes = vbytes * (own_x ? 4 + npv : 3 + npv) + sizeof(double) * 2 * G * (2 * nCTA + 1 + 2 * kBarSub) + 16 * G +
                        sizeof(GridBar) + 640 + 128 * (size_t)kMaxSeg;
-  lc_status st = dalloc(&ws, bytes, s);
+  st = dalloc(&ws, bytes, s);
   if (st) return st;
   char* w = (char*)ws;
   PcgArgs a;
@@ -1063,12 +1055,8 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   a.vec2 = (G == 1 && !job.slist &&
             ((((uintptr_t)a.x) | ((uintptr_t)a.r) | ((uintptr_t)a.z) | ((uintptr_t)a.q) | ((uintptr_t)a.p0) |
               ((uintptr_t)a.p1) | ((uintptr_t)a.p2) | ((uintptr_t)M.dinv)) & 15) == 0) ? 1 : 0;
-  // lazy x of depth 3 (LC_LAZY_X_DEPTH=2 or 3; LC_NO_LAZY_X=1: x updated every pass)
-  {
-    const char* dz = getenv("LC_LAZY_X_DEPTH");
-    const int depth = dz ? std::min(3, std::max(1, atoi(dz))) : 3;
-    a.lazyx = (kind == 0 && a.vec2 && getenv("LC_NO_LAZY_X") == nullptr && depth > 1) ? depth : 0;
-  }
+  // lazy x of depth 3 (tuning.lazy_x_depth: 2 or 3; 0 / 1: x updated every pass)
+  a.lazyx = (kind == 0 && a.vec2 && tune.lazy_x_depth > 1) ? tune.lazy_x_depth : 0;
   a.np3 = a.lazyx == 3 ? 1 : 0;
   if (e == cudaSuccess) e = cudaMemsetAsync(a.bar, 0, sizeof(GridBar), s);
   if (e == cudaSuccess && teams) e = cudaMemsetAsync(a.tctr, 0, 128 * (size_t)teams, s);
@@ -1079,11 +1067,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   cudaEventRecord(e0, s);
   void* args[] = {&a};
   if (clus) {
-    static bool nonportable_set[9] = {false};
-    if (!nonportable_set[wi]) {
-      cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      nonportable_set[wi] = true;
-    }
+    if (func_attr(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != LC_OK) cudaGetLastError();
     unsigned csz = (unsigned)std::min<int64_t>(16, std::max<int64_t>(1, (work + 4 * kPW - 1) / (4 * kPW)));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(csz);
@@ -1125,6 +1109,9 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
       info[g].status = stt[g];
       info[g].rel_residual = rr[g];
       info[g].seconds = ms * 1e-3;
+      info[g].kernel = kind == 1 ? LC_KERNEL_PCG_LOCKSTEP : kind == 2 ? LC_KERNEL_PCG_TEAMS
+                       : clus ? LC_KERNEL_PCG_CLUSTER : LC_KERNEL_PCG_GRID;
+      info[g].lazy_x_depth = a.lazyx > 1 ? a.lazyx : 1;
     }
     if (stt[g] < 0) worst = (lc_status)stt[g];
     else if (stt[g] == LC_NOT_CONVERGED && worst == LC_OK) worst = LC_NOT_CONVERGED;

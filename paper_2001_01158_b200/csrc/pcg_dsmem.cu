@@ -231,7 +231,7 @@ static size_t ds_row_bytes(int W) { return (size_t)8 * W + 8 * 8 + 1; }
 bool pcg_dsmem_eligible(const PcgJob& job) {
   const Sell& M = *job.M;
   if (M.nseg != 1 || !M.stencil || M.sym || M.block != 1 || (M.maxw != 5 && M.maxw != 7)) return false;
-  if (job.scatter_idx || getenv("LC_NO_DSMEM")) return false;
+  if (job.scatter_idx || !tuning().pcg_cluster_resident) return false;
   const int64_t rmax = (int64_t)((kSmemBudget - 64) / ds_row_bytes(M.maxw));
   return M.nunits <= rmax * kMaxCluster;
 }
@@ -241,15 +241,12 @@ lc_status run_pcg_dsmem(const PcgJob& job, const lc_solver_params* p, cudaStream
   const int W = M.maxw;
   const int n = (int)M.nunits;
   void* fn = W == 5 ? (void*)k_pcg_ds<5> : (void*)k_pcg_ds<7>;
-  static bool attr_set[2] = {false, false};
-  const int wi = W == 5 ? 0 : 1;
-  if (!attr_set[wi]) {
-    LC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
-    LC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr_set[wi] = true;
-  }
+  lc_status st = func_attr(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+  if (st) return st;
+  st = func_attr(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (st) return st;
   DevBuf ws(s);
-  lc_status st = ws.alloc(64);
+  st = ws.alloc(64);
   if (st) return st;
   DsArgs a;
   a.A = view(M);
@@ -306,6 +303,8 @@ lc_status run_pcg_dsmem(const PcgJob& job, const lc_solver_params* p, cudaStream
     info[0].status = stt;
     info[0].rel_residual = rr;
     info[0].seconds = ms * 1e-3;
+    info[0].kernel = LC_KERNEL_PCG_RESIDENT;
+    info[0].lazy_x_depth = 1;
   }
   if (stt < 0) { set_error("PCG: breakdown or non-finite value (see lc_solve_info.status)"); return (lc_status)stt; }
   return stt == LC_NOT_CONVERGED ? LC_NOT_CONVERGED : LC_OK;

@@ -451,8 +451,7 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
   CK(dalloc((void**)&A.dinv, sizeof(double) * n * bb, s));
   {
     // ---- stencil detection: candidate offsets = those of the first longest row
-    const char* no_st = getenv("LC_DISABLE_STENCIL");
-    if (h_maxw <= kMaxOff && !(no_st && no_st[0] == '1')) {
+    if (h_maxw <= kMaxOff && tuning().stencil_layout) {
       int big = INT32_MAX;
       CKC(cudaMemcpyAsync((char*)t_err + 12, &big, sizeof(int), cudaMemcpyHostToDevice, s));
       unsigned nb = (unsigned)((n + 255) / 256);
@@ -494,8 +493,7 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
         // ---- symmetric stencil?  offsets symmetric and values equal to their mirrors (block 1)
         bool offsym = (h_maxw % 2 == 1) && block == 1;
         for (int k = 0; k < h_maxw && offsym; ++k) offsym = (O.off[k] == -O.off[h_maxw - 1 - k]);
-        const char* sym_env = getenv("LC_SYMMETRIC");     // opt-in until the value stream is TMA-staged
-        if (offsym && sym_env && sym_env[0] == '1') {
+        if (offsym && tuning().symmetric_layout) {       // opt-in (slower in the PCG)
           const int kd = h_maxw / 2;
           unsigned bad = 0;
           CKC(cudaMemsetAsync((char*)t_err + 4, 0, 4, s));
@@ -560,6 +558,7 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
     goto fail;
   }
   dfree(t_rp, s); dfree(t_ci, s); dfree(t_va, s); dfree(t_w, s); dfree(t_err, s);
+  M->use.mark(s);
   *out = M;
   return LC_OK;
 fail:
@@ -590,8 +589,8 @@ extern "C" lc_status lc_matrix_info(lc_matrix A, int64_t* n_unknowns, int64_t* n
 
 extern "C" void lc_destroy_matrix(lc_matrix A) {
   if (!A) return;
+  A->use.order_free();
   A->A.release(0);
-  cudaStreamSynchronize(0);
   delete A;
 }
 
@@ -601,6 +600,7 @@ extern "C" lc_status lc_update_values(lc_matrix M, const int64_t* row_ptr, const
                                       const double* values, int32_t inputs_on_device, void* stream) {
   if (!M || !row_ptr || !col_idx || !values) { set_error("lc_update_values: null argument"); return LC_ERR_INVALID_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
+  Touch tA(M->use, s);
   Sell& A = M->A;
   const int64_t n = M->n;
   const int bb = M->block * M->block;
@@ -625,6 +625,7 @@ extern "C" lc_status lc_update_values(lc_matrix M, const int64_t* row_ptr, const
   }
   CK(dalloc(&t_err, 16, s));
   CKC(cudaMemsetAsync(t_err, 0, 16, s));
+  M->valid = 0;                 // the fill below overwrites the live layout; valid again once the checks pass
   {
     const unsigned nb = (unsigned)((n + 255) / 256);
     if (A.stencil) {
@@ -677,6 +678,7 @@ extern "C" lc_status lc_update_values(lc_matrix M, const int64_t* row_ptr, const
     set_error("lc_update_values: values no longer symmetric (symmetric stencil layout); recreate the matrix");
     goto fail;
   }
+  M->valid = 1;
 fail:
   dfree(t_rp, s); dfree(t_ci, s); dfree(t_va, s); dfree(t_err, s); dfree(t_full, s);
   if (st) cudaStreamSynchronize(s);

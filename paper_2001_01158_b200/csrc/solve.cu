@@ -46,10 +46,13 @@ extern "C" lc_status lc_solve_local(lc_sub S, const lc_solver_params* p, double*
   if (st) return st;
   if (S->K_units == 0) {   // empty Omega: x~ = x0 (R12)
     if (info)
-      for (int g = 0; g < S->nseg; ++g) info[g] = lc_solve_info{0, LC_OK, 0.0, 0.0};
+      for (int g = 0; g < S->nseg; ++g) info[g] = lc_solve_info{0, LC_OK, 0.0, 0.0, LC_KERNEL_NONE, 1};
     return LC_OK;
   }
+  Touch tS(S->use, (cudaStream_t)stream);
   if (S->masked) {
+    if (lc_status cs = check_matrix(S->A, "lc_solve_local")) return cs;
+    Touch tA(S->A->use, (cudaStream_t)stream);
     if (p->method != LC_PCG) {
       set_error("lc_solve_local: GMRES on a masked (stencil, block = 1) subsystem is not supported");
       return LC_ERR_INVALID_ARG;
@@ -73,6 +76,8 @@ extern "C" lc_status lc_solve_global(lc_matrix A, const double* b, double* x, co
   if (!A || !b || !x) { set_error("lc_solve_global: null argument"); return LC_ERR_INVALID_ARG; }
   lc_status st = check_params(p);
   if (st) return st;
+  if (lc_status cs = check_matrix(A, "lc_solve_global")) return cs;
+  Touch tA(A->use, (cudaStream_t)stream);
   return run(A->A, b, x, nullptr, nullptr, nullptr, p, (cudaStream_t)stream, info, A->seg_units,
              (A->seg_units + 31) / 32);
 }

@@ -150,8 +150,10 @@ using namespace lc;
 extern "C" lc_status lc_spmv(lc_matrix M, const double* x, double* y, void* stream) {
   if (!M || !x || !y) { set_error("lc_spmv: null argument"); return LC_ERR_INVALID_ARG; }
   if (x == y) { set_error("lc_spmv: x and y must not alias"); return LC_ERR_INVALID_ARG; }
+  if (lc_status cs = check_matrix(M, "lc_spmv")) return cs;
   const Sell& A = M->A;
   cudaStream_t s = (cudaStream_t)stream;
+  Touch tA(M->use, s);
   const unsigned nb = (unsigned)((A.nslices * 32 + kVT - 1) / kVT);
   const SellView V = view(A);
   if (M->block == 1 && A.stencil && !A.sym && A.maxw == 7)

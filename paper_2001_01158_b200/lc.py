@@ -31,7 +31,8 @@ EXPORTED = ["lc_create_csr", "lc_update_values", "lc_select_domain", "lc_domain_
             "lc_solve_global", "lc_smooth_gs", "lc_heat_assemble", "lc_heat_run", "lc_matrix_info", "lc_destroy_matrix", "lc_destroy_domain",
             "lc_destroy_sub", "lc_spmv", "lc_spmv_csr", "lc_dist_create", "lc_dist_export_handle", "lc_dist_connect", "lc_dist_connect_local",
             "lc_dist_select_domain", "lc_dist_domain_export", "lc_dist_solve_local", "lc_dist_solve_global",
-            "lc_dist_destroy", "lc_last_error", "lc_kernel_launches"]
+            "lc_dist_destroy", "lc_last_error", "lc_kernel_launches", "lc_tuning_defaults", "lc_set_tuning",
+            "lc_get_tuning", "lc_sub_export"]
 DIST_HANDLE_BYTES = 64
 
 
@@ -62,12 +63,26 @@ class HeatParams(ctypes.Structure):
 class HeatReport(ctypes.Structure):
     _fields_ = [("steps", ctypes.c_int32), ("picard_total", ctypes.c_int32), ("picard_max_hit", ctypes.c_int32),
                 ("it_local", ctypes.c_int64), ("it_global", ctypes.c_int64), ("eta_sum", ctypes.c_double),
-                ("seconds", ctypes.c_double)]
+                ("seconds", ctypes.c_double), ("local_not_converged", ctypes.c_int32),
+                ("global_not_converged", ctypes.c_int32)]
 
 
 class SolveInfo(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int32), ("status", ctypes.c_int32), ("rel_residual", ctypes.c_double),
-                ("seconds", ctypes.c_double)]
+                ("seconds", ctypes.c_double), ("kernel", ctypes.c_int32), ("lazy_x_depth", ctypes.c_int32)]
+
+
+KERNELS = {0: "none", 1: "pcg_grid", 2: "pcg_cluster", 3: "pcg_resident", 4: "pcg_lockstep", 5: "pcg_teams",
+           6: "gmres"}
+
+
+class Tuning(ctypes.Structure):
+    """lc_tuning (include/lc.h): implementation choices of the calling thread, all parity-tested."""
+    _fields_ = [("stencil_layout", ctypes.c_int32), ("symmetric_layout", ctypes.c_int32),
+                ("pcg_cluster_resident", ctypes.c_int32), ("pcg_cluster", ctypes.c_int32),
+                ("pcg_tma", ctypes.c_int32), ("lazy_x_depth", ctypes.c_int32), ("batched_schedule", ctypes.c_int32),
+                ("pcg_max_ctas", ctypes.c_int32), ("sub_repr", ctypes.c_int32), ("gmres_exact_cgs2", ctypes.c_int32),
+                ("gs_lines", ctypes.c_int32)]
 
 
 _lib = None
@@ -86,6 +101,8 @@ def load_library(path: str = LIB_PATH):
     lib.lc_select_domain.argtypes = [P, P, P, ctypes.POINTER(DomainParams), P, ctypes.POINTER(P), P]
     lib.lc_domain_export.argtypes = [P, P, P, P, P, P]
     lib.lc_extract_sub.argtypes = [P, P, P, P, P, ctypes.POINTER(P)]
+    lib.lc_sub_export.argtypes = [P, P, P, P]
+    lib.lc_sub_export.restype = ctypes.c_int
     lib.lc_solve_local.argtypes = [P, ctypes.POINTER(SolverParams), P, P, P]
     lib.lc_solve_global.argtypes = [P, P, P, ctypes.POINTER(SolverParams), P, P]
     lib.lc_matrix_info.argtypes = [P, P, P, P, P, P, P, P]
@@ -118,6 +135,12 @@ def load_library(path: str = LIB_PATH):
     for f in ("lc_destroy_matrix", "lc_destroy_domain", "lc_destroy_sub"):
         getattr(lib, f).argtypes = [P]
         getattr(lib, f).restype = None
+    lib.lc_tuning_defaults.argtypes = [ctypes.POINTER(Tuning)]
+    lib.lc_tuning_defaults.restype = None
+    lib.lc_set_tuning.argtypes = [ctypes.POINTER(Tuning)]
+    lib.lc_set_tuning.restype = ctypes.c_int
+    lib.lc_get_tuning.argtypes = [ctypes.POINTER(Tuning)]
+    lib.lc_get_tuning.restype = ctypes.c_int
     lib.lc_last_error.restype = ctypes.c_char_p
     lib.lc_kernel_launches.restype = ctypes.c_int64
     _lib = lib
@@ -146,6 +169,32 @@ def _dptr(t: torch.Tensor, dtype, n=None):
 
 def kernel_launches() -> int:
     return int(load_library().lc_kernel_launches())
+
+
+def tuning_defaults() -> dict:
+    t = Tuning()
+    load_library().lc_tuning_defaults(ctypes.byref(t))
+    return {f: getattr(t, f) for f, _ in Tuning._fields_}
+
+
+def get_tuning() -> dict:
+    t = Tuning()
+    _check(load_library().lc_get_tuning(ctypes.byref(t)), "lc_get_tuning", ok=(LC_OK,))
+    return {f: getattr(t, f) for f, _ in Tuning._fields_}
+
+
+def set_tuning(**fields) -> dict:
+    """Set the calling thread's lc_tuning: the library defaults updated by `fields` (no argument = defaults).
+    Returns the previous setting (pass it back as set_tuning(**prev) to restore)."""
+    prev = get_tuning()
+    t = Tuning()
+    load_library().lc_tuning_defaults(ctypes.byref(t))
+    for k, v in fields.items():
+        if k not in prev:
+            raise KeyError(f"unknown lc_tuning field {k!r}")
+        setattr(t, k, int(v))
+    _check(load_library().lc_set_tuning(ctypes.byref(t)), "lc_set_tuning", ok=(LC_OK,))
+    return prev
 
 
 class Matrix:
@@ -252,6 +301,15 @@ class Sub:
                                    ctypes.byref(h)), "lc_extract_sub", ok=(LC_OK,))
         self.h, self.A, self.K = h, A, list(dom.K)
 
+    def export(self):
+        """-> (b_sub, x_B0): CUDA f64 tensors [sum K] in Omega order (lc_sub_export, Eq. 3)."""
+        tot = int(sum(self.K))
+        bsub = torch.empty(max(tot, 1), dtype=torch.float64, device="cuda")
+        xb0 = torch.empty(max(tot, 1), dtype=torch.float64, device="cuda")
+        _check(load_library().lc_sub_export(self.h, ctypes.c_void_p(bsub.data_ptr()), ctypes.c_void_p(xb0.data_ptr()),
+                                            _stream()), "lc_sub_export", ok=(LC_OK,))
+        return bsub[:tot], xb0[:tot]
+
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
             _lib.lc_destroy_sub(self.h)
@@ -269,8 +327,8 @@ def _solver(method, rel_tol, max_iters, restart):
 
 
 def _infos(arr):
-    return [dict(iterations=i.iterations, status=i.status, rel_residual=i.rel_residual, seconds=i.seconds)
-            for i in arr]
+    return [dict(iterations=i.iterations, status=i.status, rel_residual=i.rel_residual, seconds=i.seconds,
+                 kernel=KERNELS.get(i.kernel, i.kernel), lazy_x_depth=i.lazy_x_depth) for i in arr]
 
 
 def solve_local(sub: Sub, x: torch.Tensor, method=PCG, rel_tol=1e-10, max_iters=20000, restart=30):
@@ -318,21 +376,47 @@ def smooth_gs(A: Matrix, b: torch.Tensor, x: torch.Tensor, sweeps=1):
 
 
 def local_method(A: Matrix, b, x0, domain: dict | None, method=PCG, rel_tol=1e-10, max_iters=20000, restart=30,
-                 gs_sweeps=0):
+                 gs_sweeps=0, keep=False, timing=False):
     """Alg. 1 composed from the C-ABI calls (domain=None: method0): domain (l.2), extraction (l.3-4),
     local solve + assembly (l.5-6), gs_sweeps Gauss-Seidel sweeps (l.7), global solve (l.8-11).
-    Returns (x, report dict)."""
+    Returns (x, report dict).  keep=True also returns the intermediate results for parity checks:
+    rep["idx"] (Omega, ascending rows), rep["tau"], rep["bsub"], rep["xB0"] (Eq. 3, Omega order) and
+    rep["xt"] (x~ of Eq. 4, before any GS sweep).  timing=True: rep["ms"] = CUDA-event times of the phases on
+    the current stream (select = l.2, extract = l.3-4, local = l.5-6, gs = l.7, global = l.8-11)."""
+    ev = {}
+
+    def mark(k):
+        if timing:
+            ev[k] = torch.cuda.Event(enable_timing=True)
+            ev[k].record()
+    mark("start")
     x = x0.clone()
     rep = {"K": [0] * A.batch}
     if domain is not None:
         dom = select_domain(A, b, x0, **domain)
+        mark("select")
         rep["K"] = dom.K
+        if keep:
+            idx, tau, _, _ = dom.export()
+            rep["idx"], rep["tau"] = idx, tau
         if sum(dom.K) > 0:
             sub = extract_sub(A, dom, b, x0)
+            mark("extract")
+            if keep:
+                rep["bsub"], rep["xB0"] = sub.export()
             rep["local"] = solve_local(sub, x, method, rel_tol, max_iters, restart)
+        mark("local")
+        if keep:
+            rep["xt"] = x.clone()
         if gs_sweeps > 0:
             smooth_gs(A, b, x, gs_sweeps)
+        mark("gs")
     rep["global"] = solve_global(A, b, x, method, rel_tol, max_iters, restart)
+    mark("global")
+    if timing:
+        ev["global"].synchronize()
+        order = [k for k in ("start", "select", "extract", "local", "gs", "global") if k in ev]
+        rep["ms"] = {k: ev[p].elapsed_time(ev[k]) for p, k in zip(order, order[1:])}
     return x, rep
 
 
@@ -354,7 +438,8 @@ def heat_assemble(nx, ny, dt, Ts: torch.Tensor, Told: torch.Tensor, khalf=3, t_l
 
 def heat_run(nx, ny, T0: torch.Tensor, steps, method=0, alpha=1e-4, e_max=1, gs_sweeps=1, dt=1e-2, khalf=3,
              t_left=1.0, t_right=1e-4, picard_tol=1e-8, picard_max=100, rel_tol=1e-10):
-    """Alg. 6 on the device (lc_heat_run).  Returns (T, picard counts per step, mean eta per step, report)."""
+    """Alg. 6 on the device (lc_heat_run).  Returns (T, picard counts per step, mean eta per step, report);
+    report.global_not_converged counts global solves that hit their cap (LC_NOT_CONVERGED, non-fatal)."""
     import numpy as np
     p = HeatParams(nx, ny, dt, khalf, t_left, t_right, steps, picard_tol, picard_max, method, alpha, e_max,
                    gs_sweeps, rel_tol)
@@ -363,7 +448,7 @@ def heat_run(nx, ny, T0: torch.Tensor, steps, method=0, alpha=1e-4, e_max=1, gs_
     eta = np.zeros(max(steps, 1), np.float64)
     rep = HeatReport()
     _check(load_library().lc_heat_run(ctypes.byref(p), _dptr(T, torch.float64, nx * ny), per.ctypes.data, eta.ctypes.data,
-                            _stream(), ctypes.byref(rep)), "lc_heat_run", ok=(LC_OK,))
+                            _stream(), ctypes.byref(rep)), "lc_heat_run")
     return T, per[:steps], eta[:steps], rep
 
 

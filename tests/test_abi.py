@@ -36,15 +36,37 @@ def test_every_declared_symbol_is_exported(lib):
     assert set(lc.EXPORTED) == set(header_functions())
 
 
-def test_struct_layouts_match_header():
-    # lc_domain_params: int32, int32, double, int32, int32 -> 24 bytes with natural alignment
-    assert ctypes.sizeof(lc.DomainParams) == 24
-    assert lc.DomainParams.param.offset == 8
-    # lc_solver_params: int32 x3, double, int32 -> 32 bytes
-    assert ctypes.sizeof(lc.SolverParams) == 32
-    assert lc.SolverParams.rel_tol.offset == 16
-    # lc_solve_info: int32, int32, double, double -> 24 bytes
-    assert ctypes.sizeof(lc.SolveInfo) == 24
+STRUCTS = {"lc_domain_params": "DomainParams", "lc_solver_params": "SolverParams", "lc_solve_info": "SolveInfo",
+           "lc_heat_params": "HeatParams", "lc_heat_report": "HeatReport", "lc_tuning": "Tuning"}
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """Every struct of include/lc.h has the binding's size and field offsets: a C program compiled against the
+    header prints sizeof / offsetof, compared with the ctypes layouts."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("gcc missing")
+    lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "lc.h"', 'int main(void) {']
+    for cname, pyname in STRUCTS.items():
+        st = getattr(lc, pyname)
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in st._fields_:
+            lines.append(f'  printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ['  return 0;', '}']
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = {}
+    for line in subprocess.check_output([str(exe)], text=True).splitlines():
+        c, f, v = line.split()
+        got[(c, f)] = int(v)
+    for cname, pyname in STRUCTS.items():
+        st = getattr(lc, pyname)
+        assert got[(cname, "size")] == ctypes.sizeof(st), cname
+        for f, _ in st._fields_:
+            assert got[(cname, f)] == getattr(st, f).offset, (cname, f)
 
 
 def test_no_cpu_fallback_without_device(lib):
@@ -77,3 +99,34 @@ def test_sass_is_sm100a():
         pytest.skip("cuobjdump missing")
     out = subprocess.run([exe, "--list-elf", lc.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_tuning_host_only_roundtrip(lib):
+    """lc_tuning lives on the host (no device needed): defaults, range checks, thread-local set / get."""
+    import threading
+    d = lc.tuning_defaults()
+    assert d == dict(stencil_layout=1, symmetric_layout=0, pcg_cluster_resident=1, pcg_cluster=1, pcg_tma=1,
+                     lazy_x_depth=3, batched_schedule=-1, pcg_max_ctas=0, sub_repr=-1, gmres_exact_cgs2=0,
+                     gs_lines=1)
+    assert lc.get_tuning() == d
+    prev = lc.set_tuning(lazy_x_depth=2, batched_schedule=1)
+    try:
+        assert lc.get_tuning()["lazy_x_depth"] == 2 and lc.get_tuning()["batched_schedule"] == 1
+        seen = {}
+        th = threading.Thread(target=lambda: seen.update(lc.get_tuning()))
+        th.start(); th.join()
+        assert seen == d                                   # other threads keep the defaults
+        for bad in (dict(lazy_x_depth=4), dict(batched_schedule=2), dict(stencil_layout=2), dict(sub_repr=-2),
+                    dict(pcg_max_ctas=-1)):
+            with pytest.raises(lc.LcError):
+                lc.set_tuning(**bad)
+    finally:
+        lc.set_tuning(**prev)
+    assert lc.get_tuning() == d
+
+
+def test_library_reads_no_environment():
+    """No getenv in the product library (every implementation choice is an explicit lc_tuning field)."""
+    import glob
+    for f in glob.glob(os.path.join(ROOT, "paper_2001_01158_b200", "csrc", "*")):
+        assert "getenv" not in open(f).read(), f

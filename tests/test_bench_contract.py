@@ -37,3 +37,34 @@ def test_reference_arm_other_ranks_silent():
                {"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.strip() == ""
+
+
+def test_cpu_baseline_workers():
+    """The cpu_baseline leg's pinned oracle processes (host logic only): fed the oracle's own results as the
+    'GPU' side, they time complete solves and report exact parity (no near / cascade differences)."""
+    sys.path.insert(0, ROOT)
+    import numpy as np
+
+    import bench
+    import oracle as orc
+    import synth
+    sy = synth.system(1, 4)
+    rules, solver = bench.CFG_RULES[1]
+    A = orc.Csr(sy.rp, sy.ci, sy.val)
+    runs = {}
+    for name, rule in rules:
+        sp = orc.SolverParams(0, 1, 30, 1e-10, 20000, 0)
+        if rule is None:
+            x, _, rep = orc.local_method(A, sy.b, sy.x0, None, sp)
+            runs[name] = (x, None, {"local": [0], "global": [rep.it_global]})
+        else:
+            dp = orc.DomainParams(rule["criterion"], rule["threshold"], rule["param"], 0, 0, 1)
+            x, flag, rep = orc.local_method(A, sy.b, sy.x0, dp, sp)
+            runs[name] = (x, np.flatnonzero(flag).astype(np.int32), {"local": [rep.it_local], "global": [rep.it_global]})
+    cb, parity = bench.CpuBaseline(1, sy, rules, solver, 0, runs).result()
+    assert cb["kind"] == "oracle" and cb["cores"] == 1 and cb["value"] > 0
+    assert len(cb["processes"]) == len(rules) and cb["host"]["nproc"] >= 1
+    for name, _ in rules:
+        p = parity["by_rule"][name]
+        assert p["max_x_rel_err"] == 0.0 and p["max_it_global_diff"] == 0
+    assert parity["by_rule"]["method2"]["omega_bit_exact"] and parity["by_rule"]["method2"]["near"] == 0

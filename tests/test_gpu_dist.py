@@ -166,7 +166,7 @@ def test_dist_matches_single_gpu_path_config5_full():
 
 
 @pytest.mark.parametrize("P", [1, 3])
-def test_dist_lazy_x_bitwise(P, monkeypatch):
+def test_dist_lazy_x_bitwise(P, tune):
     """Lazy x in the row-partitioned PCG (x updated every second iteration with the same fma roundings, the
     CONFIRM pass gathering x plus its pending update from the neighbour slabs) gives bitwise the solution
     of the every-pass update, local and global solves."""
@@ -174,9 +174,9 @@ def test_dist_lazy_x_bitwise(P, monkeypatch):
     outs = []
     for lazy in (True, False):
         if lazy:
-            monkeypatch.delenv("LC_NO_LAZY_X", raising=False)
+            tune(lazy_x_depth=3)
         else:
-            monkeypatch.setenv("LC_NO_LAZY_X", "1")
+            tune(lazy_x_depth=1)
         ranks, R = make_ranks(sy, P)
         b, x0 = slabs(sy.b, R), slabs(sy.x0, R)
         x, rep = lc.dist_local_method(ranks, b, x0, R_RES, rel_tol=EPS)

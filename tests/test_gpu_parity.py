@@ -106,17 +106,30 @@ def to_dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
 
 
+# near-threshold / cascaded index-set differences seen by check_system (reported in the session summary, conftest)
+NEAR_LOG = []
+
+
 def check_system(sy, rule, check_solution=True):
+    """Alg. 1 through the C-ABI vs the oracle's Alg. 1 on the same inputs, segment by segment (C-P rules):
+    Omega bit-exact outside the 1e-12 window (near / cascaded differences counted into NEAR_LOG), tau, the
+    criterion values bit-exact, b_sub and x_B0 of Eq. 3 bit-exact (when the sets agree), x~ of Eq. 4 within
+    1e-9 of the oracle's x~ with its complement bitwise x0 (Eq. 4 keeps x_C^(0)), iterations +-1 (local and
+    global), the final x within 1e-9, Eq. 6 re-checked by the oracle's residual."""
     cfg = sy.config
     cell = sy.block
     Ao = oracle_csr(sy)
     A = gpu_matrix(sy)
     b, x0 = to_dev(sy.b), to_dev(sy.x0)
     dom = lc.select_domain(A, b, x0, **rule)
-    idx, taus, crit, adm = dom.export(want_crit=True, want_adm=True)
-    idx = idx.cpu().numpy()
-    x_gpu, rep = lc.local_method(A, b, x0, rule, method=method_of(cfg))
+    _, _, crit, adm = dom.export(want_crit=True, want_adm=True)
+    x_gpu, rep = lc.local_method(A, b, x0, rule, method=method_of(cfg), keep=True)
     x_gpu = x_gpu.cpu().numpy()
+    idx = rep["idx"].cpu().numpy()
+    taus = rep["tau"]
+    xt_gpu = rep["xt"].cpu().numpy()
+    bsub_gpu = rep["bsub"].cpu().numpy() if "bsub" in rep else None
+    xb0_gpu = rep["xB0"].cpu().numpy() if "xB0" in rep else None
     stats = []
     off = 0
     for g, (r0, r1) in enumerate(segments(sy)):
@@ -126,7 +139,6 @@ def check_system(sy, rule, check_solution=True):
                               rule["expand_rounds"], rule["dilate_hops"], cell)
         Kg = rep["K"][g]
         gi = idx[off:off + Kg]
-        off += Kg
         units = (gi[::cell] - r0) // cell
         assert np.all(np.diff(gi) > 0), "GPU index set not ascending"
         # tau agreement (same arithmetic up to the DD rounding, R23)
@@ -135,7 +147,22 @@ def check_system(sy, rule, check_solution=True):
         cg = crit.cpu().numpy()[(r0 // cell):(r1 // cell)]
         np.testing.assert_array_equal(cg, d.crit)
         near, casc = compare_sets(As, units, d, cell)
-        xo, _, ro = orc.local_method(As, bs_, x0s, oracle_dp(rule, cell), oracle_sp(cfg))
+        same_set = np.array_equal(gi - r0, np.flatnonzero(d.flag))
+        xo, _, ro, xto = orc.local_method(As, bs_, x0s, oracle_dp(rule, cell), oracle_sp(cfg), want_xt=True)
+        # Eq. 4: the complement of the GPU's Omega keeps x0 bitwise
+        xt = xt_gpu[r0:r1]
+        comp = np.ones(r1 - r0, bool)
+        comp[gi - r0] = False
+        np.testing.assert_array_equal(xt[comp], x0s[comp])
+        if same_set and Kg > 0:
+            # Eq. 3 element by element against the oracle's extraction on the same set (same fma chains, R22)
+            so = orc.extract(As, bs_, x0s, d.flag)
+            np.testing.assert_array_equal(bsub_gpu[off:off + Kg], so.bsub)
+            np.testing.assert_array_equal(xb0_gpu[off:off + Kg], so.xB0)
+            # x~ (Eq. 4) against the oracle's x~
+            err_t = np.linalg.norm(xt - xto) / np.linalg.norm(xto)
+            assert err_t <= 1e-9, ("x~", g, err_t)
+        off += Kg
         if Kg > 0 and d.K > 0:
             assert abs(rep["local"][g]["iterations"] - ro.it_local) <= 1, (g, rep["local"][g], ro.it_local)
         assert abs(rep["global"][g]["iterations"] - ro.it_global) <= 1, (g, rep["global"][g], ro.it_global)
@@ -146,6 +173,8 @@ def check_system(sy, rule, check_solution=True):
             # Eq. 6 re-checked independently, and the manufactured bound (R31)
             res = np.linalg.norm(orc.residual(As, bs_, xs))
             assert res <= EPS * np.linalg.norm(bs_) * (1 + 1e-6)
+        if near or casc:
+            NEAR_LOG.append(dict(config=cfg, s=sy.s, n=sy.n, segment=g, rule=rule, K=int(Kg), near=near, cascade=casc))
         stats.append((Kg, near, casc))
     return stats
 
@@ -174,10 +203,10 @@ def test_config3_reduced_batched(n, G, s):
 
 @pytest.mark.parametrize("sched", ["0", "1"])
 @pytest.mark.parametrize("n,G,s", [(30, 4, 0), (64, 20, 3)])
-def test_config3_batched_schedules(n, G, s, sched, monkeypatch):
-    """Both batched PCG schedules (LC_TEAMS=0: the grid sweeps all active groups in lock step; 1: one team of
+def test_config3_batched_schedules(n, G, s, sched, tune):
+    """Both batched PCG schedules (batched_schedule 0: the grid sweeps all active groups in lock step; 1: one team of
     CTAs per group) against the oracle; the automatic choice is exercised by test_config3_reduced_batched."""
-    monkeypatch.setenv("LC_TEAMS", sched)
+    tune(batched_schedule=int(sched))
     sy = synth.system(3, s, n=n, G=G)
     check_system(sy, RULES[3][0])
 
@@ -276,55 +305,54 @@ def test_determinism_bitwise():
 
 @pytest.mark.parametrize("lazy", ["3", "2", "off"])
 @pytest.mark.parametrize("cfg,n,s,rule", [(5, 33, 4, 0), (5, 30, 9, 1), (2, 100, 7, 0), (1, 64, 2, 0)])
-def test_lazy_x_depths_parity(cfg, n, s, rule, lazy, monkeypatch):
+def test_lazy_x_depths_parity(cfg, n, s, rule, lazy, tune):
     """The flat single-segment update pass with x updated every 3rd / 2nd / every iteration (lazy x, DESIGN s6)
     on the grid-wide k_pcg: the same parity bars, and the solutions of the three variants bitwise equal (the
     deferred updates apply the same fma roundings in the same order)."""
-    monkeypatch.setenv("LC_NO_DSMEM", "1")
-    monkeypatch.setenv("LC_NO_CLUSTER", "1")
+    tune(pcg_cluster_resident=0)
+    tune(pcg_cluster=0)
     if lazy == "off":
-        monkeypatch.setenv("LC_NO_LAZY_X", "1")
+        tune(lazy_x_depth=1)
     else:
-        monkeypatch.setenv("LC_LAZY_X_DEPTH", lazy)
+        tune(lazy_x_depth=int(lazy))
     sy = synth.system(cfg, s, n=n)
     check_system(sy, RULES[cfg][rule])
     A = gpu_matrix(sy)
     x = to_dev(sy.x0)
     lc.solve_global(A, to_dev(sy.b), x)
-    monkeypatch.setenv("LC_NO_LAZY_X", "1")
+    tune(lazy_x_depth=1)
     x_ref = to_dev(sy.x0)
     lc.solve_global(A, to_dev(sy.b), x_ref)
     assert torch.equal(x, x_ref)
 
 
-@pytest.mark.parametrize("sub", ["LC_EXPLICIT_SUB", "LC_MASKED_SUB"])
+@pytest.mark.parametrize("sub", [0, 1])
 @pytest.mark.parametrize("cfg,n,s,rule", [(5, 33, 4, 0), (5, 40, 12, 1), (2, 128, 30, 0), (1, 64, 5, 0),
                                           (3, 48, 6, 0), (3, 30, 2, 0)])
-def test_subsystem_representations(cfg, n, s, rule, sub, monkeypatch):
+def test_subsystem_representations(cfg, n, s, rule, sub, tune):
     """Both subsystem representations of a stencil matrix (masked on A's layout / explicit SELL B of the Omega
     rows, chosen by size in lc_extract_sub) against the oracle, on the grid kernels and the small-system ones."""
-    monkeypatch.setenv(sub, "1")
+    tune(sub_repr=sub)
     sy = synth.system(cfg, s, n=n)
     check_system(sy, RULES[cfg][rule])
 
 
 @pytest.mark.parametrize("depth", ["3", "2"])
-def test_lazy_x_confirm_reset_and_cap(depth, monkeypatch):
+def test_lazy_x_confirm_reset_and_cap(depth, tune):
     """A tolerance below what the true residual can reach makes every recursive-residual convergence fail its
     true-residual confirmation (CONFIRM -> RESET with x updates pending) until the iteration cap: the lazy-x
     solve ends with the same status, iteration count and bitwise the same x as the every-pass update."""
-    monkeypatch.setenv("LC_NO_DSMEM", "1")
-    monkeypatch.setenv("LC_NO_CLUSTER", "1")
+    tune(pcg_cluster_resident=0)
+    tune(pcg_cluster=0)
     sy = synth.system(5, 6, n=24)
     A = gpu_matrix(sy)
     b = to_dev(sy.b)
     res = {}
     for mode in ("lazy", "off"):
         if mode == "lazy":
-            monkeypatch.delenv("LC_NO_LAZY_X", raising=False)
-            monkeypatch.setenv("LC_LAZY_X_DEPTH", depth)
+            tune(lazy_x_depth=int(depth))
         else:
-            monkeypatch.setenv("LC_NO_LAZY_X", "1")
+            tune(lazy_x_depth=1)
         for cap in (301, 302, 303):
             x = to_dev(sy.x0)
             try:
@@ -339,19 +367,19 @@ def test_lazy_x_confirm_reset_and_cap(depth, monkeypatch):
 
 
 @pytest.mark.parametrize("path", ["grid", "lock", "team", "gmres"])
-def test_determinism_short_passes(path, monkeypatch):
+def test_determinism_short_passes(path, tune):
     """Repeated solves with very short passes (tiny systems on the multi-CTA kernels, where a CTA leaving a
     barrier early races ahead of slower CTAs) are bitwise identical: guards the per-CTA partial buffers and
     the barrier/reduction protocols (a partial overwritten before it was read showed up here as breakdowns
     or run-to-run differences)."""
     if path == "grid":
-        monkeypatch.setenv("LC_NO_DSMEM", "1")
-        monkeypatch.setenv("LC_NO_CLUSTER", "1")
+        tune(pcg_cluster_resident=0)
+        tune(pcg_cluster=0)
         sy = synth.system(1, 4, n=40)
     elif path == "gmres":
         sy = synth.system(4, 4, n=16)
     else:
-        monkeypatch.setenv("LC_TEAMS", "1" if path == "team" else "0")
+        tune(batched_schedule=1 if path == "team" else 0)
         sy = synth.system(3, 5, n=30, G=6)
     A = gpu_matrix(sy)
     b, x0 = to_dev(sy.b), to_dev(sy.x0)
@@ -400,11 +428,11 @@ def test_random_tiny_systems_vs_dense():
 
 @pytest.mark.parametrize("dsmem", [True, False])
 @pytest.mark.parametrize("n", [1, 2, 31, 33])
-def test_tiny_stencil_systems(n, dsmem, monkeypatch):
+def test_tiny_stencil_systems(n, dsmem, tune):
     """Degenerate sizes on both PCG paths (cluster-resident / grid): 1, 2 rows, one slice minus / plus one
     row.  A tridiagonal (3-offset stencil, generic width) and the oracle's PCG."""
     if not dsmem:
-        monkeypatch.setenv("LC_NO_DSMEM", "1")
+        tune(pcg_cluster_resident=0)
     M = np.eye(n) * 3.0
     for i in range(n - 1):
         M[i, i + 1] = M[i + 1, i] = -1.0
@@ -421,10 +449,10 @@ def test_tiny_stencil_systems(n, dsmem, monkeypatch):
 
 
 @pytest.mark.parametrize("path", ["dsmem", "grid", "gmres"])
-def test_zero_rhs_absolute_tolerance(path, monkeypatch):
+def test_zero_rhs_absolute_tolerance(path, tune):
     """b = 0: the tolerance becomes absolute (eps, Eq. 6 with ||b|| = 0); the solution is driven to ~0."""
     if path == "grid":
-        monkeypatch.setenv("LC_NO_DSMEM", "1")
+        tune(pcg_cluster_resident=0)
     sy = synth.system(1, 2) if path != "gmres" else synth.system(4, 2, n=16)
     A = gpu_matrix(sy)
     b = torch.zeros(sy.N, dtype=torch.float64, device=DEV)
@@ -436,11 +464,11 @@ def test_zero_rhs_absolute_tolerance(path, monkeypatch):
 
 
 @pytest.mark.parametrize("path", ["dsmem", "grid"])
-def test_nonfinite_and_iteration_cap(path, monkeypatch):
+def test_nonfinite_and_iteration_cap(path, tune):
     """NaN in b -> LC_ERR_NONFINITE reported (no hang); max_iters = 3 -> LC_NOT_CONVERGED with the best
     iterate, iterations = 3 (non-fatal, R18)."""
     if path == "grid":
-        monkeypatch.setenv("LC_NO_DSMEM", "1")
+        tune(pcg_cluster_resident=0)
     sy = synth.system(1, 4)
     A = gpu_matrix(sy)
     b = to_dev(sy.b)
@@ -495,11 +523,11 @@ def test_local_method_1d_three_point(rule):
 
 
 @pytest.mark.parametrize("path", ["dsmem", "grid"])
-def test_max_iters_zero_is_the_eq6_check(path, monkeypatch):
+def test_max_iters_zero_is_the_eq6_check(path, tune):
     """max_iters = 0: only the Eq. 6 check at the start (as the oracle): 0 iterations, x untouched, status
     LC_NOT_CONVERGED when the start does not satisfy Eq. 6 (tools/param_study.py relies on it)."""
     if path == "grid":
-        monkeypatch.setenv("LC_NO_DSMEM", "1")
+        tune(pcg_cluster_resident=0)
     sy = synth.system(1, 5)
     A = gpu_matrix(sy)
     x = to_dev(sy.x0)
@@ -556,10 +584,10 @@ def test_non_default_stream():
 
 
 @pytest.mark.parametrize("case", ["c5", "c1", "c3", "c4", "sell", "tridiag"])
-def test_spmv_bitexact(case, monkeypatch):
+def test_spmv_bitexact(case, tune):
     """lc_spmv (y = A x) equals the oracle's or_spmv bitwise on every layout / width / block size."""
     if case == "sell":
-        monkeypatch.setenv("LC_DISABLE_STENCIL", "1")
+        tune(stencil_layout=0)
     if case == "tridiag":
         n = 1000
         M = np.eye(n) * 3.0
@@ -694,10 +722,10 @@ def test_full_size_local_method_vs_oracle(cfg, s, rule):
 @pytest.mark.parametrize("layout", ["sell", "symstencil"])
 @pytest.mark.parametrize("cfg,n,s,rule", [(1, 64, 4, 0), (3, 30, 3, 0), (4, 24, 2, 0), (5, 20, 6, 0), (5, 20, 6, 1),
                                           (2, 64, 11, 0)])
-def test_other_layouts_parity(cfg, n, s, rule, layout, monkeypatch):
+def test_other_layouts_parity(cfg, n, s, rule, layout, tune):
     """The explicit-column SELL-32 layout (rows without a common stencil) and the symmetric stencil layout
-    (opt-in, LC_SYMMETRIC=1) against the oracle; the default runs use the stencil layout."""
-    monkeypatch.setenv("LC_DISABLE_STENCIL" if layout == "sell" else "LC_SYMMETRIC", "1")
+    (opt-in, lc_tuning.symmetric_layout) against the oracle; the default runs use the stencil layout."""
+    tune(**({"stencil_layout": 0} if layout == "sell" else {"symmetric_layout": 1}))
     if cfg == 4 and layout == "symstencil":
         layout = "stencil"                      # the 3T blocks are nonsymmetric: never symmetric storage
     sy = synth.system(cfg, s, n=n, G=4)
@@ -707,10 +735,10 @@ def test_other_layouts_parity(cfg, n, s, rule, layout, monkeypatch):
 
 
 @pytest.mark.parametrize("cfg,n,s,rule", [(1, 64, 4, 0), (1, 64, 8, 0), (5, 20, 6, 0), (2, 96, 5, 0)])
-def test_grid_kernel_path_parity(cfg, n, s, rule, monkeypatch):
-    """Small stencil systems run the cluster-resident PCG (k_pcg_ds) by default; LC_NO_DSMEM=1 sends them
+def test_grid_kernel_path_parity(cfg, n, s, rule, tune):
+    """Small stencil systems run the cluster-resident PCG (k_pcg_ds) by default; pcg_cluster_resident = 0 sends them
     through the grid-wide kernel (k_pcg, its cluster form for <= 512 slices) instead: both against the oracle."""
-    monkeypatch.setenv("LC_NO_DSMEM", "1")
+    tune(pcg_cluster_resident=0)
     check_system(synth.system(cfg, s, n=n), RULES[cfg][rule])
 
 
@@ -724,12 +752,12 @@ def test_dsmem_and_grid_kernels_agree():
         b, x0 = to_dev(sy.b), to_dev(sy.x0)
         xa = x0.clone()
         ia = lc.solve_global(A, b, xa)[0]
-        os.environ["LC_NO_DSMEM"] = "1"
+        prev = lc.set_tuning(pcg_cluster_resident=0)
         try:
             xb = x0.clone()
             ib = lc.solve_global(A, b, xb)[0]
         finally:
-            del os.environ["LC_NO_DSMEM"]
+            lc.set_tuning(**prev)
         assert abs(ia["iterations"] - ib["iterations"]) <= 1
         xa, xb = xa.cpu().numpy(), xb.cpu().numpy()
         assert np.linalg.norm(xa - xb) / np.linalg.norm(xb) <= 1e-9
@@ -765,7 +793,7 @@ def test_irregular_pattern_uses_general_layout():
 # ------------------------------------------------- NEXT-1: Gauss-Seidel smoothing --
 
 @pytest.mark.parametrize("case", ["c1", "c5", "c3", "band", "general", "sweeps3"])
-def test_gs_sweep_bitexact(case, monkeypatch):
+def test_gs_sweep_bitexact(case, tune):
     """lc_smooth_gs reproduces the sequential natural-order sweep of the oracle bit for bit."""
     sweeps = 1
     if case == "c1":
@@ -777,7 +805,7 @@ def test_gs_sweep_bitexact(case, monkeypatch):
     elif case == "band":
         sy = synth.random_system(1000, bw=3, spd=True, seed=77)
     elif case == "general":
-        monkeypatch.setenv("LC_DISABLE_STENCIL", "1")
+        tune(stencil_layout=0)
         sy = synth.system(5, 2, n=18)
     else:
         sy = synth.system(1, 2, n=40)
@@ -935,10 +963,10 @@ def test_gs_grid_detection_guard(case):
 
 
 @pytest.mark.parametrize("variant", ["gram", "exact"])
-def test_gmres_cgs2_variants(variant, monkeypatch):
+def test_gmres_cgs2_variants(variant, tune):
     """R39: the Gram-form CGS2 (default) and the textbook two-pass CGS2 both match the oracle's GMRES."""
     if variant == "exact":
-        monkeypatch.setenv("LC_GMRES_EXACT_CGS2", "1")
+        tune(gmres_exact_cgs2=1)
     sy = synth.system(4, 7, n=48)
     Ao = oracle_csr(sy)
     A = gpu_matrix(sy)
@@ -950,13 +978,13 @@ def test_gmres_cgs2_variants(variant, monkeypatch):
 
 
 @pytest.mark.parametrize("layout", ["stencil", "sell", "symstencil"])
-def test_update_values_equals_fresh_create(layout, monkeypatch):
+def test_update_values_equals_fresh_create(layout, tune):
     """lc_update_values (same mesh, new values: the next system of the sequence) gives exactly the matrix a
     fresh lc_create_csr would: identical residual criterion and identical solve."""
     if layout == "sell":
-        monkeypatch.setenv("LC_DISABLE_STENCIL", "1")
+        tune(stencil_layout=0)
     if layout == "symstencil":
-        monkeypatch.setenv("LC_SYMMETRIC", "1")
+        tune(symmetric_layout=1)
     s1, s2 = synth.system(5, 3, n=20), synth.system(5, 4, n=20)
     A = gpu_matrix(s1)
     A.update_values(s2.rp, s2.ci, s2.val)

@@ -132,6 +132,29 @@ def test_example1_local_solve_annihilates_and_skips_global():
     assert np.linalg.norm(rB) <= 1e-5 * np.linalg.norm(sub.bsub) * (1 + 1e-12)
 
 
+def test_xt_output_is_eq4_assembly():
+    """x~ returned by or_local_method (Eq. 4, Alg. 1 l.6): on Omega the solution of B x_B = b_sub
+    (dense solve of the hand-checked Example 1 subsystem, to the subsystem tolerance times ||B^-1||), on the
+    complement x0 bitwise; one GS sweep (l.7) happens after it, so x~ does not depend on gs_sweeps."""
+    g, A, x, x0, b = example1()
+    Ac = orc.Csr.from_dense(A)
+    dp = orc.DomainParams(orc.CRIT_RESIDUAL, orc.THR_PAPER, 1e-5, 0, 0, 1)     # Omega = {1,2,3} (P:776-778)
+    for gs in (0, 1):
+        sp = orc.SolverParams(0, 1, 30, 1e-10, 20000, gs)
+        _, flag, rep, xt = orc.local_method(Ac, b, x0, dp, sp, want_xt=True)
+        assert rep.K == 3
+        np.testing.assert_array_equal(xt[3:], x0[3:])
+        B = A[:3, :3]
+        bsub = b[:3] - A[:3, 3:] @ x0[3:]
+        xB = np.linalg.solve(B, bsub)
+        bound = 1e-10 * np.linalg.norm(bsub) * np.linalg.norm(np.linalg.inv(B), 2) * (1 + 1e-6) + 1e-16
+        assert np.linalg.norm(xt[:3] - xB) <= bound
+        if gs == 0:
+            xt0 = xt
+        else:
+            np.testing.assert_array_equal(xt, xt0)
+
+
 # ------------------------------------------------------------ brute force ----
 
 @pytest.mark.parametrize("seed", range(6))
