@@ -99,7 +99,7 @@ lc_status max_coresident(const void* fn, int threads, size_t dsmem, int64_t* cta
     auto it = g_occ.find(key);
     if (it != g_occ.end()) { *ctas = it->second; return LC_OK; }
   }
-  if (dsmem > 48 * 1024) {
+  if (dsmem > 0) {                 // static + dynamic above 48 KB needs the opt-in: always opt in to `dsmem`
     st = func_attr(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
     if (st) return st;
   }

@@ -169,6 +169,7 @@ extern "C" lc_status lc_extract_sub(lc_matrix M, lc_domain D, const double* b, c
   }
   B.nslices = nsl;
   B.nslots = 32ll * B.maxw * nsl;
+  B.uniform = 1;                 // every slice maxw slots wide (k_extract pads with zero slots)
   if (S->K_units == 0) { S->use.mark(s);
   *out = S; return LC_OK; }
   lc_status st = LC_OK;

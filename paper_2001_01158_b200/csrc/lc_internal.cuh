@@ -117,6 +117,7 @@ struct Sell {
   int sym = 0, kd = 0, vw = 0;
   int32_t mir[kMaxOff] = {0};
   int reg_units = 0, spg = 0;     // equal segments (matrices from lc_create_csr)
+  int uniform = 0;                // SELL with every slice maxw slots wide (slice_ptr[s] = 32 maxw s): explicit B
   std::vector<int32_t> h_seg_unit0;
   std::vector<int64_t> h_seg_slice0;
   void release(cudaStream_t s);
@@ -150,7 +151,7 @@ inline SellView view(const Sell& m) {
   v.block = m.block; v.stencil = m.stencil; v.W = m.maxw;
   for (int k = 0; k < kMaxOff; ++k) v.off[k] = m.off[k];
   v.mask = m.mask; v.nunits = m.nunits;
-  v.sym = m.sym; v.kd = m.kd; v.vw = m.stencil ? (m.sym ? m.vw : m.maxw) : 0;
+  v.sym = m.sym; v.kd = m.kd; v.vw = m.stencil ? (m.sym ? m.vw : m.maxw) : (m.uniform ? m.maxw : 0);
   for (int k = 0; k < kMaxOff; ++k) v.mir[k] = m.mir[k];
   v.ru = m.reg_units; v.spg = m.spg;
   v.nslices = m.nslices; v.nseg = m.nseg; v.slice_ptr = m.slice_ptr; v.slice_row0 = m.slice_row0;

@@ -313,6 +313,8 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
   const int64_t njs = P.slist ? *P.nlist : A.nslices;          // index space: listed or all slices
   const int64_t nch = (njs + kPW - 1) / kPW;
   const int64_t chd = (int64_t)kPW * 32 * vw;                    // doubles per chunk
+  // uniform-width SELL (ST == 0, the explicit subsystems): the chunk's int32 columns are staged after the values
+  int32_t* const scol = reinterpret_cast<int32_t*>(stg + kStages * chd);
   const int n = (int)A.nunits, nu1 = n - 1;
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStages; ++st) mbar_init(&bars[st], 1);
@@ -327,8 +329,9 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
     const int nsl = (int)((njs - j0c) < kPW ? (njs - j0c) : kPW);
     const unsigned sbytes = (unsigned)(32 * vw * 8);
     if (!P.slist) {                                              // 8 consecutive slices: one copy
-      mbar_expect_tx(&bars[st], sbytes * nsl);
+      mbar_expect_tx(&bars[st], sbytes * nsl * (ST == 0 ? 3 : 2) / 2);
       tma_bulk_g2s(stg + st * chd, A.val + j0c * 32 * vw, sbytes * nsl, &bars[st]);
+      if (ST == 0) tma_bulk_g2s(scol + st * chd, A.col + j0c * 32 * vw, sbytes * nsl / 2, &bars[st]);
     } else {                                                     // listed slices: one copy each
       mbar_expect_tx(&bars[st], sbytes * nsl);
       for (int w = 0; w < nsl; ++w)
@@ -359,11 +362,16 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
     if (js < njs && u < n) {
       const bool in = !P.omega || om_cur != 255;
       const double* sp = stg + st * chd + (int64_t)warp * 32 * vw + lane;
+      const int32_t* scp = scol + st * chd + (int64_t)warp * 32 * vw + lane;
       double v[W], y[W];
 #pragma unroll
       for (int k = 0; k < W; ++k) {
-        int cc = u + A.off[k];
-        cc = cc < 0 ? 0 : (cc > nu1 ? nu1 : cc);
+        int cc;
+        if (ST == 0) cc = scp[32 * k];
+        else {
+          cc = u + A.off[k];
+          cc = cc < 0 ? 0 : (cc > nu1 ? nu1 : cc);
+        }
         if (ST == 2) {
           if (k >= A.kd) v[k] = sp[32 * (k - A.kd)];
           else {
@@ -394,9 +402,12 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
         }
       } else if (in) {
         double pi = 0.0;
+        if (ST == 0) pi = MODE == 1 ? P.z[u] : __fma_rn(beta, pold[u], P.z[u]);
+        else {
 #pragma unroll
-        for (int k = 0; k < W; ++k)
-          if (A.off[k] == 0) pi = y[k];
+          for (int k = 0; k < W; ++k)
+            if (A.off[k] == 0) pi = y[k];
+        }
         pnew[u] = pi;
         P.q[u] = acc;
         a0 = __fma_rn(pi, acc, a0);
@@ -585,7 +596,7 @@ __global__ void __launch_bounds__(kPT, ST == 0 ? LCV_MINB_SELL : LCV_MINB) k_pcg
       const double* xp = (KIND == 0 && S[0].pend >= 1) ? pvec(P, S[0].pbuf) : nullptr;
       const double* xp2 = (KIND == 0 && S[0].pend >= 2) ? pvec(P, S[0].pbuf2) : nullptr;
       const double xa = S[0].palpha, xa2 = S[0].palpha2;
-      if (KIND == 0 && ST && WM > 0 && P.tma) {
+      if (KIND == 0 && WM > 0 && P.tma) {
         if (mode == M_INIT || mode == M_CONFIRM)
           pass_a_tma<WM, ST, 0>(P, dsm, s_bars, bid, nCTA, warp, lane, mode == M_INIT, beta, pold, pnew, a0, a1, xp,
                                 xa, xp2, xa2);
@@ -982,8 +993,9 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   void* fn = fns[wi + 9 * kind];
   // TMA staging for contiguous slice ranges (global solves); slice-list (masked) solves keep plain loads: the
   // per-slice bulk copies were 4% slower there in the bench (profiles/r01_h_tma_ab.txt)
-  const bool tma = M.stencil && (M.maxw == 5 || M.maxw == 7) && G == 1 && !job.slist && tune.pcg_tma;
-  const size_t dsmem = tma ? (size_t)kStages * kPW * 32 * (M.sym ? M.vw : M.maxw) * sizeof(double) : 0;
+  // (the explicit subsystems' uniform-width SELL slices stream their columns through the same ring)
+  const bool tma = (M.stencil || M.uniform) && (M.maxw == 5 || M.maxw == 7) && G == 1 && !job.slist && tune.pcg_tma;
+  const size_t dsmem = tma ? (size_t)kStages * kPW * 32 * (M.sym ? M.vw : M.maxw) * (M.stencil ? 8 : 12) : 0;
   int64_t max_ctas = 0;
   st = max_coresident(fn, kPT, dsmem, &max_ctas);
   if (st) return st;

@@ -102,6 +102,9 @@ __global__ void __launch_bounds__(kVT) k_spmv(SellView A, const double* __restri
 // [rp[r0], rp[r0 + 32]) into the warp's shared-memory slot with coalesced loads (no block-wide barrier),
 // then lane l walks row r0 + l in stored order (the R22 chain, bit-exact with or_spmv) with the gathers of
 // x issued in groups of 8.  Slabs with more than kCWE entries read their rows straight from global memory.
+// Three dependent memory round trips per slab: the row pointers (each lane loads rp[u], rp[u + 1]; the slab's
+// span comes from lanes 0 and 31 by shuffle), the slab copy (all of a lane's loads issued before its shared-memory
+// stores), the x gathers.
 constexpr int kCT = 256;        // threads per CTA (8 warps)
 constexpr int kCWE = 256;       // staged entries per warp slab (8 per row on average)
 __global__ void __launch_bounds__(kCT) k_spmv_csr(int64_t n, const int64_t* __restrict__ rp,
@@ -114,22 +117,38 @@ __global__ void __launch_bounds__(kCT) k_spmv_csr(int64_t n, const int64_t* __re
   if (r0 >= n) return;
   const int64_t r1 = r0 + 32 < n ? r0 + 32 : n;
   const int64_t u = r0 + lane;
-  const int64_t e0 = rp[r0], e1 = rp[r1];
+  const int last = (int)(r1 - r0) - 1;
+  const int64_t ru0 = u < r1 ? __ldg(rp + u) : 0, ru1 = u < r1 ? __ldg(rp + u + 1) : 0;
+  const int64_t e0 = __shfl_sync(0xffffffffu, ru0, 0), e1 = __shfl_sync(0xffffffffu, ru1, last);
   const int64_t ne = e1 - e0;
   double acc = 0.0;
   if (ne > kCWE) {                                        // dense slab: rows straight from global memory
     if (u < r1)
-      for (int64_t k = rp[u]; k < rp[u + 1]; ++k) acc = __fma_rn(__ldg(va + k), __ldg(x + ci[k]), acc);
+      for (int64_t k = ru0; k < ru1; ++k) acc = __fma_rn(__ldg(va + k), __ldg(x + ci[k]), acc);
   } else {
     double* sv = s_v[warp];
     int32_t* sc = s_c[warp];
-    for (int64_t k = lane; k < ne; k += 32) {
-      sv[k] = __ldg(va + e0 + k);
-      sc[k] = __ldg(ci + e0 + k);
+    const int ni = (int)ne;
+#pragma unroll
+    for (int q = 0; q < kCWE / 32; q += 8) {                // 8 entries per lane in flight, then stored
+      double v[8];
+      int32_t c[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = lane + 32 * (q + j);
+        v[j] = k < ni ? __ldg(va + e0 + k) : 0.0;
+        c[j] = k < ni ? __ldg(ci + e0 + k) : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = lane + 32 * (q + j);
+        if (k < ni) { sv[k] = v[j]; sc[k] = c[j]; }
+      }
+      if (32 * (q + 8) >= ni) break;
     }
     __syncwarp();
     if (u < r1) {
-      const int k0 = (int)(rp[u] - e0), k1 = (int)(rp[u + 1] - e0);
+      const int k0 = (int)(ru0 - e0), k1 = (int)(ru1 - e0);
       for (int kb = k0; kb < k1; kb += 8) {
         double xv[8];
 #pragma unroll

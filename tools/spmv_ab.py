@@ -2,7 +2,6 @@
 """CSR row-slab SpMV (lc_spmv_csr) vs the handle layouts (lc_spmv: stencil / SELL-32) on configs 2 and 5:
 device time per call (CUDA events, 20 calls after 3 warm-up) and the algorithmic GB/s of each format."""
 import json
-import os
 import sys
 
 import torch
@@ -37,12 +36,10 @@ for cfg in (int(c) for c in (sys.argv[1:] or ["2", "5"])):
     y1, y2 = torch.empty_like(x), torch.empty_like(x)
     t_csr = timed(lambda: lc.spmv_csr(rp, ci, va, x, y1))
     row = dict(config=cfg, n=n, nnz=nnz, csr_us=t_csr * 1e6, csr_gbs=(12 * nnz + 8 * (n + 1) + 16 * n) / t_csr / 1e9)
-    for layout, env in (("stencil", None), ("sell", "LC_DISABLE_STENCIL")):
-        if env:
-            os.environ[env] = "1"
+    for layout, stencil in (("stencil", 1), ("sell", 0)):
+        prev = lc.set_tuning(stencil_layout=stencil)
         A = lc.Matrix(n, sy.rp, sy.ci, sy.val)
-        if env:
-            del os.environ[env]
+        lc.set_tuning(**prev)
         inf = A.info()
         t = timed(lambda: lc.spmv(A, x, y2))
         assert torch.equal(y1, y2)

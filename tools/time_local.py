@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Device time of the method2 local solve (residual domain, E_max = 1) with a given liblc build.
-usage: time_local.py LIB CONFIG [CONFIG ...]"""
+usage: time_local.py LIB CONFIG [CONFIG ...] [field=value ...]   (lc_tuning fields for an A/B)"""
 import sys
 
 import torch
@@ -10,7 +10,10 @@ import synth  # noqa: E402
 from paper_2001_01158_b200 import lc  # noqa: E402
 
 lc.load_library(sys.argv[1])
-for cfg in [int(c) for c in sys.argv[2:]]:
+tune = dict(a.split("=") for a in sys.argv[2:] if "=" in a)
+if tune:
+    lc.set_tuning(**{k: int(v) for k, v in tune.items()})
+for cfg in [int(c) for c in sys.argv[2:] if "=" not in c]:
     sy = synth.system(cfg, 3)
     A = lc.Matrix(sy.nrows, sy.rp, sy.ci, sy.val, block=sy.block, batch=sy.batch)
     b = torch.from_numpy(sy.b).cuda()
@@ -26,4 +29,5 @@ for cfg in [int(c) for c in sys.argv[2:]]:
         info = lc.solve_local(sub, x)
         best = min(best, max(i["seconds"] for i in info))
     its = max(i["iterations"] for i in info)
-    print(f"{sys.argv[1]} config {cfg} local: K {sum(dom.K)} its {its} {best * 1e3:.3f} ms", flush=True)
+    print(f"{sys.argv[1]} {tune or ''} config {cfg} local: K {sum(dom.K)} its {its} {best * 1e3:.3f} ms "
+          f"kernel {info[0]['kernel']} lazy {info[0]['lazy_x_depth']}", flush=True)
