@@ -193,6 +193,37 @@ lc_status lc_solve_local(lc_sub sub, const lc_solver_params* p, double* x, void*
 lc_status lc_solve_global(lc_matrix A, const double* b, double* x, const lc_solver_params* p, void* stream,
                           lc_solve_info* info);
 
+/* device-stream time of each phase of lc_local_method (ms, CUDA events on `stream`; launches included) */
+typedef struct {
+  double select;    /* Alg. 1 l.2   (lc_select_domain) */
+  double extract;   /* Alg. 1 l.3-4 (lc_extract_sub) */
+  double local;     /* Alg. 1 l.5-6 (lc_solve_local: xbar_B and the assembly of x~) */
+  double gs;        /* Alg. 1 l.7   (lc_smooth_gs) */
+  double global;    /* Alg. 1 l.8-11 (lc_solve_global from x~) */
+} lc_method_times;
+
+/*
+ * Alg. 1 in ONE call: input (A, b, x0), output x.  Same operations, kernels and results as the
+ * sequence lc_select_domain -> lc_extract_sub -> lc_solve_local -> gs_sweeps x lc_smooth_gs (l.7, 0 = none,
+ * R8) -> lc_solve_global, but the intermediate handles stay inside the library and the host synchronises twice
+ * (after the domain, whose K fixes the subsystem's size and kernel; at the end, for the solve reports) instead
+ * of after every step; lc_smooth_gs keeps its own syncs.  dp = NULL runs method0 (the global solve from
+ * x0).  b, x0: device [n*block], read only.  x: device [n*block], out (may not alias b or x0).
+ * Optional outputs (NULL = not wanted):
+ *   xt_dev      device [n*block]: x~ of Eq. 4 before the GS sweeps and the global solve
+ *   idx_dev     device [n*block]: Omega's ascending scalar rows (sum K entries, as lc_domain_export)
+ *   K_host      host [batch]: |Omega| per segment (scalar unknowns; 0 for method0)
+ *   local_info  host [batch]: the local solve per segment (iterations 0, kernel LC_KERNEL_NONE if K = 0)
+ *   global_info host [batch]: the global solve per segment
+ *   times       host: device time of each phase
+ * Returns the global solve's status (LC_NOT_CONVERGED non-fatal), or the first error of any phase; a local
+ * solve that stops at its cap is non-fatal (R18: it continues with the best iterate), see local_info.
+ */
+lc_status lc_local_method(lc_matrix A, const double* b, const double* x0, const lc_domain_params* dp,
+                          const lc_solver_params* sp, int32_t gs_sweeps, double* x, double* xt_dev, int32_t* idx_dev,
+                          void* stream, int64_t* K_host, lc_solve_info* local_info, lc_solve_info* global_info,
+                          lc_method_times* times);
+
 /*
  * y = A x (the operator of Eq. 1; the product inside the residual of Alg. 3 l.4, and inside every
  * Krylov iteration).  x, y: device [n*block], must not alias.  Per row the canonical chain (R22): stored
@@ -381,6 +412,8 @@ typedef struct {
   int32_t gmres_exact_cgs2;     /* 0 (default): Gram-form CGS2 (R39); 1: the textbook two passes */
   int32_t gs_lines;             /* 1 (default): 2-D five-point grids take the line-pipelined GS sweep; 0: the
                                    level schedule */
+  int32_t spmv_csr_tma;         /* 1 (default): lc_spmv_csr stages its row chunks by TMA when the three CSR arrays
+                                   are 16-byte aligned; 0: the warp row-slab kernel */
 } lc_tuning;
 
 /* the defaults listed above (host output) */

@@ -113,12 +113,83 @@ lc_status max_coresident(const void* fn, int threads, size_t dsmem, int64_t* cta
   return LC_OK;
 }
 
+// ---- completion of a Krylov launch (immediate / deferred, lc_internal.cuh) ----
+SolveClock::SolveClock(Pending* pend) {
+  if (pend && pend->e0 && pend->e1) { e0 = pend->e0; e1 = pend->e1; return; }
+  own = true;
+  if (cudaEventCreate(&e0) != cudaSuccess) { e0 = nullptr; cudaGetLastError(); }
+  if (cudaEventCreate(&e1) != cudaSuccess) { e1 = nullptr; cudaGetLastError(); }
+}
+SolveClock::~SolveClock() {
+  if (!own) return;
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+}
+
+static lc_status worst_of(const int32_t* stt, int G) {
+  lc_status worst = LC_OK;
+  for (int g = 0; g < G; ++g) {
+    if (stt[g] < 0) worst = (lc_status)stt[g];
+    else if (stt[g] == LC_NOT_CONVERGED && worst == LC_OK) worst = LC_NOT_CONVERGED;
+  }
+  if (worst < 0) set_error("Krylov solve: breakdown or non-finite value (see lc_solve_info.status)");
+  return worst;
+}
+
+static void fill_info(lc_solve_info* info, int G, const int32_t* it, const int32_t* stt, const double* rr, float ms,
+                      int kernel, int lazy) {
+  if (!info) return;
+  for (int g = 0; g < G; ++g) {
+    info[g].iterations = it[g];
+    info[g].status = stt[g];
+    info[g].rel_residual = rr[g];
+    info[g].seconds = ms * 1e-3;
+    info[g].kernel = kernel;
+    info[g].lazy_x_depth = lazy;
+  }
+}
+
+lc_status solve_finish(cudaError_t e, SolveClock& clk, Pending* pend, int G, const int* d_it, const int* d_stt,
+                       const double* d_rr, int kernel, int lazy, cudaStream_t s, lc_solve_info* info,
+                       const char* what) {
+  if (G > kMaxSegs) { set_error("solve: at most 64 segments"); return LC_ERR_DIMENSION; }
+  if (pend) {
+    pend->G = G; pend->kernel = kernel; pend->lazy = lazy; pend->armed = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(pend->it, d_it, 4 * G, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(pend->stt, d_stt, 4 * G, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(pend->rr, d_rr, 8 * G, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    pend->armed = 1;
+    return LC_OK;
+  }
+  int32_t it[kMaxSegs], stt[kMaxSegs];
+  double rr[kMaxSegs];
+  if (e == cudaSuccess) e = cudaMemcpyAsync(it, d_it, 4 * G, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(stt, d_stt, 4 * G, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(rr, d_rr, 8 * G, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  float ms = 0.f;
+  if (e == cudaSuccess && clk.e0 && clk.e1) cudaEventElapsedTime(&ms, clk.e0, clk.e1);
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  fill_info(info, G, it, stt, rr, ms, kernel, lazy);
+  return worst_of(stt, G);
+}
+
+lc_status pending_info(const Pending& pend, lc_solve_info* info) {
+  if (!pend.armed) return LC_OK;
+  float ms = 0.f;
+  if (pend.e0 && pend.e1) cudaEventElapsedTime(&ms, pend.e0, pend.e1);
+  fill_info(info, pend.G, pend.it, pend.stt, pend.rr, ms, pend.kernel, pend.lazy);
+  return worst_of(pend.stt, pend.G);
+}
+
 // ---- tuning (include/lc.h): thread-local, explicit, no environment variables ----
 static lc_tuning defaults_() {
   lc_tuning t;
   t.stencil_layout = 1; t.symmetric_layout = 0; t.pcg_cluster_resident = 1; t.pcg_cluster = 1; t.pcg_tma = 1;
   t.lazy_x_depth = 3; t.batched_schedule = -1; t.pcg_max_ctas = 0; t.sub_repr = -1; t.gmres_exact_cgs2 = 0;
   t.gs_lines = 1;
+  t.spmv_csr_tma = 1;
   return t;
 }
 static thread_local lc_tuning g_tune = defaults_();
@@ -375,7 +446,7 @@ extern "C" lc_status lc_set_tuning(const lc_tuning* t) {
   if (!bin(t->stencil_layout) || !bin(t->symmetric_layout) || !bin(t->pcg_cluster_resident) || !bin(t->pcg_cluster) ||
       !bin(t->pcg_tma) || t->lazy_x_depth < 0 || t->lazy_x_depth > 3 || t->batched_schedule < -1 ||
       t->batched_schedule > 1 || t->pcg_max_ctas < 0 || t->sub_repr < -1 || t->sub_repr > 1 ||
-      !bin(t->gmres_exact_cgs2) || !bin(t->gs_lines)) {
+      !bin(t->gmres_exact_cgs2) || !bin(t->gs_lines) || !bin(t->spmv_csr_tma)) {
     lc::set_error("lc_set_tuning: field out of range");
     return LC_ERR_INVALID_ARG;
   }

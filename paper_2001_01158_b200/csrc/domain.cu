@@ -600,6 +600,16 @@ fail:
 #undef CKL
 }
 
+namespace lc {
+// Omega's ascending scalar rows into idx_dev (device, [K_units * block]), enqueued on s without a sync
+lc_status domain_rows_out(const lc_domain_s* D, int32_t* idx_dev, cudaStream_t s) {
+  if (D->K_units == 0) return LC_OK;
+  k_expand_idx<<<(unsigned)((D->K_units + 255) / 256), 256, 0, s>>>(D->idx, D->K_units, D->A->block, idx_dev);
+  LC_LAUNCHED();
+  return LC_OK;
+}
+}  // namespace lc
+
 extern "C" lc_status lc_domain_export(lc_domain D, int32_t* idx_dev, double* tau_host, double* crit_dev,
                                       double* adm_dev, void* stream) {
   if (!D) { set_error("lc_domain_export: NULL handle"); return LC_ERR_INVALID_ARG; }

@@ -531,7 +531,8 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
 }
 
 lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* scatter_idx, double* x_full,
-                    const double* x_init, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
+                    const double* x_init, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info,
+                    Pending* defer) {
   if (M.nseg != 1) { set_error("GMRES: batched (block-diagonal) systems are not supported"); return LC_ERR_DIMENSION; }
   const int BS = M.block;
   const int m = p->restart;
@@ -575,28 +576,15 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   a.m = m;
   a.max_iters = p->max_iters;
   a.exact_cgs2 = tuning().gmres_exact_cgs2;
-  int out[2] = {0, 0};
-  double rr = 0.0;
-  float ms = 0.f;
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  SolveClock clk(defer);
   cudaError_t e = cudaMemsetAsync(a.bar, 0, sizeof(GridBar), s);
-  cudaEventRecord(e0, s);
+  cudaEventRecord(clk.e0, s);
   void* args[] = {&a};
   if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kGT), args, 0, s);
   count_launch();
-  cudaEventRecord(e1, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(out, a.out, 8, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&rr, a.out_relres, 8, cudaMemcpyDeviceToHost, s);
-  dfree(ws, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0); cudaEventDestroy(e1);
-  if (e != cudaSuccess) return cuda_fail(e, "GMRES kernel");
-  if (info) { info[0].iterations = out[0]; info[0].status = out[1]; info[0].rel_residual = rr; info[0].seconds = ms * 1e-3;
-              info[0].kernel = LC_KERNEL_GMRES; info[0].lazy_x_depth = 1; }
-  if (out[1] < 0) set_error("GMRES: non-finite value");
-  return (lc_status)out[1];
+  cudaEventRecord(clk.e1, s);
+  struct FreeAfter { void* p; cudaStream_t s; ~FreeAfter() { dfree(p, s); } } fa{ws, s};
+  return solve_finish(e, clk, defer, 1, a.out, a.out + 1, a.out_relres, LC_KERNEL_GMRES, 1, s, info, "GMRES kernel");
 }
 
 }  // namespace lc

@@ -45,6 +45,37 @@ void count_launch(int n = 1);
     if (_e != cudaSuccess) return ::lc::cuda_fail(_e, "kernel launch"); \
   } while (0)
 
+// Completion of one Krylov launch.  Every solver kernel leaves (iterations, status, relative residual) per
+// segment in device memory; the host copies them out behind the launch.  Immediate mode (the lc_solve_* entry
+// points) synchronises the stream and fills lc_solve_info.  Deferred mode (lc_local_method, Alg. 1 in one call)
+// copies them into a Pending record in pinned host memory and returns at once; the caller reads it after its one
+// synchronisation at the end (pending_info).
+constexpr int kMaxSegs = 64;
+struct Pending {
+  int32_t it[kMaxSegs];
+  int32_t stt[kMaxSegs];
+  double rr[kMaxSegs];
+  cudaEvent_t e0 = nullptr, e1 = nullptr;   // bracket the launch (timing events, owned by the record)
+  int G = 0, kernel = 0, lazy = 1, armed = 0;
+};
+// events bracketing a solve launch: the Pending record's when deferred, else created (and destroyed) here
+struct SolveClock {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  bool own = false;
+  explicit SolveClock(Pending* pend);
+  ~SolveClock();
+  SolveClock(const SolveClock&) = delete;
+  SolveClock& operator=(const SolveClock&) = delete;
+};
+// after the launch (clk.e1 recorded, launch error in e): copy the G per-segment outputs behind it.  Immediate
+// (pend == nullptr): synchronise, fill info[0..G) and return the worst status (errors set lc_last_error).
+// Deferred: return LC_OK unless the copies could not be enqueued.
+lc_status solve_finish(cudaError_t e, SolveClock& clk, Pending* pend, int G, const int* d_it, const int* d_stt,
+                       const double* d_rr, int kernel, int lazy, cudaStream_t s, lc_solve_info* info,
+                       const char* what);
+// a deferred record after the caller's synchronisation -> info[0..G), worst status
+lc_status pending_info(const Pending& pend, lc_solve_info* info);
+
 // one Krylov solve for run_pcg (pcg.cu)
 struct Sell;
 struct PcgJob {
@@ -62,6 +93,7 @@ struct PcgJob {
   double* x_user = nullptr;       // masked local solve: x_user[u] = x[u] on Omega
   int reg_units = 0, spg = 0;     // equal segments of reg_units units with spg slices each (A), else 0
   int64_t rows_hint = -1;         // rows the solve works on (masked: K), -1 = all; picks team mode for G > 1
+  Pending* defer = nullptr;       // deferred completion (lc_local_method), else immediate
 };
 
 // small single-segment stencil systems: the cluster-resident PCG (pcg_dsmem.cu)

@@ -954,9 +954,6 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   if (G > kMaxSeg) { set_error("PCG: at most 64 segments"); return LC_ERR_DIMENSION; }
   if (M.block != 1) { set_error("PCG: needs block = 1 (use LC_GMRES for block systems)"); return LC_ERR_INVALID_ARG; }
   if (pcg_dsmem_eligible(job)) return run_pcg_dsmem(job, p, s, info);     // fits one cluster's shared memory
-  std::vector<int> it(G, 0), stt(G, LC_OK);
-  std::vector<double> rr(G, 0.0);
-  float ms = 0.f;
   // compile-time width: SELL rows guard k < w, so W = 5 / 7 serve rows up to that width; stencil slices hold
   // exactly maxw slots, so they take W = 5 / 7 only when maxw is exactly that (else the generic loop)
   const int wi = (M.stencil ? (M.maxw == 5 ? 0 : M.maxw == 7 ? 1 : 2) : (M.maxw <= 5 ? 0 : M.maxw <= 7 ? 1 : 2)) +
@@ -1074,9 +1071,8 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   if (e == cudaSuccess && teams) e = cudaMemsetAsync(a.tctr, 0, 128 * (size_t)teams, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(a.out_iters, 0, 8 * G, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(a.out_relres, 0, 8 * G, s);
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0); cudaEventCreate(&e1);
-  cudaEventRecord(e0, s);
+  SolveClock clk(job.defer);
+  cudaEventRecord(clk.e0, s);
   void* args[] = {&a};
   if (clus) {
     if (func_attr(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != LC_OK) cudaGetLastError();
@@ -1105,31 +1101,13 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
     e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kPT), args, dsmem, s);
   }
   count_launch();
-  cudaEventRecord(e1, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(it.data(), a.out_iters, 4 * G, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(stt.data(), a.out_status, 4 * G, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(rr.data(), a.out_relres, 8 * G, cudaMemcpyDeviceToHost, s);
-  dfree(ws, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0); cudaEventDestroy(e1);
-  if (e != cudaSuccess) return cuda_fail(e, "PCG kernel");
-  lc_status worst = LC_OK;
-  for (int g = 0; g < G; ++g) {
-    if (info) {
-      info[g].iterations = it[g];
-      info[g].status = stt[g];
-      info[g].rel_residual = rr[g];
-      info[g].seconds = ms * 1e-3;
-      info[g].kernel = kind == 1 ? LC_KERNEL_PCG_LOCKSTEP : kind == 2 ? LC_KERNEL_PCG_TEAMS
-                       : clus ? LC_KERNEL_PCG_CLUSTER : LC_KERNEL_PCG_GRID;
-      info[g].lazy_x_depth = a.lazyx > 1 ? a.lazyx : 1;
-    }
-    if (stt[g] < 0) worst = (lc_status)stt[g];
-    else if (stt[g] == LC_NOT_CONVERGED && worst == LC_OK) worst = LC_NOT_CONVERGED;
-  }
-  if (worst < 0) set_error("PCG: breakdown or non-finite value (see lc_solve_info.status)");
-  return worst;
+  cudaEventRecord(clk.e1, s);
+  const int kernel = kind == 1 ? LC_KERNEL_PCG_LOCKSTEP : kind == 2 ? LC_KERNEL_PCG_TEAMS
+                     : clus ? LC_KERNEL_PCG_CLUSTER : LC_KERNEL_PCG_GRID;
+  // (the copies of solve_finish are enqueued before the stream-ordered free of the workspace they read)
+  struct FreeAfter { void* p; cudaStream_t s; ~FreeAfter() { dfree(p, s); } } fa{ws, s};
+  return solve_finish(e, clk, job.defer, G, a.out_iters, a.out_status, a.out_relres, kernel,
+                      a.lazyx > 1 ? a.lazyx : 1, s, info, "PCG kernel");
 }
 
 }  // namespace lc

@@ -260,10 +260,9 @@ lc_status run_pcg_dsmem(const PcgJob& job, const lc_solver_params* p, cudaStream
   a.out_iters = (int*)ws.p;
   a.out_status = (int*)ws.p + 1;
   a.out_relres = (double*)((char*)ws.p + 8);
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  SolveClock clk(job.defer);
   cudaError_t e = cudaMemsetAsync(ws.p, 0, 64, s);
-  cudaEventRecord(e0, s);
+  cudaEventRecord(clk.e0, s);
   // the largest cluster the device accepts (16 non-portable, else 8), rows split evenly
   for (int nq : {kMaxCluster, 8}) {
     a.R = (n + nq - 1) / nq;
@@ -287,27 +286,9 @@ lc_status run_pcg_dsmem(const PcgJob& job, const lc_solver_params* p, cudaStream
     cudaGetLastError();
   }
   if (e == cudaSuccess) count_launch();
-  cudaEventRecord(e1, s);
-  int it = 0, stt = LC_OK;
-  double rr = 0.0;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&it, a.out_iters, 4, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&stt, a.out_status, 4, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&rr, a.out_relres, 8, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  float ms = 0.f;
-  if (e == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0); cudaEventDestroy(e1);
-  if (e != cudaSuccess) return cuda_fail(e, "PCG (cluster-resident) kernel");
-  if (info) {
-    info[0].iterations = it;
-    info[0].status = stt;
-    info[0].rel_residual = rr;
-    info[0].seconds = ms * 1e-3;
-    info[0].kernel = LC_KERNEL_PCG_RESIDENT;
-    info[0].lazy_x_depth = 1;
-  }
-  if (stt < 0) { set_error("PCG: breakdown or non-finite value (see lc_solve_info.status)"); return (lc_status)stt; }
-  return stt == LC_NOT_CONVERGED ? LC_NOT_CONVERGED : LC_OK;
+  cudaEventRecord(clk.e1, s);
+  return solve_finish(e, clk, job.defer, 1, a.out_iters, a.out_status, a.out_relres, LC_KERNEL_PCG_RESIDENT, 1, s,
+                      info, "PCG (cluster-resident) kernel");
 }
 
 }  // namespace lc

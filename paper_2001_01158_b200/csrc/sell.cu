@@ -31,11 +31,21 @@ __global__ void k_first_maxrow(int64_t n, const int64_t* __restrict__ rp, int ma
   }
 }
 
+// the candidate offsets (those of the first longest row, *best) into *O, on the device (no host round trip)
+__global__ void k_candidate(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const int* best, int W,
+                            Offsets* O) {
+  const int k = threadIdx.x;
+  const int u = *best;
+  if (k < kMaxOff) O->off[k] = (k < W && u != INT32_MAX) ? ci[rp[u] + k] - u : 0;
+  if (k == 0) O->W = W;
+}
+
 // every stored (u, c) must have c - u in the candidate offset set
-__global__ void k_check_stencil(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, Offsets O,
-                                unsigned* err) {
+__global__ void k_check_stencil(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                const Offsets* __restrict__ Od, unsigned* err) {
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u >= n) return;
+  const Offsets O = *Od;
   for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
     int64_t d = (int64_t)ci[e] - u;
     bool hit = false;
@@ -291,9 +301,7 @@ lc_status build_slab(int64_t nglob, int64_t row0, int64_t n, const int64_t* row_
   const int32_t* d_ci = col_idx;
   const double* d_va = values;
   unsigned h_err = 0;
-  int h_maxw = 0, best = 0;
-  int64_t k0 = 0;
-  int32_t cols[kMaxOff];
+  int h_maxw = 0;
   Offsets O;
   const unsigned nb = (unsigned)((n + 255) / 256);
 #define CK(x) do { st = (x); if (st) goto done; } while (0)
@@ -308,8 +316,8 @@ lc_status build_slab(int64_t nglob, int64_t row0, int64_t n, const int64_t* row_
     d_rp = (const int64_t*)t_rp; d_ci = (const int32_t*)t_ci; d_va = (const double*)t_va;
   }
   CK(dalloc(&t_cs, sizeof(int32_t) * nnz, s));
-  CK(dalloc(&t_err, 16, s));
-  CKC(cudaMemsetAsync(t_err, 0, 16, s));
+  CK(dalloc(&t_err, 64, s));                  // [0] error bits, [4] asymmetry, [8] max width, [12] row, [16] offsets
+  CKC(cudaMemsetAsync(t_err, 0, 64, s));
   k_slab_check<<<nb, 256, 0, s>>>(n, row0, nglob, d_rp, d_ci, (int32_t*)t_cs, (unsigned*)t_err,
                                   (int*)((char*)t_err + 8));
   count_launch();
@@ -328,18 +336,15 @@ lc_status build_slab(int64_t nglob, int64_t row0, int64_t n, const int64_t* row_
     CKC(cudaMemcpyAsync((char*)t_err + 12, &big, sizeof(int), cudaMemcpyHostToDevice, s));
     k_first_maxrow<<<nb, 256, 0, s>>>(n, d_rp, h_maxw, (int*)((char*)t_err + 12));
     count_launch();
-    CKC(cudaMemcpyAsync(&best, (char*)t_err + 12, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CKC(cudaStreamSynchronize(s));
-    CKC(cudaMemcpyAsync(&k0, d_rp + best, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    CKC(cudaStreamSynchronize(s));
-    CKC(cudaMemcpyAsync(cols, (int32_t*)t_cs + k0, sizeof(int32_t) * h_maxw, cudaMemcpyDeviceToHost, s));
-    CKC(cudaStreamSynchronize(s));
+    k_candidate<<<1, 32, 0, s>>>(d_rp, (const int32_t*)t_cs, (const int*)((char*)t_err + 12), h_maxw,
+                                 (Offsets*)((char*)t_err + 16));
+    count_launch();
   }
-  O.W = h_maxw;
-  for (int k = 0; k < kMaxOff; ++k) O.off[k] = k < h_maxw ? cols[k] - best : 0;
-  k_check_stencil<<<nb, 256, 0, s>>>(n, d_rp, (const int32_t*)t_cs, O, (unsigned*)t_err);
+  k_check_stencil<<<nb, 256, 0, s>>>(n, d_rp, (const int32_t*)t_cs, (const Offsets*)((char*)t_err + 16),
+                                     (unsigned*)t_err);
   count_launch();
   CKC(cudaMemcpyAsync(&h_err, t_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  CKC(cudaMemcpyAsync(&O, (char*)t_err + 16, sizeof(Offsets), cudaMemcpyDeviceToHost, s));
   CKC(cudaStreamSynchronize(s));
   if (h_err & kErrNotStencil) {
     st = LC_ERR_PATTERN;
@@ -390,13 +395,8 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
   cudaStream_t s = (cudaStream_t)stream;
   int bb = block * block;
   // row_ptr end -> nnz
-  int64_t nnz = 0;
-  if (inputs_on_device) {
-    LC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    LC_CUDA(cudaStreamSynchronize(s));
-  } else {
-    nnz = row_ptr[n];
-  }
+  // (device inputs: nnz = row_ptr[n] is read back with the validation flags below, one round trip for both)
+  int64_t nnz = inputs_on_device ? n : row_ptr[n];
   if (nnz < n || nnz > (int64_t)INT32_MAX * 4) { set_error("lc_create_csr: bad nnz"); return LC_ERR_PATTERN; }
 
   lc_matrix_s* M = new lc_matrix_s();
@@ -424,8 +424,8 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
     d_rp = (const int64_t*)t_rp; d_ci = (const int32_t*)t_ci; d_va = (const double*)t_va;
   }
   CK(dalloc(&t_w, sizeof(int64_t) * (A.nslices + 1), s));
-  CK(dalloc(&t_err, 16, s));
-  CKC(cudaMemsetAsync(t_err, 0, 16, s));
+  CK(dalloc(&t_err, 64, s));                  // [0] error bits, [4] asymmetry, [8] max width, [12] row, [16] offsets
+  CKC(cudaMemsetAsync(t_err, 0, 64, s));
   CK(dalloc((void**)&A.rowlen, n, s));
   CK(dalloc((void**)&A.slice_ptr, sizeof(int64_t) * (A.nslices + 1), s));
   {
@@ -439,7 +439,12 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
   CKC(cudaMemcpyAsync(&A.nslots, A.slice_ptr + A.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   CKC(cudaMemcpyAsync(&h_err, t_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
   CKC(cudaMemcpyAsync(&h_maxw, (char*)t_err + 8, sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (inputs_on_device) CKC(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   CKC(cudaStreamSynchronize(s));
+  if (inputs_on_device) {
+    if (nnz < n || nnz > (int64_t)INT32_MAX * 4) { st = LC_ERR_PATTERN; set_error("lc_create_csr: bad nnz"); goto fail; }
+    M->nnz = nnz;
+  }
   if (h_err) {
     st = (h_err & kErrRowLen) ? LC_ERR_PATTERN : LC_ERR_PATTERN;
     set_error(h_err & kErrRowLen ? "lc_create_csr: row length must be in [1, 255]"
@@ -457,21 +462,14 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
       unsigned nb = (unsigned)((n + 255) / 256);
       k_first_maxrow<<<nb, 256, 0, s>>>(n, d_rp, h_maxw, (int*)((char*)t_err + 12));
       count_launch();
-      int best = 0;
-      int64_t k0 = 0;
-      int32_t cols[kMaxOff];
-      CKC(cudaMemcpyAsync(&best, (char*)t_err + 12, sizeof(int), cudaMemcpyDeviceToHost, s));
-      CKC(cudaStreamSynchronize(s));
-      CKC(cudaMemcpyAsync(&k0, d_rp + best, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-      CKC(cudaStreamSynchronize(s));
-      CKC(cudaMemcpyAsync(cols, d_ci + k0, sizeof(int32_t) * h_maxw, cudaMemcpyDeviceToHost, s));
-      CKC(cudaStreamSynchronize(s));
-      Offsets O;
-      O.W = h_maxw;
-      for (int k = 0; k < kMaxOff; ++k) O.off[k] = k < h_maxw ? cols[k] - best : 0;
-      k_check_stencil<<<nb, 256, 0, s>>>(n, d_rp, d_ci, O, (unsigned*)t_err);
+      // candidate offsets gathered and checked on the device: one host round trip for the layout decision
+      k_candidate<<<1, 32, 0, s>>>(d_rp, d_ci, (const int*)((char*)t_err + 12), h_maxw, (Offsets*)((char*)t_err + 16));
       count_launch();
+      k_check_stencil<<<nb, 256, 0, s>>>(n, d_rp, d_ci, (const Offsets*)((char*)t_err + 16), (unsigned*)t_err);
+      count_launch();
+      Offsets O;
       CKC(cudaMemcpyAsync(&h_err, t_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+      CKC(cudaMemcpyAsync(&O, (char*)t_err + 16, sizeof(Offsets), cudaMemcpyDeviceToHost, s));
       CKC(cudaStreamSynchronize(s));
       if (!(h_err & kErrNotStencil)) {
         A.stencil = 1;
@@ -623,8 +621,8 @@ extern "C" lc_status lc_update_values(lc_matrix M, const int64_t* row_ptr, const
     CKC(cudaMemcpyAsync(t_va, values, sizeof(double) * nnz * bb, cudaMemcpyHostToDevice, s));
     d_rp = (const int64_t*)t_rp; d_ci = (const int32_t*)t_ci; d_va = (const double*)t_va;
   }
-  CK(dalloc(&t_err, 16, s));
-  CKC(cudaMemsetAsync(t_err, 0, 16, s));
+  CK(dalloc(&t_err, 64, s));                  // [0] error bits, [4] asymmetry, [8] max width, [12] row, [16] offsets
+  CKC(cudaMemsetAsync(t_err, 0, 64, s));
   M->valid = 0;                 // the fill below overwrites the live layout; valid again once the checks pass
   {
     const unsigned nb = (unsigned)((n + 255) / 256);

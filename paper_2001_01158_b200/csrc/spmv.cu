@@ -162,6 +162,113 @@ __global__ void __launch_bounds__(kCT) k_spmv_csr(int64_t n, const int64_t* __re
   if (u < r1) y[u] = acc;
 }
 
+// ---- CSR SpMV with the slab stream staged by TMA (the default when the three arrays are 16-byte aligned):
+// persistent CTAs take chunks c = b + t nCTA of kCR = 256 consecutive rows (one row per thread).  Thread 0 keeps
+// kCS chunks in flight: per chunk three cp.async.bulk copies into a shared-memory stage -- the chunk's row pointers
+// rp[r0 .. r0 + 258), its values and its columns [rp[r0], rp[r0 + 256]) widened to 16-byte boundaries -- completing
+// on the stage's mbarrier; the chunk's bounds rp[r0], rp[r0 + 256] are loaded one chunk earlier, so the copies never
+// wait on them.  Each thread then walks its row in the stage (the R22 chain in stored order, gathers of x in groups
+// of 8), so the DRAM stream of values / columns / row pointers no longer waits on any warp's gather latency.
+// Chunks whose widened span exceeds a stage, or that touch the arrays' ends, read their rows from global memory.
+constexpr int kCR = 256;                       // rows per chunk (= threads per CTA)
+constexpr int kCE = 2048;                      // staged entries per chunk (8 per row on average)
+constexpr int kCS = 2;                         // stages
+constexpr int kStVal = (kCE + 4) * 8;          // bytes: values (span widened by up to 3 + 1 entries)
+constexpr int kStCol = (kCE + 4) * 4;          // columns
+constexpr int kStRp = (kCR + 2) * 8;           // row pointers rp[r0 .. r0 + kCR + 2)
+constexpr int kStage = kStVal + kStCol + kStRp;
+static_assert(kStVal % 16 == 0 && kStCol % 16 == 0 && kStRp % 16 == 0, "16-B stage parts");
+
+__global__ void __launch_bounds__(kCR) k_spmv_csr_tma(int64_t n, const int64_t* __restrict__ rp,
+                                                      const int32_t* __restrict__ ci, const double* __restrict__ va,
+                                                      const double* __restrict__ x, double* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char csm[];
+  __shared__ __align__(8) uint64_t bars[kCS];
+  __shared__ int64_t s_e0[kCS];                 // widened first entry of the staged chunk, -1 = not staged
+  const int64_t nch = (n + kCR - 1) / kCR;
+  const int64_t bid = blockIdx.x, nCTA = gridDim.x;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int st = 0; st < kCS; ++st) mbar_init(&bars[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  int64_t nnz = 0, b0 = 0, b1 = 0;              // thread 0: nnz and the next chunk's bounds
+  auto bounds = [&](int64_t t, int64_t& e0, int64_t& e1) {
+    const int64_t c = bid + t * nCTA;
+    if (c >= nch) { e0 = e1 = 0; return; }
+    const int64_t r0 = c * kCR, r1 = r0 + kCR < n ? r0 + kCR : n;
+    e0 = __ldg(rp + r0);
+    e1 = __ldg(rp + r1);
+  };
+  auto issue = [&](int64_t t, int64_t e0, int64_t e1) {
+    const int64_t c = bid + t * nCTA;
+    if (c >= nch) return;
+    const int st = (int)(t % kCS);
+    unsigned char* sb = csm + (size_t)st * kStage;
+    const int64_t r0 = c * kCR;
+    const int64_t e0a = e0 & ~(int64_t)3, e1v = (e1 + 1) & ~(int64_t)1, e1c = (e1 + 3) & ~(int64_t)3;
+    const bool ok = e1c - e0a <= kCE + 4 && e1c <= nnz && r0 + kCR + 2 <= n + 1;
+    if (!ok) {
+      s_e0[st] = -1;
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[st])) : "memory");
+      return;
+    }
+    s_e0[st] = e0a;
+    const unsigned bv = (unsigned)((e1v - e0a) * 8), bc = (unsigned)((e1c - e0a) * 4);
+    mbar_expect_tx(&bars[st], bv + bc + kStRp);
+    tma_bulk_g2s(sb + kStVal + kStCol, rp + r0, kStRp, &bars[st]);
+    if (bv) tma_bulk_g2s(sb, va + e0a, bv, &bars[st]);
+    if (bc) tma_bulk_g2s(sb + kStVal, ci + e0a, bc, &bars[st]);
+  };
+  if (tid == 0) {
+    nnz = __ldg(rp + n);
+    for (int t = 0; t < kCS; ++t) {
+      int64_t e0, e1;
+      bounds(t, e0, e1);
+      issue(t, e0, e1);
+    }
+    bounds(kCS, b0, b1);
+  }
+#pragma unroll 1
+  for (int64_t t = 0;; ++t) {
+    const int64_t c = bid + t * nCTA;
+    if (c >= nch) break;
+    const int st = (int)(t % kCS);
+    mbar_wait(&bars[st], (unsigned)((t / kCS) & 1));
+    const int64_t u = c * kCR + tid;
+    const unsigned char* sb = csm + (size_t)st * kStage;
+    const int64_t e0a = s_e0[st];
+    if (u < n) {
+      double acc = 0.0;
+      if (e0a >= 0) {
+        const double* sv = reinterpret_cast<const double*>(sb);
+        const int32_t* sc = reinterpret_cast<const int32_t*>(sb + kStVal);
+        const int64_t* srp = reinterpret_cast<const int64_t*>(sb + kStVal + kStCol);
+        const int k0 = (int)(srp[tid] - e0a), k1 = (int)(srp[tid + 1] - e0a);
+        for (int kb = k0; kb < k1; kb += 8) {
+          double xv[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) xv[j] = kb + j < k1 ? __ldg(x + sc[kb + j]) : 0.0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (kb + j < k1) acc = __fma_rn(sv[kb + j], xv[j], acc);
+        }
+      } else {
+        const int64_t k0 = __ldg(rp + u), k1 = __ldg(rp + u + 1);
+        for (int64_t k = k0; k < k1; ++k) acc = __fma_rn(__ldg(va + k), __ldg(x + __ldg(ci + k)), acc);
+      }
+      y[u] = acc;
+    }
+    __syncthreads();                               // every thread is done with stage st
+    if (tid == 0) {
+      fence_proxy_async_smem();                    // generic reads of st before the async-proxy refill
+      issue(t + kCS, b0, b1);
+      bounds(t + kCS + 1, b0, b1);
+    }
+  }
+}
+
 }  // namespace lc
 
 using namespace lc;
@@ -197,8 +304,20 @@ extern "C" lc_status lc_spmv_csr(int64_t n, const int64_t* row_ptr, const int32_
   }
   if (x == y) { set_error("lc_spmv_csr: x and y must not alias"); return LC_ERR_INVALID_ARG; }
   if (n == 0) return LC_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool aligned = ((((uintptr_t)row_ptr) | ((uintptr_t)col_idx) | ((uintptr_t)values)) & 15) == 0;
+  if (aligned && tuning().spmv_csr_tma) {
+    int64_t ctas = 0;
+    const size_t dsm = (size_t)kCS * kStage;
+    if (lc_status st = max_coresident((const void*)k_spmv_csr_tma, kCR, dsm, &ctas)) return st;
+    const int64_t nch = (n + kCR - 1) / kCR;
+    const unsigned nb = (unsigned)(nch < ctas ? nch : ctas);
+    k_spmv_csr_tma<<<nb, kCR, dsm, s>>>(n, row_ptr, col_idx, values, x, y);
+    LC_LAUNCHED();
+    return LC_OK;
+  }
   const unsigned nb = (unsigned)((n + kCT - 1) / kCT);
-  k_spmv_csr<<<nb, kCT, 0, (cudaStream_t)stream>>>(n, row_ptr, col_idx, values, x, y);
+  k_spmv_csr<<<nb, kCT, 0, s>>>(n, row_ptr, col_idx, values, x, y);
   LC_LAUNCHED();
   return LC_OK;
 }

@@ -32,7 +32,7 @@ EXPORTED = ["lc_create_csr", "lc_update_values", "lc_select_domain", "lc_domain_
             "lc_destroy_sub", "lc_spmv", "lc_spmv_csr", "lc_dist_create", "lc_dist_export_handle", "lc_dist_connect", "lc_dist_connect_local",
             "lc_dist_select_domain", "lc_dist_domain_export", "lc_dist_solve_local", "lc_dist_solve_global",
             "lc_dist_destroy", "lc_last_error", "lc_kernel_launches", "lc_tuning_defaults", "lc_set_tuning",
-            "lc_get_tuning", "lc_sub_export"]
+            "lc_get_tuning", "lc_sub_export", "lc_local_method"]
 DIST_HANDLE_BYTES = 64
 
 
@@ -72,6 +72,11 @@ class SolveInfo(ctypes.Structure):
                 ("seconds", ctypes.c_double), ("kernel", ctypes.c_int32), ("lazy_x_depth", ctypes.c_int32)]
 
 
+class MethodTimes(ctypes.Structure):
+    _fields_ = [("select", ctypes.c_double), ("extract", ctypes.c_double), ("local", ctypes.c_double),
+                ("gs", ctypes.c_double), ("global_", ctypes.c_double)]
+
+
 KERNELS = {0: "none", 1: "pcg_grid", 2: "pcg_cluster", 3: "pcg_resident", 4: "pcg_lockstep", 5: "pcg_teams",
            6: "gmres"}
 
@@ -82,7 +87,7 @@ class Tuning(ctypes.Structure):
                 ("pcg_cluster_resident", ctypes.c_int32), ("pcg_cluster", ctypes.c_int32),
                 ("pcg_tma", ctypes.c_int32), ("lazy_x_depth", ctypes.c_int32), ("batched_schedule", ctypes.c_int32),
                 ("pcg_max_ctas", ctypes.c_int32), ("sub_repr", ctypes.c_int32), ("gmres_exact_cgs2", ctypes.c_int32),
-                ("gs_lines", ctypes.c_int32)]
+                ("gs_lines", ctypes.c_int32), ("spmv_csr_tma", ctypes.c_int32)]
 
 
 _lib = None
@@ -112,11 +117,14 @@ def load_library(path: str = LIB_PATH):
     lib.lc_spmv_csr.argtypes = [I64, P, P, P, P, P, P]
     lib.lc_spmv_csr.restype = ctypes.c_int
     lib.lc_update_values.argtypes = [P, P, P, P, I32, P]
+    lib.lc_local_method.argtypes = [P, P, P, ctypes.POINTER(DomainParams), ctypes.POINTER(SolverParams), I32, P, P, P,
+                                    P, P, ctypes.POINTER(SolveInfo), ctypes.POINTER(SolveInfo),
+                                    ctypes.POINTER(MethodTimes)]
     lib.lc_heat_assemble.argtypes = [I32, I32, D, I32, D, D, P, P, P, P, P, P, P]
     lib.lc_heat_run.argtypes = [ctypes.POINTER(HeatParams), P, P, P, P, ctypes.POINTER(HeatReport)]
     for f in ("lc_create_csr", "lc_select_domain", "lc_domain_export", "lc_extract_sub", "lc_solve_local",
               "lc_solve_global", "lc_matrix_info", "lc_smooth_gs", "lc_heat_assemble", "lc_heat_run",
-              "lc_update_values"):
+              "lc_update_values", "lc_local_method"):
         getattr(lib, f).restype = ctypes.c_int
     PP = ctypes.POINTER(P)
     lib.lc_dist_create.argtypes = [I64, I64, I64, I32, I32, P, P, P, I32, P, PP]
@@ -377,7 +385,45 @@ def smooth_gs(A: Matrix, b: torch.Tensor, x: torch.Tensor, sweeps=1):
 
 def local_method(A: Matrix, b, x0, domain: dict | None, method=PCG, rel_tol=1e-10, max_iters=20000, restart=30,
                  gs_sweeps=0, keep=False, timing=False):
-    """Alg. 1 composed from the C-ABI calls (domain=None: method0): domain (l.2), extraction (l.3-4),
+    """Alg. 1 in one C-ABI call (lc_local_method; domain=None: method0): domain (l.2), extraction (l.3-4), local
+    solve + assembly (l.5-6), gs_sweeps Gauss-Seidel sweeps (l.7), global solve (l.8-11), two host syncs.
+    Returns (x, report dict): K per segment, "local" / "global" solve infos per segment, "ms" = device time of
+    each phase on the current stream (select, extract, local, gs, global).  keep=True also returns rep["idx"]
+    (Omega, ascending rows) and rep["xt"] (x~ of Eq. 4, before any GS sweep).  `timing` is accepted for the
+    composed form's signature (the phase times are always reported)."""
+    s = _stream()
+    N = A.N
+    bp, x0p = _dptr(b, torch.float64, N), _dptr(x0, torch.float64, N)
+    x = torch.empty_like(x0)
+    xt = torch.empty_like(x0) if keep else None
+    idx = torch.empty(max(N, 1), dtype=torch.int32, device=x0.device) if keep and domain is not None else None
+    dp = DomainParams(domain.get("criterion", CRIT_RESIDUAL), domain.get("threshold", THR_PAPER),
+                      domain.get("param", 1e-10), domain.get("expand_rounds", 0),
+                      domain.get("dilate_hops", 0)) if domain is not None else None
+    sp = _solver(method, rel_tol, max_iters, restart)
+    K = (ctypes.c_int64 * A.batch)()
+    li, gi = (SolveInfo * A.batch)(), (SolveInfo * A.batch)()
+    tm = MethodTimes()
+    st = load_library().lc_local_method(A.h, bp, x0p, ctypes.byref(dp) if dp is not None else None, ctypes.byref(sp),
+                                        int(gs_sweeps), ctypes.c_void_p(x.data_ptr()),
+                                        ctypes.c_void_p(xt.data_ptr()) if xt is not None else None,
+                                        ctypes.c_void_p(idx.data_ptr()) if idx is not None else None, s, K, li, gi,
+                                        ctypes.byref(tm))
+    _check(st, "lc_local_method")
+    rep = {"K": list(K), "global": _infos(gi),
+           "ms": {"select": tm.select, "extract": tm.extract, "local": tm.local, "gs": tm.gs, "global": tm.global_}}
+    if domain is not None and sum(rep["K"]) > 0:
+        rep["local"] = _infos(li)
+    if keep:
+        rep["xt"] = xt
+        if idx is not None:
+            rep["idx"] = idx[:sum(rep["K"])]
+    return x, rep
+
+
+def local_method_steps(A: Matrix, b, x0, domain: dict | None, method=PCG, rel_tol=1e-10, max_iters=20000, restart=30,
+                 gs_sweeps=0, keep=False, timing=False):
+    """Alg. 1 composed from the step-by-step C-ABI calls (domain=None: method0): domain (l.2), extraction (l.3-4),
     local solve + assembly (l.5-6), gs_sweeps Gauss-Seidel sweeps (l.7), global solve (l.8-11).
     Returns (x, report dict).  keep=True also returns the intermediate results for parity checks:
     rep["idx"] (Omega, ascending rows), rep["tau"], rep["bsub"], rep["xB0"] (Eq. 3, Omega order) and

@@ -123,13 +123,21 @@ def check_system(sy, rule, check_solution=True):
     b, x0 = to_dev(sy.b), to_dev(sy.x0)
     dom = lc.select_domain(A, b, x0, **rule)
     _, _, crit, adm = dom.export(want_crit=True, want_adm=True)
+    # Alg. 1 in one call (lc_local_method): x, x~, Omega, iterations
     x_gpu, rep = lc.local_method(A, b, x0, rule, method=method_of(cfg), keep=True)
+    # the step-by-step C-ABI sequence on the same inputs: tau, b_sub and x_B0 (Eq. 3); same kernels and launch
+    # configurations, so x, x~, Omega and the iteration counts equal the one-call path's bitwise
+    x_st, rep_st = lc.local_method_steps(A, b, x0, rule, method=method_of(cfg), keep=True)
+    assert torch.equal(x_gpu, x_st) and torch.equal(rep["xt"], rep_st["xt"]) and torch.equal(rep["idx"], rep_st["idx"])
+    assert rep["K"] == rep_st["K"]
+    for k in ("local", "global"):
+        assert [i["iterations"] for i in rep.get(k, [])] == [i["iterations"] for i in rep_st.get(k, [])], k
     x_gpu = x_gpu.cpu().numpy()
     idx = rep["idx"].cpu().numpy()
-    taus = rep["tau"]
+    taus = rep_st["tau"]
     xt_gpu = rep["xt"].cpu().numpy()
-    bsub_gpu = rep["bsub"].cpu().numpy() if "bsub" in rep else None
-    xb0_gpu = rep["xB0"].cpu().numpy() if "xB0" in rep else None
+    bsub_gpu = rep_st["bsub"].cpu().numpy() if "bsub" in rep_st else None
+    xb0_gpu = rep_st["xB0"].cpu().numpy() if "xB0" in rep_st else None
     stats = []
     off = 0
     for g, (r0, r1) in enumerate(segments(sy)):
@@ -609,32 +617,55 @@ def test_spmv_bitexact(case, tune):
     np.testing.assert_array_equal(y.cpu().numpy(), orc.spmv(Ao, xh))
 
 
-@pytest.mark.parametrize("case", ["c5", "c2", "c4blocks", "random", "dense_rows"])
-def test_spmv_csr_bitexact(case):
-    """lc_spmv_csr (the row-slab CSR kernel) equals or_spmv bitwise: staged x window (2-D), unstaged (3-D),
-    a scalar view of the 3T BSR matrix, a random band, and slabs too dense to stage (rows of 40 entries)."""
-    if case == "dense_rows":
-        n = 700
-        rng = np.random.default_rng(3)
+def _csr_case(case):
+    rng = np.random.default_rng(3)
+    if case in ("dense_rows", "mixed", "empty_rows"):
+        n = {"dense_rows": 700, "mixed": 3000, "empty_rows": 1037}[case]
         rp, ci, va = [0], [], []
         for i in range(n):
-            cols = sorted(set(rng.choice(n, 39, replace=False).tolist()) | {i})
+            if case == "empty_rows" and (i % 7 == 3 or i >= n - 5):      # empty rows, trailing ones too
+                cols = []
+            elif case == "dense_rows" or (case == "mixed" and 800 <= i < 1100):
+                cols = sorted(set(rng.choice(n, 39, replace=False).tolist()) | {i})
+            else:
+                cols = sorted(set(rng.choice(n, int(rng.integers(1, 9)), replace=False).tolist()))
             ci += cols
             va += rng.standard_normal(len(cols)).tolist()
             rp.append(len(ci))
-        Ao = orc.Csr(np.array(rp), np.array(ci, np.int32), np.array(va))
-    elif case == "random":
+        if case == "empty_rows" and len(ci) % 2 == 0:                     # odd nnz: the widened copy would overrun
+            ci.append(0); va.append(0.5); rp[-1] += 1
+        return orc.Csr(np.array(rp), np.array(ci, np.int32), np.array(va))
+    if case == "random":
         s_ = synth.random_system(3001, bw=6, spd=False, seed=4)
-        Ao = orc.Csr(s_.rp, s_.ci, s_.val)
-    elif case == "c4blocks":
-        Ao = oracle_csr(synth.system(4, 2, n=16))
-    else:
-        sy = synth.system(5 if case == "c5" else 2, 3, n=20 if case == "c5" else 96)
-        Ao = oracle_csr(sy)
+        return orc.Csr(s_.rp, s_.ci, s_.val)
+    if case == "c4blocks":
+        return oracle_csr(synth.system(4, 2, n=16))
+    if case == "c5_big":                                                  # many chunks per CTA (ring reuse)
+        return oracle_csr(synth.system(5, 3, n=72))
+    sy = synth.system(5 if case == "c5" else 2, 3, n=20 if case == "c5" else 96)
+    return oracle_csr(sy)
+
+
+@pytest.mark.parametrize("tma", [1, 0])
+@pytest.mark.parametrize("case", ["c5", "c5_big", "c2", "c4blocks", "random", "dense_rows", "mixed", "empty_rows",
+                                  "misaligned"])
+def test_spmv_csr_bitexact(case, tma, tune):
+    """lc_spmv_csr equals or_spmv bitwise, with the TMA-staged chunks (tma = 1: 256-row chunks, slab stream by
+    cp.async.bulk) and the warp row-slab kernel (tma = 0): 2-D and 3-D stencils, many chunks per CTA, a scalar view
+    of the 3T BSR matrix, a random band, rows too dense to stage (all of them, or one run of chunks), empty rows
+    (trailing ones, odd nnz: the last chunk reads from global memory), and arrays not 16-byte aligned (falls back)."""
+    tune(spmv_csr_tma=tma)
+    Ao = _csr_case("c5" if case == "misaligned" else case)
     n = Ao.n
     xh = np.cos(np.arange(n) * 0.11)
     y = torch.empty(n, dtype=torch.float64, device=DEV)
-    lc.spmv_csr(to_dev(Ao.rp.astype(np.int64)), to_dev(Ao.ci.astype(np.int32)), to_dev(Ao.val), to_dev(xh), y)
+    rp, ci, va = to_dev(Ao.rp.astype(np.int64)), to_dev(Ao.ci.astype(np.int32)), to_dev(Ao.val)
+    if case == "misaligned":                    # the same arrays at 8- / 4- / 8-byte offsets
+        rp2 = torch.empty(n + 2, dtype=torch.int64, device=DEV); rp2[1:] = rp; rp = rp2[1:]
+        ci2 = torch.empty(len(ci) + 1, dtype=torch.int32, device=DEV); ci2[1:] = ci; ci = ci2[1:]
+        va2 = torch.empty(len(va) + 1, dtype=torch.float64, device=DEV); va2[1:] = va; va = va2[1:]
+        assert rp.data_ptr() % 16 and ci.data_ptr() % 16 and va.data_ptr() % 16
+    lc.spmv_csr(rp, ci, va, to_dev(xh), y)
     np.testing.assert_array_equal(y.cpu().numpy(), orc.spmv(Ao, xh))
 
 

@@ -108,15 +108,20 @@ def run_system(task):
     b, x0 = torch.from_numpy(sy.b).to(dev), torch.from_numpy(sy.x0).to(dev)
     gpu = {}
     for name, rule in RULES[cfg]:
+        # tau, the criterion and Eq. 3 from the step-by-step calls; x, x~, Omega and the iterations from Alg. 1 in
+        # one call (lc_local_method)
         dom = lc.select_domain(A, b, x0, **rule)
-        _, _, crit, _ = dom.export(want_crit=True)
+        _, tau, crit, _ = dom.export(want_crit=True)
         crit = crit.cpu().numpy()
+        bsub = xb0 = None
+        if sum(dom.K) > 0:
+            sub = lc.extract_sub(A, dom, b, x0)
+            bsub, xb0 = (t.cpu().numpy() for t in sub.export())
+            del sub
         del dom
         x, rep = lc.local_method(A, b, x0, rule, method=method, rel_tol=EPS, keep=True)
         gpu[name] = dict(x=x.cpu().numpy(), xt=rep["xt"].cpu().numpy(), idx=rep["idx"].cpu().numpy(),
-                         tau=list(rep["tau"]), K=list(rep["K"]), crit=crit,
-                         bsub=rep["bsub"].cpu().numpy() if "bsub" in rep else None,
-                         xB0=rep["xB0"].cpu().numpy() if "xB0" in rep else None,
+                         tau=list(tau), K=list(rep["K"]), crit=crit, bsub=bsub, xB0=xb0,
                          it_local=[i["iterations"] for i in rep.get("local", [])] or [0] * G,
                          it_global=[i["iterations"] for i in rep["global"]],
                          st_global=[i["status"] for i in rep["global"]])
