@@ -414,6 +414,12 @@ typedef struct {
                                    level schedule */
   int32_t spmv_csr_tma;         /* 1 (default): lc_spmv_csr stages its row chunks by TMA when the three CSR arrays
                                    are 16-byte aligned; 0: the warp row-slab kernel */
+  int32_t spmv_tma;             /* 1 (default): lc_spmv stages the SELL-32 slice stream by TMA (block 1); 2: the
+                                   stencil layouts (5 / 7 slots) too (slower there); 0: plain loads */
+  int32_t batched_cluster;      /* 0 (default): batched lock-step PCG reduces through the two-level reducing
+                                   barrier; 2..16: launched in clusters of that many CTAs, reductions through
+                                   distributed shared memory + one counter level (measured no faster in situ,
+                                   profiles/r02_e_batched_reduce.md) */
 } lc_tuning;
 
 /* the defaults listed above (host output) */

@@ -113,6 +113,37 @@ lc_status max_coresident(const void* fn, int threads, size_t dsmem, int64_t* cta
   return LC_OK;
 }
 
+static std::map<std::tuple<int, const void*, int, size_t, int>, int> g_occ_cl;   // clusters per (dev, fn, thr, smem, cl)
+
+lc_status max_clusters(const void* fn, int threads, size_t dsmem, int cl, int64_t* clusters) {
+  int dev = 0;
+  lc_status st = device_of_caller(&dev);
+  if (st) return st;
+  const auto key = std::make_tuple(dev, fn, threads, dsmem, cl);
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto it = g_occ_cl.find(key);
+    if (it != g_occ_cl.end()) { *clusters = it->second; return LC_OK; }
+  }
+  if (dsmem > 0 && (st = func_attr(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem))) return st;
+  if (cl > 8 && (st = func_attr(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1))) return st;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)cl);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = dsmem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)cl; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  LC_CUDA(cudaOccupancyMaxActiveClusters(&n, fn, &cfg));
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  g_occ_cl[key] = n;
+  *clusters = n;
+  return LC_OK;
+}
+
 // ---- completion of a Krylov launch (immediate / deferred, lc_internal.cuh) ----
 SolveClock::SolveClock(Pending* pend) {
   if (pend && pend->e0 && pend->e1) { e0 = pend->e0; e1 = pend->e1; return; }
@@ -190,6 +221,8 @@ static lc_tuning defaults_() {
   t.lazy_x_depth = 3; t.batched_schedule = -1; t.pcg_max_ctas = 0; t.sub_repr = -1; t.gmres_exact_cgs2 = 0;
   t.gs_lines = 1;
   t.spmv_csr_tma = 1;
+  t.spmv_tma = 1;
+  t.batched_cluster = 0;
   return t;
 }
 static thread_local lc_tuning g_tune = defaults_();
@@ -446,7 +479,8 @@ extern "C" lc_status lc_set_tuning(const lc_tuning* t) {
   if (!bin(t->stencil_layout) || !bin(t->symmetric_layout) || !bin(t->pcg_cluster_resident) || !bin(t->pcg_cluster) ||
       !bin(t->pcg_tma) || t->lazy_x_depth < 0 || t->lazy_x_depth > 3 || t->batched_schedule < -1 ||
       t->batched_schedule > 1 || t->pcg_max_ctas < 0 || t->sub_repr < -1 || t->sub_repr > 1 ||
-      !bin(t->gmres_exact_cgs2) || !bin(t->gs_lines) || !bin(t->spmv_csr_tma)) {
+      !bin(t->gmres_exact_cgs2) || !bin(t->gs_lines) || !bin(t->spmv_csr_tma) || t->spmv_tma < 0 || t->spmv_tma > 2 ||
+      t->batched_cluster < 0 || t->batched_cluster == 1 || t->batched_cluster > 16) {
     lc::set_error("lc_set_tuning: field out of range");
     return LC_ERR_INVALID_ARG;
   }

@@ -80,6 +80,7 @@ struct PcgArgs {
   int lazyx;                    // (vec2 solves) x is updated every lazyx-th iteration (0: every one): pass B
   int cluster;                  // launched as ONE thread-block cluster (small G = 1 systems): cluster
                                 // barriers and DSMEM partial exchange instead of the global grid barrier
+  int clus;                     // (G > 1, lock step) launched in thread-block clusters: cluster_reduce_barrier
   int teams;                    // > 0 (G > 1): the CTAs form `teams` contiguous teams; team t solves segments
                                 // t, t + teams, ... one after another as G = 1 systems with its own barrier
   unsigned long long* tctr;     // [teams][16] team barrier counters (zeroed at launch)
@@ -434,6 +435,10 @@ __global__ void __launch_bounds__(kPT, ST == 0 ? LCV_MINB_SELL : LCV_MINB) k_pcg
   __shared__ int s_act[kMaxSeg + 1];           // active segments of the current pass (+ sentinel)
   __shared__ long long s_actj[kMaxSeg + 1];    // their runs concatenated
   __shared__ double s_cpart[2][2];             // cluster mode: this CTA's partials, double-buffered by pass
+  // batched solves launched in clusters (P.clus): the CTA's partials for the cluster reduction, and its scratch
+  __shared__ double s_mine[KIND == 1 ? 2 * kMaxSeg : 1];
+  __shared__ double s_chunk[KIND == 1 ? kPT : 1];
+  unsigned long long ctr_target = 0;
   int cpar = 0;
   extern __shared__ __align__(128) double dsm[];   // TMA stages (P.tma): kStages x 8 slices x 32 x vw values
   __shared__ __align__(8) uint64_t s_bars[kStages];
@@ -499,6 +504,17 @@ __global__ void __launch_bounds__(kPT, ST == 0 ? LCV_MINB_SELL : LCV_MINB) k_pcg
     // G = 1: the partials are double-buffered by pass, since a CTA that leaves the barrier early may finish its
     // next pass and store its next partial before a slower CTA has read this one (short passes)
     double* const pt = P.part + (G == 1 ? (size_t)cpar * 2 * nCTA : 0);
+    if (KIND == 1 && P.clus) {
+      // batched, launched in clusters: the CTA's partials stay in shared memory for the cluster reduction
+      for (int t = threadIdx.x; t < G * 2; t += kPT) {
+        double v = 0.0;
+        for (int w = 0; w < kPW; ++w) v += s_acc[w][t >> 1][t & 1];
+        s_mine[t] = v;
+      }
+      cluster_reduce_barrier<kPT, 2 * kMaxSeg>(P.bar, P.part, s_mine, &s_sum[0][0], 2 * G, s_chunk, ctr_target,
+                                               tree_gen);
+      return;
+    }
     for (int t = threadIdx.x; t < G * 2; t += kPT) {
       double v = 0.0;
       for (int w = 0; w < kPW; ++w) v += s_acc[w][t >> 1][t & 1];
@@ -945,6 +961,7 @@ __global__ void __launch_bounds__(kPT, ST == 0 ? LCV_MINB_SELL : LCV_MINB) k_pcg
     }
   }
   }                                             // segments of the team
+  if (KIND == 1 && P.clus) cg::this_cluster().sync();   // no CTA exits while its rank 0 may read its partials
 }
 
 // ---------------------------------------------------------------- host ----
@@ -1003,6 +1020,14 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   int64_t nCTA = std::min<int64_t>(max_ctas, (std::max<int64_t>(work, 1) + kPW - 1) / kPW);
   if (tune.pcg_max_ctas > 0) nCTA = std::max<int64_t>(1, std::min<int64_t>(nCTA, tune.pcg_max_ctas));
   if (nCTA < 1) nCTA = 1;
+  // batched lock step: launched in clusters of CL CTAs (cluster_reduce_barrier: one level of global latency per
+  // reduction instead of two), as many whole clusters as are co-resident
+  int CL = (kind == 1 && tune.batched_cluster > 1) ? tune.batched_cluster : 0;
+  if (CL) {
+    int64_t maxcl = 0;
+    if (max_clusters(fn, kPT, dsmem, CL, &maxcl) != LC_OK || maxcl < 1) { cudaGetLastError(); CL = 0; }
+    else nCTA = std::max<int64_t>(1, std::min<int64_t>(maxcl, (nCTA + CL - 1) / CL)) * CL;
+  }
   void* ws = nullptr;
   const size_t vec = sizeof(double) * (size_t)n;
   const size_t vbytes = (vec + 255) & ~(size_t)255;
@@ -1046,6 +1071,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   a.out_relres = (double*)((((uintptr_t)w) + 7) & ~(uintptr_t)7);
   a.tctr = (unsigned long long*)((((uintptr_t)(a.out_relres + G)) + 127) & ~(uintptr_t)127);
   a.teams = teams;
+  a.clus = CL ? 1 : 0;
   a.slist = job.slist;
   a.nlist = job.nlist_dev;
   a.omega = job.omega;
@@ -1097,6 +1123,21 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
       attr[0].val.clusterDim.x = csz;
       e = cudaLaunchKernelExC(&cfg, fn, args);
     }
+  } else if (e == cudaSuccess && CL) {
+    // cooperative (co-residency is checked by the driver) and clustered
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)nCTA);
+    cfg.blockDim = dim3(kPT);
+    cfg.dynamicSmemBytes = dsmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)CL; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    e = cudaLaunchKernelExC(&cfg, fn, args);
   } else if (e == cudaSuccess) {
     e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kPT), args, dsmem, s);
   }

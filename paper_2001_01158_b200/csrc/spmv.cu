@@ -97,6 +97,109 @@ __global__ void __launch_bounds__(kVT) k_spmv(SellView A, const double* __restri
   for (int a = 0; a < BS; ++a) y[BS * u + a] = acc[a];
 }
 
+// ---- lc_spmv with the slice stream staged by TMA (stencil and SELL-32 layouts, block 1): persistent CTAs take
+// chunks of kSC = 8 consecutive slices (warp w of the CTA computes slice w of the chunk, lane l its row).  The
+// chunk's slots [slice_ptr[s0], slice_ptr[s0 + 8]) are contiguous and 256-byte aligned in both layouts, so thread 0
+// copies its values (and, SELL, its int32 columns) into a stage of a 2-deep shared-memory ring with one or two
+// cp.async.bulk per chunk, completing on the stage's mbarrier; the warps read their slots from shared memory
+// (lane-consecutive, conflict-free) and gather x.  SELL chunks wider than a stage read from global memory.
+constexpr int kSC = 8;                         // slices per chunk (= warps per CTA)
+constexpr int kSSlots = 8 * 32 * 8;            // staged slots per chunk (8 slots per row)
+constexpr int kSStage = kSSlots * 12;          // values + columns
+
+template <int ST, int WM>
+__global__ void __launch_bounds__(kVT) k_spmv_tma(SellView A, const double* __restrict__ x, double* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char ssm[];
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ int64_t s_p0[2];                  // first slot of the staged chunk, -1 = not staged
+  const int64_t nch = (A.nslices + kSC - 1) / kSC;
+  const int64_t bid = blockIdx.x, nCTA = gridDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int64_t t) {
+    const int64_t c = bid + t * nCTA;
+    if (c >= nch) return;
+    const int st = (int)(t & 1);
+    const int64_t s0 = c * kSC, s1 = s0 + kSC < A.nslices ? s0 + kSC : A.nslices;
+    const int64_t p0 = ST ? 32ll * WM * s0 : A.slice_ptr[s0];
+    const int64_t p1 = ST ? 32ll * WM * s1 : A.slice_ptr[s1];
+    if (p1 - p0 > kSSlots) {
+      s_p0[st] = -1;
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bars[st])) : "memory");
+      return;
+    }
+    s_p0[st] = p0;
+    unsigned char* sb = ssm + (size_t)st * kSStage;
+    const unsigned bv = (unsigned)((p1 - p0) * 8), bc = ST ? 0u : (unsigned)((p1 - p0) * 4);
+    mbar_expect_tx(&bars[st], bv + bc);
+    tma_bulk_g2s(sb, A.val + p0, bv, &bars[st]);
+    if (!ST) tma_bulk_g2s(sb + (size_t)kSSlots * 8, A.col + p0, bc, &bars[st]);
+  };
+  if (threadIdx.x == 0) { issue(0); issue(1); }
+  const int n1 = (int)A.nunits - 1;
+#pragma unroll 1
+  for (int64_t t = 0;; ++t) {
+    const int64_t c = bid + t * nCTA;
+    if (c >= nch) break;
+    const int st = (int)(t & 1);
+    mbar_wait(&bars[st], (unsigned)((t >> 1) & 1));
+    const int64_t s = c * kSC + warp;
+    if (s < A.nslices) {
+      const int g = A.slice_seg[s];
+      const int64_t u = A.slice_row0[s] + lane;
+      if (u < A.seg_unit0[g + 1]) {
+        const int64_t p0 = s_p0[st];
+        const int64_t ps = ST ? 32ll * WM * s : A.slice_ptr[s];
+        const int w = ST ? WM : (int)((A.slice_ptr[s + 1] - ps) >> 5);
+        const unsigned char* sb = ssm + (size_t)st * kSStage;
+        const double* sv = p0 >= 0 ? reinterpret_cast<const double*>(sb) + (ps - p0) + lane : A.val + ps + lane;
+        const int32_t* sc = p0 >= 0 ? reinterpret_cast<const int32_t*>(sb + (size_t)kSSlots * 8) + (ps - p0) + lane
+                                    : A.col + ps + lane;
+        double acc = 0.0;
+        if (ST) {
+          double v[WM > 0 ? WM : 1], xv[WM > 0 ? WM : 1];
+#pragma unroll
+          for (int k = 0; k < WM; ++k) {
+            int cc = (int)u + A.off[k];
+            cc = cc < 0 ? 0 : (cc > n1 ? n1 : cc);
+            v[k] = sv[32 * k];
+            xv[k] = __ldg(x + cc);
+          }
+#pragma unroll
+          for (int k = 0; k < WM; ++k) acc = __fma_rn(v[k], xv[k], acc);
+        } else {
+          for (int k0 = 0; k0 < w; k0 += 4) {
+            int cc[4];
+            double v[4], xv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const bool ok = k0 + j < w;
+              cc[j] = ok ? sc[32 * (k0 + j)] : 0;
+              v[j] = ok ? sv[32 * (k0 + j)] : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) xv[j] = __ldg(x + cc[j]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (k0 + j < w) acc = __fma_rn(v[j], xv[j], acc);
+          }
+        }
+        y[u] = acc;
+      }
+    }
+    __syncthreads();                               // every warp is done with stage st
+    if (threadIdx.x == 0) {
+      fence_proxy_async_smem();
+      issue(t + 2);
+    }
+  }
+}
+
 // ---- CSR row-slab SpMV (SURVEY 8(a) kernel notes; the format the handles do NOT keep -- DESIGN.md s5):
 // a warp owns a slab of 32 consecutive rows; its lanes copy the slab's values and columns
 // [rp[r0], rp[r0 + 32]) into the warp's shared-memory slot with coalesced loads (no block-wide barrier),
@@ -282,6 +385,24 @@ extern "C" lc_status lc_spmv(lc_matrix M, const double* x, double* y, void* stre
   Touch tA(M->use, s);
   const unsigned nb = (unsigned)((A.nslices * 32 + kVT - 1) / kVT);
   const SellView V = view(A);
+  // SELL-32 (block 1): the slice stream staged by TMA, 298 -> 289 us at 256^3 (5.66 -> 5.82 TB/s); the stencil layout
+  // keeps plain loads (179 us with them, 222 us staged: its 8-byte slots leave too little in flight per stage,
+  // profiles/r02_d_spmv_tma.jsonl).  lc_tuning.spmv_tma = 0: plain loads everywhere; 2: the stencil layout staged too
+  if (M->block == 1 && !A.sym && tuning().spmv_tma && (!A.stencil || (tuning().spmv_tma == 2 &&
+                                                                      (A.maxw == 5 || A.maxw == 7)))) {
+    const void* fn = !A.stencil ? (const void*)k_spmv_tma<0, 0>
+                                : A.maxw == 7 ? (const void*)k_spmv_tma<1, 7> : (const void*)k_spmv_tma<1, 5>;
+    int64_t ctas = 0;
+    const size_t dsm = 2 * (size_t)kSStage;
+    if (lc_status st = max_coresident(fn, kVT, dsm, &ctas)) return st;
+    const int64_t nch = (A.nslices + kSC - 1) / kSC;
+    const unsigned grid = (unsigned)(nch < ctas ? nch : ctas);
+    if (!A.stencil) k_spmv_tma<0, 0><<<grid, kVT, dsm, s>>>(V, x, y);
+    else if (A.maxw == 7) k_spmv_tma<1, 7><<<grid, kVT, dsm, s>>>(V, x, y);
+    else k_spmv_tma<1, 5><<<grid, kVT, dsm, s>>>(V, x, y);
+    LC_LAUNCHED();
+    return LC_OK;
+  }
   if (M->block == 1 && A.stencil && !A.sym && A.maxw == 7)
     k_spmv_stencil<7><<<nb, kVT, 0, s>>>(V, x, y);
   else if (M->block == 1 && A.stencil && !A.sym && A.maxw == 5)

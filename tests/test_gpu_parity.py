@@ -219,6 +219,22 @@ def test_config3_batched_schedules(n, G, s, sched, tune):
     check_system(sy, RULES[3][0])
 
 
+@pytest.mark.parametrize("cl", [0, 2, 4, 8, 16])
+@pytest.mark.parametrize("n,G,s", [(30, 4, 0), (64, 20, 5)])
+def test_config3_lockstep_cluster_sizes(n, G, s, cl, tune):
+    """The lock-step batched PCG with its reductions through clusters of cl CTAs (distributed shared memory, then
+    one counter level; 0: the two-level reducing barrier without clusters) against the oracle, and bitwise
+    repeatable run to run."""
+    tune(batched_schedule=0, batched_cluster=cl)
+    sy = synth.system(3, s, n=n, G=G)
+    check_system(sy, RULES[3][0])
+    A = gpu_matrix(sy)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    x1, r1 = lc.local_method(A, b, x0, None)
+    x2, r2 = lc.local_method(A, b, x0, None)
+    assert torch.equal(x1, x2) and [i["iterations"] for i in r1["global"]] == [i["iterations"] for i in r2["global"]]
+
+
 @pytest.mark.parametrize("n,s", [(20, 0), (45, 4), (64, 29)])
 def test_config4_reduced_gmres(n, s):
     sy = synth.system(4, s, n=n)
@@ -591,12 +607,21 @@ def test_non_default_stream():
     assert rep2["K"] == rep_ref["K"]
 
 
-@pytest.mark.parametrize("case", ["c5", "c1", "c3", "c4", "sell", "tridiag"])
-def test_spmv_bitexact(case, tune):
-    """lc_spmv (y = A x) equals the oracle's or_spmv bitwise on every layout / width / block size."""
-    if case == "sell":
+@pytest.mark.parametrize("tma", [2, 1, 0])
+@pytest.mark.parametrize("case", ["c5", "c1", "c3", "c4", "sell", "tridiag", "c5_big", "sell_big", "sell_c3",
+                                  "wide_sell"])
+def test_spmv_bitexact(case, tma, tune):
+    """lc_spmv (y = A x) equals the oracle's or_spmv bitwise on every layout / width / block size, with the slice
+    stream staged by TMA (tma = 2: every layout, 1: SELL-32 only; many chunks per CTA in the *_big cases, batched
+    segments, rows too wide to stage) and with plain loads (tma = 0)."""
+    tune(spmv_tma=tma)
+    if case in ("sell", "sell_big", "sell_c3"):
         tune(stencil_layout=0)
-    if case == "tridiag":
+    if case == "wide_sell":
+        Ao = _csr_case("mixed", diag=True)          # rows 800-1099 hold 40 entries: chunks wider than a stage
+        A = lc.Matrix(Ao.n, Ao.rp, Ao.ci, Ao.val)
+        xh = np.sin(np.arange(Ao.n) * 0.37)
+    elif case == "tridiag":
         n = 1000
         M = np.eye(n) * 3.0
         for i in range(n - 1):
@@ -606,7 +631,8 @@ def test_spmv_bitexact(case, tune):
         A = lc.Matrix(n, Ao.rp, Ao.ci, Ao.val)
         xh = np.sin(np.arange(n) * 0.37)
     else:
-        cfg, nn = {"c5": (5, 20), "c1": (1, 64), "c3": (3, 30), "c4": (4, 24), "sell": (5, 16)}[case]
+        cfg, nn = {"c5": (5, 20), "c1": (1, 64), "c3": (3, 30), "c4": (4, 24), "sell": (5, 16), "c5_big": (5, 72),
+                   "sell_big": (5, 72), "sell_c3": (3, 30)}[case]
         sy = synth.system(cfg, 3, n=nn, G=4)
         Ao = oracle_csr(sy)
         A = gpu_matrix(sy)
@@ -617,7 +643,7 @@ def test_spmv_bitexact(case, tune):
     np.testing.assert_array_equal(y.cpu().numpy(), orc.spmv(Ao, xh))
 
 
-def _csr_case(case):
+def _csr_case(case, diag=False):
     rng = np.random.default_rng(3)
     if case in ("dense_rows", "mixed", "empty_rows"):
         n = {"dense_rows": 700, "mixed": 3000, "empty_rows": 1037}[case]
@@ -629,6 +655,8 @@ def _csr_case(case):
                 cols = sorted(set(rng.choice(n, 39, replace=False).tolist()) | {i})
             else:
                 cols = sorted(set(rng.choice(n, int(rng.integers(1, 9)), replace=False).tolist()))
+            if diag:
+                cols = sorted(set(cols) | {i})
             ci += cols
             va += rng.standard_normal(len(cols)).tolist()
             rp.append(len(ci))

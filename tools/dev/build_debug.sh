@@ -1,7 +1,7 @@
 #!/bin/bash
 # Debug build of liblc with the device timelines (-DLC_DEBUG_TIMELINE): build_dbg/liblc_dbg.so
 set -e
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p build_dbg
 objs=()
 for f in paper_2001_01158_b200/csrc/*.cu; do
