@@ -176,7 +176,8 @@ enum { LC_KERNEL_NONE = 0      /* no launch (empty subsystem) */,
        LC_KERNEL_PCG_RESIDENT = 3 /* cluster with the system resident in shared memory (<= ~30k rows) */,
        LC_KERNEL_PCG_LOCKSTEP = 4 /* batched, all active segments swept in lock step */,
        LC_KERNEL_PCG_TEAMS = 5    /* batched, one team of CTAs per segment */,
-       LC_KERNEL_GMRES = 6 };
+       LC_KERNEL_GMRES = 6,
+       LC_KERNEL_PCG_DYNTEAMS = 7 /* batched, one team per active segment, re-teamed as segments converge */ };
 
 /*
  * Alg. 1 l.5-6: solve B xbar_B = b_sub from x_B0 to ||b_sub - B xbar|| <= eps ||b_sub||
@@ -406,7 +407,8 @@ typedef struct {
   int32_t pcg_tma;              /* 1 (default): TMA bulk-copy ring for the value stream of contiguous solves */
   int32_t lazy_x_depth;         /* 3 (default) or 2: x updated every 3rd / 2nd PCG iteration (same roundings,
                                    DESIGN.md s6); 0 or 1: every iteration */
-  int32_t batched_schedule;     /* -1 (default) automatic, 0 lock step, 1 teams (batched PCG, G > 1) */
+  int32_t batched_schedule;     /* -1 (default) automatic, 0 lock step, 1 static teams, 2 dynamic teams (batched
+                                   PCG, G > 1; dynamic teams need equal segments without a slice list) */
   int32_t pcg_max_ctas;         /* 0 (default): occupancy x SMs; > 0 caps the grid of the PCG kernels */
   int32_t sub_repr;             /* -1 (default) automatic, 0 explicit SELL B, 1 masked on A's stencil layout */
   int32_t gmres_exact_cgs2;     /* 0 (default): Gram-form CGS2 (R39); 1: the textbook two passes */

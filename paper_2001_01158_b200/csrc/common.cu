@@ -478,7 +478,7 @@ extern "C" lc_status lc_set_tuning(const lc_tuning* t) {
   auto bin = [](int32_t v) { return v == 0 || v == 1; };
   if (!bin(t->stencil_layout) || !bin(t->symmetric_layout) || !bin(t->pcg_cluster_resident) || !bin(t->pcg_cluster) ||
       !bin(t->pcg_tma) || t->lazy_x_depth < 0 || t->lazy_x_depth > 3 || t->batched_schedule < -1 ||
-      t->batched_schedule > 1 || t->pcg_max_ctas < 0 || t->sub_repr < -1 || t->sub_repr > 1 ||
+      t->batched_schedule > 2 || t->pcg_max_ctas < 0 || t->sub_repr < -1 || t->sub_repr > 1 ||
       !bin(t->gmres_exact_cgs2) || !bin(t->gs_lines) || !bin(t->spmv_csr_tma) || t->spmv_tma < 0 || t->spmv_tma > 2 ||
       t->batched_cluster < 0 || t->batched_cluster == 1 || t->batched_cluster > 16) {
     lc::set_error("lc_set_tuning: field out of range");

@@ -38,6 +38,13 @@ constexpr int kCC = LC_GMRES_CC;             // slices per warp chunk in the SpM
 // basis vectors per unrolled block of the dot / update loops: 1 (config 4 Arnoldi step 67.2 us) beats 2 (69.0),
 // 3 (69.1), 4 (72.3), 8 (81.0): the wider blocks' register arrays spill (tools/build_variant.sh A/B)
 constexpr int kIB = LC_GMRES_IB;
+#ifndef LC_GMRES_REV
+#define LC_GMRES_REV 0
+#endif
+// 1: the update pass sweeps the slices in reverse, starting on the rows the SpMV + dots pass read last (L2 reuse
+// of the basis): config 4 Arnoldi step 67.2 -> 68.3 us, not adopted (the update pass already runs above the DRAM
+// rate, 19 us for 145 MB at j = 15, tools/tl_gmres.py)
+constexpr bool kGRev = LC_GMRES_REV != 0;
 
 struct GmresArgs {
   SellView A;
@@ -342,7 +349,8 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
         clear(1);
         {
           double a0 = 0.0;
-          for (int64_t s = s_begin; s < A.nslices; s += s_step) {
+          for (int64_t sr = s_begin; sr < A.nslices; sr += s_step) {
+            const int64_t s = kGRev ? A.nslices - 1 - sr : sr;
             int64_t u = A.slice_row0[s] + lane;
             if (u >= nunits) continue;
             double ww[BS];

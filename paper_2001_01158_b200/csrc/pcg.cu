@@ -964,6 +964,269 @@ __global__ void __launch_bounds__(kPT, ST == 0 ? LCV_MINB_SELL : LCV_MINB) k_pcg
   if (KIND == 1 && P.clus) cg::this_cluster().sync();   // no CTA exits while its rank 0 may read its partials
 }
 
+// ------------------------------------------------ batched: dynamic teams ----
+// Batched global solves (G > 1 equal segments, no slice list): the CTAs form one TEAM per active group -- team t of
+// A active groups = CTAs [t nCTA / A, (t + 1) nCTA / A) -- and each team iterates its group's PCG with its own
+// counter barrier, so teams never wait for each other's passes.  When a group converges its team raises the
+// re-team request; every other team sees it at its next pass end (an OR over its CTAs' observations, so the whole
+// team decides alike), stores its group's state and joins one grid barrier, after which the CTAs are split over the
+// groups still active.  The slowest groups end up with the whole GPU, and no pass waits for the slowest of all
+// CTAs of the grid (config 3 lock step: 7-11 us from a CTA's pass end to the end of its reducing barrier).
+// Reductions do not depend on the team: the rows are cut into fixed chunks of kDynR slices, a warp adds a chunk's
+// rows in a fixed order into one chunk partial, and every CTA of the team adds the group's chunk partials in a
+// fixed order -- the results are bitwise the same whatever team sizes the timing of the re-team events produced.
+#ifndef LC_DYN_R
+#define LC_DYN_R 4
+#endif
+constexpr int kDynR = LC_DYN_R;          // slices per chunk
+struct DynGroup {                        // a group's solver state between teams (global memory)
+  int mode, par, it, final_, npass;
+  unsigned gone;                         // 0, or the first phase without the group (its team finished it in phase
+                                         // gone - 1): read for the active list, which must not depend on when a CTA
+                                         // reads it -- a fast team may finish its group while a slow CTA still reads
+  double rho, alpha, beta, tgt, nb, pad1;
+  unsigned long long cbase;              // arrivals so far on the group's team counter
+};
+struct DynArgs {
+  PcgArgs P;
+  DynGroup* gst;                         // [G]
+  double* cpart;                         // [2][G][nchk][2] chunk partials, double-buffered by the group's pass parity
+  unsigned* fobs;                        // [2][nCTA] re-team request seen by the CTA before its team barrier
+  unsigned long long* gctr;              // [G][16] team barrier counters (monotonic)
+  unsigned* req;                         // re-team requests: phase k ends once *req > k
+  int nchk;                              // chunks per group (the largest group's), the stride of cpart
+};
+
+template <int WM, int ST>
+__global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg_dyn(DynArgs D) {
+  const PcgArgs& P = D.P;
+  const SellView& A = P.A;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nCTA = gridDim.x, bid = blockIdx.x;
+  const int G = P.G;
+  __shared__ SegState S;
+  __shared__ int s_act[kMaxSeg + 1];
+  __shared__ int s_na, s_rt;
+  __shared__ double s_w[kPW][2];
+  __shared__ double s_sum[2];
+  unsigned long long gepoch = 0;         // grid barriers (re-team phases) * nCTA
+  unsigned phase = 0;
+#ifdef LC_DEBUG_TIMELINE
+  int tlk = 0;                           // CTA 0: per pass (start, chunks done, reduced) + the team size
+#endif
+  for (;;) {
+    grid_barrier(P.bar, gepoch);         // phase boundary: every group's state is in D.gst
+    if (threadIdx.x == 0) {
+      int na = 0;
+      for (int g = 0; g < G; ++g) {
+        const unsigned gone = __ldcg(&D.gst[g].gone);
+        if (gone == 0 || gone > phase) s_act[na++] = g;
+      }
+      s_na = na;
+    }
+    __syncthreads();
+    const int na = s_na;
+    if (na == 0) break;
+    int t = (int)((bid * na) / nCTA);
+    while (t > 0 && bid < (int64_t)t * nCTA / na) --t;
+    while (t < na - 1 && bid >= (int64_t)(t + 1) * nCTA / na) ++t;
+    const int64_t tb0 = (int64_t)t * nCTA / na, tn = (int64_t)(t + 1) * nCTA / na - tb0;
+    const int g = s_act[t];
+    if (threadIdx.x == 0) {
+      const DynGroup& q = D.gst[g];
+      S.mode = __ldcg(&q.mode); S.par = __ldcg(&q.par); S.it = __ldcg(&q.it); S.final_ = __ldcg(&q.final_);
+      S.pend = __ldcg(&q.npass);             // (npass kept in the pend field: no lazy x in batched solves)
+      S.rho = __ldcg(&q.rho); S.alpha = __ldcg(&q.alpha); S.beta = __ldcg(&q.beta); S.tgt = __ldcg(&q.tgt);
+      S.nb = __ldcg(&q.nb);
+    }
+    unsigned long long* ctr = D.gctr + 16 * g;
+    // the counter's arrivals so far come from the group's state (not from the counter itself: a fast member of
+    // the new team may already have arrived for its first pass)
+    unsigned long long target = 0;
+    if (threadIdx.x == 0) target = __ldcg(&D.gst[g].cbase);
+    __syncthreads();
+    __shared__ long long s_g0, s_g1;
+    if (threadIdx.x == 0) { s_g0 = P.A.seg_slice0[g]; s_g1 = P.A.seg_slice0[g + 1]; }
+    __syncthreads();
+    const int64_t s0g = s_g0, s1g = s_g1;
+    const int64_t nchg = (s1g - s0g + kDynR - 1) / kDynR;   // this group's chunks
+    const int64_t kw = (bid - tb0) * kPW + warp, TW = tn * kPW;
+    bool leave = false;
+    while (!leave) {
+      TL(tlk);
+      const int mode = S.mode;
+      const int par = S.pend & 1;
+      double* cp = D.cpart + ((size_t)par * G + g) * (size_t)D.nchk * 2;
+      // ---- the pass over this team's chunks
+      const bool passA = mode == M_INIT || mode == M_CONFIRM || mode == M_FIRST || mode == M_NORMAL;
+      const double beta = S.beta, alpha = S.alpha;
+      const double* pold = S.par ? P.p1 : P.p0;
+      double* pnew = S.par ? P.p0 : P.p1;
+      for (int64_t c = kw; c < nchg; c += TW) {
+        double a0 = 0.0, a1 = 0.0;
+        for (int i = 0; i < kDynR; ++i) {
+          const int64_t s = s0g + (int64_t)kDynR * c + i;
+          if (s >= s1g) break;
+          int64_t row0, end;
+          slice_map_g(P, s, g, row0, end);
+          const int64_t u = row0 + lane;
+          if (u >= end) continue;
+          if (passA) {
+            const int64_t pl = (ST ? 32ll * A.vw * s : A.slice_ptr[s]) + lane;
+            const int w = ST ? A.W : (int)((A.slice_ptr[s + 1] - (pl - lane)) >> 5);
+            double own = 0.0;
+            if (mode == M_INIT || mode == M_CONFIRM) {
+              const double* xx = P.x;
+              const double acc = row_dot<WM, ST>(A, pl, w, u, [&](int cc) { return xx[cc]; }, &own);
+              const double bi = P.b[u];
+              const double ri = bi - acc;
+              P.r[u] = ri;
+              a0 = __fma_rn(ri, ri, a0);
+              if (mode == M_INIT) a1 = __fma_rn(bi, bi, a1);
+            } else {
+              const double* zz = P.z;
+              double acc;
+              if (mode == M_FIRST) acc = row_dot<WM, ST>(A, pl, w, u, [&](int cc) { return zz[cc]; }, &own);
+              else acc = row_dot<WM, ST>(A, pl, w, u, [&](int cc) { return __fma_rn(beta, pold[cc], zz[cc]); }, &own);
+              const double pi = ST ? own : (mode == M_FIRST ? zz[u] : __fma_rn(beta, pold[u], zz[u]));
+              pnew[u] = pi;
+              P.q[u] = acc;
+              a0 = __fma_rn(pi, acc, a0);
+            }
+          } else {
+            const double di = A.dinv[u];
+            if (mode == M_UPDATE) {
+              const double* pp = S.par ? P.p1 : P.p0;
+              const double xi = __fma_rn(alpha, pp[u], P.x[u]);
+              const double ri = __fma_rn(-alpha, P.q[u], P.r[u]);
+              const double zi = ri * di;
+              P.x[u] = xi; P.r[u] = ri; P.z[u] = zi;
+              a0 = __fma_rn(ri, zi, a0);
+              a1 = __fma_rn(ri, ri, a1);
+            } else {                                           // M_RESET
+              const double ri = P.r[u];
+              const double zi = ri * di;
+              P.z[u] = zi;
+              a0 = __fma_rn(ri, zi, a0);
+            }
+          }
+        }
+        a0 = warp_sum(a0);
+        a1 = warp_sum(a1);
+        if (lane == 0) { cp[2 * c] = a0; cp[2 * c + 1] = a1; }
+      }
+      TL(tlk);
+      // ---- re-team request seen by this CTA (raises the group's flag word; ordered before the arrival by the
+      // barrier's release), then the team barrier
+      if (threadIdx.x == 0) {
+        unsigned rq;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(rq) : "l"(D.req) : "memory");
+        D.fobs[(size_t)par * nCTA + bid] = rq > phase ? 1u : 0u;
+      }
+      team_barrier(ctr, target, (unsigned)tn);
+      // ---- the group's sums over its chunks (fixed order) and the team's decision
+      {
+        // thread i adds chunks i, i + kPT, ... in order, 8 loads in flight (one L2 round trip for 2048 chunks)
+        double a0 = 0.0, a1 = 0.0;
+        const double2* cp2 = reinterpret_cast<const double2*>(cp);
+        for (int64_t c0 = threadIdx.x; c0 < nchg; c0 += 8 * kPT) {
+          double2 v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = c0 + q * kPT < nchg ? __ldcg(cp2 + c0 + q * kPT) : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) { a0 += v[q].x; a1 += v[q].y; }
+        }
+        a0 = warp_sum(a0);
+        a1 = warp_sum(a1);
+        if (lane == 0) { s_w[warp][0] = a0; s_w[warp][1] = a1; }
+        unsigned f = 0;                        // some member saw the request before this pass's barrier
+        for (int64_t m = threadIdx.x; m < tn; m += kPT) f |= __ldcg(D.fobs + (size_t)par * nCTA + tb0 + m);
+        f = __syncthreads_or(f);
+        if (threadIdx.x == 0) {
+          double o0 = 0.0, o1 = 0.0;
+          for (int ww = 0; ww < kPW; ++ww) { o0 += s_w[ww][0]; o1 += s_w[ww][1]; }
+          s_sum[0] = o0; s_sum[1] = o1;
+          s_rt = (int)f;
+        }
+        __syncthreads();
+      }
+      TL(tlk);
+#ifdef LC_DEBUG_TIMELINE
+      if (bid == 0 && threadIdx.x == 0 && tlk < 8192) g_tl[tlk] = (unsigned long long)tn;
+      ++tlk;
+#endif
+      // ---- scalars (thread 0; every CTA of the team computes the same)
+      if (threadIdx.x == 0) {
+        SegState& T = S;
+        const double s0 = s_sum[0], s1 = s_sum[1];
+        T.pend += 1;
+        int fin = -100;
+        double frn = 0.0;
+        if (T.mode == M_INIT) {
+          T.nb = sqrt(s1);
+          T.tgt = T.nb > 0 ? P.eps * T.nb : P.eps;
+          const double rn = sqrt(s0);
+          if (!isfinite(rn)) { fin = LC_ERR_NONFINITE; frn = rn; }
+          else if (rn <= T.tgt) { fin = LC_OK; frn = rn; }
+          else if (P.max_iters == 0) { fin = LC_NOT_CONVERGED; frn = rn; }
+          else T.mode = M_RESET;
+        } else if (T.mode == M_FIRST || T.mode == M_NORMAL) {
+          const double pq = s0;
+          if (!(pq > 0)) { fin = isfinite(pq) ? LC_ERR_BREAKDOWN : LC_ERR_NONFINITE; frn = NAN; }
+          else { T.alpha = T.rho / pq; T.mode = M_UPDATE; T.par ^= 1; }
+        } else if (T.mode == M_CONFIRM) {
+          const double rn = sqrt(s0);
+          if (!isfinite(rn)) { fin = LC_ERR_NONFINITE; frn = rn; }
+          else if (rn <= T.tgt) { fin = LC_OK; frn = rn; }
+          else if (T.final_) { fin = LC_NOT_CONVERGED; frn = rn; }
+          else T.mode = M_RESET;
+        } else if (T.mode == M_UPDATE) {
+          T.it += 1;
+          const double rz = s0, rr = s1;
+          if (!isfinite(rr) || sqrt(rr) <= T.tgt || T.it >= P.max_iters) {
+            T.mode = M_CONFIRM;
+            T.final_ = (T.it >= P.max_iters) || !isfinite(rr);
+          } else {
+            T.beta = rz / T.rho;
+            T.rho = rz;
+            T.mode = M_NORMAL;
+          }
+        } else if (T.mode == M_RESET) {
+          T.rho = s0;
+          T.mode = M_FIRST;
+        }
+        if (fin != -100) {
+          T.mode = M_DONE;
+          if (bid == tb0) {
+            P.out_iters[g] = T.it;
+            P.out_status[g] = fin;
+            P.out_relres[g] = T.nb > 0 ? frn / T.nb : frn;
+          }
+        }
+      }
+      __syncthreads();
+      if (S.mode == M_DONE || s_rt) {
+        // store the group's state (first CTA of the team), request the re-team (a finished group), leave
+        if (bid == tb0 && threadIdx.x == 0) {
+          DynGroup& q = D.gst[g];
+          q.mode = S.mode; q.par = S.par; q.it = S.it; q.final_ = S.final_; q.npass = S.pend;
+          q.rho = S.rho; q.alpha = S.alpha; q.beta = S.beta; q.tgt = S.tgt; q.nb = S.nb;
+          q.cbase = target;
+          if (S.mode == M_DONE) {
+            q.gone = phase + 1;
+            atomicMax(D.req, phase + 1);
+          }
+        }
+        leave = true;
+      }
+    }
+    ++phase;
+  }
+  // a8: x~[Omega] = xbar_B (Eq. 4) for explicit local subsystems, after every group converged
+  if (P.scatter_idx)
+    for (int64_t u = bid * kPT + threadIdx.x; u < A.nunits; u += nCTA * kPT) P.x_full[P.scatter_idx[u]] = P.x[u];
+}
+
 // ---------------------------------------------------------------- host ----
 lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, lc_solve_info* info) {
   const Sell& M = *job.M;
@@ -992,6 +1255,8 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   const int64_t rows_work = job.rows_hint >= 0 ? job.rows_hint : M.nunits;
   bool team_k = G > 1;
   lc_status st;
+  // dynamic teams (k_pcg_dyn): batched global solves over equal segments (no slice list, no mask)
+  const bool dyn_ok = G > 1 && !job.slist && !job.omega;
   if (team_k) {
     if (tune.batched_schedule >= 0) team_k = tune.batched_schedule == 1;
     else {
@@ -1003,8 +1268,20 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
     }
   }
   // (larger batched solves: lock step; two task-flow schedules measured slower, profiles/r01_aj)
-  const int kind = G == 1 ? 0 : team_k ? 2 : 1;
+  int kind = G == 1 ? 0 : team_k ? 2 : 1;
   void* fn = fns[wi + 9 * kind];
+  // lock-step candidates without a slice list run as dynamic teams (lc_tuning.batched_schedule -1; 2 forces them
+  // for the static-team candidates too: config 3's explicit local subsystems 4.70 ms with static teams, 5.60 with
+  // dynamic ones -- their groups are small and converge alike, so the re-team stops cost more than they balance)
+  if (kind >= 1 && dyn_ok && ((tune.batched_schedule == -1 && kind == 1) || tune.batched_schedule == 2)) {
+    void* const dfns[9] = {(void*)k_pcg_dyn<5, 0>, (void*)k_pcg_dyn<7, 0>, (void*)k_pcg_dyn<0, 0>,
+                           (void*)k_pcg_dyn<5, 1>, (void*)k_pcg_dyn<7, 1>, (void*)k_pcg_dyn<0, 1>,
+                           (void*)k_pcg_dyn<5, 2>, (void*)k_pcg_dyn<7, 2>, (void*)k_pcg_dyn<0, 2>};
+    int64_t dctas = 0;
+    st = max_coresident(dfns[wi], kPT, 0, &dctas);
+    if (st) return st;
+    if (dctas >= G) { kind = 3; fn = dfns[wi]; }
+  }
   // TMA staging for contiguous slice ranges (global solves); slice-list (masked) solves keep plain loads: the
   // per-slice bulk copies were 4% slower there in the bench (profiles/r01_h_tma_ab.txt)
   // (the explicit subsystems' uniform-width SELL slices stream their columns through the same ring)
@@ -1020,6 +1297,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   int64_t nCTA = std::min<int64_t>(max_ctas, (std::max<int64_t>(work, 1) + kPW - 1) / kPW);
   if (tune.pcg_max_ctas > 0) nCTA = std::max<int64_t>(1, std::min<int64_t>(nCTA, tune.pcg_max_ctas));
   if (nCTA < 1) nCTA = 1;
+  if (kind == 3) nCTA = max_ctas;          // every co-resident CTA: the teams split the grid among the groups
   // batched lock step: launched in clusters of CL CTAs (cluster_reduce_barrier: one level of global latency per
   // reduction instead of two), as many whole clusters as are co-resident
   int CL = (kind == 1 && tune.batched_cluster > 1) ? tune.batched_cluster : 0;
@@ -1029,6 +1307,7 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
     else nCTA = std::max<int64_t>(1, std::min<int64_t>(maxcl, (nCTA + CL - 1) / CL)) * CL;
   }
   void* ws = nullptr;
+  void* dws = nullptr;                            // dynamic teams' extra workspace
   const size_t vec = sizeof(double) * (size_t)n;
   const size_t vbytes = (vec + 255) & ~(size_t)255;
   const bool own_x = job.x_init != nullptr;
@@ -1123,6 +1402,30 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
       attr[0].val.clusterDim.x = csz;
       e = cudaLaunchKernelExC(&cfg, fn, args);
     }
+  } else if (e == cudaSuccess && kind == 3) {
+    // dynamic teams: per-group state, chunk partials, per-CTA request flags, team counters, request word
+    int64_t spg_max = 0;                          // the largest segment's slices
+    for (int g = 0; g < G; ++g) spg_max = std::max<int64_t>(spg_max, M.h_seg_slice0[g + 1] - M.h_seg_slice0[g]);
+    const int nchk = (int)((spg_max + kDynR - 1) / kDynR);
+    const size_t b_gst = ((sizeof(DynGroup) * G + 255) & ~(size_t)255);
+    const size_t b_cp = ((sizeof(double) * 2 * 2 * (size_t)G * nchk + 255) & ~(size_t)255);
+    const size_t b_fo = ((sizeof(unsigned) * 2 * (size_t)nCTA + 255) & ~(size_t)255);
+    const size_t b_ct = (size_t)128 * G + 256;
+    if (st = dalloc(&dws, b_gst + b_cp + b_fo + b_ct, s); st) { dfree(ws, s); return st; }
+    DynArgs da;
+    da.P = a;
+    char* dw = (char*)dws;
+    da.gst = (DynGroup*)dw; dw += b_gst;
+    da.cpart = (double*)dw; dw += b_cp;
+    da.fobs = (unsigned*)dw; dw += b_fo;
+    da.gctr = (unsigned long long*)dw;
+    da.req = (unsigned*)(dw + 128 * G);
+    da.nchk = nchk;
+    e = cudaMemsetAsync(da.gst, 0, b_gst, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(da.fobs, 0, b_fo, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(da.gctr, 0, b_ct, s);
+    void* dargs[] = {&da};
+    if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kPT), dargs, 0, s);
   } else if (e == cudaSuccess && CL) {
     // cooperative (co-residency is checked by the driver) and clustered
     cudaLaunchConfig_t cfg = {};
@@ -1144,9 +1447,9 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   count_launch();
   cudaEventRecord(clk.e1, s);
   const int kernel = kind == 1 ? LC_KERNEL_PCG_LOCKSTEP : kind == 2 ? LC_KERNEL_PCG_TEAMS
-                     : clus ? LC_KERNEL_PCG_CLUSTER : LC_KERNEL_PCG_GRID;
+                     : kind == 3 ? LC_KERNEL_PCG_DYNTEAMS : clus ? LC_KERNEL_PCG_CLUSTER : LC_KERNEL_PCG_GRID;
   // (the copies of solve_finish are enqueued before the stream-ordered free of the workspace they read)
-  struct FreeAfter { void* p; cudaStream_t s; ~FreeAfter() { dfree(p, s); } } fa{ws, s};
+  struct FreeAfter { void* p; cudaStream_t s; ~FreeAfter() { dfree(p, s); } } fa{ws, s}, fd{dws, s};
   return solve_finish(e, clk, job.defer, G, a.out_iters, a.out_status, a.out_relres, kernel,
                       a.lazyx > 1 ? a.lazyx : 1, s, info, "PCG kernel");
 }

@@ -78,7 +78,7 @@ class MethodTimes(ctypes.Structure):
 
 
 KERNELS = {0: "none", 1: "pcg_grid", 2: "pcg_cluster", 3: "pcg_resident", 4: "pcg_lockstep", 5: "pcg_teams",
-           6: "gmres"}
+           6: "gmres", 7: "pcg_dynteams"}
 
 
 class Tuning(ctypes.Structure):

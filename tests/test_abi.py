@@ -116,7 +116,7 @@ def test_tuning_host_only_roundtrip(lib):
         th = threading.Thread(target=lambda: seen.update(lc.get_tuning()))
         th.start(); th.join()
         assert seen == d                                   # other threads keep the defaults
-        for bad in (dict(lazy_x_depth=4), dict(batched_schedule=2), dict(stencil_layout=2), dict(sub_repr=-2),
+        for bad in (dict(lazy_x_depth=4), dict(batched_schedule=3), dict(stencil_layout=2), dict(sub_repr=-2),
                     dict(pcg_max_ctas=-1)):
             with pytest.raises(lc.LcError):
                 lc.set_tuning(**bad)

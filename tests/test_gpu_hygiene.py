@@ -181,7 +181,7 @@ def test_solve_info_reports_kernel_and_lazy_x(tune):
     sy3 = synth.system(3, 3, n=32, G=4)
     A3 = lc.Matrix(sy3.nrows, sy3.rp, sy3.ci, sy3.val, batch=4)
     infos = lc.solve_global(A3, to_dev(sy3.b), to_dev(sy3.x0))
-    assert all(i["kernel"] in ("pcg_lockstep", "pcg_teams") for i in infos)
+    assert all(i["kernel"] in ("pcg_lockstep", "pcg_teams", "pcg_dynteams") for i in infos)
     sy4 = synth.system(4, 3, n=16)
     A4 = lc.Matrix(sy4.nrows, sy4.rp, sy4.ci, sy4.val, block=3)
     assert lc.solve_global(A4, to_dev(sy4.b), to_dev(sy4.x0), method=lc.GMRES)[0]["kernel"] == "gmres"

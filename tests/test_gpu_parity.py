@@ -209,14 +209,40 @@ def test_config3_reduced_batched(n, G, s):
     check_system(sy, RULES[3][0])
 
 
-@pytest.mark.parametrize("sched", ["0", "1"])
+@pytest.mark.parametrize("sched", ["0", "1", "2"])
 @pytest.mark.parametrize("n,G,s", [(30, 4, 0), (64, 20, 3)])
 def test_config3_batched_schedules(n, G, s, sched, tune):
-    """Both batched PCG schedules (batched_schedule 0: the grid sweeps all active groups in lock step; 1: one team of
-    CTAs per group) against the oracle; the automatic choice is exercised by test_config3_reduced_batched."""
+    """The batched PCG schedules (batched_schedule 0: the grid sweeps all active groups in lock step; 1: static teams,
+    one team of CTAs per group; 2: dynamic teams, re-teamed as groups converge) against the oracle; the automatic
+    choice is exercised by test_config3_reduced_batched."""
     tune(batched_schedule=int(sched))
     sy = synth.system(3, s, n=n, G=G)
     check_system(sy, RULES[3][0])
+
+
+@pytest.mark.parametrize("n,G,s", [(30, 4, 0), (64, 20, 3), (128, 20, 9), (40, 64, 2)])
+def test_config3_dynamic_teams_deterministic(n, G, s, tune):
+    """Dynamic teams: the re-team events depend on timing, the results must not (chunk partials of fixed rows, summed
+    in a fixed order whatever the team): five global solves bitwise equal, iterations per group +-1 vs the oracle's
+    PCG on each group, solutions within 1e-9; G = 64 is the most segments a handle holds."""
+    tune(batched_schedule=2)
+    sy = synth.system(3, s, n=n, G=G)
+    A = gpu_matrix(sy)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    xs, its = [], []
+    for _ in range(5):
+        x = x0.clone()
+        info = lc.solve_global(A, b, x)
+        assert all(i["kernel"] == "pcg_dynteams" for i in info)
+        xs.append(x)
+        its.append([i["iterations"] for i in info])
+    assert all(torch.equal(xs[0], x) for x in xs[1:]) and all(i == its[0] for i in its[1:])
+    Ao = oracle_csr(sy)
+    xg = xs[0].cpu().numpy()
+    for g, (r0, r1) in enumerate(segments(sy)):
+        xo, it, st, _ = orc.pcg(Ao.segment(r0, r1), sy.b[r0:r1], sy.x0[r0:r1], EPS, 20000)
+        assert abs(its[0][g] - it) <= 1, (g, its[0][g], it)
+        assert np.linalg.norm(xg[r0:r1] - xo) / np.linalg.norm(xo) <= 1e-9
 
 
 @pytest.mark.parametrize("cl", [0, 2, 4, 8, 16])
