@@ -422,6 +422,9 @@ typedef struct {
                                    barrier; 2..16: launched in clusters of that many CTAs, reductions through
                                    distributed shared memory + one counter level (measured no faster in situ,
                                    profiles/r02_e_batched_reduce.md) */
+  int32_t block_dcoup;          /* 1 (default): block 3 stencil matrices whose off-diagonal blocks are diagonal (the
+                                   3T couplings) keep a compact copy without those blocks' explicit zeros for the
+                                   GMRES SpMVs (21 instead of 45 values per cell, bitwise the same chains); 0: no */
 } lc_tuning;
 
 /* the defaults listed above (host output) */
@@ -432,7 +435,8 @@ lc_status lc_set_tuning(const lc_tuning* t);
 lc_status lc_get_tuning(lc_tuning* t);
 
 /* introspection (host outputs, each optional): unknowns n*block, stored scalars, batch, SELL slices, max row
-   length (slots), layout (LC_LAYOUT_*), bytes one SpMV streams for the matrix (values + columns + metadata) */
+   length (slots), layout (LC_LAYOUT_*), bytes one SpMV streams for the matrix (values + columns + metadata; for
+   block 3 stencil matrices with diagonal coupling blocks, the compact copy the GMRES SpMVs read) */
 lc_status lc_matrix_info(lc_matrix A, int64_t* n_unknowns, int64_t* nnz, int32_t* batch, int64_t* nslices,
                          int32_t* max_row, int32_t* layout, int64_t* matrix_bytes);
 

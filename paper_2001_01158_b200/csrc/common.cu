@@ -223,6 +223,7 @@ static lc_tuning defaults_() {
   t.spmv_csr_tma = 1;
   t.spmv_tma = 1;
   t.batched_cluster = 0;
+  t.block_dcoup = 1;
   return t;
 }
 static thread_local lc_tuning g_tune = defaults_();
@@ -230,8 +231,8 @@ const lc_tuning& tuning() { return g_tune; }
 
 void Sell::release(cudaStream_t s) {
   dfree(slice_ptr, s); dfree(slice_row0, s); dfree(slice_seg, s); dfree(seg_unit0, s); dfree(seg_slice0, s);
-  dfree(col, s); dfree(val, s); dfree(rowlen, s); dfree(dinv, s); dfree(mask, s);
-  mask = nullptr;
+  dfree(col, s); dfree(val, s); dfree(rowlen, s); dfree(dinv, s); dfree(mask, s); dfree(cval, s);
+  mask = nullptr; cval = nullptr;
   slice_ptr = nullptr; slice_row0 = slice_seg = seg_unit0 = nullptr; seg_slice0 = nullptr;
   col = nullptr; val = nullptr; rowlen = nullptr; dinv = nullptr;
 }
@@ -480,7 +481,7 @@ extern "C" lc_status lc_set_tuning(const lc_tuning* t) {
       !bin(t->pcg_tma) || t->lazy_x_depth < 0 || t->lazy_x_depth > 3 || t->batched_schedule < -1 ||
       t->batched_schedule > 2 || t->pcg_max_ctas < 0 || t->sub_repr < -1 || t->sub_repr > 1 ||
       !bin(t->gmres_exact_cgs2) || !bin(t->gs_lines) || !bin(t->spmv_csr_tma) || t->spmv_tma < 0 || t->spmv_tma > 2 ||
-      t->batched_cluster < 0 || t->batched_cluster == 1 || t->batched_cluster > 16) {
+      t->batched_cluster < 0 || t->batched_cluster == 1 || t->batched_cluster > 16 || !bin(t->block_dcoup)) {
     lc::set_error("lc_set_tuning: field out of range");
     return LC_ERR_INVALID_ARG;
   }

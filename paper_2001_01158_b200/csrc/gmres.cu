@@ -33,10 +33,12 @@ constexpr int kMaxQ = 2 * (kMaxM + 1) + 2;   // reduced quantities per phase
 constexpr int kCC = LC_GMRES_CC;             // slices per warp chunk in the SpMV + dots pass (with kIB = 2: 1: 78.2,
                                              // 2: 69.0, 3: 81.3 us/step)
 #ifndef LC_GMRES_IB
-#define LC_GMRES_IB 1
+#define LC_GMRES_IB 3
 #endif
-// basis vectors per unrolled block of the dot / update loops: 1 (config 4 Arnoldi step 67.2 us) beats 2 (69.0),
-// 3 (69.1), 4 (72.3), 8 (81.0): the wider blocks' register arrays spill (tools/build_variant.sh A/B)
+// basis vectors per unrolled block of the dot / update loops.  Round 1 (full 3x3 coupling blocks): 1 (config 4
+// Arnoldi step 67.2 us) beat 2 (69.0), 3 (69.1), 4 (72.3), 8 (81.0).  Round 2, with the compact diagonal couplings
+// (fewer registers in the SpMV): 3 (62.8 us) beats 1 (65.5), 2 (68.0), 4 (64.5), 6 (66.9); kCC 2 stays (kCC 1
+// 64.8, 3 70.3 with kIB 3) -- tools/dev/build_variant.sh + tools/dev/ab_solves.py, profiles/r02_k
 constexpr int kIB = LC_GMRES_IB;
 #ifndef LC_GMRES_REV
 #define LC_GMRES_REV 0
@@ -66,6 +68,35 @@ struct GmresArgs {
   int max_iters;
   int exact_cgs2;       // 1: textbook two-pass CGS2 (4 barriers, 4 passes over V per step); 0: Gram form (R39)
 };
+
+// the 3T SpMV row (cell u of slice s) on the compact diagonal-coupling values (Sell::cval): slots in ascending
+// column order, the diagonal block's 9-term chain, 1 term per component for a diagonal coupling block -- the
+// same chains as the full 3x3 blocks minus their exact-zero terms, bitwise (an fma chain that starts at +0 never
+// holds -0, so adding 0 * y is the identity)
+__device__ __forceinline__ void block_row_dcoup(const SellView& A, int64_t s, int lane, int wd, int64_t u,
+                                                const double* __restrict__ y, double* acc) {
+  const double* cb = A.cval + 32ll * A.cw * s + lane;
+  int o = 0;
+#pragma unroll 5
+  for (int k = 0; k < wd; ++k) {
+    const int64_t c = sv_col(A, 0, k, u);
+    const double y0 = y[3 * c], y1 = y[3 * c + 1], y2 = y[3 * c + 2];
+    if (k == A.kdiag) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        acc[a] = __fma_rn(cb[32 * (3 * a)], y0, acc[a]);
+        acc[a] = __fma_rn(cb[32 * (3 * a + 1)], y1, acc[a]);
+        acc[a] = __fma_rn(cb[32 * (3 * a + 2)], y2, acc[a]);
+      }
+    } else {
+      const double* cd = cb + 32 * (9 + 3 * o);
+      acc[0] = __fma_rn(cd[0], y0, acc[0]);
+      acc[1] = __fma_rn(cd[32], y1, acc[1]);
+      acc[2] = __fma_rn(cd[64], y2, acc[2]);
+      ++o;
+    }
+  }
+}
 
 template <int BS>
 __device__ __forceinline__ void block_apply(const double* __restrict__ Mi, const double* v, double* t) {
@@ -167,6 +198,9 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
         double acc[BS];
 #pragma unroll
         for (int a = 0; a < BS; ++a) acc[a] = 0.0;
+        if (BS == 3 && A.cval) {
+          block_row_dcoup(A, s, lane, wd, u, P.x, acc);
+        } else
         for (int k = 0; k < wd; ++k) {
           int64_t c = sv_col(A, p0 + lane, k, u);
           if (BS == 1) {
@@ -259,6 +293,9 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
             const int64_t u = uu[cc];
             const int64_t p0 = A.slice_ptr[s];
             const int wd = A.stencil ? A.W : (int)((A.slice_ptr[s + 1] - p0) >> 5);
+            if (BS == 3 && A.cval) {
+              block_row_dcoup(A, s, lane, wd, u, P.t, wv[cc]);
+            } else
 #pragma unroll 5
             for (int k = 0; k < wd; ++k) {
               const int64_t c = sv_col(A, p0 + lane, k, u);

@@ -152,6 +152,12 @@ struct Sell {
   int32_t mir[kMaxOff] = {0};
   int reg_units = 0, spg = 0;     // equal segments (matrices from lc_create_csr)
   int uniform = 0;                // SELL with every slice maxw slots wide (slice_ptr[s] = 32 maxw s): explicit B
+  // block 3 stencil layout whose off-diagonal 3x3 blocks are diagonal (the 3T couplings): a compact
+  // copy of the values without the blocks' explicit zeros for the Krylov SpMVs -- per slice, the diagonal block's 9
+  // components, then 3 per off-diagonal slot in slot order (cw = 9 + 3 (W - 1) doubles per lane); kdiag = the slot
+  // with offset 0.  Skipping exact zeros leaves every fma chain bitwise unchanged (the chains never hold -0).
+  double* cval = nullptr;
+  int cw = 0, kdiag = -1;
   std::vector<int32_t> h_seg_unit0;
   std::vector<int64_t> h_seg_slice0;
   void release(cudaStream_t s);
@@ -179,6 +185,8 @@ struct SellView {
   const double* val;
   const uint8_t* rowlen;
   const double* dinv;
+  const double* cval;       // compact diagonal-coupling values (block 3 stencil) or nullptr
+  int cw, kdiag;
 };
 inline SellView view(const Sell& m) {
   SellView v;
@@ -191,6 +199,7 @@ inline SellView view(const Sell& m) {
   v.nslices = m.nslices; v.nseg = m.nseg; v.slice_ptr = m.slice_ptr; v.slice_row0 = m.slice_row0;
   v.slice_seg = m.slice_seg; v.seg_unit0 = m.seg_unit0; v.seg_slice0 = m.seg_slice0; v.col = m.col;
   v.val = m.val; v.rowlen = m.rowlen; v.dinv = m.dinv;
+  v.cval = m.cval; v.cw = m.cw; v.kdiag = m.kdiag;
   return v;
 }
 
@@ -598,6 +607,10 @@ lc_status build_slice_map(Sell& M, cudaStream_t s);
 // LC_ERR_INVALID_ARG (with a message naming `where`) for a null handle or one a failed lc_update_values left
 // half-written
 lc_status check_matrix(const lc_matrix_s* M, const char* where);
+// block 3 stencil layout: (re)build A.cval from A.val and raise *d_bad if an off-diagonal block holds a nonzero
+// off-diagonal entry (the caller reads *d_bad after its sync and drops cval then: drop_dcoup)
+lc_status build_dcoup(Sell& A, unsigned* d_bad, cudaStream_t s);
+void drop_dcoup(Sell& A, cudaStream_t s);
 // NEXT-4: stencil layout of the rank slab [row0, row0 + n) of an nglob-row matrix (sell.cu)
 lc_status build_slab(int64_t nglob, int64_t row0, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                      const double* values, int on_device, cudaStream_t s, Sell& A, int64_t* nnz_out);

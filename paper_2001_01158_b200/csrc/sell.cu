@@ -101,6 +101,34 @@ __global__ void k_fill_stencil(int64_t n, int seg_units, int spg, const int64_t*
 
 // value symmetry on the full stencil layout: every lower slot equals its mirror (row u + off[k], upper slot
 // of -off[k]); a lower slot whose mirror row lies outside the segment must be a zero hole.
+// compact diagonal-coupling copy of a block 3 stencil layout (Sell::cval): thread per (slice, lane)
+__global__ void k_dcoup_fill(int64_t nslices, int W, int kd, const double* __restrict__ val, double* __restrict__ cval,
+                             unsigned* bad) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t sl = t >> 5;
+  const int lane = (int)(t & 31);
+  if (sl >= nslices) return;
+  const int cw = 9 + 3 * (W - 1);
+  double* cb = cval + 32ll * cw * sl + lane;
+  unsigned nz = 0;
+  int o = 0;
+  for (int k = 0; k < W; ++k) {
+    const double* vb = val + 9 * (32ll * W * sl + 32ll * k) + lane;
+    if (k == kd) {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) cb[32 * q] = vb[32 * q];
+    } else {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) cb[32 * (9 + 3 * o + a)] = vb[32 * (4 * a)];
+#pragma unroll
+      for (int q = 0; q < 9; ++q)
+        if (q % 4 != 0 && vb[32 * q] != 0.0) nz = 1;
+      ++o;
+    }
+  }
+  if (nz) atomicOr(bad, 1u);
+}
+
 __global__ void k_check_sym(int64_t n, int seg_units, int spg, Offsets O, int kd, const double* __restrict__ val,
                             unsigned* bad) {
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -375,6 +403,32 @@ done:
 #undef CKC
 }
 
+lc_status build_dcoup(Sell& A, unsigned* d_bad, cudaStream_t s) {
+  if (A.block != 3 || !A.stencil || A.sym) return LC_OK;
+  if (!tuning().block_dcoup) { drop_dcoup(A, s); return LC_OK; }
+  int kd = -1;
+  for (int k = 0; k < A.maxw; ++k)
+    if (A.off[k] == 0) kd = k;
+  if (kd < 0) return LC_OK;
+  const int cw = 9 + 3 * (A.maxw - 1);
+  if (!A.cval) {
+    lc_status st = dalloc((void**)&A.cval, sizeof(double) * 32ll * cw * A.nslices, s);
+    if (st) return st;
+  }
+  A.cw = cw;
+  A.kdiag = kd;
+  const unsigned nb = (unsigned)((A.nslices * 32 + 255) / 256);
+  k_dcoup_fill<<<nb, 256, 0, s>>>(A.nslices, A.maxw, kd, A.val, A.cval, d_bad);
+  LC_LAUNCHED();
+  return LC_OK;
+}
+void drop_dcoup(Sell& A, cudaStream_t s) {
+  dfree(A.cval, s);
+  A.cval = nullptr;
+  A.cw = 0;
+  A.kdiag = -1;
+}
+
 }  // namespace lc
 
 using namespace lc;
@@ -410,7 +464,7 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
   const int32_t* d_ci = col_idx;
   const double* d_va = values;
   void *t_rp = nullptr, *t_ci = nullptr, *t_va = nullptr, *t_w = nullptr, *t_err = nullptr;
-  unsigned h_err = 0;
+  unsigned h_err = 0, h_bad_dc = 0;
   int h_maxw = 0;
 #define CK(x) do { st = (x); if (st) goto fail; } while (0)
 #define CKC(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { st = cuda_fail(_e, #x); goto fail; } } while (0)
@@ -548,13 +602,16 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
   CK(dalloc((void**)&A.slice_row0, sizeof(int32_t) * A.nslices, s));
   CK(dalloc((void**)&A.slice_seg, sizeof(int32_t) * A.nslices, s));
   CK(build_slice_map(A, s));
+  if (A.stencil && block == 3) CK(build_dcoup(A, (unsigned*)((char*)t_err + 56), s));   // 3T couplings
   CKC(cudaMemcpyAsync(&h_err, t_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  CKC(cudaMemcpyAsync(&h_bad_dc, (char*)t_err + 56, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
   CKC(cudaStreamSynchronize(s));
   if (h_err & kErrZeroDiag) {
     st = LC_ERR_ZERO_DIAGONAL;
     set_error("lc_create_csr: zero diagonal (or singular 3x3 cell block)");
     goto fail;
   }
+  if (h_bad_dc) drop_dcoup(A, s);                // an off-diagonal block is not diagonal: full blocks only
   dfree(t_rp, s); dfree(t_ci, s); dfree(t_va, s); dfree(t_w, s); dfree(t_err, s);
   M->use.mark(s);
   *out = M;
@@ -575,7 +632,8 @@ extern "C" lc_status lc_matrix_info(lc_matrix A, int64_t* n_unknowns, int64_t* n
   const int bb = A->block * A->block;
   if (layout) *layout = A->A.sym ? LC_LAYOUT_SYMSTENCIL : A->A.stencil ? LC_LAYOUT_STENCIL : LC_LAYOUT_SELL;
   if (matrix_bytes)
-    *matrix_bytes = A->A.stencil ? (int64_t)8 * bb * A->A.nslots
+    *matrix_bytes = A->A.cval ? (int64_t)8 * 32 * A->A.cw * A->A.nslices    // compact 3T couplings (GMRES)
+                  : A->A.stencil ? (int64_t)8 * bb * A->A.nslots
                                  : (int64_t)(8 * bb + 4) * A->A.nslots + 8 * (A->A.nslices + 1) + 8 * A->A.nslices;
   if (n_unknowns) *n_unknowns = A->n * A->block;
   if (nnz) *nnz = A->nnz * A->block * A->block;
@@ -664,11 +722,14 @@ extern "C" lc_status lc_update_values(lc_matrix M, const int64_t* row_ptr, const
       CKC(cudaGetLastError());
     }
   }
+  if (A.stencil && M->block == 3) CK(build_dcoup(A, (unsigned*)((char*)t_err + 56), s));
   {
-    unsigned e2[2] = {0, 0};
+    unsigned e2[2] = {0, 0}, bad_dc = 0;
     CKC(cudaMemcpyAsync(e2, t_err, 8, cudaMemcpyDeviceToHost, s));
+    CKC(cudaMemcpyAsync(&bad_dc, (char*)t_err + 56, 4, cudaMemcpyDeviceToHost, s));
     CKC(cudaStreamSynchronize(s));
     h_err = e2[0] | (e2[1] ? kErrNotStencil : 0u);
+    if (bad_dc) drop_dcoup(A, s);
   }
   if (h_err & kErrZeroDiag) { st = LC_ERR_ZERO_DIAGONAL; set_error("lc_update_values: zero diagonal"); goto fail; }
   if (h_err & kErrNotStencil) {

@@ -88,7 +88,8 @@ class Tuning(ctypes.Structure):
                 ("pcg_tma", ctypes.c_int32), ("lazy_x_depth", ctypes.c_int32), ("batched_schedule", ctypes.c_int32),
                 ("pcg_max_ctas", ctypes.c_int32), ("sub_repr", ctypes.c_int32), ("gmres_exact_cgs2", ctypes.c_int32),
                 ("gs_lines", ctypes.c_int32), ("spmv_csr_tma", ctypes.c_int32),
-                ("spmv_tma", ctypes.c_int32), ("batched_cluster", ctypes.c_int32)]
+                ("spmv_tma", ctypes.c_int32), ("batched_cluster", ctypes.c_int32),
+                ("block_dcoup", ctypes.c_int32)]
 
 
 _lib = None

@@ -261,6 +261,37 @@ def test_config3_lockstep_cluster_sizes(n, G, s, cl, tune):
     assert torch.equal(x1, x2) and [i["iterations"] for i in r1["global"]] == [i["iterations"] for i in r2["global"]]
 
 
+def test_config4_compact_couplings_bitwise(tune):
+    """The 3T matrices' off-diagonal 3x3 blocks are diagonal: the GMRES SpMVs run on the compact copy without their
+    explicit zeros (lc_tuning.block_dcoup = 1) and give bitwise the solution, iterations and residual of the full
+    blocks (= 0); a matrix with one non-diagonal coupling block falls back to the full blocks and still matches the
+    oracle."""
+    sy = synth.system(4, 3, n=24)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    out = {}
+    for dc in (1, 0):
+        tune(block_dcoup=dc)
+        A = gpu_matrix(sy)
+        x, rep = lc.local_method(A, b, x0, None, method=lc.GMRES)
+        xl, repl = lc.local_method(A, b, x0, RULES[4][0], method=lc.GMRES)
+        out[dc] = (x, rep["global"][0]["iterations"], rep["global"][0]["rel_residual"], xl,
+                   repl["local"][0]["iterations"])
+    assert torch.equal(out[0][0], out[1][0]) and out[0][1:3] == out[1][1:3]
+    assert torch.equal(out[0][3], out[1][3]) and out[0][4] == out[1][4]
+    tune(block_dcoup=1)
+    val = sy.val.copy()
+    bs = val.reshape(-1, 9)
+    # one coupling block (not the diagonal one) of cell 77 gets an off-diagonal entry
+    r0, r1 = sy.rp[77], sy.rp[78]
+    k = [e for e in range(r0, r1) if sy.ci[e] != 77][0]
+    bs[k, 1] = -1e-3
+    A = lc.Matrix(sy.nrows, sy.rp, sy.ci, val, block=3)
+    x, rep = lc.local_method(A, b, x0, None, method=lc.GMRES)
+    xo, it, st, _ = orc.gmres_bj(orc.Csr.from_bsr(sy.rp, sy.ci, val), sy.b, sy.x0, bs=3)
+    assert abs(rep["global"][0]["iterations"] - it) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xo) / np.linalg.norm(xo) <= 1e-9
+
+
 @pytest.mark.parametrize("n,s", [(20, 0), (45, 4), (64, 29)])
 def test_config4_reduced_gmres(n, s):
     sy = synth.system(4, s, n=n)
