@@ -39,7 +39,7 @@ constexpr int kCC = LC_GMRES_CC;             // slices per warp chunk in the SpM
 // Arnoldi step 67.2 us) beat 2 (69.0), 3 (69.1), 4 (72.3), 8 (81.0).  Round 2, with the compact diagonal couplings
 // (fewer registers in the SpMV): 3 (62.8 us) beats 1 (65.5), 2 (68.0), 4 (64.5), 6 (66.9); kCC 2 stays (kCC 1
 // 64.8, 3 70.3 with kIB 3) -- tools/dev/build_variant.sh + tools/dev/ab_solves.py, profiles/r02_k
-constexpr int kIB = LC_GMRES_IB;
+constexpr int kIB = LC_GMRES_IB;           // with the compact 3T couplings; the full-block paths keep 1
 #ifndef LC_GMRES_REV
 #define LC_GMRES_REV 0
 #endif
@@ -117,7 +117,7 @@ __device__ unsigned long long g_tlg[16384];
 #define TLG(k) (void)0
 #endif
 
-template <int BS>
+template <int BS, int IB>
 __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
   unsigned long long bar_epoch = 0;
 #ifdef LC_DEBUG_TIMELINE
@@ -322,12 +322,12 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
         for (int cc = 0; cc < kCC; ++cc)
 #pragma unroll
           for (int a = 0; a < BS; ++a) vj[cc][a] = (ok[cc] && !P.exact_cgs2) ? Vj[BS * uu[cc] + a] : 0.0;
-        // i in blocks of kIB with compile-time indices: the block's V loads issue together (one DRAM
+        // i in blocks of IB with compile-time indices: the block's V loads issue together (one DRAM
         // latency per block instead of one per basis vector)
-        for (int i0 = 0; i0 <= j; i0 += kIB) {
-          double d[kIB], gq[kIB];
+        for (int i0 = 0; i0 <= j; i0 += IB) {
+          double d[IB], gq[IB];
 #pragma unroll
-          for (int ii = 0; ii < kIB; ++ii) {
+          for (int ii = 0; ii < IB; ++ii) {
             d[ii] = 0.0;
             gq[ii] = 0.0;
             const int i = i0 + ii;
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
             }
           }
 #pragma unroll
-          for (int ii = 0; ii < kIB; ++ii) {
+          for (int ii = 0; ii < IB; ++ii) {
             if (i0 + ii > j) break;
             lane_flush(i0 + ii, d[ii]);
             if (!P.exact_cgs2) lane_flush(j + 1 + i0 + ii, gq[ii]);
@@ -393,14 +393,14 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
             double ww[BS];
 #pragma unroll
             for (int a = 0; a < BS; ++a) ww[a] = sj * P.w[BS * u + a];
-            for (int i0 = 0; i0 <= j; i0 += kIB) {
-              double vv[kIB][BS];
+            for (int i0 = 0; i0 <= j; i0 += IB) {
+              double vv[IB][BS];
 #pragma unroll
-              for (int ii = 0; ii < kIB; ++ii)
+              for (int ii = 0; ii < IB; ++ii)
 #pragma unroll
                 for (int a = 0; a < BS; ++a) vv[ii][a] = i0 + ii <= j ? P.V[(size_t)(i0 + ii) * n + BS * u + a] : 0.0;
 #pragma unroll
-              for (int ii = 0; ii < kIB; ++ii) {
+              for (int ii = 0; ii < IB; ++ii) {
                 if (i0 + ii > j) break;
                 const double hi = hh[i0 + ii];
 #pragma unroll
@@ -582,7 +582,9 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   const int BS = M.block;
   const int m = p->restart;
   const int64_t n = M.nunits * BS;
-  void* fn = BS == 1 ? (void*)k_gmres<1> : (void*)k_gmres<3>;
+  // basis blocking: kIB with the compact 3T couplings, 1 on the full-block paths (the explicit subsystems: their
+  // registers spill at 3; config 4 local solve 1.70 vs 1.82 ms)
+  void* fn = BS == 1 ? (void*)k_gmres<1, 1> : M.cval ? (void*)k_gmres<3, kIB> : (void*)k_gmres<3, 1>;
   int64_t max_ctas = 0;
   lc_status st = max_coresident(fn, kGT, 0, &max_ctas);
   if (st) return st;
