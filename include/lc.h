@@ -245,7 +245,7 @@ lc_status lc_spmv_csr(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
 
 /* storage layout chosen by lc_create_csr */
 enum { LC_LAYOUT_SELL = 0     /* SELL-32 with explicit int32 column per slot (12 B per slot) */,
-       LC_LAYOUT_STENCIL = 1  /* every row's column offsets lie in one sorted set of <= 8 offsets: values only,
+       LC_LAYOUT_STENCIL = 1  /* every row's column offsets lie in one sorted set of <= 16 offsets: values only,
                                  slot k = column row + off[k] (zero "holes" where a row lacks it), 8 B per slot */,
        LC_LAYOUT_SYMSTENCIL = 2 /* stencil layout of a bitwise-symmetric matrix (block 1): only the diagonal and
                                    upper-offset slots are stored; a_uv (v < u) is read as a_vu */ };

@@ -25,7 +25,8 @@
 namespace lc {
 
 constexpr int kWarp = 32;
-constexpr int kMaxOff = 8;   // stencil layout: at most 8 slots (offsets) per row
+constexpr int kMaxOff = 16;  // stencil layout: at most 16 slots (offsets) per row (9-point 2-D, 15-point 3-D)
+constexpr int kMaxOffDist = 8;  // the row-partitioned form (NEXT-4): its kernels hold <= 8 slots
 
 // ---------------------------------------------------------------- errors ----
 void set_error(const std::string& msg);
@@ -145,7 +146,7 @@ struct Sell {
   // slot k of a row holds the entry at column row + off[k] or a zero "hole"; no col array is stored.
   int stencil = 0;
   int32_t off[kMaxOff] = {0};
-  uint8_t* mask = nullptr;        // [nunits] bit k = slot k holds a stored entry (stencil layout)
+  uint16_t* mask = nullptr;       // [nunits] bit k = slot k holds a stored entry (stencil layout)
   // symmetric stencil layout (block 1, a_uv == a_vu bitwise): only slots k >= kd (diagonal + upper offsets)
   // are stored, vw = W - kd per slice; a lower slot's value is read from the mirror row's upper slot mir[k]
   int sym = 0, kd = 0, vw = 0;
@@ -169,7 +170,7 @@ struct SellView {
   int stencil;              // 1: col(u, k) = u + off[k] (clamped), real(u, k) = mask[u] bit k
   int W;                    // stencil width (= maxw)
   int32_t off[kMaxOff];
-  const uint8_t* mask;
+  const uint16_t* mask;
   int64_t nunits;
   int sym, kd, vw;          // symmetric stencil storage (see Sell)
   int32_t mir[kMaxOff];

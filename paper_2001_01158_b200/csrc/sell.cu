@@ -13,6 +13,9 @@ enum : unsigned { kErrPattern = 1u, kErrZeroDiag = 2u, kErrRowLen = 4u, kErrNotS
 __device__ bool inv3(const double* A, double* Ai);
 
 struct Offsets { int W; int32_t off[kMaxOff]; };
+// the host-visible scratch words of lc_create_csr / lc_update_values / build_slab
+constexpr int kErrOff = 64;                             // byte offset of the candidate Offsets
+constexpr size_t kErrBytes = kErrOff + ((sizeof(Offsets) + 63) & ~(size_t)63);
 
 // first row whose length equals the maximal row length (its offsets are the stencil candidate); one
 // atomic per warp (most rows of a stencil have the maximal length)
@@ -59,7 +62,7 @@ __global__ void k_check_stencil(int64_t n, const int64_t* __restrict__ rp, const
 template <int BS>
 __global__ void k_fill_stencil(int64_t n, int seg_units, int spg, const int64_t* __restrict__ rp,
                                const int32_t* __restrict__ ci, const double* __restrict__ va, Offsets O,
-                               double* __restrict__ val, uint8_t* __restrict__ mask, double* __restrict__ dinv,
+                               double* __restrict__ val, uint16_t* __restrict__ mask, double* __restrict__ dinv,
                                unsigned* err) {
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u >= n) return;
@@ -87,7 +90,7 @@ __global__ void k_fill_stencil(int64_t n, int seg_units, int spg, const int64_t*
       }
     }
   }
-  mask[u] = (uint8_t)m;
+  mask[u] = (uint16_t)m;
   if (BS == 1) {
     if (D[0] == 0.0) atomicOr(err, kErrZeroDiag);
     dinv[u] = 1.0 / D[0];
@@ -292,7 +295,7 @@ __global__ void k_slab_check(int64_t n, int64_t row0, int64_t nglob, const int64
   if (u >= n) return;
   const int64_t k0 = rp[u], k1 = rp[u + 1], l = k1 - k0;
   unsigned e = 0;
-  if (l < 1 || l > kMaxOff) e |= kErrRowLen;
+  if (l < 1 || l > kMaxOffDist) e |= kErrRowLen;
   bool diag = false;
   int64_t prev = -1;
   for (int64_t k = k0; k < k1 && !(e & kErrRowLen); ++k) {
@@ -319,7 +322,7 @@ lc_status build_slab(int64_t nglob, int64_t row0, int64_t n, const int64_t* row_
     rp0 = row_ptr[0];
     nnz = row_ptr[n];
   }
-  if (rp0 != 0 || nnz < n || nnz > (int64_t)kMaxOff * n) {
+  if (rp0 != 0 || nnz < n || nnz > (int64_t)kMaxOffDist * n) {
     set_error("lc_dist_create: row_ptr must start at 0 with 1..8 entries per row");
     return LC_ERR_PATTERN;
   }
@@ -344,8 +347,8 @@ lc_status build_slab(int64_t nglob, int64_t row0, int64_t n, const int64_t* row_
     d_rp = (const int64_t*)t_rp; d_ci = (const int32_t*)t_ci; d_va = (const double*)t_va;
   }
   CK(dalloc(&t_cs, sizeof(int32_t) * nnz, s));
-  CK(dalloc(&t_err, 64, s));                  // [0] error bits, [4] asymmetry, [8] max width, [12] row, [16] offsets
-  CKC(cudaMemsetAsync(t_err, 0, 64, s));
+  CK(dalloc(&t_err, kErrBytes, s));           // [0] error bits, [4] asymmetry, [8] max width, [12] row,
+  CKC(cudaMemsetAsync(t_err, 0, kErrBytes, s)); // [16] 3T couplings not diagonal, [64] candidate offsets
   k_slab_check<<<nb, 256, 0, s>>>(n, row0, nglob, d_rp, d_ci, (int32_t*)t_cs, (unsigned*)t_err,
                                   (int*)((char*)t_err + 8));
   count_launch();
@@ -365,14 +368,14 @@ lc_status build_slab(int64_t nglob, int64_t row0, int64_t n, const int64_t* row_
     k_first_maxrow<<<nb, 256, 0, s>>>(n, d_rp, h_maxw, (int*)((char*)t_err + 12));
     count_launch();
     k_candidate<<<1, 32, 0, s>>>(d_rp, (const int32_t*)t_cs, (const int*)((char*)t_err + 12), h_maxw,
-                                 (Offsets*)((char*)t_err + 16));
+                                 (Offsets*)((char*)t_err + kErrOff));
     count_launch();
   }
-  k_check_stencil<<<nb, 256, 0, s>>>(n, d_rp, (const int32_t*)t_cs, (const Offsets*)((char*)t_err + 16),
+  k_check_stencil<<<nb, 256, 0, s>>>(n, d_rp, (const int32_t*)t_cs, (const Offsets*)((char*)t_err + kErrOff),
                                      (unsigned*)t_err);
   count_launch();
   CKC(cudaMemcpyAsync(&h_err, t_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-  CKC(cudaMemcpyAsync(&O, (char*)t_err + 16, sizeof(Offsets), cudaMemcpyDeviceToHost, s));
+  CKC(cudaMemcpyAsync(&O, (char*)t_err + kErrOff, sizeof(Offsets), cudaMemcpyDeviceToHost, s));
   CKC(cudaStreamSynchronize(s));
   if (h_err & kErrNotStencil) {
     st = LC_ERR_PATTERN;
@@ -385,7 +388,7 @@ lc_status build_slab(int64_t nglob, int64_t row0, int64_t n, const int64_t* row_
   for (int k = 0; k < kMaxOff; ++k) A.off[k] = O.off[k];
   A.nslots = 32ll * h_maxw * A.nslices;
   CK(dalloc((void**)&A.val, sizeof(double) * A.nslots, s));
-  CK(dalloc((void**)&A.mask, n, s));
+  CK(dalloc((void**)&A.mask, sizeof(uint16_t) * n, s));
   CK(dalloc((void**)&A.dinv, sizeof(double) * n, s));
   CKC(cudaMemsetAsync(A.val, 0, sizeof(double) * A.nslots, s));
   k_fill_stencil<1><<<nb, 256, 0, s>>>(n, (int)n, A.spg, d_rp, (const int32_t*)t_cs, d_va, O, A.val, A.mask, A.dinv,
@@ -478,8 +481,8 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
     d_rp = (const int64_t*)t_rp; d_ci = (const int32_t*)t_ci; d_va = (const double*)t_va;
   }
   CK(dalloc(&t_w, sizeof(int64_t) * (A.nslices + 1), s));
-  CK(dalloc(&t_err, 64, s));                  // [0] error bits, [4] asymmetry, [8] max width, [12] row, [16] offsets
-  CKC(cudaMemsetAsync(t_err, 0, 64, s));
+  CK(dalloc(&t_err, kErrBytes, s));           // [0] error bits, [4] asymmetry, [8] max width, [12] row,
+  CKC(cudaMemsetAsync(t_err, 0, kErrBytes, s)); // [16] 3T couplings not diagonal, [64] candidate offsets
   CK(dalloc((void**)&A.rowlen, n, s));
   CK(dalloc((void**)&A.slice_ptr, sizeof(int64_t) * (A.nslices + 1), s));
   {
@@ -517,20 +520,20 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
       k_first_maxrow<<<nb, 256, 0, s>>>(n, d_rp, h_maxw, (int*)((char*)t_err + 12));
       count_launch();
       // candidate offsets gathered and checked on the device: one host round trip for the layout decision
-      k_candidate<<<1, 32, 0, s>>>(d_rp, d_ci, (const int*)((char*)t_err + 12), h_maxw, (Offsets*)((char*)t_err + 16));
+      k_candidate<<<1, 32, 0, s>>>(d_rp, d_ci, (const int*)((char*)t_err + 12), h_maxw, (Offsets*)((char*)t_err + kErrOff));
       count_launch();
-      k_check_stencil<<<nb, 256, 0, s>>>(n, d_rp, d_ci, (const Offsets*)((char*)t_err + 16), (unsigned*)t_err);
+      k_check_stencil<<<nb, 256, 0, s>>>(n, d_rp, d_ci, (const Offsets*)((char*)t_err + kErrOff), (unsigned*)t_err);
       count_launch();
       Offsets O;
       CKC(cudaMemcpyAsync(&h_err, t_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-      CKC(cudaMemcpyAsync(&O, (char*)t_err + 16, sizeof(Offsets), cudaMemcpyDeviceToHost, s));
+      CKC(cudaMemcpyAsync(&O, (char*)t_err + kErrOff, sizeof(Offsets), cudaMemcpyDeviceToHost, s));
       CKC(cudaStreamSynchronize(s));
       if (!(h_err & kErrNotStencil)) {
         A.stencil = 1;
         for (int k = 0; k < kMaxOff; ++k) A.off[k] = O.off[k];
         A.nslots = 32ll * h_maxw * A.nslices;
         CK(dalloc((void**)&A.val, sizeof(double) * A.nslots * bb, s));
-        CK(dalloc((void**)&A.mask, n, s));
+        CK(dalloc((void**)&A.mask, sizeof(uint16_t) * n, s));
         CKC(cudaMemsetAsync(A.val, 0, sizeof(double) * A.nslots * bb, s));
         k_uniform_slice_ptr<<<(unsigned)((A.nslices + 256) / 256), 256, 0, s>>>(A.nslices, h_maxw, A.slice_ptr);
         count_launch();
@@ -602,9 +605,9 @@ extern "C" lc_status lc_create_csr(int64_t n, int32_t block, int32_t batch, cons
   CK(dalloc((void**)&A.slice_row0, sizeof(int32_t) * A.nslices, s));
   CK(dalloc((void**)&A.slice_seg, sizeof(int32_t) * A.nslices, s));
   CK(build_slice_map(A, s));
-  if (A.stencil && block == 3) CK(build_dcoup(A, (unsigned*)((char*)t_err + 56), s));   // 3T couplings
+  if (A.stencil && block == 3) CK(build_dcoup(A, (unsigned*)((char*)t_err + 16), s));   // 3T couplings
   CKC(cudaMemcpyAsync(&h_err, t_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-  CKC(cudaMemcpyAsync(&h_bad_dc, (char*)t_err + 56, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  CKC(cudaMemcpyAsync(&h_bad_dc, (char*)t_err + 16, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
   CKC(cudaStreamSynchronize(s));
   if (h_err & kErrZeroDiag) {
     st = LC_ERR_ZERO_DIAGONAL;
@@ -679,8 +682,8 @@ extern "C" lc_status lc_update_values(lc_matrix M, const int64_t* row_ptr, const
     CKC(cudaMemcpyAsync(t_va, values, sizeof(double) * nnz * bb, cudaMemcpyHostToDevice, s));
     d_rp = (const int64_t*)t_rp; d_ci = (const int32_t*)t_ci; d_va = (const double*)t_va;
   }
-  CK(dalloc(&t_err, 64, s));                  // [0] error bits, [4] asymmetry, [8] max width, [12] row, [16] offsets
-  CKC(cudaMemsetAsync(t_err, 0, 64, s));
+  CK(dalloc(&t_err, kErrBytes, s));           // [0] error bits, [4] asymmetry, [8] max width, [12] row,
+  CKC(cudaMemsetAsync(t_err, 0, kErrBytes, s)); // [16] 3T couplings not diagonal, [64] candidate offsets
   M->valid = 0;                 // the fill below overwrites the live layout; valid again once the checks pass
   {
     const unsigned nb = (unsigned)((n + 255) / 256);
@@ -722,11 +725,11 @@ extern "C" lc_status lc_update_values(lc_matrix M, const int64_t* row_ptr, const
       CKC(cudaGetLastError());
     }
   }
-  if (A.stencil && M->block == 3) CK(build_dcoup(A, (unsigned*)((char*)t_err + 56), s));
+  if (A.stencil && M->block == 3) CK(build_dcoup(A, (unsigned*)((char*)t_err + 16), s));
   {
     unsigned e2[2] = {0, 0}, bad_dc = 0;
     CKC(cudaMemcpyAsync(e2, t_err, 8, cudaMemcpyDeviceToHost, s));
-    CKC(cudaMemcpyAsync(&bad_dc, (char*)t_err + 56, 4, cudaMemcpyDeviceToHost, s));
+    CKC(cudaMemcpyAsync(&bad_dc, (char*)t_err + 16, 4, cudaMemcpyDeviceToHost, s));
     CKC(cudaStreamSynchronize(s));
     h_err = e2[0] | (e2[1] ? kErrNotStencil : 0u);
     if (bad_dc) drop_dcoup(A, s);
