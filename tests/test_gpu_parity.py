@@ -822,7 +822,7 @@ def test_full_size_solution_properties(cfg, s):
                 assert np.max(np.abs(xn[r0:r1] - sy.xs[r0:r1])) <= np.max(np.abs(r)) * (1 + 1e-6) + 1e-300
 
 
-@pytest.mark.parametrize("cfg,s,rule", [(3, 10, 0), (4, 15, 0), (5, 10, 0), (2, 25, 0)])
+@pytest.mark.parametrize("cfg,s,rule", [(3, 10, 0), (4, 15, 0), (5, 10, 0), (2, 25, 0), (5, 11, 1)])
 def test_full_size_local_method_vs_oracle(cfg, s, rule):
     """BASELINE sizes, in the bench's launch configuration (explicit subsystems, teams / lock step, the TMA
     and lazy-x global kernels), element by element against the oracle's Alg. 1: domain sets, tau, criterion,
@@ -831,6 +831,19 @@ def test_full_size_local_method_vs_oracle(cfg, s, rule):
     test above)."""
     sy = synth.system(cfg, s)
     check_system(sy, RULES[cfg][rule])
+
+
+@pytest.mark.parametrize("cfg,s", [(5, 12), (4, 16)])
+def test_full_size_method0_vs_oracle(cfg, s):
+    """method0 (the global solve from x0) at BASELINE size through lc_local_method, in the bench's launch
+    configuration (config 5: the TMA / lazy-x k_pcg; config 4: k_gmres on the compact 3T couplings), against the
+    oracle's global solve: iterations +-1, solution within 1e-9 (the oracle side takes ~40 s for config 5)."""
+    sy = synth.system(cfg, s)
+    A = gpu_matrix(sy)
+    x, rep = lc.local_method(A, to_dev(sy.b), to_dev(sy.x0), None, method=method_of(cfg))
+    xo, _, ro = orc.local_method(oracle_csr(sy), sy.b, sy.x0, None, oracle_sp(cfg))
+    assert abs(rep["global"][0]["iterations"] - ro.it_global) <= 1, (rep["global"], ro.it_global)
+    assert np.linalg.norm(x.cpu().numpy() - xo) / np.linalg.norm(xo) <= 1e-9
 
 
 # ------------------------------------------------- general (non-stencil) SELL --
