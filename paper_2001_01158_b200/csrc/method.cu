@@ -20,7 +20,8 @@ lc_status domain_rows_out(const lc_domain_s* D, int32_t* idx_dev, cudaStream_t s
 
 namespace {
 // per (host thread, device): two pinned solve records (local, global) and the phase events.  A call returns only
-// after its final synchronisation, so one set per thread and device is never in use twice.
+// after its final synchronisation, so one set per thread and device is never in use twice.  (Kept for the life of
+// the process: a few hundred bytes of pinned memory and 10 events per host thread and device.)
 struct MethodArena {
   Pending* pend = nullptr;        // pinned [2]
   cudaEvent_t ph[6] = {};

@@ -90,6 +90,7 @@ struct SegState {
   int mode, par, it, final_;
   double rho, alpha, beta, tgt, nb;
   int pend, pbuf, pbuf2;        // lazy x (P.lazyx): x lacks palpha p[pbuf] (pend >= 1), then palpha2 p[pbuf2]
+  int npass;                    // dynamic teams: passes done on the segment (parity of its chunk partials)
   double palpha, palpha2;       // (pend = 2), p[i] = p0 / p1 / p2
 };
 
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(kPT, ST == 0 ? LCV_MINB_SELL : LCV_MINB) k_pcg
   if (threadIdx.x < kMaxSeg) {
     S[threadIdx.x].mode = M_INIT; S[threadIdx.x].par = 0; S[threadIdx.x].it = 0; S[threadIdx.x].final_ = 0;
     S[threadIdx.x].beta = 0.0; S[threadIdx.x].alpha = 0.0; S[threadIdx.x].rho = 0.0;
-    S[threadIdx.x].pend = 0; S[threadIdx.x].pbuf = 0; S[threadIdx.x].palpha = 0.0;
+    S[threadIdx.x].pend = 0; S[threadIdx.x].pbuf = 0; S[threadIdx.x].palpha = 0.0; S[threadIdx.x].npass = 0;
     S[threadIdx.x].pbuf2 = 0; S[threadIdx.x].palpha2 = 0.0;
   }
   __syncthreads();
@@ -1035,7 +1036,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg_dyn(DynArgs D) {
     if (threadIdx.x == 0) {
       const DynGroup& q = D.gst[g];
       S.mode = __ldcg(&q.mode); S.par = __ldcg(&q.par); S.it = __ldcg(&q.it); S.final_ = __ldcg(&q.final_);
-      S.pend = __ldcg(&q.npass);             // (npass kept in the pend field: no lazy x in batched solves)
+      S.npass = __ldcg(&q.npass);
       S.rho = __ldcg(&q.rho); S.alpha = __ldcg(&q.alpha); S.beta = __ldcg(&q.beta); S.tgt = __ldcg(&q.tgt);
       S.nb = __ldcg(&q.nb);
     }
@@ -1055,7 +1056,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg_dyn(DynArgs D) {
     while (!leave) {
       TL(tlk);
       const int mode = S.mode;
-      const int par = S.pend & 1;
+      const int par = S.npass & 1;
       double* cp = D.cpart + ((size_t)par * G + g) * (size_t)D.nchk * 2;
       // ---- the pass over this team's chunks
       const bool passA = mode == M_INIT || mode == M_CONFIRM || mode == M_FIRST || mode == M_NORMAL;
@@ -1159,7 +1160,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg_dyn(DynArgs D) {
       if (threadIdx.x == 0) {
         SegState& T = S;
         const double s0 = s_sum[0], s1 = s_sum[1];
-        T.pend += 1;
+        T.npass += 1;
         int fin = -100;
         double frn = 0.0;
         if (T.mode == M_INIT) {
@@ -1209,7 +1210,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg_dyn(DynArgs D) {
         // store the group's state (first CTA of the team), request the re-team (a finished group), leave
         if (bid == tb0 && threadIdx.x == 0) {
           DynGroup& q = D.gst[g];
-          q.mode = S.mode; q.par = S.par; q.it = S.it; q.final_ = S.final_; q.npass = S.pend;
+          q.mode = S.mode; q.par = S.par; q.it = S.it; q.final_ = S.final_; q.npass = S.npass;
           q.rho = S.rho; q.alpha = S.alpha; q.beta = S.beta; q.tgt = S.tgt; q.nb = S.nb;
           q.cbase = target;
           if (S.mode == M_DONE) {
