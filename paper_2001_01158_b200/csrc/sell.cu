@@ -46,15 +46,21 @@ __global__ void k_candidate(const int64_t* __restrict__ rp, const int32_t* __res
 // every stored (u, c) must have c - u in the candidate offset set
 __global__ void k_check_stencil(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                 const Offsets* __restrict__ Od, unsigned* err) {
+  __shared__ int s_off[kMaxOff];
+  __shared__ int s_w;
+  if (threadIdx.x < kMaxOff) s_off[threadIdx.x] = Od->off[threadIdx.x];
+  if (threadIdx.x == 0) s_w = Od->W;
+  __syncthreads();
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u >= n) return;
-  const Offsets O = *Od;
+  // the row's offsets and the candidate set are both ascending: one merge walk
+  const int W = s_w;
+  int k = 0;
   for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
-    int64_t d = (int64_t)ci[e] - u;
-    bool hit = false;
-#pragma unroll
-    for (int k = 0; k < kMaxOff; ++k) hit |= (k < O.W && O.off[k] == d);
-    if (!hit) { atomicOr(err, kErrNotStencil); return; }
+    const int64_t d = (int64_t)ci[e] - u;
+    while (k < W && s_off[k] < d) ++k;
+    if (k == W || s_off[k] != d) { atomicOr(err, kErrNotStencil); return; }
+    ++k;
   }
 }
 
