@@ -2,11 +2,16 @@
 // persistent cooperative kernel (SURVEY 8(a) a7/a9 for the nonsymmetric 3T
 // systems of config 4; readings R20/R21/R33).
 //
-// One Arnoldi step = four grid-synchronised passes, each fused with its dots:
-//   1a  v_j = src / h (src = r or the last w), t = M^-1 v_j        (block inverse per cell)
-//   1b  w = A t (BSR-in-SELL SpMV) fused with h_i = V_i^T w, i <= j  (CGS pass 1 dots)
-//   2   w -= V h fused with h2_i = V_i^T w                           (CGS pass 2 dots)
-//   3   w -= V h2 fused with ||w||^2
+// One Arnoldi step of the default (Gram-form CGS2, R39) kernel = two grid-synchronised passes:
+//   A  w = A t (BSR-in-SELL SpMV, t = M^-1 U_j from the previous pass) fused with the dots h_i = V_i^T w and
+//      the new Gram column V_i^T V_j, i <= j
+//   B  w <- w - V (h + h2) with h2 = h - (V^T V) h from the scalars, U_{j+1} = w, t = M^-1 U_{j+1}, ||w||^2
+// (lc_tuning.gmres_exact_cgs2 keeps the textbook form: normalise, SpMV + dots, project + dots, project + norm.)
+// Memory-level parallelism is what the passes live on (a warp owns 1-2 slices, every pass is ~20 us):
+// the five-point 3T row is branch-free (block_row_dcoup5), the basis loads of the dot and update blocks are
+// clamped instead of guarded so that they all issue before their first use, the update pass walks the basis
+// downwards so each pass starts on what the previous one left in L2, the matrix and preconditioner values load
+// with L2 evict_first and the basis with evict_last: config 4 Arnoldi step 63.5 -> 50 us (profiles/r02_p).
 // The Hessenberg column, Givens rotations and the residual estimate |g_{j+1}|
 // are computed redundantly (bitwise identically) by every CTA from the same
 // fixed-order reductions, so control flow is grid-uniform without any host
@@ -24,6 +29,10 @@ namespace lc {
 #define LC_GMRES_GT 512
 #endif
 constexpr int kGT = LC_GMRES_GT;             // threads per CTA (1024 / kGT CTAs per SM)
+#ifndef LC_GMRES_MINB
+#define LC_GMRES_MINB (1024 / LC_GMRES_GT)
+#endif
+constexpr int kGMinB = LC_GMRES_MINB;        // CTAs per SM the kernel is compiled (registers) and launched for
 constexpr int kGW = kGT / 32;
 constexpr int kMaxM = 40;
 constexpr int kMaxQ = 2 * (kMaxM + 1) + 2;   // reduced quantities per phase
@@ -33,13 +42,13 @@ constexpr int kMaxQ = 2 * (kMaxM + 1) + 2;   // reduced quantities per phase
 constexpr int kCC = LC_GMRES_CC;             // slices per warp chunk in the SpMV + dots pass (with kIB = 2: 1: 78.2,
                                              // 2: 69.0, 3: 81.3 us/step)
 #ifndef LC_GMRES_IB
-#define LC_GMRES_IB 3
+#define LC_GMRES_IB 1
 #endif
-// basis vectors per unrolled block of the dot / update loops.  Round 1 (full 3x3 coupling blocks): 1 (config 4
-// Arnoldi step 67.2 us) beat 2 (69.0), 3 (69.1), 4 (72.3), 8 (81.0).  Round 2, with the compact diagonal couplings
-// (fewer registers in the SpMV): 3 (62.8 us) beats 1 (65.5), 2 (68.0), 4 (64.5), 6 (66.9); kCC 2 stays (kCC 1
-// 64.8, 3 70.3 with kIB 3) -- tools/dev/build_variant.sh + tools/dev/ab_solves.py, profiles/r02_k
-constexpr int kIB = LC_GMRES_IB;           // with the compact 3T couplings; the full-block paths keep 1
+// basis vectors per block of the dot / update loops.  With guarded loads (rounds 1-2: one memory round trip per
+// vector whatever the block) 1 or 3 won by a few percent (profiles/r01_ar, r02_k).  With the clamped, branch-free
+// loads of this round every block's loads issue together and the blocks overlap: 1 (49.7 us per config 4 Arnoldi
+// step) <= 2 (50.2) <= 4 (50.6) <= 3 (51.4); kCC 2 stays (kCC 1: 50.6) -- profiles/r02_p
+constexpr int kIB = LC_GMRES_IB;
 #ifndef LC_GMRES_REV
 #define LC_GMRES_REV 0
 #endif
@@ -47,6 +56,43 @@ constexpr int kIB = LC_GMRES_IB;           // with the compact 3T couplings; the
 // of the basis): config 4 Arnoldi step 67.2 -> 68.3 us, not adopted (the update pass already runs above the DRAM
 // rate, 19 us for 145 MB at j = 15, tools/tl_gmres.py)
 constexpr bool kGRev = LC_GMRES_REV != 0;
+#ifndef LC_GMRES_RED1
+#define LC_GMRES_RED1 2
+#endif
+#ifndef LC_GMRES_VREV
+#define LC_GMRES_VREV 1
+#endif
+// 1: the update pass walks the basis from V_j down to V_0, so it starts on the vectors the SpMV + dots pass read
+// last and ends on V_0, V_1, ... where the next step's dots begin: each pass finds in L2 what the previous one
+// touched last (both ascending, a cycle's basis (j + 1) x 6.3 MB streams through the 126 MB L2 in LRU order and
+// every access misses once it no longer fits)
+#ifndef LC_GMRES_HINT
+#define LC_GMRES_HINT 2
+#endif
+// 1: the matrix values and preconditioner blocks (read once per step) load with L2 evict_first; 2: also the basis
+// with evict_last
+__device__ __forceinline__ double ld_first(const double* p) {
+#if LC_GMRES_HINT >= 1
+  unsigned long long pol;
+  double v;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ double ld_last(const double* p) {
+#if LC_GMRES_HINT >= 2
+  unsigned long long pol;
+  double v;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  return *p;
+#endif
+}
 
 struct GmresArgs {
   SellView A;
@@ -98,13 +144,61 @@ __device__ __forceinline__ void block_row_dcoup(const SellView& A, int64_t s, in
   }
 }
 
+// the same row for the five-point cell stencil (W = 5, the diagonal in slot 2: offsets {-nx, -1, 0, 1, nx}): no
+// branch on the slot and no slot loop, so the row's 15 gathers and 21 values all issue before the chains (the slot
+// loop above takes one memory round trip per slot: config 4's SpMV part of an Arnoldi step ran at 3 TB/s,
+// profiles/r02_g).  Same chains in the same slot order, so bitwise the results of block_row_dcoup.
+#ifndef LC_GMRES_SPMV5
+#define LC_GMRES_SPMV5 1
+#endif
+__device__ __forceinline__ void block_row_dcoup5(const SellView& A, int64_t s, int lane, int64_t u,
+                                                 const double* __restrict__ y, double* acc) {
+  const double* cb = A.cval + 32ll * 21 * s + lane;
+  const int64_t n1 = A.nunits - 1;
+  double yy[5][3], dv[9], cv[4][3];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    int64_t c = u + A.off[k];
+    c = c < 0 ? 0 : (c > n1 ? n1 : c);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) yy[k][a] = y[3 * c + a];
+  }
+#pragma unroll
+  for (int q = 0; q < 9; ++q) dv[q] = ld_first(cb + 32 * q);
+#pragma unroll
+  for (int o = 0; o < 4; ++o)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) cv[o][a] = ld_first(cb + 32 * (9 + 3 * o + a));
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    if (k == 2) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        acc[a] = __fma_rn(dv[3 * a], yy[2][0], acc[a]);
+        acc[a] = __fma_rn(dv[3 * a + 1], yy[2][1], acc[a]);
+        acc[a] = __fma_rn(dv[3 * a + 2], yy[2][2], acc[a]);
+      }
+    } else {
+      const int o = k < 2 ? k : k - 1;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) acc[a] = __fma_rn(cv[o][a], yy[k][a], acc[a]);
+    }
+  }
+}
+// dispatch: the branch-free row when the layout is the five-point one
+__device__ __forceinline__ void block_row_dc(const SellView& A, int64_t s, int lane, int wd, int64_t u,
+                                             const double* __restrict__ y, double* acc) {
+  if (LC_GMRES_SPMV5 && wd == 5 && A.kdiag == 2) block_row_dcoup5(A, s, lane, u, y, acc);
+  else block_row_dcoup(A, s, lane, wd, u, y, acc);
+}
+
 template <int BS>
 __device__ __forceinline__ void block_apply(const double* __restrict__ Mi, const double* v, double* t) {
 #pragma unroll
   for (int a = 0; a < BS; ++a) {
     double s = 0.0;
 #pragma unroll
-    for (int be = 0; be < BS; ++be) s = __fma_rn(Mi[a * BS + be], v[be], s);
+    for (int be = 0; be < BS; ++be) s = __fma_rn(ld_first(Mi + a * BS + be), v[be], s);
     t[a] = s;
   }
 }
@@ -117,8 +211,58 @@ __device__ unsigned long long g_tlg[16384];
 #define TLG(k) (void)0
 #endif
 
+// sums of N (a power of two <= 32) per-lane values over the warp with N - 1 + log2(32 / N) shuffles instead of
+// 5 N: at each of the first log2 N levels a lane keeps one half of its values and sends the other half to its
+// partner; afterwards lane l holds the warp's sum of v[l % N].  Fixed order, so deterministic.
+template <int N>
+__device__ __forceinline__ double warp_sum_multi(double* v, int lane) {
+#pragma unroll
+  for (int half = N / 2, bit = 1; half >= 1; half >>= 1, bit <<= 1) {
+    const bool up = lane & bit;
+#pragma unroll
+    for (int q = 0; q < half; ++q) {
+      const double keep = up ? v[2 * q + 1] : v[2 * q];
+      const double send = up ? v[2 * q] : v[2 * q + 1];
+      v[q] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+    }
+  }
+  double r = v[0];
+#pragma unroll
+  for (int o = N; o < 32; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
+
+// fixed-order sums of nq quantities over the CTAs' partials pt[q * nCTA + cta] into red[q] (shared memory): a
+// lane adds CTAs lane, lane + 32, ... in that order, then the warp's lanes are combined by shuffles.  The loads of
+// TWO quantities (10 each per lane for <= 320 CTAs) issue together, so 2 (j + 1) <= 32 quantities cost one L2
+// round trip per warp instead of four.  Out of line: the 20 loads in flight need the registers the Arnoldi loop
+// holds live (inlined, ptxas spilled the loaded values themselves).
+__device__ __noinline__ void reduce_partials(const double* __restrict__ pt, int nq, int nCTA, double* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q0 = warp; q0 < nq; q0 += 2 * kGW) {
+    const int q1 = q0 + kGW;
+    const bool two = q1 < nq;
+    double v0 = 0.0, v1 = 0.0;
+    for (int c0 = lane; c0 < nCTA; c0 += 32 * 10) {
+      double t0[10], t1[10];
+#pragma unroll
+      for (int k = 0; k < 10; ++k) {
+        const bool in = c0 + 32 * k < nCTA;
+        t0[k] = in ? __ldcg(pt + (size_t)q0 * nCTA + c0 + 32 * k) : 0.0;
+        t1[k] = in && two ? __ldcg(pt + (size_t)q1 * nCTA + c0 + 32 * k) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 10; ++k)
+        if (c0 + 32 * k < nCTA) { v0 += t0[k]; v1 += t1[k]; }
+    }
+    v0 = warp_sum(v0);
+    v1 = warp_sum(v1);
+    if (lane == 0) { red[q0] = v0; if (two) red[q1] = v1; }
+  }
+}
+
 template <int BS, int IB>
-__global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
+__global__ void __launch_bounds__(kGT, kGMinB) k_gmres(GmresArgs P) {
   unsigned long long bar_epoch = 0;
 #ifdef LC_DEBUG_TIMELINE
   int tk = 0;
@@ -137,6 +281,7 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
   __shared__ double s_acc[kGW][kMaxQ];
   __shared__ double Gm[(kMaxM + 1) * (kMaxM + 1)];   // Gram matrix V^T V (low-sync CGS2, R39)
 
+  constexpr int kNP = 2 * IB <= 2 ? 2 : 2 * IB <= 4 ? 4 : 2 * IB <= 8 ? 8 : 16;   // the dots block's sums, padded
   // per-lane accumulators -> per-warp smem -> CTA partial part[q*nCTA + bid]
   auto clear = [&](int nq) {
     for (int t = threadIdx.x; t < kGW * kMaxQ; t += kGT) (&s_acc[0][0])[t] = 0.0;
@@ -159,6 +304,31 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
   auto reduce = [&](int nq) {
     const double* pt = P.part + (size_t)ppar * kMaxQ * nCTA;
     ppar ^= 1;
+#if LC_GMRES_RED1 == 1
+    reduce_partials(pt, nq, (int)nCTA, red);
+#elif LC_GMRES_RED1 == 2
+    // two quantities per warp at a time, 5 loads each in flight
+    for (int q0 = warp; q0 < nq; q0 += 2 * kGW) {
+      const int q1 = q0 + kGW;
+      const bool two = q1 < nq;
+      double v0 = 0.0, v1 = 0.0;
+      for (int64_t c0 = lane; c0 < nCTA; c0 += 32 * 5) {
+        double t0[5], t1[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const bool in = c0 + 32 * k < nCTA;
+          t0[k] = in ? pt[q0 * nCTA + c0 + 32 * k] : 0.0;
+          t1[k] = in && two ? pt[q1 * nCTA + c0 + 32 * k] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+          if (c0 + 32 * k < nCTA) { v0 += t0[k]; v1 += t1[k]; }
+      }
+      v0 = warp_sum(v0);
+      v1 = warp_sum(v1);
+      if (lane == 0) { red[q0] = v0; if (two) red[q1] = v1; }
+    }
+#else
     for (int q = warp; q < nq; q += kGW) {
       // a lane's partials (CTAs lane, lane + 32, ...) are loaded 8 at a time and added in that order
       double v = 0.0;
@@ -173,6 +343,7 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
       v = warp_sum(v);
       if (lane == 0) red[q] = v;
     }
+#endif
     __syncthreads();
   };
   auto lane_flush = [&](int q, double v) {
@@ -199,7 +370,7 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
 #pragma unroll
         for (int a = 0; a < BS; ++a) acc[a] = 0.0;
         if (BS == 3 && A.cval) {
-          block_row_dcoup(A, s, lane, wd, u, P.x, acc);
+          block_row_dc(A, s, lane, wd, u, P.x, acc);
         } else
         for (int k = 0; k < wd; ++k) {
           int64_t c = sv_col(A, p0 + lane, k, u);
@@ -280,21 +451,21 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
       clear(j + 1);
       for (int64_t s0 = s_begin; s0 < A.nslices; s0 += kCC * s_step) {
         double wv[kCC][BS];
-        int64_t uu[kCC];
+        int64_t ea[kCC];                 // this lane's first element (a row past the end reads element 0, times w = 0)
         bool ok[kCC];
 #pragma unroll
         for (int cc = 0; cc < kCC; ++cc) {
           const int64_t s = s0 + cc * s_step;
-          uu[cc] = s < A.nslices ? A.slice_row0[s] + lane : nunits;
-          ok[cc] = uu[cc] < nunits;
+          const int64_t u = s < A.nslices ? A.slice_row0[s] + lane : nunits;
+          ok[cc] = u < nunits;
+          ea[cc] = ok[cc] ? BS * u : 0;
 #pragma unroll
           for (int a = 0; a < BS; ++a) wv[cc][a] = 0.0;
           if (ok[cc]) {
-            const int64_t u = uu[cc];
             const int64_t p0 = A.slice_ptr[s];
             const int wd = A.stencil ? A.W : (int)((A.slice_ptr[s + 1] - p0) >> 5);
             if (BS == 3 && A.cval) {
-              block_row_dcoup(A, s, lane, wd, u, P.t, wv[cc]);
+              block_row_dc(A, s, lane, wd, u, P.t, wv[cc]);
             } else
 #pragma unroll 5
             for (int k = 0; k < wd; ++k) {
@@ -321,35 +492,39 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
 #pragma unroll
         for (int cc = 0; cc < kCC; ++cc)
 #pragma unroll
-          for (int a = 0; a < BS; ++a) vj[cc][a] = (ok[cc] && !P.exact_cgs2) ? Vj[BS * uu[cc] + a] : 0.0;
-        // i in blocks of IB with compile-time indices: the block's V loads issue together (one DRAM
-        // latency per block instead of one per basis vector)
+          for (int a = 0; a < BS; ++a) vj[cc][a] = (ok[cc] && !P.exact_cgs2) ? Vj[ea[cc] + a] : 0.0;
+        // i in blocks of IB.  Every load of the block issues before its first use: the addresses are clamped
+        // (vector min(i, j), element 0 for a row past the end) instead of guarded, so no branch separates the
+        // loads -- guarded, ptxas issued one vector's loads, waited, multiplied, and only then loaded the next
+        // (18.5% of the kernel's stall samples sat on the first multiply, profiles/r02_p).  The block's 2 IB
+        // sums are combined over the lanes by one merged butterfly (warp_sum_multi).
         for (int i0 = 0; i0 <= j; i0 += IB) {
-          double d[IB], gq[IB];
+          double vi[IB][kCC][BS];
 #pragma unroll
           for (int ii = 0; ii < IB; ++ii) {
-            d[ii] = 0.0;
-            gq[ii] = 0.0;
-            const int i = i0 + ii;
-            if (i <= j) {
-              const double* Vi = P.V + (size_t)i * n;
+            const double* Vi = P.V + (size_t)(i0 + ii <= j ? i0 + ii : j) * n;
 #pragma unroll
-              for (int cc = 0; cc < kCC; ++cc)
-                if (ok[cc]) {
+            for (int cc = 0; cc < kCC; ++cc)
 #pragma unroll
-                  for (int a = 0; a < BS; ++a) {
-                    const double vi = Vi[BS * uu[cc] + a];
-                    d[ii] = __fma_rn(vi, wv[cc][a], d[ii]);
-                    gq[ii] = __fma_rn(vi, vj[cc][a], gq[ii]);
-                  }
-                }
-            }
+              for (int a = 0; a < BS; ++a) vi[ii][cc][a] = ld_last(Vi + ea[cc] + a);
           }
+          double dq[kNP];                 // d[0..IB), then gq[0..IB), zero padding up to a power of two
 #pragma unroll
-          for (int ii = 0; ii < IB; ++ii) {
-            if (i0 + ii > j) break;
-            lane_flush(i0 + ii, d[ii]);
-            if (!P.exact_cgs2) lane_flush(j + 1 + i0 + ii, gq[ii]);
+          for (int q = 0; q < kNP; ++q) dq[q] = 0.0;
+#pragma unroll
+          for (int ii = 0; ii < IB; ++ii)
+#pragma unroll
+            for (int cc = 0; cc < kCC; ++cc)
+#pragma unroll
+              for (int a = 0; a < BS; ++a) {
+                dq[ii] = __fma_rn(vi[ii][cc][a], wv[cc][a], dq[ii]);
+                dq[IB + ii] = __fma_rn(vi[ii][cc][a], vj[cc][a], dq[IB + ii]);
+              }
+          const double tot = warp_sum_multi<kNP>(dq, lane);     // lane l: the sum of dq[l % kNP]
+          const int q = lane & (kNP - 1);
+          if (lane < kNP && q < 2 * IB) {
+            const int ii = q < IB ? q : q - IB;
+            if (i0 + ii <= j && (q < IB || !P.exact_cgs2)) s_acc[warp][(q < IB ? 0 : j + 1) + i0 + ii] += tot;
           }
         }
       }
@@ -388,20 +563,25 @@ __global__ void __launch_bounds__(kGT, 1024 / kGT) k_gmres(GmresArgs P) {
           double a0 = 0.0;
           for (int64_t sr = s_begin; sr < A.nslices; sr += s_step) {
             const int64_t s = kGRev ? A.nslices - 1 - sr : sr;
-            int64_t u = A.slice_row0[s] + lane;
+            const int64_t u = A.slice_row0[s] + lane;
             if (u >= nunits) continue;
             double ww[BS];
 #pragma unroll
             for (int a = 0; a < BS; ++a) ww[a] = sj * P.w[BS * u + a];
-            for (int i0 = 0; i0 <= j; i0 += IB) {
+            // blocks of IB basis vectors, from V_j down (LC_GMRES_VREV); clamped vector index with a zero
+            // coefficient instead of a guard, so the block's loads all issue together
+            for (int ib = 0; ib <= j / IB; ++ib) {
+              const int i0 = LC_GMRES_VREV ? (j / IB - ib) * IB : ib * IB;
               double vv[IB][BS];
 #pragma unroll
               for (int ii = 0; ii < IB; ++ii)
 #pragma unroll
-                for (int a = 0; a < BS; ++a) vv[ii][a] = i0 + ii <= j ? P.V[(size_t)(i0 + ii) * n + BS * u + a] : 0.0;
+                for (int a = 0; a < BS; ++a)
+                  vv[ii][a] = ld_last(P.V + (size_t)(i0 + ii <= j ? i0 + ii : j) * n + BS * u + a);
 #pragma unroll
-              for (int ii = 0; ii < IB; ++ii) {
-                if (i0 + ii > j) break;
+              for (int i2 = 0; i2 < IB; ++i2) {          // descending inside the block too: the same chain for any IB
+                const int ii = LC_GMRES_VREV ? IB - 1 - i2 : i2;
+                if (i0 + ii > j) continue;
                 const double hi = hh[i0 + ii];
 #pragma unroll
                 for (int a = 0; a < BS; ++a) ww[a] = __fma_rn(-hi, vv[ii][a], ww[a]);
@@ -582,13 +762,13 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   const int BS = M.block;
   const int m = p->restart;
   const int64_t n = M.nunits * BS;
-  // basis blocking: kIB with the compact 3T couplings, 1 on the full-block paths (the explicit subsystems: their
-  // registers spill at 3; config 4 local solve 1.70 vs 1.82 ms)
-  void* fn = BS == 1 ? (void*)k_gmres<1, 1> : M.cval ? (void*)k_gmres<3, kIB> : (void*)k_gmres<3, 1>;
+  // basis blocking kIB for every kernel (the 3T kernel is instantiated once whatever the couplings' storage)
+  void* fn = BS == 1 ? (void*)k_gmres<1, kIB> : (void*)k_gmres<3, kIB>;
   int64_t max_ctas = 0;
-  lc_status st = max_coresident(fn, kGT, 0, &max_ctas);
+  const size_t dsmem = 0;
+  lc_status st = max_coresident(fn, kGT, dsmem, &max_ctas);
   if (st) return st;
-  max_ctas = std::min<int64_t>(max_ctas, (int64_t)(1024 / kGT) * num_sms());
+  max_ctas = std::min<int64_t>(max_ctas, (int64_t)kGMinB * num_sms());
   int64_t nCTA = std::min<int64_t>(max_ctas, (M.nslices + kGW - 1) / kGW);
   if (nCTA < 1) nCTA = 1;
   size_t vbytes = ((sizeof(double) * (size_t)n) + 255) & ~(size_t)255;
@@ -627,7 +807,7 @@ lc_status run_gmres(const Sell& M, const double* b, double* x, const int32_t* sc
   cudaError_t e = cudaMemsetAsync(a.bar, 0, sizeof(GridBar), s);
   cudaEventRecord(clk.e0, s);
   void* args[] = {&a};
-  if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kGT), args, 0, s);
+  if (e == cudaSuccess) e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)nCTA), dim3(kGT), args, dsmem, s);
   count_launch();
   cudaEventRecord(clk.e1, s);
   struct FreeAfter { void* p; cudaStream_t s; ~FreeAfter() { dfree(p, s); } } fa{ws, s};
