@@ -425,6 +425,10 @@ typedef struct {
   int32_t block_dcoup;          /* 1 (default): block 3 stencil matrices whose off-diagonal blocks are diagonal (the
                                    3T couplings) keep a compact copy without those blocks' explicit zeros for the
                                    GMRES SpMVs (21 instead of 45 values per cell, bitwise the same chains); 0: no */
+  int32_t l2_stream_hint;       /* -1 (default): the PCG kernels load the matrix stream (values, columns) with the L2
+                                   evict_first policy when the solve's working set exceeds L2 while its vectors
+                                   are at most twice L2 (they then stay cached between passes); 0: never; 1: always.
+                                   Cache policy only: results are bitwise the same */
 } lc_tuning;
 
 /* the defaults listed above (host output) */

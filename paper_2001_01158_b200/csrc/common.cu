@@ -73,6 +73,26 @@ int num_sms() {
   return sms;
 }
 
+const lc_tuning& tuning();
+static std::map<int, int64_t> g_l2;                                     // L2 bytes per device
+int64_t l2_bytes() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto it = g_l2.find(dev);
+  if (it != g_l2.end()) return it->second;
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
+  g_l2[dev] = v;
+  return v;
+}
+bool stream_policy_wanted(int64_t matrix_bytes, int64_t vector_bytes) {
+  const int f = tuning().l2_stream_hint;
+  if (f >= 0) return f != 0;
+  const int64_t l2 = l2_bytes();
+  return l2 > 0 && 4 * (matrix_bytes + vector_bytes) > 3 * l2 && vector_bytes <= 2 * l2;
+}
+
 lc_status func_attr(const void* fn, cudaFuncAttribute attr, int value) {
   int dev = 0;
   lc_status st = device_of_caller(&dev);
@@ -224,6 +244,7 @@ static lc_tuning defaults_() {
   t.spmv_tma = 1;
   t.batched_cluster = 0;
   t.block_dcoup = 1;
+  t.l2_stream_hint = -1;
   return t;
 }
 static thread_local lc_tuning g_tune = defaults_();
@@ -481,7 +502,8 @@ extern "C" lc_status lc_set_tuning(const lc_tuning* t) {
       !bin(t->pcg_tma) || t->lazy_x_depth < 0 || t->lazy_x_depth > 3 || t->batched_schedule < -1 ||
       t->batched_schedule > 2 || t->pcg_max_ctas < 0 || t->sub_repr < -1 || t->sub_repr > 1 ||
       !bin(t->gmres_exact_cgs2) || !bin(t->gs_lines) || !bin(t->spmv_csr_tma) || t->spmv_tma < 0 || t->spmv_tma > 2 ||
-      t->batched_cluster < 0 || t->batched_cluster == 1 || t->batched_cluster > 16 || !bin(t->block_dcoup)) {
+      t->batched_cluster < 0 || t->batched_cluster == 1 || t->batched_cluster > 16 || !bin(t->block_dcoup) ||
+      t->l2_stream_hint < -1 || t->l2_stream_hint > 1) {
     lc::set_error("lc_set_tuning: field out of range");
     return LC_ERR_INVALID_ARG;
   }

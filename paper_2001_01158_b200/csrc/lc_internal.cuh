@@ -105,6 +105,10 @@ lc_status run_pcg_dsmem(const PcgJob& job, const lc_solver_params* p, cudaStream
 lc_status dalloc(void** p, size_t bytes, cudaStream_t s);
 void dfree(void* p, cudaStream_t s);
 int num_sms();                                   // SMs of the calling thread's current device (cached per device)
+int64_t l2_bytes();                              // L2 cache size of the current device (cached per device)
+// whether a solve whose passes stream `matrix_bytes` once and re-read `vector_bytes` should mark the matrix
+// stream evict_first (see l2_evict_first_policy): lc_tuning.l2_stream_hint -1 = this rule, 0 / 1 force
+bool stream_policy_wanted(int64_t matrix_bytes, int64_t vector_bytes);
 // co-resident CTAs (occupancy x SMs) of `fn` on the current device, cached per (device, fn, threads, smem); opts the
 // function into > 48 KB of dynamic shared memory on that device first when needed
 lc_status max_coresident(const void* fn, int threads, size_t dsmem, int64_t* ctas);
@@ -586,10 +590,37 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+// L2 eviction policy for the streams that are read once per pass (matrix values, column indices).  The vectors
+// of a Krylov iteration are re-read within the iteration and, when they fit L2, across iterations; the matrix
+// stream is not, and marked evict_first it stops displacing them.  The launchers decide (stream_policy_wanted):
+// the hint pays when the whole working set exceeds L2 but the vectors are of about its size (config 2 global
+// PCG 24.6 -> 23.0 us per iteration, config 5's explicit local subsystem 4.91 -> 4.31 ms, config 3 batched
+// global 37.7 -> 35.7 ms); it changes nothing for systems far larger than L2 (config 5 global: +0.5%) and
+// L2-resident ones keep plain loads (config 3's local teams were 3.5% slower with hinted loads).
+// the policy word of a kernel's matrix stream: evict_first when `stream`, else evict_normal (what a plain load
+// gets) -- one register pair per thread, so the loads below are single instructions whatever the choice
+__device__ __forceinline__ unsigned long long l2_stream_policy(bool stream) {
+  unsigned long long a, b;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(a));
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(b));
+  return stream ? a : b;
+}
+// read-only value load with an L2 policy word
+__device__ __forceinline__ double ldg_pol(const double* p, unsigned long long pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
 // 1-D bulk copy global -> shared, completing `bytes` of transaction count on `bar` (16-B aligned, multiple of 16)
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// the same copy with an L2 policy word
+__device__ __forceinline__ void tma_bulk_g2s_pol(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                                 unsigned long long pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(

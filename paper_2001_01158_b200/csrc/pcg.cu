@@ -84,6 +84,8 @@ struct PcgArgs {
   int teams;                    // > 0 (G > 1): the CTAs form `teams` contiguous teams; team t solves segments
                                 // t, t + teams, ... one after another as G = 1 systems with its own barrier
   unsigned long long* tctr;     // [teams][16] team barrier counters (zeroed at launch)
+  int stream_vals;              // the matrix stream loads with the L2 evict_first policy (stream_policy_wanted)
+  long long l2_bytes;           // dynamic teams: the policy follows the active groups' working set
 };
 
 struct SegState {
@@ -148,7 +150,8 @@ __device__ __forceinline__ double sym_val(const SellView& A, const double* __res
 }
 
 template <int WM, int ST, class Ld>
-__device__ __forceinline__ double row_dot(const SellView& A, int64_t pl, int w, int64_t u, Ld ld, double* own) {
+__device__ __forceinline__ double row_dot(const SellView& A, int64_t pl, int w, int64_t u, Ld ld, double* own,
+                                          unsigned long long pol) {
   double acc = 0.0;
   const double* vp = A.val + pl;
   if (WM > 0) {
@@ -165,7 +168,7 @@ __device__ __forceinline__ double row_dot(const SellView& A, int64_t pl, int w, 
       } else {
         c = (k < w) ? __ldg(A.col + pl + 32 * k) : 0;
       }
-      v[k] = ST == 2 ? sym_val(A, vp, k, ui) : (ST || k < w) ? __ldg(vp + 32 * k) : 0.0;
+      v[k] = ST == 2 ? sym_val(A, vp, k, ui) : (ST || k < w) ? ldg_pol(vp + 32 * k, pol) : 0.0;
       y[k] = (ST || k < w) ? ld(c) : 0.0;
     }
 #pragma unroll
@@ -197,6 +200,7 @@ __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_
                                             const double* __restrict__ xp = nullptr, double xa = 0.0,
                                             const double* __restrict__ xp2 = nullptr, double xa2 = 0.0) {
   const SellView& A = P.A;
+  const unsigned long long strm = l2_stream_policy(P.stream_vals != 0);
   // (gk >= 0: every slice belongs to segment gk)
   // the slice list entry and the row's Omega flag are loaded one slice ahead (masked solves walk a list of
   // slices; without the prefetch every slice starts with two dependent load latencies)
@@ -237,8 +241,8 @@ __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_
       const double* xx = P.x;
       double acc = xp ? row_dot<WM, ST>(A, pl, w, u, [&](int c) {
                           const double t = __fma_rn(xa, xp[c], xx[c]);
-                          return xp2 ? __fma_rn(xa2, xp2[c], t) : t; }, &own)
-                      : row_dot<WM, ST>(A, pl, w, u, [&](int c) { return xx[c]; }, &own);
+                          return xp2 ? __fma_rn(xa2, xp2[c], t) : t; }, &own, strm)
+                      : row_dot<WM, ST>(A, pl, w, u, [&](int c) { return xx[c]; }, &own, strm);
       if (in) {
         double bi = P.b[u];
         double ri = bi - acc;
@@ -249,8 +253,8 @@ __device__ __forceinline__ void pass_a_loop(const PcgArgs& P, int64_t j0, int64_
     } else {
       const double* zz = P.z;
       double acc;
-      if (MODE == 1) acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return zz[c]; }, &own);
-      else acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return __fma_rn(beta, pold[c], zz[c]); }, &own);
+      if (MODE == 1) acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return zz[c]; }, &own, strm);
+      else acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return __fma_rn(beta, pold[c], zz[c]); }, &own, strm);
       if (in) {
         double pi = ST ? own : (MODE == 1 ? zz[u] : __fma_rn(beta, pold[u], zz[u]));
         pnew[u] = pi;
@@ -323,6 +327,7 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
     fence_mbar_init();
   }
   __syncthreads();
+  const unsigned long long pol = l2_stream_policy(P.stream_vals != 0);
   auto issue = [&](int64_t t) {
     const int64_t c = bid + t * nCTA;
     if (c >= nch) return;
@@ -332,8 +337,8 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
     const unsigned sbytes = (unsigned)(32 * vw * 8);
     if (!P.slist) {                                              // 8 consecutive slices: one copy
       mbar_expect_tx(&bars[st], sbytes * nsl * (ST == 0 ? 3 : 2) / 2);
-      tma_bulk_g2s(stg + st * chd, A.val + j0c * 32 * vw, sbytes * nsl, &bars[st]);
-      if (ST == 0) tma_bulk_g2s(scol + st * chd, A.col + j0c * 32 * vw, sbytes * nsl / 2, &bars[st]);
+      tma_bulk_g2s_pol(stg + st * chd, A.val + j0c * 32 * vw, sbytes * nsl, &bars[st], pol);
+      if (ST == 0) tma_bulk_g2s_pol(scol + st * chd, A.col + j0c * 32 * vw, sbytes * nsl / 2, &bars[st], pol);
     } else {                                                     // listed slices: one copy each
       mbar_expect_tx(&bars[st], sbytes * nsl);
       for (int w = 0; w < nsl; ++w)
@@ -427,6 +432,7 @@ __device__ __forceinline__ void pass_a_tma(const PcgArgs& P, double* stg, uint64
 template <int WM, int ST, int KIND>
 __global__ void __launch_bounds__(kPT, ST == 0 ? LCV_MINB_SELL : LCV_MINB) k_pcg(PcgArgs P) {
   unsigned long long bar_epoch = 0;
+  const unsigned long long strm = l2_stream_policy(P.stream_vals != 0);   // the matrix stream's L2 policy word
   unsigned tree_gen = 0;                        // tree barriers passed (G > 1)
   __shared__ SegState S[kMaxSeg];
   __shared__ double s_acc[kPW][kMaxSeg][2];
@@ -659,7 +665,7 @@ __global__ void __launch_bounds__(kPT, ST == 0 ? LCV_MINB_SELL : LCV_MINB) k_pcg
         double own = 0.0;
         if (mode == M_INIT || mode == M_CONFIRM) {
           const double* xx = P.x;
-          double acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return xx[c]; }, &own);
+          double acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return xx[c]; }, &own, strm);
           if (in_omega(u)) {
             double bi = P.b[u];
             double ri = bi - acc;
@@ -670,8 +676,8 @@ __global__ void __launch_bounds__(kPT, ST == 0 ? LCV_MINB_SELL : LCV_MINB) k_pcg
         } else {
           const double* zz = P.z;
           double acc;
-          if (mode == M_FIRST) acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return zz[c]; }, &own);
-          else acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return __fma_rn(beta, pold[c], zz[c]); }, &own);
+          if (mode == M_FIRST) acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return zz[c]; }, &own, strm);
+          else acc = row_dot<WM, ST>(A, pl, w, u, [&](int c) { return __fma_rn(beta, pold[c], zz[c]); }, &own, strm);
           if (in_omega(u)) {
             double pi = ST ? own : (mode == M_FIRST ? zz[u] : __fma_rn(beta, pold[u], zz[u]));
             pnew[u] = pi;
@@ -1051,6 +1057,10 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg_dyn(DynArgs D) {
     __syncthreads();
     const int64_t s0g = s_g0, s1g = s_g1;
     const int64_t nchg = (s1g - s0g + kDynR - 1) / kDynR;   // this group's chunks
+    // matrix-stream policy of this phase: evict_first while the active groups' working sets (values + 7 vectors)
+    // exceed 3/4 of L2 together (the head of the solve); plain loads once they fit (the tail)
+    const unsigned long long strm = l2_stream_policy(
+        P.stream_vals >= 0 ? P.stream_vals != 0 : 4ll * na * (s1g - s0g) * 32 * (8 * A.W + 56) > 3 * P.l2_bytes);
     const int64_t kw = (bid - tb0) * kPW + warp, TW = tn * kPW;
     bool leave = false;
     while (!leave) {
@@ -1078,7 +1088,7 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg_dyn(DynArgs D) {
             double own = 0.0;
             if (mode == M_INIT || mode == M_CONFIRM) {
               const double* xx = P.x;
-              const double acc = row_dot<WM, ST>(A, pl, w, u, [&](int cc) { return xx[cc]; }, &own);
+              const double acc = row_dot<WM, ST>(A, pl, w, u, [&](int cc) { return xx[cc]; }, &own, strm);
               const double bi = P.b[u];
               const double ri = bi - acc;
               P.r[u] = ri;
@@ -1087,8 +1097,8 @@ __global__ void __launch_bounds__(kPT, LCV_MINB) k_pcg_dyn(DynArgs D) {
             } else {
               const double* zz = P.z;
               double acc;
-              if (mode == M_FIRST) acc = row_dot<WM, ST>(A, pl, w, u, [&](int cc) { return zz[cc]; }, &own);
-              else acc = row_dot<WM, ST>(A, pl, w, u, [&](int cc) { return __fma_rn(beta, pold[cc], zz[cc]); }, &own);
+              if (mode == M_FIRST) acc = row_dot<WM, ST>(A, pl, w, u, [&](int cc) { return zz[cc]; }, &own, strm);
+              else acc = row_dot<WM, ST>(A, pl, w, u, [&](int cc) { return __fma_rn(beta, pold[cc], zz[cc]); }, &own, strm);
               const double pi = ST ? own : (mode == M_FIRST ? zz[u] : __fma_rn(beta, pold[u], zz[u]));
               pnew[u] = pi;
               P.q[u] = acc;
@@ -1373,6 +1383,14 @@ lc_status run_pcg(const PcgJob& job, const lc_solver_params* p, cudaStream_t s, 
   // lazy x of depth 3 (tuning.lazy_x_depth: 2 or 3; 0 / 1: x updated every pass)
   a.lazyx = (kind == 0 && a.vec2 && tune.lazy_x_depth > 1) ? tune.lazy_x_depth : 0;
   a.np3 = a.lazyx == 3 ? 1 : 0;
+  {
+    // L2 policy of the matrix stream (lc_internal.cuh): bytes an iteration streams once, and the vectors it re-reads
+    // (r, z, q, the search directions, x, 1/a_ii) over the rows worked on; dynamic teams decide per phase
+    const int64_t mbytes = rows_work * (int64_t)M.maxw * (M.stencil ? 8 : 12);
+    const int64_t wbytes = rows_work * 8 * (int64_t)(5 + npv);
+    a.l2_bytes = l2_bytes();
+    a.stream_vals = kind == 3 ? tune.l2_stream_hint : (stream_policy_wanted(mbytes, wbytes) ? 1 : 0);
+  }
   if (e == cudaSuccess) e = cudaMemsetAsync(a.bar, 0, sizeof(GridBar), s);
   if (e == cudaSuccess && teams) e = cudaMemsetAsync(a.tctr, 0, 128 * (size_t)teams, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(a.out_iters, 0, 8 * G, s);

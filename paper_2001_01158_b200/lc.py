@@ -89,7 +89,7 @@ class Tuning(ctypes.Structure):
                 ("pcg_max_ctas", ctypes.c_int32), ("sub_repr", ctypes.c_int32), ("gmres_exact_cgs2", ctypes.c_int32),
                 ("gs_lines", ctypes.c_int32), ("spmv_csr_tma", ctypes.c_int32),
                 ("spmv_tma", ctypes.c_int32), ("batched_cluster", ctypes.c_int32),
-                ("block_dcoup", ctypes.c_int32)]
+                ("block_dcoup", ctypes.c_int32), ("l2_stream_hint", ctypes.c_int32)]
 
 
 _lib = None

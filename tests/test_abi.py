@@ -107,7 +107,7 @@ def test_tuning_host_only_roundtrip(lib):
     d = lc.tuning_defaults()
     assert d == dict(stencil_layout=1, symmetric_layout=0, pcg_cluster_resident=1, pcg_cluster=1, pcg_tma=1,
                      lazy_x_depth=3, batched_schedule=-1, pcg_max_ctas=0, sub_repr=-1, gmres_exact_cgs2=0,
-                     gs_lines=1, spmv_csr_tma=1, spmv_tma=1, batched_cluster=0, block_dcoup=1)
+                     gs_lines=1, spmv_csr_tma=1, spmv_tma=1, batched_cluster=0, block_dcoup=1, l2_stream_hint=-1)
     assert lc.get_tuning() == d
     prev = lc.set_tuning(lazy_x_depth=2, batched_schedule=1)
     try:
@@ -117,7 +117,7 @@ def test_tuning_host_only_roundtrip(lib):
         th.start(); th.join()
         assert seen == d                                   # other threads keep the defaults
         for bad in (dict(lazy_x_depth=4), dict(batched_schedule=3), dict(stencil_layout=2), dict(sub_repr=-2),
-                    dict(pcg_max_ctas=-1)):
+                    dict(pcg_max_ctas=-1), dict(l2_stream_hint=2)):
             with pytest.raises(lc.LcError):
                 lc.set_tuning(**bad)
     finally:

@@ -407,6 +407,30 @@ def test_lazy_x_depths_parity(cfg, n, s, rule, lazy, tune):
     assert torch.equal(x, x_ref)
 
 
+@pytest.mark.parametrize("cfg,n,s,rule,sub", [(5, 40, 4, 0, -1), (5, 40, 4, 0, 0), (2, 128, 7, 0, 0),
+                                              (3, 48, 6, 0, -1), (3, 48, 6, 0, 0), (1, 64, 2, 0, -1)])
+def test_l2_stream_hint_is_cache_policy_only(cfg, n, s, rule, sub, tune):
+    """lc_tuning.l2_stream_hint = 1 loads the matrix stream of every PCG kernel (TMA ring of the global and the
+    explicit-subsystem solves, plain loads of the masked, batched and dynamic-team solves) with the L2 evict_first
+    policy: the parity bars hold and the results are bitwise those of plain loads (hint 0)."""
+    tune(pcg_cluster_resident=0)
+    tune(sub_repr=sub)
+    sy = synth.system(cfg, s, n=n)
+    A = gpu_matrix(sy)
+    b, x0 = to_dev(sy.b), to_dev(sy.x0)
+    out = {}
+    for hint in (1, 0):
+        tune(l2_stream_hint=hint)
+        if hint == 1:
+            check_system(sy, RULES[cfg][rule])
+        x, rep = lc.local_method(A, b, x0, RULES[cfg][rule], method=method_of(cfg))
+        xg = x0.clone()
+        info = lc.solve_global(A, b, xg, method=method_of(cfg))
+        out[hint] = (x, xg, [i["iterations"] for i in rep["local"] + rep["global"] + info])
+    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
+
+
 @pytest.mark.parametrize("sub", [0, 1])
 @pytest.mark.parametrize("cfg,n,s,rule", [(5, 33, 4, 0), (5, 40, 12, 1), (2, 128, 30, 0), (1, 64, 5, 0),
                                           (3, 48, 6, 0), (3, 30, 2, 0)])
