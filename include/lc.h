@@ -362,8 +362,9 @@ lc_status lc_dist_connect_local(lc_dist* ranks, int32_t nranks);
  * handles this call drives (see above); b, x0: host arrays of nr device pointers to each rank's slab
  * [n_local].  The threshold uses the GLOBAL ||b||_2 (double-double, R23) and N, or the global max of the
  * criterion; an expansion round stops when the GLOBAL admission count is 0 (R40), so Omega equals
- * the one lc_select_domain finds on the whole matrix.  Dilation hops as in lc_select_domain; the percentile
- * threshold is not supported here.  K_global (host, optional): |Omega| over all ranks.  Syncs `stream`.
+ * the one lc_select_domain finds on the whole matrix.  Dilation hops as in lc_select_domain.  The percentile
+ * threshold (R14) is the nearest-rank quantile over ALL ranks' rows: a radix select whose digit counts are
+ * exchanged like the other reductions, so every rank holds bitwise lc_select_domain's tau.  K_global (host, optional): |Omega| over all ranks.  Syncs `stream`.
  */
 lc_status lc_dist_select_domain(lc_dist* ranks, int32_t nr, const double* const* b, const double* const* x0,
                                 const lc_domain_params* p, void* stream, int64_t* K_global);

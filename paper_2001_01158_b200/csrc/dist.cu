@@ -620,7 +620,38 @@ __global__ void __launch_bounds__(kDT, 2) k_ddomain(const __grid_constant__ DPac
   }
   xreduce(P, bid, nCTA, 1, a, s_w, s_out, ++seq, bep);
   double tau, tc;
-  if (P.thr == LC_THR_PAPER) {
+  if (P.thr == LC_THR_PERCENTILE) {
+    // nearest-rank p-quantile of c over ALL ranks (R14): radix select on the f64 bit patterns (c >= 0, so the
+    // patterns order like the values), 2 bits per pass -- the four digit counts of the keys that still match
+    // the prefix are one exchange (exact integers in doubles), every CTA of every rank takes the same digit
+    long long k = (long long)ceil(P.param * (double)P.nglob) - 1;
+    if (k < 0) k = 0;
+    if (k > P.nglob - 1) k = P.nglob - 1;
+    unsigned long long prefix = 0ull, mask = 0ull;
+    for (int shift = 62; shift >= 0; shift -= 2) {
+      a[0] = a[1] = a[2] = a[3] = 0.0;
+      for (int64_t u = (int64_t)bid * kDT + threadIdx.x; u < n; u += (int64_t)nCTA * kDT) {
+        const unsigned long long key = (unsigned long long)__double_as_longlong(crit[u]);
+        if ((key & mask) != prefix) continue;
+        const int d = (int)((key >> shift) & 3ull);
+        a[0] += d == 0 ? 1.0 : 0.0; a[1] += d == 1 ? 1.0 : 0.0; a[2] += d == 2 ? 1.0 : 0.0; a[3] += d == 3 ? 1.0 : 0.0;
+      }
+      xreduce(P, bid, nCTA, 0, a, s_w, s_out, ++seq, bep);
+      long long cum = 0;
+      int d = 0;
+      for (; d < 3; ++d) {
+        const long long cnt = (long long)s_out[d];
+        if (k < cum + cnt) break;
+        cum += cnt;
+      }
+      k -= cum;
+      prefix |= (unsigned long long)d << shift;
+      mask |= 3ull << shift;
+      __syncthreads();                                                       // s_out is rewritten by the next pass
+    }
+    tau = __longlong_as_double((long long)prefix);
+    tc = tau;
+  } else if (P.thr == LC_THR_PAPER) {
     const double nb = sqrt(s_out[0] + s_out[1]);
     tau = P.param * nb / sqrt((double)P.nglob);                              // Eq. 7 with the global N
     tc = tau;
@@ -1008,8 +1039,9 @@ extern "C" lc_status lc_dist_select_domain(lc_dist* R, int32_t nr, const double*
     set_error("lc_dist_select_domain: bad criterion"); return LC_ERR_INVALID_ARG;
   }
   if (p->threshold == LC_THR_PAPER ? !(p->param > 0)
-      : p->threshold == LC_THR_REL_MAX ? !(p->param >= 0 && p->param <= 1) : true) {
-    set_error("lc_dist_select_domain: threshold must be LC_THR_PAPER (eps > 0) or LC_THR_REL_MAX (theta in [0,1])");
+      : p->threshold == LC_THR_REL_MAX ? !(p->param >= 0 && p->param <= 1)
+      : p->threshold == LC_THR_PERCENTILE ? !(p->param > 0 && p->param < 1) : true) {
+    set_error("lc_dist_select_domain: bad threshold / param (eps > 0, theta in [0,1], p in (0,1))");
     return LC_ERR_INVALID_ARG;
   }
   if (p->expand_rounds < 0 || p->expand_rounds > 64 || p->dilate_hops < 0 || p->dilate_hops > 64 ||

@@ -101,6 +101,23 @@ def test_dist_config2_reduced_dilation(P):
     run_and_check(synth.system(2, 3, n=96), R_C2, P)
 
 
+@pytest.mark.parametrize("P,n,s", [(1, 96, 3), (2, 96, 3), (5, 96, 3), (3, 128, 30), (8, 160, 11)])
+def test_dist_config2_percentile_rule(P, n, s):
+    """Config 2's own rule on the partition: gradient criterion, nearest-rank P90 threshold over ALL ranks' rows
+    (radix select whose digit counts go through the rank exchange), 2 dilation hops: tau and Omega equal the
+    oracle's on the whole matrix for every p."""
+    rule = dict(criterion=1, threshold=2, param=0.9, expand_rounds=0, dilate_hops=2)
+    rep = run_and_check(synth.system(2, s, n=n), rule, P)
+    assert rep["K"] > 0
+
+
+@pytest.mark.parametrize("p", [0.5, 0.999])
+def test_dist_percentile_of_residual(p):
+    """The percentile threshold with the residual criterion (ties at c = 0 included: x0 is exact on most rows)."""
+    sy = synth.system(5, 6, n=20)
+    run_and_check(sy, dict(criterion=0, threshold=2, param=p, expand_rounds=0, dilate_hops=0), 3)
+
+
 def test_dist_ragged_slabs():
     """Slab boundaries off the 32-row slices (ragged first and last slices in every rank)."""
     sy = synth.system(5, 4, n=20)

@@ -19,3 +19,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_pc
   python tools/one_solve.py 3 > $O/ncu_pcgdyn_c3.log 2>&1
 timeout 600 python tools/ncu_traffic.py > $O/ncu_traffic.log 2>&1
 ls -la $O gpurun_out/ncu_traffic > $O/ls.txt
+timeout 600 python tools/parity_sweep.py --configs 1,4 --out $O/parity_sweep_c1_c4.json > $O/parity_sweep_c1_c4.log 2>&1
