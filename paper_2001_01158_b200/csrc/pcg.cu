@@ -985,7 +985,9 @@ __global__ void __launch_bounds__(kPT, ST == 0 ? LCV_MINB_SELL : LCV_MINB) k_pcg
 #ifndef LC_DYN_R
 #define LC_DYN_R 4
 #endif
-constexpr int kDynR = LC_DYN_R;          // slices per chunk
+constexpr int kDynR = LC_DYN_R;          // slices per chunk (config 3 global: 4: 35.0 ms; 2: 35.8; 1: 39.8; 8: 37.7;
+                                         // loading the update pass's operands of all 4 slices before the first
+                                         // update spilled: 43.3 ms -- profiles/r02_t)
 struct DynGroup {                        // a group's solver state between teams (global memory)
   int mode, par, it, final_, npass;
   unsigned gone;                         // 0, or the first phase without the group (its team finished it in phase
