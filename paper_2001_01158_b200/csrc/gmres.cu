@@ -18,6 +18,7 @@
 // round trip.  End of cycle: x += M^-1 (V y), then the true residual (R19).
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "lc_internal.cuh"
 
@@ -182,6 +183,27 @@ __device__ __forceinline__ void block_row_dcoup5(const SellView& A, int64_t s, i
       const int o = k < 2 ? k : k - 1;
 #pragma unroll
       for (int a = 0; a < 3; ++a) acc[a] = __fma_rn(cv[o][a], yy[k][a], acc[a]);
+    }
+  }
+}
+// The explicit 3T subsystems (SELL-32 of uniform width, full 3x3 blocks): for width 5 the five column indices
+// load first and every slot's gathers and values follow without a loop guard between them (the slot loop took
+// two dependent round trips per slot: column, then gather).  Padding slots hold their own row and zeros.  Same
+// chains in the same order as the loop.
+__device__ __forceinline__ void block_row_sell5(const SellView& A, int64_t p0, int lane, const double* __restrict__ y,
+                                                double* acc) {
+  int32_t c[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) c[k] = A.col[p0 + lane + 32 * k];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const double* vb = A.val + 9 * (p0 + 32ll * k) + lane;
+    const double y0 = y[3 * c[k]], y1 = y[3 * c[k] + 1], y2 = y[3 * c[k] + 2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      acc[a] = __fma_rn(ld_first(vb + 32 * (3 * a)), y0, acc[a]);
+      acc[a] = __fma_rn(ld_first(vb + 32 * (3 * a + 1)), y1, acc[a]);
+      acc[a] = __fma_rn(ld_first(vb + 32 * (3 * a + 2)), y2, acc[a]);
     }
   }
 }
@@ -371,6 +393,8 @@ __global__ void __launch_bounds__(kGT, kGMinB) k_gmres(GmresArgs P) {
         for (int a = 0; a < BS; ++a) acc[a] = 0.0;
         if (BS == 3 && A.cval) {
           block_row_dc(A, s, lane, wd, u, P.x, acc);
+        } else if (BS == 3 && !A.stencil && A.vw == 5) {
+          block_row_sell5(A, p0, lane, P.x, acc);
         } else
         for (int k = 0; k < wd; ++k) {
           int64_t c = sv_col(A, p0 + lane, k, u);
@@ -449,12 +473,16 @@ __global__ void __launch_bounds__(kGT, kGMinB) k_gmres(GmresArgs P) {
       // ---- 1b: w = A t, h_i = V_i . w.  A warp owns 1-2 slices per chunk: their w values stay in registers
       // and the (j+1) dots are formed i by i (no per-thread accumulator array in local memory).
       clear(j + 1);
-      for (int64_t s0 = s_begin; s0 < A.nslices; s0 += kCC * s_step) {
-        double wv[kCC][BS];
-        int64_t ea[kCC];                 // this lane's first element (a row past the end reads element 0, times w = 0)
-        bool ok[kCC];
+      // (CC slices per chunk: kCC, or 1 when no warp has a second slice -- a small subsystem -- so that no
+      // warp issues the clamped loads of an absent slice)
+      auto dots_pass = [&](auto cc_tag) {
+      constexpr int CC = decltype(cc_tag)::value;
+      for (int64_t s0 = s_begin; s0 < A.nslices; s0 += CC * s_step) {
+        double wv[CC][BS];
+        int64_t ea[CC];                 // this lane's first element (a row past the end reads element 0, times w = 0)
+        bool ok[CC];
 #pragma unroll
-        for (int cc = 0; cc < kCC; ++cc) {
+        for (int cc = 0; cc < CC; ++cc) {
           const int64_t s = s0 + cc * s_step;
           const int64_t u = s < A.nslices ? A.slice_row0[s] + lane : nunits;
           ok[cc] = u < nunits;
@@ -466,6 +494,8 @@ __global__ void __launch_bounds__(kGT, kGMinB) k_gmres(GmresArgs P) {
             const int wd = A.stencil ? A.W : (int)((A.slice_ptr[s + 1] - p0) >> 5);
             if (BS == 3 && A.cval) {
               block_row_dc(A, s, lane, wd, u, P.t, wv[cc]);
+            } else if (BS == 3 && !A.stencil && A.vw == 5) {
+              block_row_sell5(A, p0, lane, P.t, wv[cc]);
             } else
 #pragma unroll 5
             for (int k = 0; k < wd; ++k) {
@@ -488,23 +518,25 @@ __global__ void __launch_bounds__(kGT, kGMinB) k_gmres(GmresArgs P) {
           }
         }
         const double* Vj = P.V + (size_t)j * n;
-        double vj[kCC][BS];
+        double vj[CC][BS];
 #pragma unroll
-        for (int cc = 0; cc < kCC; ++cc)
+        for (int cc = 0; cc < CC; ++cc)
 #pragma unroll
           for (int a = 0; a < BS; ++a) vj[cc][a] = (ok[cc] && !P.exact_cgs2) ? Vj[ea[cc] + a] : 0.0;
-        // i in blocks of IB.  Every load of the block issues before its first use: the addresses are clamped
+        // i in blocks of IB (the loop is left to ptxas' own unrolling: #pragma unroll 1 / 2 / 4 measured 52.7 / 49.1 /
+        // 51.7 us per config 4 step against 49.2, and 1.59 / 1.43 / 1.40 ms against 1.36 ms for its local solve).
+        // Every load of the block issues before its first use: the addresses are clamped
         // (vector min(i, j), element 0 for a row past the end) instead of guarded, so no branch separates the
         // loads -- guarded, ptxas issued one vector's loads, waited, multiplied, and only then loaded the next
         // (18.5% of the kernel's stall samples sat on the first multiply, profiles/r02_p).  The block's 2 IB
         // sums are combined over the lanes by one merged butterfly (warp_sum_multi).
         for (int i0 = 0; i0 <= j; i0 += IB) {
-          double vi[IB][kCC][BS];
+          double vi[IB][CC][BS];
 #pragma unroll
           for (int ii = 0; ii < IB; ++ii) {
             const double* Vi = P.V + (size_t)(i0 + ii <= j ? i0 + ii : j) * n;
 #pragma unroll
-            for (int cc = 0; cc < kCC; ++cc)
+            for (int cc = 0; cc < CC; ++cc)
 #pragma unroll
               for (int a = 0; a < BS; ++a) vi[ii][cc][a] = ld_last(Vi + ea[cc] + a);
           }
@@ -514,7 +546,7 @@ __global__ void __launch_bounds__(kGT, kGMinB) k_gmres(GmresArgs P) {
 #pragma unroll
           for (int ii = 0; ii < IB; ++ii)
 #pragma unroll
-            for (int cc = 0; cc < kCC; ++cc)
+            for (int cc = 0; cc < CC; ++cc)
 #pragma unroll
               for (int a = 0; a < BS; ++a) {
                 dq[ii] = __fma_rn(vi[ii][cc][a], wv[cc][a], dq[ii]);
@@ -528,6 +560,9 @@ __global__ void __launch_bounds__(kGT, kGMinB) k_gmres(GmresArgs P) {
           }
         }
       }
+      };
+      if (A.nslices > s_step) dots_pass(std::integral_constant<int, kCC>{});
+      else dots_pass(std::integral_constant<int, 1>{});
       if (!P.exact_cgs2) {
         // ---- low-sync CGS2 (R39): G = V^T V gains column j in the same pass; the second projection
         // h2 = V^T (w - V h) = h - G h comes from scalars, and both updates merge into one pass.

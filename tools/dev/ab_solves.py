@@ -31,9 +31,10 @@ for cfg in (int(c) for c in args):
         info = lc.solve_global(A, b, x, method=m)
         best = min(best, info[0]["seconds"]); its = max(i["iterations"] for i in info)
     print(f"{tag} config {cfg} global: its {its} {best*1e3:.3f} ms {best/its*1e6:.2f} us/it", flush=True)
-    if cfg in (2, 3, 5):
+    if cfg in (2, 3, 4, 5):
         rule = {2: dict(criterion=1, threshold=2, param=0.9, dilate_hops=2),
                 3: dict(criterion=0, threshold=0, param=1e-10, expand_rounds=1),
+                4: dict(criterion=0, threshold=0, param=1e-10, expand_rounds=1),
                 5: dict(criterion=0, threshold=0, param=1e-10, expand_rounds=1)}[cfg]
         bl = 1e9
         for _ in range(3):
