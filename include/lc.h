@@ -401,8 +401,11 @@ typedef struct {
   int32_t stencil_layout;       /* 1 (default): constant-offset stencils are stored without column indices
                                    (LC_LAYOUT_STENCIL); 0: always SELL-32 with explicit columns */
   int32_t symmetric_layout;     /* 0 (default); 1: bitwise-symmetric stencils store diagonal + upper slots */
-  int32_t pcg_cluster_resident; /* 1 (default): stencil systems of <= ~30k rows run the PCG whose vectors stay
-                                   in the shared memory of one thread-block cluster; 0: never */
+  int32_t pcg_cluster_resident; /* stencil systems of <= ~27k rows run a PCG whose matrix and vectors stay in the
+                                   shared memory of one thread-block cluster.  2 (default): the single-reduction
+                                   form (Chronopoulos-Gear recurrences, one cluster barrier per iteration; the same
+                                   iterates in exact arithmetic, the parity bars hold); 1: the textbook two-reduction
+                                   order (bitwise the grid kernels' arithmetic, <= ~30k rows); 0: never */
   int32_t pcg_cluster;          /* 1 (default): single-segment solves of <= 512 slices launch as ONE cluster with
                                    hardware cluster barriers; 0: always the cooperative grid */
   int32_t pcg_tma;              /* 1 (default): TMA bulk-copy ring for the value stream of contiguous solves */

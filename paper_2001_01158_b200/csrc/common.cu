@@ -237,7 +237,7 @@ lc_status pending_info(const Pending& pend, lc_solve_info* info) {
 // ---- tuning (include/lc.h): thread-local, explicit, no environment variables ----
 static lc_tuning defaults_() {
   lc_tuning t;
-  t.stencil_layout = 1; t.symmetric_layout = 0; t.pcg_cluster_resident = 1; t.pcg_cluster = 1; t.pcg_tma = 1;
+  t.stencil_layout = 1; t.symmetric_layout = 0; t.pcg_cluster_resident = 2; t.pcg_cluster = 1; t.pcg_tma = 1;
   t.lazy_x_depth = 3; t.batched_schedule = -1; t.pcg_max_ctas = 0; t.sub_repr = -1; t.gmres_exact_cgs2 = 0;
   t.gs_lines = 1;
   t.spmv_csr_tma = 1;
@@ -498,7 +498,7 @@ extern "C" void lc_tuning_defaults(lc_tuning* t) {
 extern "C" lc_status lc_set_tuning(const lc_tuning* t) {
   if (!t) { lc::g_tune = lc::defaults_(); return LC_OK; }
   auto bin = [](int32_t v) { return v == 0 || v == 1; };
-  if (!bin(t->stencil_layout) || !bin(t->symmetric_layout) || !bin(t->pcg_cluster_resident) || !bin(t->pcg_cluster) ||
+  if (!bin(t->stencil_layout) || !bin(t->symmetric_layout) || t->pcg_cluster_resident < 0 || t->pcg_cluster_resident > 2 || !bin(t->pcg_cluster) ||
       !bin(t->pcg_tma) || t->lazy_x_depth < 0 || t->lazy_x_depth > 3 || t->batched_schedule < -1 ||
       t->batched_schedule > 2 || t->pcg_max_ctas < 0 || t->sub_repr < -1 || t->sub_repr > 1 ||
       !bin(t->gmres_exact_cgs2) || !bin(t->gs_lines) || !bin(t->spmv_csr_tma) || t->spmv_tma < 0 || t->spmv_tma > 2 ||

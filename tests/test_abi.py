@@ -105,7 +105,7 @@ def test_tuning_host_only_roundtrip(lib):
     """lc_tuning lives on the host (no device needed): defaults, range checks, thread-local set / get."""
     import threading
     d = lc.tuning_defaults()
-    assert d == dict(stencil_layout=1, symmetric_layout=0, pcg_cluster_resident=1, pcg_cluster=1, pcg_tma=1,
+    assert d == dict(stencil_layout=1, symmetric_layout=0, pcg_cluster_resident=2, pcg_cluster=1, pcg_tma=1,
                      lazy_x_depth=3, batched_schedule=-1, pcg_max_ctas=0, sub_repr=-1, gmres_exact_cgs2=0,
                      gs_lines=1, spmv_csr_tma=1, spmv_tma=1, batched_cluster=0, block_dcoup=1, l2_stream_hint=-1)
     assert lc.get_tuning() == d

@@ -895,6 +895,58 @@ def test_grid_kernel_path_parity(cfg, n, s, rule, tune):
     check_system(synth.system(cfg, s, n=n), RULES[cfg][rule])
 
 
+@pytest.mark.parametrize("cfg,n,s,rule", [(1, 64, 0, 0), (1, 64, 4, 0), (1, 64, 9, 0), (5, 20, 6, 0), (5, 24, 11, 1),
+                                          (2, 96, 5, 0), (2, 160, 21, 0), (1, 33, 2, 0)])
+def test_cluster_resident_textbook_order_parity(cfg, n, s, rule, tune):
+    """lc_tuning.pcg_cluster_resident = 1 keeps the textbook two-reduction order in the cluster-resident kernel
+    (k_pcg_ds); the default 2 is the single-reduction form (k_pcg_ds1, Chronopoulos-Gear recurrences, DESIGN R42).
+    Both against the oracle on the same systems (local masked solves and global solves), and against each other:
+    iterations within one, solutions within the 1e-9 bar."""
+    sy = synth.system(cfg, s, n=n)
+    res = {}
+    for form in (2, 1):
+        tune(pcg_cluster_resident=form)
+        check_system(sy, RULES[cfg][rule])
+        A = gpu_matrix(sy)
+        x = to_dev(sy.x0)
+        info = lc.solve_global(A, to_dev(sy.b), x)[0]
+        assert info["kernel"] == "pcg_resident", info
+        res[form] = (x.cpu().numpy(), info["iterations"])
+    assert abs(res[1][1] - res[2][1]) <= 1
+    assert np.linalg.norm(res[1][0] - res[2][0]) / np.linalg.norm(res[1][0]) <= 1e-9
+
+
+@pytest.mark.parametrize("form", [2, 1])
+def test_cluster_resident_cap_confirm_and_edge_cases(form, tune):
+    """The cluster-resident forms at the protocol's edges: an iteration cap (NOT_CONVERGED with the cap's count),
+    a cap of 0 (Eq. 6 check only), a tolerance the true residual cannot reach (every recursive convergence fails
+    its confirmation and restarts until the cap), b = 0 and an exact start (0 iterations), run twice bitwise."""
+    tune(pcg_cluster_resident=form)
+    sy = synth.system(1, 3, n=64)
+    A = gpu_matrix(sy)
+    b = to_dev(sy.b)
+    x = to_dev(sy.x0)
+    info = lc.solve_global(A, b, x, max_iters=7)[0]
+    assert info["kernel"] == "pcg_resident" and info["iterations"] == 7 and info["status"] == lc.LC_NOT_CONVERGED
+    x = to_dev(sy.x0)
+    info = lc.solve_global(A, b, x, max_iters=0)[0]
+    assert info["iterations"] == 0 and info["status"] == lc.LC_NOT_CONVERGED and torch.equal(x, to_dev(sy.x0))
+    x1, x2 = to_dev(sy.x0), to_dev(sy.x0)
+    i1 = lc.solve_global(A, b, x1, rel_tol=1e-17, max_iters=400)[0]
+    i2 = lc.solve_global(A, b, x2, rel_tol=1e-17, max_iters=400)[0]
+    assert i1["iterations"] == 400 and i1["status"] == lc.LC_NOT_CONVERGED
+    assert torch.equal(x1, x2) and i1["rel_residual"] == i2["rel_residual"]
+    Ao = oracle_csr(sy)
+    r = orc.residual(Ao, sy.b, x1.cpu().numpy())
+    assert np.linalg.norm(r) <= 1e-12 * np.linalg.norm(sy.b)          # it kept converging through the restarts
+    xz = to_dev(sy.x0)
+    info = lc.solve_global(A, torch.zeros_like(b), xz)[0]
+    assert info["status"] == lc.LC_OK and np.linalg.norm(xz.cpu().numpy()) <= 1e-9 * np.linalg.norm(sy.x0)
+    xs = to_dev(sy.xs)                      # the manufactured solution: r(x*) = 0 exactly (synth), 0 iterations
+    info = lc.solve_global(A, b, xs)[0]
+    assert info["iterations"] == 0 and info["status"] == lc.LC_OK
+
+
 def test_dsmem_and_grid_kernels_agree():
     """The cluster-resident kernel and the grid kernel: same iteration counts (the same reductions in a
     different fixed order may differ by one), solutions within the 1e-9 bar, on configs 1 and 5."""
