@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round evidence on one box: GPU tests, smoke, bench lines of every config + the reference arm, the ncu launch
 # list of the default bench, full ncu captures of the top kernels and the k_pcg DRAM traffic stamp.
-O=gpurun_out/ev; mkdir -p $O
+O=gpurun_out/ev2; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit,temperature.gpu --format=csv > $O/smi.txt
 timeout 1200 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "EXIT $?" >> $O/pytest_gpu.log
@@ -20,3 +20,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_pc
 timeout 600 python tools/ncu_traffic.py > $O/ncu_traffic.log 2>&1
 ls -la $O gpurun_out/ncu_traffic > $O/ls.txt
 timeout 600 python tools/parity_sweep.py --configs 1,4 --out $O/parity_sweep_c1_c4.json > $O/parity_sweep_c1_c4.log 2>&1
+timeout 1500 python tools/parity_sweep.py --configs 2,3,5 --out $O/parity_sweep_c2_c3_c5.json > $O/parity_sweep_c2_c3_c5.log 2>&1
