@@ -58,7 +58,7 @@ constexpr int kIB = LC_GMRES_IB;
 // rate, 19 us for 145 MB at j = 15, tools/tl_gmres.py)
 constexpr bool kGRev = LC_GMRES_REV != 0;
 #ifndef LC_GMRES_RED1
-#define LC_GMRES_RED1 2
+#define LC_GMRES_RED1 1
 #endif
 #ifndef LC_GMRES_VREV
 #define LC_GMRES_VREV 1
@@ -254,35 +254,6 @@ __device__ __forceinline__ double warp_sum_multi(double* v, int lane) {
   return r;
 }
 
-// fixed-order sums of nq quantities over the CTAs' partials pt[q * nCTA + cta] into red[q] (shared memory): a
-// lane adds CTAs lane, lane + 32, ... in that order, then the warp's lanes are combined by shuffles.  The loads of
-// TWO quantities (10 each per lane for <= 320 CTAs) issue together, so 2 (j + 1) <= 32 quantities cost one L2
-// round trip per warp instead of four.  Out of line: the 20 loads in flight need the registers the Arnoldi loop
-// holds live (inlined, ptxas spilled the loaded values themselves).
-__device__ __noinline__ void reduce_partials(const double* __restrict__ pt, int nq, int nCTA, double* red) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int q0 = warp; q0 < nq; q0 += 2 * kGW) {
-    const int q1 = q0 + kGW;
-    const bool two = q1 < nq;
-    double v0 = 0.0, v1 = 0.0;
-    for (int c0 = lane; c0 < nCTA; c0 += 32 * 10) {
-      double t0[10], t1[10];
-#pragma unroll
-      for (int k = 0; k < 10; ++k) {
-        const bool in = c0 + 32 * k < nCTA;
-        t0[k] = in ? __ldcg(pt + (size_t)q0 * nCTA + c0 + 32 * k) : 0.0;
-        t1[k] = in && two ? __ldcg(pt + (size_t)q1 * nCTA + c0 + 32 * k) : 0.0;
-      }
-#pragma unroll
-      for (int k = 0; k < 10; ++k)
-        if (c0 + 32 * k < nCTA) { v0 += t0[k]; v1 += t1[k]; }
-    }
-    v0 = warp_sum(v0);
-    v1 = warp_sum(v1);
-    if (lane == 0) { red[q0] = v0; if (two) red[q1] = v1; }
-  }
-}
-
 template <int BS, int IB>
 __global__ void __launch_bounds__(kGT, kGMinB) k_gmres(GmresArgs P) {
   unsigned long long bar_epoch = 0;
@@ -326,10 +297,9 @@ __global__ void __launch_bounds__(kGT, kGMinB) k_gmres(GmresArgs P) {
   auto reduce = [&](int nq) {
     const double* pt = P.part + (size_t)ppar * kMaxQ * nCTA;
     ppar ^= 1;
-#if LC_GMRES_RED1 == 1
-    reduce_partials(pt, nq, (int)nCTA, red);
-#elif LC_GMRES_RED1 == 2
-    // two quantities per warp at a time, 5 loads each in flight
+#if LC_GMRES_RED1
+    // two quantities per warp at a time, 5 partial loads each in flight (one quantity after the other with 8
+    // loads: +1.4 us per Arnoldi step; 10 + 10 loads in flight, inline or out of line: spills / +4.5 us)
     for (int q0 = warp; q0 < nq; q0 += 2 * kGW) {
       const int q1 = q0 + kGW;
       const bool two = q1 < nq;
