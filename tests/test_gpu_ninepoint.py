@@ -103,3 +103,63 @@ def test_local_method_vs_oracle(dims, offs, rule):
             assert abs(rep["local"][0]["iterations"] - ro.it_local) <= 1
     assert abs(rep["global"][0]["iterations"] - ro.it_global) <= 1
     assert np.linalg.norm(x.cpu().numpy() - xo) / np.linalg.norm(xo) <= 1e-9
+
+
+def three_t_system(dims, offsets_nd, seed, diagonal_couplings=True):
+    """A nonsymmetric 3T-like block system on a regular grid: per cell a full 3x3 diagonal block (identity +
+    exchange terms + the cell's share of the diffusion), per stored neighbour a coupling block -w diag(kappa_a)
+    (diagonal, as the 3T couplings P:1477-1482) or, with diagonal_couplings=False, one coupling block with an
+    off-diagonal entry.  Returns BSR arrays (row-major 3x3 blocks) + b, x0 for the 3 N unknowns."""
+    A1, _, _ = stencil_system(dims, offsets_nd, seed)
+    rng = np.random.default_rng(seed + 100)
+    n = A1.n
+    rp, ci, v1 = np.asarray(A1.rp), np.asarray(A1.ci), np.asarray(A1.val)
+    kap = np.array([1.0, 0.35, 2.5])
+    val = np.zeros((ci.size, 9))
+    for u in range(n):
+        off = 0.0
+        for p in range(rp[u], rp[u + 1]):
+            if ci[p] != u:
+                val[p, [0, 4, 8]] = v1[p] * kap
+                off += -v1[p]
+        p = rp[u] + int(np.flatnonzero(ci[rp[u]:rp[u + 1]] == u)[0])
+        W = rng.uniform(0.01, 30.0, (3, 3))
+        np.fill_diagonal(W, 0.0)
+        D = np.diag(1.0 + off * kap + W.sum(axis=1)) - W          # rows sum to 1 + diffusion: nonsymmetric, dominant
+        val[p] = D.reshape(9)
+    if not diagonal_couplings:
+        u = n // 2
+        p = rp[u] + (0 if ci[rp[u]] != u else 1)
+        val[p, 1] = 0.25 * val[p, 0]
+    xs = np.sin(0.03 * np.arange(3 * n)) + 0.7
+    Ao = orc.Csr.from_bsr(rp, ci, val.reshape(-1))
+    b = orc.spmv(Ao, xs)
+    x0 = xs.copy()
+    hot = slice(3 * (n // 3), 3 * (n // 3) + 3 * max(8, n // 40))
+    x0[hot] += 0.4 * np.cos(0.11 * np.arange(hot.stop - hot.start))
+    return rp, ci, val.reshape(-1), Ao, b, x0
+
+
+@pytest.mark.parametrize("dims,offs,diag", [((33, 35), NINE, True), ((33, 35), NINE, False),
+                                            ((40, 37), [(-1, 0), (0, -1), (0, 1), (1, 0)], True)])
+@pytest.mark.parametrize("rule", [dict(criterion=0, threshold=0, param=1e-10, expand_rounds=1), None])
+def test_three_t_block_stencils_gmres(dims, offs, diag, rule):
+    """Block 3 (3T) systems on the nine-point scheme and on a five-point grid with a ragged last slice:
+    the GMRES kernel's rows -- the branch-free five-point row, the slot loop for other widths, the full-block path
+    when a coupling block is not diagonal, the uniform-width explicit subsystem -- against the oracle's
+    right-preconditioned block-Jacobi GMRES(30): cell-granular Omega equal, Arnoldi steps +-1, x within 1e-9."""
+    rp, ci, val, Ao, b, x0 = three_t_system(dims, offs, 11, diag)
+    n = rp.size - 1
+    M = lc.Matrix(n, rp, ci, val, block=3)
+    assert M.info()["layout"] == "stencil" and M.info()["max_row"] == len(offs) + 1
+    x, rep = lc.local_method(M, dev(b), dev(x0), rule, method=lc.GMRES, keep=rule is not None)
+    dp = None
+    if rule is not None:
+        dp = orc.DomainParams(rule["criterion"], rule["threshold"], rule["param"], rule["expand_rounds"], 0, 3)
+    xo, flag, ro = orc.local_method(Ao, b, x0, dp, orc.SolverParams(1, 3, 30, EPS, 3000))
+    if rule is not None:
+        np.testing.assert_array_equal(rep["idx"].cpu().numpy(), np.flatnonzero(flag))
+        assert rep["K"][0] > 0
+        assert abs(rep["local"][0]["iterations"] - ro.it_local) <= 1
+    assert abs(rep["global"][0]["iterations"] - ro.it_global) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xo) / np.linalg.norm(xo) <= 1e-9
