@@ -151,6 +151,10 @@ def run_lc(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     from paper_2001_01158_b200 import build as lcbuild
+    if world > 1:       # a stale liblc.so is rebuilt by rank 0 alone (the ranks share the tree)
+        if rank == 0:
+            lcbuild.build()
+        dist.barrier()
     lcbuild.build()
     from paper_2001_01158_b200 import lc
     if args.tune:
