@@ -331,7 +331,7 @@ def run_lc(args):
         nlaunch = len(reps)
         kname = "k_pcg" if solver == "pcg" else "k_gmres"
         tr, tr_note = None, "no ncu capture for this config"
-        tdb = trafficdb.get(kname, {})
+        tdb = trafficdb.get(f"{kname}@c{cfg}") or trafficdb.get(kname, {})
         if tdb and cfg == tdb.get("config") and Ainfo["layout"] == tdb.get("layout"):
             if tdb.get("source_sha256") == src_sha and sorted(depths) == tdb.get("lazy_x_depths", sorted(depths)):
                 # measured DRAM bytes per iteration (ncu, this build) x the mean iterations per launch, like `achieved`
