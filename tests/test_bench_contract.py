@@ -68,3 +68,16 @@ def test_cpu_baseline_workers():
         p = parity["by_rule"][name]
         assert p["max_x_rel_err"] == 0.0 and p["max_it_global_diff"] == 0
     assert parity["by_rule"]["method2"]["omega_bit_exact"] and parity["by_rule"]["method2"]["near"] == 0
+
+
+def test_traffic_stamp_file():
+    """profiles/ncu_traffic.json (roofline.traffic's source): one entry per measured config under the key bench.py
+    looks up (kernel@cCONFIG), each stamped with the source hash of the build it measured and positive bytes."""
+    db = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    assert "k_pcg@c5" in db                                     # the default bench's config
+    for key, e in db.items():
+        assert e["dram_bytes_per_iteration"] > 0 and len(e["source_sha256"]) == 64 and e["source"]
+        if "@c" in key:
+            kname, c = key.split("@c")
+            assert int(c) == e["config"] and kname in ("k_pcg", "k_gmres")
+            assert (kname == "k_gmres") == (e["config"] == 4)
